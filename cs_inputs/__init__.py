@@ -1,0 +1,137 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU tests and bench.py.
+
+This module holds NONE of the method's arithmetic: it only draws the random
+objects a compressive-sensing trial is made of:
+
+* the sign diagonal sigma of A = P.DCT-II.diag(sigma), packed as bits
+  (bit j of word j//32 set  <=>  sigma_j = -1);
+* the row set of P: M distinct indices of [0, N), strictly increasing
+  ("randomly choose M indices");
+* the planted signal s (exact-K) and its support;
+* the measurement noise eta ~ N(0, sigma_eta^2) i.i.d. (Eq.13).
+
+y = A s + eta is NOT formed here: tests form it with `oracle/`, bench.py forms
+it with the product operator (cs_operator_apply) outside the timed region.
+
+Seeds: numpy PCG64(SeedSequence([cfg, trial, b, tag])), tag 0 = sigma,
+1 = rows, 2 = positions, 3 = values, 4 = noise, 5 = permutation.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import numpy as np
+
+TAG_SIGMA, TAG_ROWS, TAG_POS, TAG_VAL, TAG_NOISE, TAG_PERM = range(6)
+
+
+def rng(cfg: int, trial: int, b: int, tag: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([cfg, trial, b, tag])))
+
+
+@dataclasses.dataclass(frozen=True)
+class Config:
+    """One BASELINE.json config."""
+    cid: int
+    alg: str            # "omp" | "sp" | "ompr"
+    N: int
+    M: int
+    K: int
+    signal: str         # "gauss" | "pm1" | "power"
+    noise: float        # sigma_eta
+    batch: int = 1
+
+    def scaled(self, div: int, batch: Optional[int] = None) -> "Config":
+        """Same recipe at N/div, M/div, K/div (ratios kept); used for parity tests."""
+        return dataclasses.replace(self, N=self.N // div, M=self.M // div,
+                                   K=max(1, self.K // div),
+                                   batch=self.batch if batch is None else batch)
+
+
+# BASELINE.json "configs" (0-based index in that list = cid - 1).
+CONFIGS = {
+    1: Config(1, "omp", 4096, 1024, 64, "gauss", 0.0),
+    2: Config(2, "sp", 65536, 16384, 2048, "gauss", 1e-3),
+    3: Config(3, "ompr", 1 << 20, 1 << 18, 8192, "pm1", 0.0),
+    4: Config(4, "sp", 16384, 4096, 256, "gauss", 0.0, batch=4096),
+    5: Config(5, "sp", 1 << 24, 1 << 22, 65536, "power", 1e-4),
+}
+
+
+def pack_sign_bits(neg: np.ndarray) -> np.ndarray:
+    """Pack a boolean 'sigma_j = -1' vector into ceil(N/32) uint32 words (zero padded)."""
+    neg = np.asarray(neg, dtype=bool)
+    pad = (-neg.size) % 32
+    if pad:
+        neg = np.concatenate([neg, np.zeros(pad, dtype=bool)])
+    return np.packbits(neg, bitorder="little").view("<u4").astype(np.uint32)
+
+
+def unpack_sign_bits(bits: np.ndarray, N: int) -> np.ndarray:
+    """Inverse of pack_sign_bits: returns the boolean 'negative' mask (input decoding only)."""
+    b = np.unpackbits(np.asarray(bits, dtype="<u4").view(np.uint8), bitorder="little")
+    return b[:N].astype(bool)
+
+
+def draw_sign_bits(N: int, g: np.random.Generator) -> np.ndarray:
+    if N % 32:
+        raise ValueError("N must be a multiple of 32 for packed sign bits")
+    return pack_sign_bits(g.integers(0, 2, N).astype(bool))
+
+
+def draw_rows(N: int, M: int, g: np.random.Generator) -> np.ndarray:
+    return np.sort(g.choice(N, M, replace=False)).astype(np.int32)
+
+
+def draw_signal(kind: str, N: int, K: int, g_pos: np.random.Generator,
+                g_val: np.random.Generator, g_perm: np.random.Generator):
+    """Planted signal s (float64[N]) and its sorted support (int64)."""
+    s = np.zeros(N, dtype=np.float64)
+    if kind == "power":
+        # |s|_(i) = i^-1.5, i = 1..N, random signs, random positions
+        perm = g_perm.permutation(N)
+        mag = np.arange(1, N + 1, dtype=np.float64) ** -1.5
+        sgn = np.where(g_val.integers(0, 2, N) == 1, -1.0, 1.0)
+        s[perm] = sgn * mag
+        return s, np.sort(perm[:K])
+    pos = np.sort(g_pos.choice(N, K, replace=False))
+    if kind == "gauss":
+        vals = g_val.standard_normal(K)
+    elif kind == "pm1":
+        sgn = np.where(g_val.integers(0, 2, K) == 1, -1.0, 1.0)
+        vals = sgn * (1.0 + np.abs(g_val.standard_normal(K)))
+    else:
+        raise ValueError(kind)
+    s[pos] = vals
+    return s, pos
+
+
+@dataclasses.dataclass
+class Problem:
+    N: int
+    M: int
+    K: int
+    alg: str
+    sign_bits: np.ndarray   # uint32[N/32]
+    rows: np.ndarray        # int32[M], strictly increasing
+    s: np.ndarray           # float64[N] planted signal
+    support: np.ndarray     # planted support (sorted)
+    noise: np.ndarray       # float64[M] eta
+
+
+def make_problem(cfg: Config, trial: int = 0, b: int = 0) -> Problem:
+    c = cfg.cid
+    N, M, K = cfg.N, cfg.M, cfg.K
+    bits = draw_sign_bits(N, rng(c, trial, b, TAG_SIGMA))
+    rows = draw_rows(N, M, rng(c, trial, b, TAG_ROWS))
+    s, supp = draw_signal(cfg.signal, N, K, rng(c, trial, b, TAG_POS),
+                          rng(c, trial, b, TAG_VAL), rng(c, trial, b, TAG_PERM))
+    eta = rng(c, trial, b, TAG_NOISE).standard_normal(M) * cfg.noise if cfg.noise > 0 \
+        else np.zeros(M)
+    return Problem(N, M, K, cfg.alg, bits, rows, s, supp, eta)
+
+
+def make_batch(cfg: Config, trial: int = 0, b0: int = 0, count: Optional[int] = None):
+    count = cfg.batch if count is None else count
+    return [make_problem(cfg, trial, b0 + i) for i in range(count)]

@@ -1,0 +1,69 @@
+"""Oracle sensing operator A = P . F . diag(sigma)  (fp64, CPU).  TEST INFRASTRUCTURE.
+
+Paper: Eq.(7) Phi = D F R: D samples M of N rows
+("randomly choose M indices"), F is an orthonormal DCT (P:309-313,
+"DCT can be speeded by FFT"), R is a randomizer.  BASELINE.json
+binds the randomizer to a +-1 sign diagonal and Psi = I (reading R1),
+so A x = (C_N (sigma . x))[rows] and A^T w = sigma . C_N^T scatter_rows(w)
+(SURVEY §8c.1).  C_N is the orthonormal DCT-II
+    C_N[k, n] = c_k sqrt(2/N) cos(pi (2n+1) k / (2N)),  c_0 = 1/sqrt 2, else 1
+(S:129), applied here with scipy.fft.dct(type=2, norm="ortho") and its
+inverse; `dct_matrix` writes the same definition out as an explicit matrix for
+tiny N (the check path, SURVEY §8c.1 "For N <= 4096, use a dense C_N").
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.fft
+
+from cs_inputs import unpack_sign_bits
+
+
+def dct_matrix(N: int) -> np.ndarray:
+    """Explicit orthonormal DCT-II matrix C_N, O(N^2): tiny N only."""
+    k = np.arange(N)[:, None].astype(np.float64)
+    n = np.arange(N)[None, :].astype(np.float64)
+    C = np.sqrt(2.0 / N) * np.cos(np.pi * (2.0 * n + 1.0) * k / (2.0 * N))
+    C[0, :] *= 1.0 / np.sqrt(2.0)
+    return C
+
+
+def dense_srm(N: int, sign_bits: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    """A = C_N[rows] diag(sigma) as a dense M x N matrix (tiny N only)."""
+    sigma = np.where(unpack_sign_bits(sign_bits, N), -1.0, 1.0)
+    return dct_matrix(N)[np.asarray(rows)] * sigma[None, :]
+
+
+class SrmOperator:
+    """Matrix-free A and A^T: O(N log N) time, O(N) memory."""
+
+    def __init__(self, N: int, sign_bits: np.ndarray, rows: np.ndarray):
+        self.N = int(N)
+        self.rows = np.asarray(rows, dtype=np.int64)
+        self.M = self.rows.size
+        self.sigma = np.where(unpack_sign_bits(sign_bits, N), -1.0, 1.0)
+
+    def apply(self, x: np.ndarray) -> np.ndarray:
+        """A x = P C_N (sigma . x): sign, DCT-II (ortho), keep rows."""
+        X = scipy.fft.dct(self.sigma * np.asarray(x, dtype=np.float64), type=2, norm="ortho")
+        return X[self.rows]
+
+    def adjoint(self, w: np.ndarray) -> np.ndarray:
+        """A^T w = sigma . C_N^T P^T w: zero-fill unselected rows, DCT-III, sign."""
+        z = np.zeros(self.N)
+        z[self.rows] = np.asarray(w, dtype=np.float64)
+        return self.sigma * scipy.fft.idct(z, type=2, norm="ortho")
+
+
+class DenseOperator:
+    """A given as an explicit matrix (M-OMP style); used for toy pins."""
+
+    def __init__(self, A: np.ndarray):
+        self.A = np.asarray(A, dtype=np.float64)
+        self.M, self.N = self.A.shape
+
+    def apply(self, x):
+        return self.A @ np.asarray(x, dtype=np.float64)
+
+    def adjoint(self, w):
+        return self.A.T @ np.asarray(w, dtype=np.float64)

@@ -1,0 +1,111 @@
+"""Pins for oracle/operator.py against facts fixed by the paper and the mathematics.
+
+The oracle applies A with scipy's DCT; these tests check it against (a) the
+explicit DCT-II definition written as a matrix, (b) closed-form DCT
+facts (constant and cosine inputs), (c) SPEC's worked examples, and (d) the
+structural invariants A A^T = I_M, adjoint identity, linearity.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.fft
+
+from cs_inputs import pack_sign_bits, draw_sign_bits, draw_rows, rng
+from oracle import SrmOperator, dct_matrix, dense_srm
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def _op(N, M, seed=0):
+    bits = draw_sign_bits(max(N, 32), rng(99, seed, N, 0))
+    rows = draw_rows(N, M, rng(99, seed, N, 1))
+    return SrmOperator(N, bits, rows), bits, rows
+
+
+def test_dct_constant_worked_example():
+    g = GOLD["dct_constant"]
+    op = SrmOperator(4, pack_sign_bits(np.zeros(4, bool)), np.arange(4))
+    np.testing.assert_allclose(op.apply(np.array(g["x"], float)), g["X"], atol=1e-15)
+    gi = GOLD["dct_inverse_constant"]
+    np.testing.assert_allclose(op.adjoint(np.array(gi["X"], float)), gi["x"], atol=1e-15)
+
+
+@pytest.mark.parametrize("N", [4, 8, 32, 256])
+def test_dct_cosine_inputs_are_impulses(N):
+    # u_n = cos(pi (2n+1) k0 / 2N) is row k0 of the unnormalised DCT-II basis;
+    # with orthonormal scaling X = sqrt(N/2) e_k0 (k0 >= 1), sqrt(N) e_0 for k0 = 0.
+    op = SrmOperator(N, pack_sign_bits(np.zeros(N, bool)), np.arange(N))
+    n = np.arange(N)
+    for k0 in [0, 1, N // 2, N - 1]:
+        u = np.cos(np.pi * (2 * n + 1) * k0 / (2 * N))
+        X = op.apply(u)
+        e = np.zeros(N)
+        e[k0] = np.sqrt(N) if k0 == 0 else np.sqrt(N / 2)
+        np.testing.assert_allclose(X, e, atol=1e-12 * np.sqrt(N))
+
+
+@pytest.mark.parametrize("N,M", [(8, 2), (16, 4), (64, 16), (256, 64), (1024, 256), (4096, 1024)])
+def test_operator_matches_dense_definition(N, M):
+    """BASELINE.json oracle check (1): operator and adjoint exact to 1e-12 vs explicit A."""
+    op, bits, rows = _op(N, M)
+    A = dense_srm(N, bits, rows)
+    g = np.random.default_rng(N)
+    for _ in range(3):
+        x = g.standard_normal(N)
+        w = g.standard_normal(M)
+        np.testing.assert_allclose(op.apply(x), A @ x, atol=1e-12 * np.linalg.norm(x))
+        np.testing.assert_allclose(op.adjoint(w), A.T @ w, atol=1e-12 * np.linalg.norm(w))
+
+
+def test_dct_matrix_is_orthonormal():
+    for N in [4, 16, 128]:
+        C = dct_matrix(N)
+        np.testing.assert_allclose(C @ C.T, np.eye(N), atol=1e-13)
+    # and equals scipy's orthonormal DCT-II applied to the identity (independent routine)
+    C = dct_matrix(64)
+    np.testing.assert_allclose(C, scipy.fft.dct(np.eye(64), type=2, norm="ortho", axis=0), atol=1e-13)
+
+
+@pytest.mark.parametrize("N,M", [(32, 8), (256, 64), (2048, 512)])
+def test_rows_orthonormal_AAT_identity(N, M):
+    """unscaled SRM with orthonormal transform has A A^T = I_M."""
+    op, _, _ = _op(N, M)
+    AAT = np.stack([op.apply(op.adjoint(e)) for e in np.eye(M)], axis=1)
+    np.testing.assert_allclose(AAT, np.eye(M), atol=1e-13)
+
+
+def test_adjoint_identity_linearity_zero():
+    N, M = 1 << 14, 1 << 12
+    op, _, _ = _op(N, M, seed=3)
+    g = np.random.default_rng(7)
+    for _ in range(10):
+        x, w = g.standard_normal(N), g.standard_normal(M)
+        lhs, rhs = op.apply(x) @ w, x @ op.adjoint(w)
+        assert abs(lhs - rhs) <= 1e-12 * np.linalg.norm(x) * np.linalg.norm(w)
+    x, z = g.standard_normal(N), g.standard_normal(N)
+    np.testing.assert_allclose(op.apply(2 * x - 3 * z), 2 * op.apply(x) - 3 * op.apply(z), atol=1e-11)
+    assert not np.any(op.apply(np.zeros(N)))
+    assert not np.any(op.adjoint(np.zeros(M)))
+
+
+def test_sign_diagonal_effect():
+    # flipping sigma_j flips column j of A exactly
+    N, M = 64, 16
+    bits0 = pack_sign_bits(np.zeros(N, bool))
+    neg = np.zeros(N, bool)
+    neg[5] = True
+    bits1 = pack_sign_bits(neg)
+    rows = np.arange(0, N, 4)
+    A0, A1 = dense_srm(N, bits0, rows), dense_srm(N, bits1, rows)
+    np.testing.assert_array_equal(A1[:, 5], -A0[:, 5])
+    np.testing.assert_array_equal(np.delete(A1, 5, 1), np.delete(A0, 5, 1))
+
+
+def test_first_row_is_mean_scaled():
+    # C_N[0, :] = 1/sqrt(N): with rows = [0] and sigma = +1, A x = sum(x)/sqrt(N)
+    N = 32
+    op = SrmOperator(N, pack_sign_bits(np.zeros(N, bool)), np.array([0]))
+    x = np.arange(N, dtype=float)
+    np.testing.assert_allclose(op.apply(x), [x.sum() / np.sqrt(N)], rtol=1e-14)

@@ -1,0 +1,120 @@
+"""Pins for oracle/pursuits.py: worked examples, brute force, dense-LS backend
+equivalence (Thm 1-2 at algorithm level), exact noiseless recovery (BJ check 4)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import cs_inputs
+from cs_inputs import CONFIGS
+from oracle import DenseOperator, SrmOperator, omp, sp, ompr, brute_force_l0, topk
+from helpers import measure, oracle_recover
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+@pytest.mark.parametrize("fn", [omp, sp, ompr])
+def test_identity_worked_example(fn):
+    g = GOLD["pursuit_identity"]
+    op = DenseOperator(np.eye(4))
+    res = fn(op, np.array(g["y"], float), g["K"], tol=1e-13)
+    np.testing.assert_array_equal(res.support, g["support"])
+    np.testing.assert_allclose(res.s_hat, g["s_hat"], atol=1e-14)
+
+
+def test_brute_force_identity_worked_example():
+    g = GOLD["brute_force_identity"]
+    S, v, res = brute_force_l0(np.eye(4), np.array(g["y"], float), g["k"])
+    np.testing.assert_array_equal(S, g["support"])
+    assert res <= 1e-14
+
+
+def test_topk_ties_go_to_lowest_index():
+    v = np.array([1.0, 3.0, 3.0, 0.5, 3.0, 2.0])
+    np.testing.assert_array_equal(topk(v, 2), [1, 2])
+    np.testing.assert_array_equal(topk(v, 4), [1, 2, 4, 5])
+    allowed = np.array([True, False, True, True, True, True])
+    np.testing.assert_array_equal(topk(v, 2, allowed), [2, 4])
+    np.testing.assert_array_equal(topk(np.zeros(5), 3), [0, 1, 2])
+
+
+@pytest.mark.parametrize("fn", [omp, sp, ompr])
+def test_matches_brute_force_on_tiny_planted(fn):
+    """l0 enumeration (Eq.(3)) on noiseless planted 2-sparse instances."""
+    g = np.random.default_rng(11)
+    hits = 0
+    for trial in range(20):
+        M, N, k = 16, 24, 2
+        A = g.standard_normal((M, N))
+        S0 = np.sort(g.choice(N, k, replace=False))
+        s = np.zeros(N)
+        s[S0] = g.standard_normal(k) + np.sign(g.standard_normal(k))
+        y = A @ s
+        Sb, _, rb = brute_force_l0(A, y, k)
+        np.testing.assert_array_equal(Sb, S0)
+        assert rb <= 1e-10
+        res = fn(DenseOperator(A), y, k, tol=1e-13)
+        if res.resid_norm <= 1e-9 * np.linalg.norm(y):
+            np.testing.assert_array_equal(res.support, Sb)    # residual 0 => the l0 solution
+            hits += 1
+        else:
+            assert res.resid_norm >= rb                        # l0 lower-bounds every pursuit
+    assert hits >= 16
+
+
+@pytest.mark.parametrize("alg", ["omp", "sp", "ompr"])
+def test_cg_backend_equals_dense_ls_backend(alg):
+    """S:484 acceptance 4: CG_WEIGHTED == DENSE_LS, N=128, M=32, K=8."""
+    for trial in range(10):
+        cfg = cs_inputs.Config(90, alg, 128, 32, 8, "gauss", 0.0 if trial % 2 else 1e-2)
+        p = cs_inputs.make_problem(cfg, trial)
+        op, y32 = measure(p)
+        a = oracle_recover(p, y32, tol=1e-13)
+        b = oracle_recover(p, y32, tol=1e-13, solver="lstsq")
+        np.testing.assert_array_equal(a.support, b.support)
+        assert np.linalg.norm(a.s_hat - b.s_hat) <= 1e-8 * np.linalg.norm(b.s_hat)
+
+
+def _check_exact(p, res, rtol):
+    np.testing.assert_array_equal(res.support, p.support)
+    assert np.linalg.norm(res.s_hat - p.s) <= rtol * np.linalg.norm(p.s)
+
+
+def test_exact_recovery_c1_omp_full_size():
+    """BJ check (4): noiseless OMP recovers the planted support, config 1 at full size."""
+    p = cs_inputs.make_problem(CONFIGS[1])
+    op, y32 = measure(p)
+    res = oracle_recover(p, y32)
+    _check_exact(p, res, 1e-6)        # y is rounded to fp32 (R21): error ~ 6e-8 relative
+    assert res.outer_iters == 64
+
+
+def test_exact_recovery_c4_sp_full_size_problem():
+    p = cs_inputs.make_problem(CONFIGS[4], b=3)
+    op, y32 = measure(p)
+    res = oracle_recover(p, y32)
+    _check_exact(p, res, 1e-6)
+
+
+def test_exact_recovery_c3_ompr_scaled():
+    p = cs_inputs.make_problem(CONFIGS[3].scaled(32))
+    op, y32 = measure(p)
+    res = oracle_recover(p, y32)
+    _check_exact(p, res, 1e-6)
+    assert res.termination == 3       # support fixed point
+
+
+def test_sp_noisy_invariants_c2_scaled():
+    """c2 is noisy: parity unpinned beyond invariants."""
+    p = cs_inputs.make_problem(CONFIGS[2].scaled(8))
+    op, y32 = measure(p)
+    res = oracle_recover(p, y32)
+    h = res.resid_history
+    assert all(h[i + 1] < h[i] for i in range(len(h) - 1))
+    y = y32.astype(np.float64)
+    grad = op.adjoint(y - op.apply(res.s_hat))[res.support]
+    assert np.linalg.norm(grad) <= 1e-9 * np.linalg.norm(op.adjoint(y)[res.support])
+    assert res.support.size == p.K
+    # noise floor: ||r|| is about sigma sqrt(M - K)
+    assert res.resid_norm <= 2.0 * CONFIGS[2].noise * np.sqrt(p.M)
