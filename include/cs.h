@@ -1,0 +1,172 @@
+/*
+ * cs.h — C ABI of the B200-native greedy compressive-sensing library (libcsgpu.so).
+ *
+ * Method: Hsieh, Lu, Pei, "Fast Greedy Approaches for Compressive Sensing of
+ * Large-Scale Signals", arXiv:1509.03979.  Citation key: P:n = PAPER.md line n,
+ * S:n = SPEC.md line n (both under the reference mount).
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ *  - Every pointer named d_* is CALLER-OWNED DEVICE memory on the current
+ *    CUDA device (torch allocates it).  The library never allocates device
+ *    memory; the only library-owned object is the small host struct behind
+ *    cs_operator*.
+ *  - Every compute call is asynchronous on `stream` (0 = legacy default stream).
+ *    Results are valid after the caller synchronises that stream.
+ *  - Errors are status codes; nothing throws across the ABI.  Host-side
+ *    argument validation is synchronous and happens before any launch.
+ *    cs_last_error() returns a thread-local detail string for the last
+ *    non-CS_OK status of the calling thread.
+ *  - fp32 and fp64 variants exist for each compute call (suffix _f64); the
+ *    element type of the buffers is the arithmetic type of the whole path.
+ *  - Vectors are row-major; batched arrays are [B][len].
+ *  - Supported N: power of two with 8 <= N <= 2^25.  Other N return
+ *    CS_ERR_UNSUPPORTED (the paper's grid is 2^11..2^24).
+ */
+#ifndef CS_H_
+#define CS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* cs_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  CS_OK = 0,
+  CS_ERR_INVALID_ARG = 1,   /* bad sizes, NULL pointers, bad rows (checked at create) */
+  CS_ERR_UNSUPPORTED = 2,   /* N not a power of two / outside [8, 2^25]; device not sm_100 */
+  CS_ERR_WORKSPACE = 3,     /* ws_bytes / meta_bytes smaller than required */
+  CS_ERR_CUDA = 4,          /* a CUDA runtime call failed (detail in cs_last_error) */
+  CS_ERR_NONFINITE = 5      /* reserved for host-detected non-finite input */
+} cs_status;
+
+typedef enum { CS_OMP = 0, CS_SP = 1, CS_OMPR = 2 } cs_alg;
+
+/* cs_report.termination — why the OUTER pursuit loop stopped. */
+typedef enum {
+  CS_TERM_DONE = 0,          /* OMP ran its K iterations                 */
+  CS_TERM_ITER_CAP = 1,      /* SP/OMPR hit max_outer                                   */
+  CS_TERM_STAGNATION = 2,    /* a CG solve broke down (d^T H d <= 0)             */
+  CS_TERM_SUPPORT_FIXED = 3, /* SP/OMPR: new support == old support                     */
+  CS_TERM_RESID_ROSE = 4     /* SP: ||r'|| >= ||r|| — previous (S, x) kept      */
+} cs_term;
+
+/* cs_report.status bits — conditions found on the device. */
+#define CS_DEV_NONFINITE_Y   1u  /* y contained NaN/Inf: outputs are undefined */
+#define CS_DEV_CG_CAP        2u  /* some CG solve stopped at its iteration cap          */
+#define CS_DEV_CG_BREAKDOWN  4u  /* some CG solve stopped on d^T H d <= 0               */
+
+typedef struct {
+  int32_t outer_iters;     /* pursuit outer iterations executed                       */
+  int32_t cg_iters_total;  /* sum of CG iterations over all solves                    */
+  int32_t cg_solves;       /* number of CG solves                                     */
+  int32_t applies;         /* number of A / A^T pairs ("sandwiches") executed         */
+  int32_t termination;     /* cs_term                                                 */
+  uint32_t status;         /* CS_DEV_* bits                                           */
+  double resid_norm;       /* ||y - A s_hat||_2 at exit                               */
+  double cg_rel_resid;     /* largest ||r_j||/||b|| at the exit of any CG solve       */
+} cs_report;               /* 40 bytes */
+
+typedef struct {
+  int32_t max_outer;    /* SP/OMPR outer cap; 0 -> SP 30, OMPR 2K */
+  int32_t cg_max_iters; /* 0 -> |S| + 50 (Thm 5 bound |S| plus slack, SURVEY #29)           */
+  int32_t ompr_l;       /* OMPR(l): indices swapped in per outer iteration; 0 -> 1  */
+  float ompr_eta;       /* OMPR step eta; 0 -> 1.0                                   */
+  int32_t reserved[4];  /* must be zero                                                      */
+} cs_options;
+
+/* ---------------------------------------------------------------- operator ---
+ * A = P . C_N . diag(sigma)   (Eq.(7) Phi = D F R, with BASELINE.json's
+ * sign randomizer and Psi = I; C_N = orthonormal DCT-II; P = row selection,
+ * P:485).  A x = (C_N (sigma . x))[rows], A^T w = sigma . C_N^T scatter_rows(w).
+ *
+ * An operator holds `batch` independent instances (each with its own sigma and
+ * rows), used by the batched calls.  Instance b occupies row b of every batched
+ * array.
+ */
+typedef struct cs_operator cs_operator;
+
+/* Bytes of device metadata `cs_operator_create` needs (sign words, row bitmask,
+ * row-rank prefix: 3 * ceil(N/32) * 4 bytes per instance, 256-byte aligned). */
+size_t cs_operator_meta_bytes(int64_t N, int64_t M, int64_t batch);
+
+/* Build an operator.
+ *   d_sign_bits [batch][ceil(N/32)] uint32: bit (j % 32) of word j/32 set <=> sigma_j = -1.
+ *   d_rows      [batch][M] int32: strictly increasing, each in [0, N).  Checked HERE on
+ *               the device; violations return CS_ERR_INVALID_ARG.
+ *   d_meta      caller buffer of >= cs_operator_meta_bytes bytes; must outlive the operator.
+ * Synchronises `stream` (the row check is read back).  Inputs may be freed afterwards. */
+cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
+                             const int32_t* d_rows, void* d_meta, size_t meta_bytes,
+                             cs_stream_t stream, cs_operator** out);
+cs_status cs_operator_destroy(cs_operator* op);
+cs_status cs_operator_info(const cs_operator* op, int64_t* N, int64_t* M, int64_t* batch);
+
+/* Workspace bytes for apply/adjoint (0 for N <= 16384, else the four-step scratch). */
+size_t cs_operator_ws_bytes(const cs_operator* op, int precision /*0 fp32, 1 fp64*/);
+
+/* y[b] = A_b x[b] for every instance b.  x [batch][N], y [batch][M]. */
+cs_status cs_operator_apply(const cs_operator* op, const float* d_x, float* d_y, void* d_ws,
+                            size_t ws_bytes, cs_stream_t stream);
+cs_status cs_operator_apply_f64(const cs_operator* op, const double* d_x, double* d_y,
+                                void* d_ws, size_t ws_bytes, cs_stream_t stream);
+/* x[b] = A_b^T y[b] (zero-fill unselected rows, DCT-III, sign).  y [batch][M], x [batch][N]. */
+cs_status cs_operator_adjoint(const cs_operator* op, const float* d_y, float* d_x, void* d_ws,
+                              size_t ws_bytes, cs_stream_t stream);
+cs_status cs_operator_adjoint_f64(const cs_operator* op, const double* d_y, double* d_x,
+                                  void* d_ws, size_t ws_bytes, cs_stream_t stream);
+
+/* ---------------------------------------------------------------- recovery ---
+ * Greedy recovery with the CG-solved weighted least squares of Eq.(11) (P:376,
+ * Algorithm 1) in place of the pseudo-inverse:
+ *   CS_OMP  — Algorithm 1, exactly K outer iterations;
+ *   CS_SP   — CG-SP (named P:574-576; body per S:286-294, R15);
+ *   CS_OMPR — CG-OMPR(l, eta) (named P:574-576; body per S:296-304, R16).
+ * Each CG solve is warm-started from the previous iterate and stops when
+ * ||r_j|| <= tol * ||b|| (relative; R6/R7), at cg_max_iters, or on breakdown.
+ *
+ * Outputs: d_support [K] int32 ascending, d_vals [K] the LS coefficients on it,
+ * d_report one cs_report (DEVICE memory).  Requirements: 1 <= K; OMP: K <= M;
+ * SP: 2K <= M; OMPR: K + l <= M; K <= N/2; 0 <= tol.
+ */
+cs_status cs_workspace_bytes(int alg, int64_t N, int64_t M, int32_t K, int64_t batch,
+                             int precision /*0 fp32, 1 fp64*/, const cs_options* opts,
+                             size_t* bytes);
+
+cs_status cs_recover(const cs_operator* op, int alg, const float* d_y, int64_t M, int64_t N,
+                     int32_t K, double tol, const cs_options* opts, float* d_vals,
+                     int32_t* d_support, cs_report* d_report, void* d_ws, size_t ws_bytes,
+                     cs_stream_t stream);
+cs_status cs_recover_f64(const cs_operator* op, int alg, const double* d_y, int64_t M, int64_t N,
+                         int32_t K, double tol, const cs_options* opts, double* d_vals,
+                         int32_t* d_support, cs_report* d_report, void* d_ws, size_t ws_bytes,
+                         cs_stream_t stream);
+
+/* B independent problems; problem b uses operator instance b (op batch == B).
+ * d_Y [B][M], d_vals [B][K], d_support [B][K], d_reports [B]. */
+cs_status cs_recover_batched(const cs_operator* op, int alg, const float* d_Y, int64_t B,
+                             int64_t M, int64_t N, int32_t K, double tol,
+                             const cs_options* opts, float* d_vals, int32_t* d_support,
+                             cs_report* d_reports, void* d_ws, size_t ws_bytes,
+                             cs_stream_t stream);
+cs_status cs_recover_batched_f64(const cs_operator* op, int alg, const double* d_Y, int64_t B,
+                                 int64_t M, int64_t N, int32_t K, double tol,
+                                 const cs_options* opts, double* d_vals, int32_t* d_support,
+                                 cs_report* d_reports, void* d_ws, size_t ws_bytes,
+                                 cs_stream_t stream);
+
+/* ---------------------------------------------------------------- misc ------ */
+const char* cs_status_string(cs_status s);
+const char* cs_last_error(void);
+/* Number of kernels this library launched on the calling thread since the last reset. */
+uint64_t cs_launch_count(int reset);
+const char* cs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CS_H_ */

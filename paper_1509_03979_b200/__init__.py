@@ -1,0 +1,268 @@
+"""paper_1509_03979_b200 — B200-native greedy compressive sensing (arXiv:1509.03979).
+
+Thin ctypes binding over the C ABI of libcsgpu.so (include/cs.h).  It only
+marshals arguments: every step of the method (operator, detection, CG-based
+weighted least squares, pursuits) runs in the library's sm_100a kernels.
+PyTorch supplies device memory and the current CUDA stream.
+
+There is NO CPU fallback: if the shared library is missing or the device is
+not a B200 the calls raise.
+
+Names follow include/cs.h:
+    cs_operator_create / cs_operator_apply / cs_operator_adjoint
+    cs_recover / cs_recover_batched / cs_workspace_bytes
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcsgpu.so")
+
+ALGS = {"omp": 0, "sp": 1, "ompr": 2}
+TERM_NAMES = {0: "done", 1: "iter_cap", 2: "stagnation", 3: "support_fixed", 4: "resid_rose"}
+STATUS = {0: "CS_OK", 1: "CS_ERR_INVALID_ARG", 2: "CS_ERR_UNSUPPORTED", 3: "CS_ERR_WORKSPACE",
+          4: "CS_ERR_CUDA", 5: "CS_ERR_NONFINITE"}
+
+REPORT_DTYPE = np.dtype([("outer_iters", "<i4"), ("cg_iters_total", "<i4"), ("cg_solves", "<i4"),
+                         ("applies", "<i4"), ("termination", "<i4"), ("status", "<u4"),
+                         ("resid_norm", "<f8"), ("cg_rel_resid", "<f8")])
+assert REPORT_DTYPE.itemsize == 40
+
+
+class CsError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+class cs_options(ctypes.Structure):
+    _fields_ = [("max_outer", ctypes.c_int32), ("cg_max_iters", ctypes.c_int32),
+                ("ompr_l", ctypes.c_int32), ("ompr_eta", ctypes.c_float),
+                ("reserved", ctypes.c_int32 * 4)]
+
+
+_lib = None
+
+EXPORTS = [
+    "cs_operator_meta_bytes", "cs_operator_create", "cs_operator_destroy", "cs_operator_info",
+    "cs_operator_ws_bytes", "cs_operator_apply", "cs_operator_apply_f64", "cs_operator_adjoint",
+    "cs_operator_adjoint_f64", "cs_workspace_bytes", "cs_recover", "cs_recover_f64",
+    "cs_recover_batched", "cs_recover_batched_f64", "cs_status_string", "cs_last_error",
+    "cs_launch_count", "cs_version",
+]
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libcsgpu.so and declare the signatures.  Raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(path)
+    P, I64, I32, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+    sig = {
+        "cs_operator_meta_bytes": (SZ, [I64, I64, I64]),
+        "cs_operator_create": (I32, [I64, I64, I64, P, P, P, SZ, P, ctypes.POINTER(P)]),
+        "cs_operator_destroy": (I32, [P]),
+        "cs_operator_info": (I32, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+        "cs_operator_ws_bytes": (SZ, [P, ctypes.c_int]),
+        "cs_operator_apply": (I32, [P, P, P, P, SZ, P]),
+        "cs_operator_apply_f64": (I32, [P, P, P, P, SZ, P]),
+        "cs_operator_adjoint": (I32, [P, P, P, P, SZ, P]),
+        "cs_operator_adjoint_f64": (I32, [P, P, P, P, SZ, P]),
+        "cs_workspace_bytes": (I32, [ctypes.c_int, I64, I64, I32, I64, ctypes.c_int,
+                                     ctypes.POINTER(cs_options), ctypes.POINTER(SZ)]),
+        "cs_recover": (I32, [P, ctypes.c_int, P, I64, I64, I32, ctypes.c_double,
+                             ctypes.POINTER(cs_options), P, P, P, P, SZ, P]),
+        "cs_recover_f64": (I32, [P, ctypes.c_int, P, I64, I64, I32, ctypes.c_double,
+                                 ctypes.POINTER(cs_options), P, P, P, P, SZ, P]),
+        "cs_recover_batched": (I32, [P, ctypes.c_int, P, I64, I64, I64, I32, ctypes.c_double,
+                                     ctypes.POINTER(cs_options), P, P, P, P, SZ, P]),
+        "cs_recover_batched_f64": (I32, [P, ctypes.c_int, P, I64, I64, I64, I32, ctypes.c_double,
+                                         ctypes.POINTER(cs_options), P, P, P, P, SZ, P]),
+        "cs_status_string": (ctypes.c_char_p, [I32]),
+        "cs_last_error": (ctypes.c_char_p, []),
+        "cs_launch_count": (ctypes.c_uint64, [ctypes.c_int]),
+        "cs_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    _lib = L
+    return L
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise CsError(status, where, _lib.cs_last_error().decode())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def make_options(max_outer=0, cg_max_iters=0, ompr_l=0, ompr_eta=0.0) -> cs_options:
+    o = cs_options()
+    o.max_outer, o.cg_max_iters, o.ompr_l, o.ompr_eta = max_outer, cg_max_iters, ompr_l, ompr_eta
+    return o
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(load_library().cs_launch_count(1 if reset else 0))
+
+
+class Operator:
+    """Handle for A = P . DCT-II . diag(sigma) with `batch` independent instances."""
+
+    def __init__(self, N: int, M: int, sign_bits, rows, batch: int = 1, stream=None):
+        torch = _torch()
+        L = load_library()
+        self.N, self.M, self.batch = int(N), int(M), int(batch)
+        dev = rows.device
+        nb = L.cs_operator_meta_bytes(N, M, batch)
+        self.meta = torch.empty(nb, dtype=torch.uint8, device=dev)
+        sb = sign_bits.to(device=dev).contiguous()
+        rw = rows.to(device=dev, dtype=torch.int32).contiguous()
+        h = ctypes.c_void_p()
+        _check(L.cs_operator_create(N, M, batch, _ptr(sb), _ptr(rw), _ptr(self.meta), nb,
+                                    _stream(stream), ctypes.byref(h)), "cs_operator_create")
+        self.handle = h
+        self._ws = {}
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and _lib is not None:
+                _lib.cs_operator_destroy(self.handle)
+        except Exception:
+            pass
+
+    def ws(self, dtype):
+        torch = _torch()
+        prec = 1 if dtype == torch.float64 else 0
+        nb = int(_lib.cs_operator_ws_bytes(self.handle, prec))
+        if nb == 0:
+            return None, 0
+        key = (prec, nb)
+        if key not in self._ws:
+            self._ws[key] = torch.empty(nb, dtype=torch.uint8, device=self.meta.device)
+        return self._ws[key], nb
+
+
+def cs_operator_create(N, M, batch, sign_bits, rows, stream=None) -> Operator:
+    return Operator(N, M, sign_bits, rows, batch, stream)
+
+
+def cs_operator_apply(op: Operator, x, out=None, stream=None):
+    """y[b] = A_b x[b]; x is [batch, N] (or [N]) float32/float64 on the GPU."""
+    torch = _torch()
+    x = x.contiguous()
+    y = out if out is not None else torch.empty(x.shape[:-1] + (op.M,), dtype=x.dtype, device=x.device)
+    ws, nb = op.ws(x.dtype)
+    f = _lib.cs_operator_apply_f64 if x.dtype == torch.float64 else _lib.cs_operator_apply
+    _check(f(op.handle, _ptr(x), _ptr(y), _ptr(ws) if ws is not None else None, nb, _stream(stream)),
+           "cs_operator_apply")
+    return y
+
+
+def cs_operator_adjoint(op: Operator, y, out=None, stream=None):
+    torch = _torch()
+    y = y.contiguous()
+    x = out if out is not None else torch.empty(y.shape[:-1] + (op.N,), dtype=y.dtype, device=y.device)
+    ws, nb = op.ws(y.dtype)
+    f = _lib.cs_operator_adjoint_f64 if y.dtype == torch.float64 else _lib.cs_operator_adjoint
+    _check(f(op.handle, _ptr(y), _ptr(x), _ptr(ws) if ws is not None else None, nb, _stream(stream)),
+           "cs_operator_adjoint")
+    return x
+
+
+def cs_workspace_bytes(alg, N, M, K, batch=1, dtype=None, opts: Optional[cs_options] = None) -> int:
+    torch = _torch()
+    L = load_library()
+    n = ctypes.c_size_t()
+    prec = 1 if dtype == torch.float64 else 0
+    _check(L.cs_workspace_bytes(ALGS[alg] if isinstance(alg, str) else alg, N, M, K, batch, prec,
+                                ctypes.byref(opts) if opts is not None else None, ctypes.byref(n)),
+           "cs_workspace_bytes")
+    return n.value
+
+
+@dataclass
+class Recovery:
+    support: "object"   # torch int32 [.., K]
+    values: "object"    # torch float [.., K]
+    report_dev: "object"  # torch uint8 [.., 40] (device)
+
+    def reports(self):
+        raw = self.report_dev.cpu().numpy().reshape(-1, 40)
+        return np.frombuffer(raw.tobytes(), dtype=REPORT_DTYPE)
+
+
+class Workspace:
+    """Caller-owned workspace reused across calls (torch is the allocator)."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes, device):
+        torch = _torch()
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+def cs_recover_batched(op: Operator, alg, Y, K: int, tol: float, opts: Optional[cs_options] = None,
+                       workspace: Optional[Workspace] = None, out: Optional[Recovery] = None,
+                       stream=None) -> Recovery:
+    """Recover B = Y.shape[0] independent problems; problem b uses operator instance b."""
+    torch = _torch()
+    Y = Y.contiguous()
+    B, M = Y.shape
+    a = ALGS[alg] if isinstance(alg, str) else alg
+    nb = cs_workspace_bytes(a, op.N, M, K, B, Y.dtype, opts)
+    ws = (workspace or Workspace()).get(nb, Y.device)
+    if out is None:
+        out = Recovery(torch.empty((B, K), dtype=torch.int32, device=Y.device),
+                       torch.empty((B, K), dtype=Y.dtype, device=Y.device),
+                       torch.empty((B, 40), dtype=torch.uint8, device=Y.device))
+    f = _lib.cs_recover_batched_f64 if Y.dtype == torch.float64 else _lib.cs_recover_batched
+    _check(f(op.handle, a, _ptr(Y), B, M, op.N, K, tol,
+             ctypes.byref(opts) if opts is not None else None, _ptr(out.values), _ptr(out.support),
+             _ptr(out.report_dev), _ptr(ws), ws.numel(), _stream(stream)), "cs_recover_batched")
+    return out
+
+
+def cs_recover(op: Operator, alg, y, M: int, N: int, K: int, tol: float,
+               opts: Optional[cs_options] = None, workspace: Optional[Workspace] = None,
+               stream=None) -> Recovery:
+    """Single-signal recovery (operator instance 0)."""
+    torch = _torch()
+    y = y.contiguous()
+    a = ALGS[alg] if isinstance(alg, str) else alg
+    nb = cs_workspace_bytes(a, N, M, K, 1, y.dtype, opts)
+    ws = (workspace or Workspace()).get(nb, y.device)
+    out = Recovery(torch.empty(K, dtype=torch.int32, device=y.device),
+                   torch.empty(K, dtype=y.dtype, device=y.device),
+                   torch.empty(40, dtype=torch.uint8, device=y.device))
+    f = _lib.cs_recover_f64 if y.dtype == torch.float64 else _lib.cs_recover
+    _check(f(op.handle, a, _ptr(y), M, N, K, tol, ctypes.byref(opts) if opts is not None else None,
+             _ptr(out.values), _ptr(out.support), _ptr(out.report_dev), _ptr(ws), ws.numel(),
+             _stream(stream)), "cs_recover")
+    return out

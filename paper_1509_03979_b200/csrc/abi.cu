@@ -1,0 +1,372 @@
+// abi.cu — the extern "C" boundary of libcsgpu.so (declared in include/cs.h).
+//
+// Host-side validation, workspace sizing, operator metadata construction and
+// tier dispatch:
+//   Tier S (N <= 16384 and the per-problem working set fits in shared memory):
+//     one thread block per problem (tier_s.cuh);
+//   Tier L (larger N): one cooperative persistent grid per problem with a
+//     four-step FFT over L2-resident scratch (tier_l.cuh).
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "tier_l.cuh"
+#include "tier_s.cuh"
+
+using namespace cs;
+
+struct cs_operator {
+  int64_t N, M, B, nw;
+  uint32_t* meta;   // device: [B][3][nw]
+  int* errflag;     // device int in the meta tail
+  int device;
+};
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+cs_status fail(cs_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+cs_status cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return CS_ERR_CUDA;
+}
+#define CS_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+#define CS_LAUNCHED()                                               \
+  do {                                                              \
+    g_launches.fetch_add(1, std::memory_order_relaxed);             \
+    cudaError_t e_ = cudaGetLastError();                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, "kernel launch");   \
+  } while (0)
+
+bool pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+
+cs_status check_N(int64_t N) {
+  if (!pow2(N) || N < 8 || N > ((int64_t)1 << 25))
+    return fail(CS_ERR_UNSUPPORTED, "N must be a power of two in [8, 2^25]");
+  return CS_OK;
+}
+
+cs_status check_device() {
+  int dev;
+  CS_CUDA(cudaGetDevice(&dev));
+  int major = 0;
+  CS_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) return fail(CS_ERR_UNSUPPORTED, "libcsgpu is built for sm_100a (B200)");
+  return CS_OK;
+}
+
+int64_t ucap_of(int alg, int K, int l) {
+  if (alg == CS_SP) return 2 * (int64_t)K;
+  if (alg == CS_OMPR) return (int64_t)K + (l > 0 ? l : 1);
+  return K;
+}
+
+template <typename T> bool tier_s_fits(int64_t N, int K, int64_t ucap, bool pursuit) {
+  if (N > TIER_S_MAX_N) return false;
+  SLayout s = s_layout<T>(N, K, (int)ucap, pursuit);
+  return s.bytes <= 227 * 1024;
+}
+
+__global__ void k_rows_mask(int64_t N, int64_t M, int64_t B, int64_t nw, const int32_t* rows,
+                            const uint32_t* sign_in, uint32_t* meta, int* err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < B * nw) {  // copy sign words
+    int64_t b = i / nw, w = i % nw;
+    meta[b * 3 * nw + w] = sign_in[b * nw + w];
+  }
+  if (i >= B * M) return;
+  int64_t b = i / M, m = i % M;
+  int32_t r = rows[i];
+  bool ok = (r >= 0) && (r < N) && (m == 0 || rows[i - 1] < r);
+  if (!ok) { atomicOr(err, 1); return; }
+  atomicOr(&meta[b * 3 * nw + nw + (r >> 5)], 1u << (r & 31));
+}
+
+// exclusive prefix of popcounts per instance: one block per instance
+__global__ void k_rows_prefix(int64_t nw, uint32_t* meta) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry;
+  const int64_t b = blockIdx.x;
+  const uint32_t* mask = meta + b * 3 * nw + nw;
+  int32_t* pre = reinterpret_cast<int32_t*>(meta + b * 3 * nw + 2 * nw);
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int64_t base = 0; base < nw; base += blockDim.x) {
+    int64_t w = base + threadIdx.x;
+    int32_t v = (w < nw) ? __popc(mask[w]) : 0;
+    int32_t inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    int32_t off = carry;
+    int32_t tot = 0;
+    for (int k = 0; k < nwarp; ++k) {
+      if (k < warp) off += wsum[k];
+      tot += wsum[k];
+    }
+    if (w < nw) pre[w] = off + inc - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+template <typename T> cs_status set_smem(const void* fn, int64_t bytes) {
+  CS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return CS_OK;
+}
+
+OpMeta meta_of(const cs_operator* op) {
+  OpMeta m;
+  m.base = op->meta;
+  m.N = op->N;
+  m.M = op->M;
+  m.nw = op->nw;
+  return m;
+}
+
+Params make_params(int alg, int32_t K, double tol, const cs_options* o) {
+  Params P;
+  P.K = K;
+  P.alg = alg;
+  P.tol = tol;
+  P.max_outer = o ? o->max_outer : 0;
+  P.cg_cap = o ? o->cg_max_iters : 0;
+  P.ompr_l = (o && o->ompr_l > 0) ? o->ompr_l : 1;
+  P.eta = (o && o->ompr_eta > 0) ? (double)o->ompr_eta : 1.0;
+  return P;
+}
+
+template <typename T>
+cs_status apply_impl(const cs_operator* op, const T* x, T* y, void* ws, size_t ws_bytes,
+                     cudaStream_t st, bool adjoint) {
+  if (!op) return fail(CS_ERR_INVALID_ARG, "null operator");
+  if (!x || !y) return fail(CS_ERR_INVALID_ARG, "null vector");
+  if (cs_status s = check_device()) return s;
+  if (op->N <= TIER_S_MAX_N) {
+    SLayout lay = s_layout<T>(op->N, 0, 0, false);
+    OpMeta m = meta_of(op);
+    if (!adjoint) {
+      if (cs_status s = set_smem<T>((const void*)k_s_apply<T>, lay.bytes)) return s;
+      k_s_apply<T><<<(unsigned)op->B, lay.nthreads, lay.bytes, st>>>(m, lay, x, y);
+    } else {
+      if (cs_status s = set_smem<T>((const void*)k_s_adjoint<T>, lay.bytes)) return s;
+      k_s_adjoint<T><<<(unsigned)op->B, lay.nthreads, lay.bytes, st>>>(m, lay, x, y);
+    }
+    CS_LAUNCHED();
+    return CS_OK;
+  }
+  return tier_l_apply<T>(meta_of(op), op->B, x, y, ws, ws_bytes, st, adjoint, g_launches,
+                         g_last_error);
+}
+
+template <typename T>
+cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, int64_t M, int64_t N,
+                       int32_t K, double tol, const cs_options* opts, T* vals, int32_t* supp,
+                       cs_report* reps, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!op) return fail(CS_ERR_INVALID_ARG, "null operator");
+  if (!Y || !vals || !supp || !reps) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
+  if (alg < CS_OMP || alg > CS_OMPR) return fail(CS_ERR_INVALID_ARG, "unknown algorithm");
+  if (cs_status s = check_N(N)) return s;
+  if (N != op->N || M != op->M) return fail(CS_ERR_INVALID_ARG, "M/N do not match the operator");
+  if (B < 1 || B > op->B) return fail(CS_ERR_INVALID_ARG, "batch exceeds operator instances");
+  if (!(tol >= 0)) return fail(CS_ERR_INVALID_ARG, "tol must be >= 0");
+  if (opts) {
+    for (int i = 0; i < 4; ++i)
+      if (opts->reserved[i]) return fail(CS_ERR_INVALID_ARG, "cs_options.reserved must be zero");
+    if (opts->max_outer < 0 || opts->cg_max_iters < 0 || opts->ompr_l < 0 || opts->ompr_eta < 0)
+      return fail(CS_ERR_INVALID_ARG, "negative option");
+  }
+  const int l = (opts && opts->ompr_l > 0) ? opts->ompr_l : 1;
+  if (K < 1 || (int64_t)K > N / 2) return fail(CS_ERR_INVALID_ARG, "K must be in [1, N/2]");
+  if (alg == CS_OMP && K > M) return fail(CS_ERR_INVALID_ARG, "OMP needs K <= M");
+  if (alg == CS_SP && 2 * (int64_t)K > M) return fail(CS_ERR_INVALID_ARG, "SP needs 2K <= M");
+  if (alg == CS_OMPR && (int64_t)K + l > M) return fail(CS_ERR_INVALID_ARG, "OMPR needs K + l <= M");
+  if (cs_status s = check_device()) return s;
+  size_t need = 0;
+  const int prec = sizeof(T) == 8 ? 1 : 0;
+  if (cs_status s = cs_workspace_bytes(alg, N, M, K, B, prec, opts, &need)) return s;
+  if (!ws || ws_bytes < need) return fail(CS_ERR_WORKSPACE, "workspace too small");
+  Params P = make_params(alg, K, tol, opts);
+  const int64_t ucap = ucap_of(alg, K, l);
+  if (tier_s_fits<T>(N, K, ucap, true)) {
+    SRecArgs<T> a;
+    a.meta = meta_of(op);
+    a.lay = s_layout<T>(N, K, (int)ucap, true);
+    a.P = P;
+    a.ucap = (int)ucap;
+    a.Y = Y;
+    a.vals = vals;
+    a.supp = supp;
+    a.reps = reps;
+    a.c0ws = reinterpret_cast<T*>(ws);
+    if (cs_status s = set_smem<T>((const void*)k_s_recover<T>, a.lay.bytes)) return s;
+    k_s_recover<T><<<(unsigned)B, a.lay.nthreads, a.lay.bytes, st>>>(a);
+    CS_LAUNCHED();
+    return CS_OK;
+  }
+  return tier_l_recover<T>(meta_of(op), P, (int)ucap, Y, B, vals, supp, reps, ws, ws_bytes, st,
+                           g_launches, g_last_error);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t cs_operator_meta_bytes(int64_t N, int64_t M, int64_t batch) {
+  (void)M;
+  if (N <= 0 || batch <= 0) return 0;
+  int64_t nw = (N + 31) / 32;
+  return (size_t)(align_up(batch * 3 * nw * 4, 256) + 256);
+}
+
+cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
+                             const int32_t* d_rows, void* d_meta, size_t meta_bytes,
+                             cs_stream_t stream, cs_operator** out) {
+  if (!out) return fail(CS_ERR_INVALID_ARG, "out is null");
+  *out = nullptr;
+  if (cs_status s = check_N(N)) return s;
+  if (M < 1 || M > N) return fail(CS_ERR_INVALID_ARG, "M must be in [1, N]");
+  if (batch < 1 || batch > (1 << 30)) return fail(CS_ERR_INVALID_ARG, "bad batch");
+  if (!d_sign_bits || !d_rows || !d_meta) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
+  if (meta_bytes < cs_operator_meta_bytes(N, M, batch)) return fail(CS_ERR_WORKSPACE, "meta buffer too small");
+  if (cs_status s = check_device()) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t nw = (N + 31) / 32;
+  uint32_t* meta = reinterpret_cast<uint32_t*>(d_meta);
+  int* err = reinterpret_cast<int*>(reinterpret_cast<char*>(d_meta) + align_up(batch * 3 * nw * 4, 256));
+  CS_CUDA(cudaMemsetAsync(d_meta, 0, meta_bytes, st));
+  int64_t nthr = std::max(batch * M, batch * nw);
+  k_rows_mask<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(N, M, batch, nw, d_rows, d_sign_bits,
+                                                           meta, err);
+  CS_LAUNCHED();
+  k_rows_prefix<<<(unsigned)batch, 1024, 0, st>>>(nw, meta);
+  CS_LAUNCHED();
+  int herr = 0;
+  CS_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CS_CUDA(cudaStreamSynchronize(st));
+  if (herr) return fail(CS_ERR_INVALID_ARG, "rows must be strictly increasing and in [0, N)");
+  cs_operator* op = new cs_operator;
+  op->N = N;
+  op->M = M;
+  op->B = batch;
+  op->nw = nw;
+  op->meta = meta;
+  op->errflag = err;
+  CS_CUDA(cudaGetDevice(&op->device));
+  *out = op;
+  return CS_OK;
+}
+
+cs_status cs_operator_destroy(cs_operator* op) {
+  delete op;
+  return CS_OK;
+}
+
+cs_status cs_operator_info(const cs_operator* op, int64_t* N, int64_t* M, int64_t* batch) {
+  if (!op) return fail(CS_ERR_INVALID_ARG, "null operator");
+  if (N) *N = op->N;
+  if (M) *M = op->M;
+  if (batch) *batch = op->B;
+  return CS_OK;
+}
+
+size_t cs_operator_ws_bytes(const cs_operator* op, int precision) {
+  if (!op || op->N <= TIER_S_MAX_N) return 0;
+  return precision ? tier_l_apply_ws_bytes<double>(op->N) : tier_l_apply_ws_bytes<float>(op->N);
+}
+
+cs_status cs_operator_apply(const cs_operator* op, const float* d_x, float* d_y, void* d_ws,
+                            size_t ws_bytes, cs_stream_t stream) {
+  return apply_impl<float>(op, d_x, d_y, d_ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), false);
+}
+cs_status cs_operator_apply_f64(const cs_operator* op, const double* d_x, double* d_y, void* d_ws,
+                                size_t ws_bytes, cs_stream_t stream) {
+  return apply_impl<double>(op, d_x, d_y, d_ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), false);
+}
+cs_status cs_operator_adjoint(const cs_operator* op, const float* d_y, float* d_x, void* d_ws,
+                              size_t ws_bytes, cs_stream_t stream) {
+  return apply_impl<float>(op, d_y, d_x, d_ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), true);
+}
+cs_status cs_operator_adjoint_f64(const cs_operator* op, const double* d_y, double* d_x, void* d_ws,
+                                  size_t ws_bytes, cs_stream_t stream) {
+  return apply_impl<double>(op, d_y, d_x, d_ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), true);
+}
+
+cs_status cs_workspace_bytes(int alg, int64_t N, int64_t M, int32_t K, int64_t batch, int precision,
+                             const cs_options* opts, size_t* bytes) {
+  if (!bytes) return fail(CS_ERR_INVALID_ARG, "bytes is null");
+  if (cs_status s = check_N(N)) return s;
+  if (K < 1 || batch < 1 || M < 1) return fail(CS_ERR_INVALID_ARG, "bad sizes");
+  const int l = (opts && opts->ompr_l > 0) ? opts->ompr_l : 1;
+  const int64_t ucap = ucap_of(alg, K, l);
+  const bool dbl = precision != 0;
+  bool s = dbl ? tier_s_fits<double>(N, K, ucap, true) : tier_s_fits<float>(N, K, ucap, true);
+  if (s) {
+    *bytes = (size_t)(batch * N * (dbl ? 8 : 4));
+  } else {
+    *bytes = dbl ? tier_l_recover_ws_bytes<double>(N, M, K, (int)ucap)
+                 : tier_l_recover_ws_bytes<float>(N, M, K, (int)ucap);
+  }
+  return CS_OK;
+}
+
+cs_status cs_recover(const cs_operator* op, int alg, const float* d_y, int64_t M, int64_t N, int32_t K,
+                     double tol, const cs_options* opts, float* d_vals, int32_t* d_support,
+                     cs_report* d_report, void* d_ws, size_t ws_bytes, cs_stream_t stream) {
+  return recover_impl<float>(op, alg, d_y, 1, M, N, K, tol, opts, d_vals, d_support, d_report, d_ws,
+                             ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+cs_status cs_recover_f64(const cs_operator* op, int alg, const double* d_y, int64_t M, int64_t N,
+                         int32_t K, double tol, const cs_options* opts, double* d_vals,
+                         int32_t* d_support, cs_report* d_report, void* d_ws, size_t ws_bytes,
+                         cs_stream_t stream) {
+  return recover_impl<double>(op, alg, d_y, 1, M, N, K, tol, opts, d_vals, d_support, d_report, d_ws,
+                              ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+cs_status cs_recover_batched(const cs_operator* op, int alg, const float* d_Y, int64_t B, int64_t M,
+                             int64_t N, int32_t K, double tol, const cs_options* opts, float* d_vals,
+                             int32_t* d_support, cs_report* d_reports, void* d_ws, size_t ws_bytes,
+                             cs_stream_t stream) {
+  return recover_impl<float>(op, alg, d_Y, B, M, N, K, tol, opts, d_vals, d_support, d_reports, d_ws,
+                             ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+cs_status cs_recover_batched_f64(const cs_operator* op, int alg, const double* d_Y, int64_t B,
+                                 int64_t M, int64_t N, int32_t K, double tol, const cs_options* opts,
+                                 double* d_vals, int32_t* d_support, cs_report* d_reports, void* d_ws,
+                                 size_t ws_bytes, cs_stream_t stream) {
+  return recover_impl<double>(op, alg, d_Y, B, M, N, K, tol, opts, d_vals, d_support, d_reports, d_ws,
+                              ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+const char* cs_status_string(cs_status s) {
+  switch (s) {
+    case CS_OK: return "CS_OK";
+    case CS_ERR_INVALID_ARG: return "CS_ERR_INVALID_ARG";
+    case CS_ERR_UNSUPPORTED: return "CS_ERR_UNSUPPORTED";
+    case CS_ERR_WORKSPACE: return "CS_ERR_WORKSPACE";
+    case CS_ERR_CUDA: return "CS_ERR_CUDA";
+    case CS_ERR_NONFINITE: return "CS_ERR_NONFINITE";
+  }
+  return "CS_ERR_UNKNOWN";
+}
+const char* cs_last_error(void) { return g_last_error.c_str(); }
+uint64_t cs_launch_count(int reset) {
+  return reset ? g_launches.exchange(0) : g_launches.load();
+}
+const char* cs_version(void) { return "csgpu 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

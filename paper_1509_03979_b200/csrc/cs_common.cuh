@@ -1,0 +1,73 @@
+// cs_common.cuh — shared device utilities for the sm_100a compressive-sensing path.
+//
+// Complex arithmetic, the Makhoul index map, bit-mask helpers and the
+// packed-key helpers used by selection.  Everything is templated on the
+// arithmetic type T in {float, double}.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/cs.h"
+
+#define CS_DEV __device__ __forceinline__
+#define CS_HD __host__ __device__ __forceinline__
+#define CS_NOINL __device__ __noinline__
+
+namespace cs {
+
+template <typename T> struct cplx_t;
+template <> struct cplx_t<float> { using type = float2; };
+template <> struct cplx_t<double> { using type = double2; };
+template <typename T> using C2 = typename cplx_t<T>::type;
+
+template <typename T> CS_HD C2<T> mk(T re, T im) { C2<T> r; r.x = re; r.y = im; return r; }
+template <typename T> CS_HD C2<T> cadd(C2<T> a, C2<T> b) { return mk<T>(a.x + b.x, a.y + b.y); }
+template <typename T> CS_HD C2<T> csub(C2<T> a, C2<T> b) { return mk<T>(a.x - b.x, a.y - b.y); }
+template <typename T> CS_HD C2<T> cmul(C2<T> a, C2<T> b) {
+  return mk<T>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename T> CS_HD C2<T> cmulc(C2<T> a, C2<T> b) {
+  return mk<T>(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <typename T> CS_HD C2<T> cconj(C2<T> a) { return mk<T>(a.x, -a.y); }
+template <typename T> CS_HD C2<T> cscale(C2<T> a, T s) { return mk<T>(a.x * s, a.y * s); }
+// multiply by -i (forward) or +i (inverse)
+template <typename T, bool INV> CS_HD C2<T> mul_mi(C2<T> a) {
+  return INV ? mk<T>(-a.y, a.x) : mk<T>(a.y, -a.x);
+}
+
+// ---------------------------------------------------------------------------
+// Makhoul reorder.  Natural index j of u (length N) maps to
+// position p of v: v_n = u_{2n}, v_{N-1-n} = u_{2n+1}.  The complex half-length
+// sequence z_m = v_{2m} + i v_{2m+1} is v itself viewed as C2<T>[N/2].
+CS_HD int64_t mk_pos(int64_t j, int64_t N) { return (j & 1) ? (N - 1 - (j >> 1)) : (j >> 1); }
+CS_HD int64_t mk_nat(int64_t p, int64_t N) { return (2 * p < N) ? 2 * p : 2 * (N - 1 - p) + 1; }
+
+// sigma_j from packed sign bits (bit set => -1)
+template <typename T> CS_DEV T sign_of(const uint32_t* bits, int64_t j) {
+  return ((bits[j >> 5] >> (j & 31)) & 1u) ? T(-1) : T(1);
+}
+template <typename T> CS_DEV T apply_sign(const uint32_t* bits, int64_t j, T v) {
+  return ((bits[j >> 5] >> (j & 31)) & 1u) ? -v : v;
+}
+CS_DEV bool bit_test(const uint32_t* bits, int64_t j) { return (bits[j >> 5] >> (j & 31)) & 1u; }
+// rank of a selected row k among selected rows (prefix popcount)
+CS_DEV int64_t row_rank(const uint32_t* mask, const int32_t* prefix, int64_t k) {
+  uint32_t w = mask[k >> 5];
+  uint32_t below = (k & 31) ? (w & ((1u << (k & 31)) - 1u)) : 0u;
+  return (int64_t)prefix[k >> 5] + __popc(below);
+}
+
+// Order-preserving keys of |v| (sign cleared, +1 so that key 0 means "excluded";
+// NaN sorts above +inf).  64-bit keys for double keep the full order.
+template <typename T> struct KeyT;
+template <> struct KeyT<float> { using type = uint32_t; };
+template <> struct KeyT<double> { using type = uint64_t; };
+// full-precision order-preserving magnitude key, 0 reserved for "excluded"
+CS_DEV uint32_t full_key(float v) { return (__float_as_uint(v) & 0x7fffffffu) + 1u; }
+CS_DEV uint64_t full_key(double v) {
+  return ((uint64_t)__double_as_longlong(v) & 0x7fffffffffffffffull) + 1ull;
+}
+
+}  // namespace cs

@@ -1,0 +1,186 @@
+// ctx_cta.cuh — "CTA context": one thread block owns one recovery problem and
+// keeps its whole working set in shared memory (Tier S, N <= 16384).
+//
+// The pursuit / CG / selection code (pursuit.cuh, select.cuh) is written once
+// against a context interface:
+//   gtid, gnthr, lane, gwarp, gnwarps      thread / warp ids within the context
+//   sync()                                  context-wide barrier
+//   sum(double) / argmax(key, idx) / excl_scan(int64)   deterministic collectives
+//   hist_*                                  256-bin histogram for radix select
+//   set_input_support / H / RES / c_at / c0_at / save_c0   the operator sandwich
+// and instantiated for this CTA context and for the cooperative-grid context
+// (ctx_grid.cuh, Tier L).  All collectives use a fixed reduction order, so a
+// run is bitwise reproducible.
+#pragma once
+#include "cs_common.cuh"
+#include "dct_mid.cuh"
+#include "fft_cta.cuh"
+
+namespace cs {
+
+CS_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;  // lane 0 holds the total
+}
+
+template <typename T> struct CtaCtx {
+  using Key = typename KeyT<T>::type;
+  // ids
+  int gtid, gnthr, lane, gwarp, gnwarps;
+  int64_t N, M, L;
+  // shared-memory state
+  C2<T>* Z;          // [L] working transform buffer; viewed as T[N] it is v (Makhoul order)
+  uint32_t* sign;    // [nw]
+  uint32_t* rowmask; // [nw]
+  int32_t* prefix;   // [nw]
+  TwTable<T> twL, tw4;
+  double* redd;      // [32]
+  int64_t* redi;     // [33]
+  Key* redk;         // [32]
+  unsigned* hist;    // [256]
+  int64_t* pick;     // [4]
+  // global state of this problem
+  const T* y;        // [M]
+  T* c0;             // [N] A^T y in Makhoul order (sign not applied), global scratch
+  // remembered input support of the sandwich
+  const int* in_supp;
+  int in_ns;
+  int applies;
+
+  CS_DEV void sync() { __syncthreads(); }
+
+  CS_NOINL double sum(double v) {
+    v = warp_sum(v);
+    if (lane == 0) redd[gwarp] = v;
+    __syncthreads();
+    double t = 0;
+    for (int w = 0; w < gnwarps; ++w) t += redd[w];
+    __syncthreads();
+    return t;
+  }
+  // argmax of (key, idx): larger key wins, ties -> smaller idx.  Returns idx (-1 if all keys 0).
+  CS_NOINL int64_t argmax(Key k, int64_t idx) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Key k2 = __shfl_down_sync(0xffffffffu, k, o);
+      int64_t i2 = __shfl_down_sync(0xffffffffu, idx, o);
+      if (k2 > k || (k2 == k && i2 < idx)) { k = k2; idx = i2; }
+    }
+    if (lane == 0) { redk[gwarp] = k; redi[gwarp] = idx; }
+    __syncthreads();
+    Key bk = 0;
+    int64_t bi = -1;
+    for (int w = 0; w < gnwarps; ++w) {
+      Key kw = redk[w];
+      int64_t iw = redi[w];
+      if (kw > bk || (kw == bk && kw != 0 && iw < bi)) { bk = kw; bi = iw; }
+    }
+    __syncthreads();
+    return bk ? bi : -1;
+  }
+  // exclusive scan over threads in gtid order; *total receives the sum.
+  CS_NOINL int64_t excl_scan(int64_t v, int64_t* total) {
+    int64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) redi[gwarp] = inc;
+    __syncthreads();
+    int64_t base = 0, tot = 0;
+    for (int w = 0; w < gnwarps; ++w) {
+      int64_t x = redi[w];
+      if (w < gwarp) base += x;
+      tot += x;
+    }
+    __syncthreads();
+    *total = tot;
+    return base + inc - v;
+  }
+  // ---- 256-bin histogram for radix select ----
+  CS_DEV void hist_clear() {
+    for (int i = gtid; i < 256; i += gnthr) hist[i] = 0;
+    __syncthreads();
+  }
+  CS_DEV void hist_add(unsigned digit) {
+    // warp-aggregated: one shared atomic per distinct digit in the warp
+    unsigned peers = __match_any_sync(__activemask(), digit);
+    int leader = __ffs(peers) - 1;
+    if (lane == leader) atomicAdd(&hist[digit], (unsigned)__popc(peers));
+  }
+  CS_DEV void hist_done() { __syncthreads(); }
+  CS_DEV const unsigned* hist_smem() const { return hist; }
+
+  // ---- correlation access: c_j = sigma_j * v[p(j)] ----
+  CS_DEV const T* cbuf() const { return reinterpret_cast<const T*>(Z); }
+  CS_DEV T c_at(int64_t j) const { return apply_sign<T>(sign, j, cbuf()[mk_pos(j, N)]); }
+  CS_DEV T c0_at(int64_t j) const { return apply_sign<T>(sign, j, c0[mk_pos(j, N)]); }
+  CS_DEV void save_c0() {
+    const T* cb = cbuf();
+    for (int64_t p = gtid; p < N; p += gnthr) c0[p] = cb[p];
+    __syncthreads();
+  }
+
+  // ---- the operator sandwich ----
+  CS_DEV void set_input_support(const int* supp, int ns) {
+    in_supp = supp;
+    in_ns = ns;
+  }
+  CS_DEV void zero_Z() {
+    T* zb = reinterpret_cast<T*>(Z);
+    for (int64_t p = gtid; p < N; p += gnthr) zb[p] = T(0);
+    __syncthreads();
+  }
+  // scatter sigma . vals on the remembered support into the zeroed buffer
+  CS_DEV void load_input(const T* vals) {
+    zero_Z();
+    T* zb = reinterpret_cast<T*>(Z);
+    for (int i = gtid; i < in_ns; i += gnthr) {
+      int64_t j = in_supp[i];
+      zb[mk_pos(j, N)] = apply_sign<T>(sign, j, vals[i]);
+    }
+    __syncthreads();
+  }
+  template <int MODE> CS_NOINL double middle(T* yout) {
+    MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, yout);
+    double rn2 = 0;
+    for (int64_t k = gtid; k <= L / 2; k += gnthr) {
+      if (k == 0) {
+        mid_zero<T, MODE>(Z[0], m, rn2);
+      } else {
+        C2<T> a = tw4(k);
+        mid_pair<T, MODE>(Z[k], Z[L - k], k, a, m, rn2);
+      }
+    }
+    __syncthreads();
+    return rn2;
+  }
+  // q = (A^T A scatter_S(d))[S] on the remembered support S (cg2)
+  CS_NOINL void H(const T* d, T* q) {
+    load_input(d);
+    fft_cta<T, false>(Z, (int)L, 1, twL);
+    middle<MID_H>(nullptr);
+    fft_cta<T, true>(Z, (int)L, 1, twL);
+    for (int i = gtid; i < in_ns; i += gnthr) q[i] = c_at(in_supp[i]);
+    __syncthreads();
+    ++applies;
+  }
+  // c = A^T (y - A scatter_S(x)) into the buffer (b1 + cg5); returns ||y - A x||^2.
+  // x == nullptr means x = 0 (c = A^T y).
+  CS_NOINL double RES(const T* x) {
+    if (x) {
+      load_input(x);
+      fft_cta<T, false>(Z, (int)L, 1, twL);
+    } else {
+      zero_Z();
+    }
+    double rn2 = middle<MID_RES>(nullptr);
+    fft_cta<T, true>(Z, (int)L, 1, twL);
+    ++applies;
+    return sum(rn2);
+  }
+};
+
+}  // namespace cs

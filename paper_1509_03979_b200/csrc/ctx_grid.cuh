@@ -1,0 +1,361 @@
+// ctx_grid.cuh — "grid context": one cooperative, persistent grid (all SMs) owns
+// one problem (Tier L, N >= 32768).  Same interface as CtaCtx (ctx_cta.cuh), so
+// pursuit.cuh / select.cuh run unchanged; the differences are
+//   * sync() is a grid-wide barrier (sense counter in global memory, bounded
+//     spin with a watchdog trap so a bug cannot hang the GPU);
+//   * collectives reduce per-CTA partials in a fixed order (deterministic);
+//   * the operator sandwich is a four-step FFT: L = N/2 = L1*L2,
+//       pass A  column FFTs (length L1) of z, times W_L^{k1 m2}      -> Wk
+//       pass B  row FFTs (length L2), DCT split / row-select / residual on
+//               mirror row pairs (k1, L1-k1), inverse split, inverse row FFTs,
+//               times W_L^{-k1 m2}                                   -> Wk
+//       pass C  inverse column FFTs                                  -> Cb
+//     with all vectors resident in L2 / HBM and each sub-FFT in shared memory.
+#pragma once
+#include "cs_common.cuh"
+#include "dct_mid.cuh"
+#include "fft_cta.cuh"
+
+namespace cs {
+
+struct GridBar {
+  unsigned count;
+  unsigned gen;
+};
+
+CS_DEV unsigned ld_volatile(const unsigned* p) { return *reinterpret_cast<const volatile unsigned*>(p); }
+
+CS_NOINL void grid_barrier(GridBar* gb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned g = ld_volatile(&gb->gen);
+    __threadfence();
+    unsigned arrived = atomicAdd(&gb->count, 1u) + 1u;
+    if (arrived == gridDim.x) {
+      atomicExch(&gb->count, 0u);
+      __threadfence();
+      atomicAdd(&gb->gen, 1u);
+    } else {
+      long long t0 = clock64();
+      while (ld_volatile(&gb->gen) == g) {
+        __nanosleep(32);
+        if (clock64() - t0 > (1ll << 35)) __trap();  // ~15 s watchdog: never hang the GPU
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Global two-level twiddle table: W^m = hi[m >> sh] * lo[m & (2^sh - 1)]
+template <typename T> struct GTw {
+  const C2<T>* lo;
+  const C2<T>* hi;
+  int sh;
+  CS_DEV C2<T> operator()(int64_t m) const {
+    return cmul<T>(__ldg(&hi[m >> sh]), __ldg(&lo[m & ((1ll << sh) - 1)]));
+  }
+};
+
+// scratch for collectives (global, zeroed before launch)
+template <typename T> struct GridScratch {
+  GridBar* bar;
+  double* pd;       // [2][maxgrid]
+  int64_t* pi;      // [2][maxgrid]
+  uint64_t* pk;     // [2][maxgrid]
+  unsigned* ghist;  // [3][256]
+  int maxgrid;
+};
+
+template <typename T> struct GridCtx {
+  using Key = typename KeyT<T>::type;
+  int gtid, gnthr, lane, gwarp, gnwarps;
+  int64_t N, M, L, L1, L2;
+  int CT;
+  // global per-problem state
+  const uint32_t* sign;
+  const uint32_t* rowmask;
+  const int32_t* prefix;
+  const T* y;
+  T* c0;        // [N] Makhoul order
+  T* U;         // [N] dense input (Makhoul order, sign applied)
+  C2<T>* Wk;    // [L] four-step intermediate
+  T* Cb;        // [N] output (Makhoul order)
+  int64_t* in_pos;  // [cap] positions of the remembered input support
+  GTw<T> twF;   // W_L
+  GTw<T> tw4;   // W_4N
+  // shared memory
+  C2<T>* buf;   // [8192] sub-FFT tile
+  TwTable<T> tw1, tw2;  // W_L1, W_L2
+  double* sd;   // [33]
+  int64_t* si;  // [34]
+  Key* sk;      // [32]
+  unsigned* shist;  // [256]
+  int64_t* pick;    // [4]
+  GridScratch<T> g;
+  int bank, hpass;
+  const int* in_supp;
+  int in_ns;
+  int applies;
+
+  CS_DEV void sync() { grid_barrier(g.bar); }
+
+  // block-level deterministic sum; result valid in thread 0
+  CS_DEV double block_sum(double v) {
+    v = warp_sum_g(v);
+    if (lane == 0) sd[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0;
+    if (threadIdx.x == 0)
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sd[w];
+    __syncthreads();
+    return t;
+  }
+  CS_DEV static double warp_sum_g(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+  }
+  CS_NOINL double sum(double v) {
+    double t = block_sum(v);
+    double* P = g.pd + bank * g.maxgrid;
+    if (threadIdx.x == 0) P[blockIdx.x] = t;
+    sync();
+    if (threadIdx.x < 32) {
+      double a = 0;
+      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) a += P[c];
+      a = warp_sum_g(a);
+      if (threadIdx.x == 0) sd[32] = a;
+    }
+    __syncthreads();
+    double tot = sd[32];
+    __syncthreads();
+    bank ^= 1;
+    return tot;
+  }
+  CS_NOINL int64_t argmax(Key k, int64_t idx) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Key k2 = __shfl_down_sync(0xffffffffu, k, o);
+      int64_t i2 = __shfl_down_sync(0xffffffffu, idx, o);
+      if (k2 > k || (k2 == k && i2 < idx)) { k = k2; idx = i2; }
+    }
+    if (lane == 0) { sk[threadIdx.x >> 5] = k; si[threadIdx.x >> 5] = idx; }
+    __syncthreads();
+    uint64_t* PK = g.pk + bank * g.maxgrid;
+    int64_t* PI = g.pi + bank * g.maxgrid;
+    if (threadIdx.x == 0) {
+      Key bk = 0;
+      int64_t bi = -1;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        if (sk[w] > bk || (sk[w] == bk && bk != 0 && si[w] < bi)) { bk = sk[w]; bi = si[w]; }
+      PK[blockIdx.x] = (uint64_t)bk;
+      PI[blockIdx.x] = bi;
+    }
+    sync();
+    if (threadIdx.x == 0) {
+      Key bk = 0;
+      int64_t bi = -1;
+      for (int c = 0; c < (int)gridDim.x; ++c) {
+        Key kc = (Key)PK[c];
+        if (kc > bk || (kc == bk && bk != 0 && PI[c] < bi)) { bk = kc; bi = PI[c]; }
+      }
+      si[33] = bk ? bi : -1;
+    }
+    __syncthreads();
+    int64_t r = si[33];
+    __syncthreads();
+    bank ^= 1;
+    return r;
+  }
+  CS_NOINL int64_t excl_scan(int64_t v, int64_t* total) {
+    int64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 31) si[w] = inc;
+    __syncthreads();
+    int64_t base = 0, ctot = 0;
+    for (int k = 0; k < nw; ++k) {
+      if (k < w) base += si[k];
+      ctot += si[k];
+    }
+    int64_t* P = g.pi + bank * g.maxgrid;
+    if (threadIdx.x == 0) P[blockIdx.x] = ctot;
+    sync();
+    if (threadIdx.x == 0) {
+      int64_t before = 0, all = 0;
+      for (int c = 0; c < (int)gridDim.x; ++c) {
+        if (c < (int)blockIdx.x) before += P[c];
+        all += P[c];
+      }
+      si[32] = before;
+      si[33] = all;
+    }
+    __syncthreads();
+    int64_t before = si[32];
+    *total = si[33];
+    __syncthreads();
+    bank ^= 1;
+    return before + base + inc - v;
+  }
+  // histogram: shared per-CTA counts, merged into a rotating global bank
+  CS_DEV void hist_clear() {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) shist[i] = 0;
+    if (blockIdx.x == 0) {
+      unsigned* nb = g.ghist + ((hpass + 1) % 3) * 256;
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) nb[i] = 0;
+    }
+    __syncthreads();
+  }
+  CS_DEV void hist_add(unsigned digit) {
+    unsigned peers = __match_any_sync(__activemask(), digit);
+    int leader = __ffs(peers) - 1;
+    if (lane == leader) atomicAdd(&shist[digit], (unsigned)__popc(peers));
+  }
+  CS_DEV void hist_done() {
+    __syncthreads();
+    unsigned* gb = g.ghist + (hpass % 3) * 256;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+      if (shist[i]) atomicAdd(&gb[i], shist[i]);
+    sync();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) shist[i] = gb[i];
+    __syncthreads();
+    ++hpass;
+  }
+  CS_DEV const unsigned* hist_smem() const { return shist; }
+
+  // ---- correlation access ----
+  CS_DEV const T* cbuf() const { return Cb; }
+  CS_DEV T c_at(int64_t j) const { return apply_sign<T>(sign, j, Cb[mk_pos(j, N)]); }
+  CS_DEV T c0_at(int64_t j) const { return apply_sign<T>(sign, j, c0[mk_pos(j, N)]); }
+  CS_DEV void save_c0() {
+    for (int64_t p = gtid; p < N; p += gnthr) c0[p] = Cb[p];
+    sync();
+  }
+
+  // ---- sandwich ----
+  CS_DEV void set_input_support(const int* supp, int ns) {
+    for (int i = gtid; i < in_ns; i += gnthr) U[in_pos[i]] = T(0);
+    sync();
+    for (int i = gtid; i < ns; i += gnthr) in_pos[i] = mk_pos(supp[i], N);
+    in_supp = supp;
+    in_ns = ns;
+  }
+  CS_DEV void scatter(const T* vals) {
+    for (int i = gtid; i < in_ns; i += gnthr) U[in_pos[i]] = apply_sign<T>(sign, in_supp[i], vals[i]);
+    sync();
+  }
+  // pass A: columns of z = U viewed as complex [L1][L2]
+  CS_NOINL void passA() {
+    const C2<T>* Uc = reinterpret_cast<const C2<T>*>(U);
+    const int64_t ntiles = L2 / CT;
+    const int tile = (int)(L1 * CT);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t c0i = t * CT;
+      for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+        int64_t m1 = e / CT, cc = e % CT;
+        buf[e] = Uc[m1 * L2 + c0i + cc];
+      }
+      __syncthreads();
+      fft_cta<T, false>(buf, (int)L1, CT, tw1);
+      for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+        int64_t k1 = e / CT, m2 = c0i + e % CT;
+        Wk[k1 * L2 + m2] = cmul<T>(buf[e], twF(k1 * m2));
+      }
+      __syncthreads();
+    }
+  }
+  template <int MODE> CS_NOINL double passB(bool zero_input, T* yout) {
+    MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, yout);
+    double rn2 = 0;
+    const int64_t nitems = L1 / 2 + 1;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int64_t ka = it, kb = L1 - it;
+      const bool self = (it == 0 || it == L1 / 2);
+      const int B = self ? 1 : 2;
+      for (int e = threadIdx.x; e < B * L2; e += blockDim.x) {
+        int64_t m2 = e / B, k1 = (e % B) ? kb : ka;
+        buf[e] = zero_input ? mk<T>(0, 0) : Wk[k1 * L2 + m2];
+      }
+      __syncthreads();
+      if (!zero_input) fft_cta<T, false>(buf, (int)L2, B, tw2);
+      if (it == 0) {
+        for (int64_t k2 = threadIdx.x; k2 <= L2 / 2; k2 += blockDim.x) {
+          if (k2 == 0) mid_zero<T, MODE>(buf[0], m, rn2);
+          else {
+            int64_t k = L1 * k2;
+            mid_pair<T, MODE>(buf[k2], buf[L2 - k2], k, tw4(k), m, rn2);
+          }
+        }
+      } else if (it == L1 / 2) {
+        for (int64_t k2 = threadIdx.x; k2 < L2 / 2; k2 += blockDim.x) {
+          int64_t k = L1 / 2 + L1 * k2;
+          mid_pair<T, MODE>(buf[k2], buf[L2 - 1 - k2], k, tw4(k), m, rn2);
+        }
+      } else {
+        for (int64_t k2 = threadIdx.x; k2 < L2; k2 += blockDim.x) {
+          int64_t k = ka + L1 * k2;
+          mid_pair<T, MODE>(buf[2 * k2], buf[2 * (L2 - 1 - k2) + 1], k, tw4(k), m, rn2);
+        }
+      }
+      __syncthreads();
+      if constexpr (MODE != MID_FWD) {
+        fft_cta<T, true>(buf, (int)L2, B, tw2);
+        for (int e = threadIdx.x; e < B * L2; e += blockDim.x) {
+          int64_t m2 = e / B, k1 = (e % B) ? kb : ka;
+          Wk[k1 * L2 + m2] = cmulc<T>(buf[e], twF(k1 * m2));
+        }
+      }
+      __syncthreads();
+    }
+    return rn2;
+  }
+  CS_NOINL void passC() {
+    C2<T>* Cc = reinterpret_cast<C2<T>*>(Cb);
+    const int64_t ntiles = L2 / CT;
+    const int tile = (int)(L1 * CT);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t c0i = t * CT;
+      for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+        int64_t k1 = e / CT, cc = e % CT;
+        buf[e] = Wk[k1 * L2 + c0i + cc];
+      }
+      __syncthreads();
+      fft_cta<T, true>(buf, (int)L1, CT, tw1);
+      for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+        int64_t m1 = e / CT, cc = e % CT;
+        Cc[m1 * L2 + c0i + cc] = buf[e];
+      }
+      __syncthreads();
+    }
+  }
+  CS_NOINL void H(const T* d, T* q) {
+    scatter(d);
+    passA();
+    sync();
+    passB<MID_H>(false, nullptr);
+    sync();
+    passC();
+    sync();
+    for (int i = gtid; i < in_ns; i += gnthr) q[i] = c_at(in_supp[i]);
+    ++applies;
+  }
+  CS_NOINL double RES(const T* x) {
+    if (x) {
+      scatter(x);
+      passA();
+      sync();
+    }
+    double rn2 = passB<MID_RES>(x == nullptr, nullptr);
+    sync();
+    passC();
+    ++applies;
+    return sum(rn2);  // the reduction's barrier also publishes Cb
+  }
+};
+
+}  // namespace cs

@@ -1,0 +1,123 @@
+// dct_mid.cuh — the DCT "sandwich middle": real-split of the half-length FFT into
+// DCT-II coefficients, the row-select / residual operation in the DCT domain,
+// and the inverse split that feeds the inverse FFT (DCT-III).
+//
+// Orthonormal DCT-II via Makhoul's reorder and an N/2-point complex FFT
+// ("DCT can be speeded by FFT"):
+//   z_m = v_{2m} + i v_{2m+1},  Z = FFT_L(z),  L = N/2
+//   for the pair (k, kk = L-k):  P = (Z_k + conj Z_kk)/2,  O = -i (Z_k - conj Z_kk)/2,
+//   a = W_4N^k = e^{-i pi k / 2N},  w = W_N^k = a^4,  Q = w O,
+//   c_k  = a (P + Q)                -> X_k = Re c_k,   X_{N-k}  = -Im c_k
+//   c_kk = e^{-i pi/4} conj(a (P - Q)) -> X_kk = Re c_kk, X_{N-kk} = -Im c_kk
+//   k = 0: X_0 = Re Z_0 + Im Z_0,  X_L = (Re Z_0 - Im Z_0)/sqrt 2
+// X is the unnormalised DCT-II; the orthonormal one is s_k X_k with
+// s_0 = 1/sqrt N, s_k = sqrt(2/N).  The inverse split runs the same algebra
+// backwards.  In between, the operation of the step being computed:
+//   MID_H   : X'_k = [k in rows] X_k / L                (H = W A^T A W, Eq.(11))
+//   MID_RES : X'_k = [k in rows] (y_rank(k)/s_k - X_k) / L, ||r||^2 += (y - s X)^2
+//             (pursuit residual + correlation A^T(y - A x), Alg.1 lines 03/07)
+//   MID_FWD : y_rank(k) = s_k X_k  (forward apply only, no inverse)
+// The 1/L of the unnormalised inverse FFT is folded into X'.
+#pragma once
+#include "cs_common.cuh"
+#include "fft_cta.cuh"
+
+namespace cs {
+
+enum MidMode { MID_H = 0, MID_RES = 1, MID_FWD = 2 };
+
+template <typename T> struct MidCtx {
+  const uint32_t* rowmask;  // [N/32] row-selection bitmask (P)
+  const int32_t* prefix;    // [N/32] rows in words before
+  const T* y;               // [M] measurements (RES)
+  T* yout;                  // [M] forward output (FWD)
+  int64_t N;
+  T s0, sk, inv_s0, inv_sk, invL;
+};
+
+template <typename T, int MODE>
+CS_DEV T mid_op(const MidCtx<T>& m, int64_t k, T X, double& rn2) {
+  const bool sel = bit_test(m.rowmask, k);
+  const T s = (k == 0) ? m.s0 : m.sk;
+  if constexpr (MODE == MID_H) {
+    return sel ? X * m.invL : T(0);
+  } else if constexpr (MODE == MID_RES) {
+    if (!sel) return T(0);
+    const T d = m.y[row_rank(m.rowmask, m.prefix, k)] - s * X;
+    rn2 += (double)d * (double)d;
+    const T is = (k == 0) ? m.inv_s0 : m.inv_sk;
+    return d * is * m.invL;
+  } else {
+    if (sel) m.yout[row_rank(m.rowmask, m.prefix, k)] = s * X;
+    return T(0);
+  }
+}
+
+// k = 0 element (self-contained: X_0 and X_L)
+template <typename T, int MODE>
+CS_DEV void mid_zero(C2<T>& Z0, const MidCtx<T>& m, double& rn2) {
+  constexpr T r2 = (T)0.70710678118654752440;
+  const int64_t L = m.N >> 1;
+  T X0 = Z0.x + Z0.y;
+  T XL = (Z0.x - Z0.y) * r2;
+  T Y0 = mid_op<T, MODE>(m, 0, X0, rn2);
+  T YL = mid_op<T, MODE>(m, L, XL, rn2);
+  if constexpr (MODE != MID_FWD) {
+    T V0 = Y0, VL = YL * (T)1.41421356237309504880;
+    Z0 = mk<T>((V0 + VL) * (T)0.5, (V0 - VL) * (T)0.5);
+  }
+}
+
+// pair (k, kk = L - k), 1 <= k <= L/2; `a` = W_4N^k.  Zk, Zkk updated in place.
+template <typename T, int MODE>
+CS_DEV void mid_pair(C2<T>& Zk, C2<T>& Zkk, int64_t k, C2<T> a, const MidCtx<T>& m, double& rn2) {
+  constexpr T r2 = (T)0.70710678118654752440;
+  const int64_t N = m.N, L = N >> 1, kk = L - k;
+  const C2<T> e4 = mk<T>(r2, -r2);  // e^{-i pi/4}
+  C2<T> a2 = cmul<T>(a, a);
+  C2<T> w = cmul<T>(a2, a2);
+  C2<T> P = cscale<T>(cadd<T>(Zk, cconj<T>(Zkk)), (T)0.5);
+  C2<T> D = csub<T>(Zk, cconj<T>(Zkk));
+  C2<T> O = mk<T>(D.y * (T)0.5, -D.x * (T)0.5);  // -i D / 2
+  C2<T> Q = cmul<T>(w, O);
+  C2<T> ck = cmul<T>(a, cadd<T>(P, Q));
+  C2<T> ckk = cmul<T>(e4, cconj<T>(cmul<T>(a, csub<T>(P, Q))));
+  const bool self = (k == kk);
+  T Xk = mid_op<T, MODE>(m, k, ck.x, rn2);
+  T Xnk = mid_op<T, MODE>(m, N - k, -ck.y, rn2);
+  T Xkk = Xk, Xnkk = Xnk;
+  if (!self) {
+    Xkk = mid_op<T, MODE>(m, kk, ckk.x, rn2);
+    Xnkk = mid_op<T, MODE>(m, N - kk, -ckk.y, rn2);
+  }
+  if constexpr (MODE != MID_FWD) {
+    C2<T> cpk = mk<T>(Xk, -Xnk);
+    C2<T> cpkk = mk<T>(Xkk, -Xnkk);
+    C2<T> Vk = cmulc<T>(cpk, a);                              // conj(a) c'_k
+    C2<T> Vkk = cmul<T>(cconj<T>(e4), cmul<T>(a, cpkk));        // e^{i pi/4} a c'_kk
+    C2<T> cVkk = cconj<T>(Vkk);
+    C2<T> E = cscale<T>(cadd<T>(Vk, cVkk), (T)0.5);
+    C2<T> Od = cscale<T>(cmulc<T>(csub<T>(Vk, cVkk), w), (T)0.5);  // conj(w)(Vk - conj Vkk)/2
+    C2<T> iO = mk<T>(-Od.y, Od.x);
+    Zk = cadd<T>(E, iO);
+    if (!self) Zkk = cconj<T>(csub<T>(E, iO));
+  }
+}
+
+template <typename T> CS_DEV MidCtx<T> make_mid(int64_t N, const uint32_t* rowmask,
+                                               const int32_t* prefix, const T* y, T* yout) {
+  MidCtx<T> m;
+  m.rowmask = rowmask;
+  m.prefix = prefix;
+  m.y = y;
+  m.yout = yout;
+  m.N = N;
+  m.s0 = (T)rsqrt((double)N);
+  m.sk = (T)sqrt(2.0 / (double)N);
+  m.inv_s0 = (T)sqrt((double)N);
+  m.inv_sk = (T)sqrt((double)N / 2.0);
+  m.invL = (T)(2.0 / (double)N);
+  return m;
+}
+
+}  // namespace cs

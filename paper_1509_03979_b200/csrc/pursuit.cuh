@@ -1,0 +1,298 @@
+// pursuit.cuh — CG-based weighted least squares and the three greedy pursuits,
+// written once against the context interface (CTA context = one problem per
+// thread block; grid context = one problem per cooperative grid).
+//
+//  cg_solve : Algorithm 1 function CG on Eq.(11) restricted
+//             to the support (Thm 5 / Eq.(12)): compact |S| vectors,
+//             H d = (A^T A scatter_S d)[S] via the operator sandwich, warm start,
+//             relative stopping rule (R6, R7, R9, R29).
+//  omp      : Algorithm 1 lines 01-10, exactly K iterations.
+//  sp       : CG-SP, body per S:289 / SURVEY §8c.4 (R15).
+//  ompr     : CG-OMPR(l, eta), body per S:299 / SURVEY §8c.5 (R16).
+//
+// Every thread of the context runs the same control flow; scalars come out of
+// deterministic collectives, so every branch is uniform.
+#pragma once
+#include "cs_common.cuh"
+#include "select.cuh"
+
+namespace cs {
+
+template <typename T> struct Bufs {
+  int *S, *S2, *U;        // supports: current (K), candidate (K), union/merge (K + l or 2K)
+  T *x, *x2, *xU;         // coefficients on them
+  T *r, *d, *q, *b;       // CG vectors (cap 2K)
+  uint32_t *Sbits, *Ubits, *Pbits;  // [N/32], [N/32], [ceil(2K/32)]
+};
+
+struct Stats {
+  int outer, cg_iters, cg_solves, term;
+  unsigned status;
+  double rel_max;
+};
+
+struct Params {
+  int K, alg, max_outer, cg_cap, ompr_l;
+  double tol, eta;
+};
+
+// ------------------------------------------------------------------ CG ------
+// Solves H x = b on supp (b = c0[supp]).  x holds the warm start on entry.
+// If r_given, r holds r0 = b - H x0 on entry (free when x0 is the previous LS
+// iterate and r = c[supp], see pursuits.py); otherwise one H apply computes it.
+template <class Ctx, typename T>
+CS_NOINL void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q, T* b, bool r_given,
+                     const Params& P, Stats& st) {
+  ctx.set_input_support(supp, ns);
+  for (int i = ctx.gtid; i < ns; i += ctx.gnthr) b[i] = ctx.c0_at(supp[i]);  // line 12
+  ctx.sync();
+  if (!r_given) {
+    ctx.H(x, q);
+    for (int i = ctx.gtid; i < ns; i += ctx.gnthr) r[i] = b[i] - q[i];
+  }
+  double bb = 0, rr = 0;
+  for (int i = ctx.gtid; i < ns; i += ctx.gnthr) {
+    bb += (double)b[i] * (double)b[i];
+    rr += (double)r[i] * (double)r[i];
+    d[i] = r[i];                                                             // line 13
+  }
+  bb = ctx.sum(bb);
+  rr = ctx.sum(rr);
+  const double thr = P.tol * P.tol * bb;
+  const int cap = P.cg_cap > 0 ? P.cg_cap : ns + 50;
+  int j = 0;
+  while (rr > thr) {                                                         // line 15 (R6, R7)
+    if (j >= cap) { st.status |= CS_DEV_CG_CAP; break; }
+    ctx.H(d, q);                                                             // H d_j
+    double dq = 0;
+    for (int i = ctx.gtid; i < ns; i += ctx.gnthr) dq += (double)d[i] * (double)q[i];
+    dq = ctx.sum(dq);
+    if (!(dq > 0.0)) { st.status |= CS_DEV_CG_BREAKDOWN; break; }
+    const T alpha = (T)(rr / dq);                                            // line 16
+    double rr2 = 0;
+    for (int i = ctx.gtid; i < ns; i += ctx.gnthr) {
+      x[i] += alpha * d[i];                                                  // line 17
+      T ri = r[i] - alpha * q[i];                                            // line 18
+      r[i] = ri;
+      rr2 += (double)ri * (double)ri;
+    }
+    rr2 = ctx.sum(rr2);
+    const T beta = (T)(rr2 / rr);                                            // line 19
+    for (int i = ctx.gtid; i < ns; i += ctx.gnthr) d[i] = r[i] + beta * d[i]; // line 20
+    rr = rr2;
+    ++j;                                                                     // line 21
+    if (!(rr == rr)) { st.status |= CS_DEV_CG_BREAKDOWN; break; }
+  }
+  ctx.sync();
+  st.cg_iters += j;
+  st.cg_solves += 1;
+  double rel = bb > 0 ? sqrt(rr / bb) : 0.0;
+  if (rel > st.rel_max) st.rel_max = rel;
+}
+
+// rebuild Sbits from the list S (ns entries)
+template <class Ctx, typename T>
+CS_DEV void bits_from_list(Ctx& ctx, uint32_t* bits, int64_t nwords, const int* S, int ns) {
+  for (int64_t w = ctx.gtid; w < nwords; w += ctx.gnthr) bits[w] = 0u;
+  ctx.sync();
+  for (int i = ctx.gtid; i < ns; i += ctx.gnthr) atomicOr(&bits[S[i] >> 5], 1u << (S[i] & 31));
+  ctx.sync();
+}
+
+template <class Ctx, typename T>
+CS_DEV bool same_list(Ctx& ctx, const int* a, const int* b, int n) {
+  double diff = 0;
+  for (int i = ctx.gtid; i < n; i += ctx.gnthr) diff += (a[i] != b[i]) ? 1.0 : 0.0;
+  return ctx.sum(diff) == 0.0;
+}
+
+template <class Ctx, typename T>
+CS_DEV void swap_ptr(T*& a, T*& b) { T* t = a; a = b; b = t; }
+
+// top-K of |c_j| over j in [0,N) \ excl (excl may be null) -> out bits over [0, N)
+template <class Ctx, typename T>
+CS_NOINL void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* out) {
+  const int64_t N = ctx.N;
+  const T* cb = ctx.cbuf();
+  topk_bits(ctx, N, K, [&](int64_t j) {
+    if (excl && bit_test(excl, j)) return decltype(full_key(T(0)))(0);
+    return full_key(cb[mk_pos(j, N)]);
+  }, out);
+}
+
+template <class Ctx, typename T>
+CS_NOINL int64_t detect_argmax(Ctx& ctx, const uint32_t* excl) {
+  const int64_t N = ctx.N;
+  const T* cb = ctx.cbuf();
+  return argmax_key(ctx, N, [&](int64_t j) {
+    if (bit_test(excl, j)) return decltype(full_key(T(0)))(0);
+    return full_key(cb[mk_pos(j, N)]);
+  });
+}
+
+// ------------------------------------------------------------------ OMP -----
+template <class Ctx, typename T>
+CS_NOINL int run_omp(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& rn2) {
+  const int64_t nwords = (ctx.N + 31) >> 5;
+  rn2 = ctx.RES((const T*)nullptr);      // c = A^T y   (r_0 = y)
+  ctx.save_c0();
+  for (int64_t w = ctx.gtid; w < nwords; w += ctx.gnthr) B.Sbits[w] = 0u;
+  ctx.sync();
+  int ns = 0;
+  int *S = B.S, *S2 = B.S2;
+  T *x = B.x, *x2 = B.x2;
+  for (int it = 0; it < P.K; ++it) {                                   // line 02
+    if (it > 0) {
+      ctx.set_input_support(S, ns);
+      rn2 = ctx.RES(x);                                               // lines 07 + 03
+    }
+    int64_t t = detect_argmax<Ctx, T>(ctx, B.Sbits);                  // line 03, Eq.(6)
+    if (t < 0) break;
+    if (ctx.gtid == 0) B.Sbits[t >> 5] |= 1u << (t & 31);             // line 04
+    ctx.sync();
+    int ns2 = (int)compact_bits(ctx, B.Sbits, ctx.N, [&](int64_t k, int64_t j) { S2[k] = (int)j; });
+    remap(ctx, S, x, ns, S2, x2, ns2);                                // warm start (R9)
+    for (int i = ctx.gtid; i < ns2; i += ctx.gnthr) B.r[i] = ctx.c_at(S2[i]);  // free r0
+    swap_ptr<Ctx>(S, S2);
+    swap_ptr<Ctx>(x, x2);
+    ns = ns2;
+    cg_solve(ctx, S, ns, x, B.r, B.d, B.q, B.b, true, P, st);        // line 06
+    st.outer = it + 1;
+  }
+  ctx.set_input_support(S, ns);
+  rn2 = ctx.RES(x);                                                   // final r_K (line 07)
+  st.term = CS_TERM_DONE;
+  B.S = S; B.S2 = S2; B.x = x; B.x2 = x2;
+  return ns;
+}
+
+// ------------------------------------------------------------------ SP ------
+template <class Ctx, typename T>
+CS_NOINL int run_sp(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& rn2) {
+  const int64_t N = ctx.N, nwords = (N + 31) >> 5;
+  const int K = P.K;
+  int *S = B.S, *S2 = B.S2, *U = B.U;
+  T *x = B.x, *x2 = B.x2, *xU = B.xU;
+  double ry2 = ctx.RES((const T*)nullptr);                       // c0 = A^T y
+  (void)ry2;
+  ctx.save_c0();
+  detect_topk<Ctx, T>(ctx, K, nullptr, B.Sbits);                 // S = top-K |A^T y|
+  int ns = (int)compact_bits(ctx, B.Sbits, N, [&](int64_t k, int64_t j) { S[k] = (int)j; });
+  for (int i = ctx.gtid; i < ns; i += ctx.gnthr) { x[i] = T(0); B.r[i] = ctx.c_at(S[i]); }
+  cg_solve(ctx, S, ns, x, B.r, B.d, B.q, B.b, true, P, st);
+  ctx.set_input_support(S, ns);
+  rn2 = ctx.RES(x);                                              // r = y - A x, c = A^T r
+  const int max_outer = P.max_outer > 0 ? P.max_outer : 30;
+  st.term = CS_TERM_ITER_CAP;
+  for (int it = 1; it <= max_outer; ++it) {
+    st.outer = it;
+    detect_topk<Ctx, T>(ctx, K, B.Sbits, B.Ubits);               // J = top-K off S
+    for (int64_t w = ctx.gtid; w < nwords; w += ctx.gnthr) B.Ubits[w] |= B.Sbits[w];  // T = S u J
+    ctx.sync();
+    int nu = (int)compact_bits(ctx, B.Ubits, N, [&](int64_t k, int64_t j) { U[k] = (int)j; });
+    remap(ctx, S, x, ns, U, xU, nu);                             // x0 = x on S, 0 on J
+    for (int i = ctx.gtid; i < nu; i += ctx.gnthr) B.r[i] = ctx.c_at(U[i]);   // r0 = c[T]
+    cg_solve(ctx, U, nu, xU, B.r, B.d, B.q, B.b, true, P, st);
+    // prune: S' = top-K of |x_T| over T (positions ascending == indices ascending)
+    const T* xUc = xU;
+    topk_bits(ctx, (int64_t)nu, (int64_t)K, [&](int64_t i) { return full_key(xUc[i]); }, B.Pbits);
+    int ns2 = (int)compact_bits(ctx, B.Pbits, nu, [&](int64_t k, int64_t pos) {
+      S2[k] = U[pos];
+      x2[k] = xU[pos];
+    });
+    if (same_list<Ctx, T>(ctx, S, S2, ns)) { st.term = CS_TERM_SUPPORT_FIXED; break; }
+    cg_solve(ctx, S2, ns2, x2, B.r, B.d, B.q, B.b, false, P, st);
+    ctx.set_input_support(S2, ns2);
+    double rn2new = ctx.RES(x2);
+    if (rn2new >= rn2) { st.term = CS_TERM_RESID_ROSE; break; }   // keep (S, x)
+    swap_ptr<Ctx>(S, S2);
+    swap_ptr<Ctx>(x, x2);
+    ns = ns2;
+    rn2 = rn2new;
+    bits_from_list<Ctx, T>(ctx, B.Sbits, nwords, S, ns);
+  }
+  B.S = S; B.S2 = S2; B.x = x; B.x2 = x2;
+  return ns;
+}
+
+// ------------------------------------------------------------------ OMPR ----
+template <class Ctx, typename T>
+CS_NOINL int run_ompr(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& rn2) {
+  const int64_t N = ctx.N, nwords = (N + 31) >> 5;
+  const int K = P.K;
+  const int l = P.ompr_l > 0 ? P.ompr_l : 1;
+  const T eta = (T)(P.eta > 0 ? P.eta : 1.0);
+  int *S = B.S, *S2 = B.S2, *U = B.U;
+  T *x = B.x, *x2 = B.x2, *xU = B.xU;
+  ctx.RES((const T*)nullptr);
+  ctx.save_c0();
+  detect_topk<Ctx, T>(ctx, K, nullptr, B.Sbits);
+  int ns = (int)compact_bits(ctx, B.Sbits, N, [&](int64_t k, int64_t j) { S[k] = (int)j; });
+  for (int i = ctx.gtid; i < ns; i += ctx.gnthr) { x[i] = T(0); B.r[i] = ctx.c_at(S[i]); }
+  cg_solve(ctx, S, ns, x, B.r, B.d, B.q, B.b, true, P, st);
+  ctx.set_input_support(S, ns);
+  rn2 = ctx.RES(x);
+  const int max_outer = P.max_outer > 0 ? P.max_outer : 2 * K;
+  st.term = CS_TERM_ITER_CAP;
+  for (int it = 1; it <= max_outer; ++it) {
+    st.outer = it;
+    // J = top-l of |z| = |x~ + eta c| off S (x~ = 0 there)
+    if (l == 1) {
+      int64_t j = detect_argmax<Ctx, T>(ctx, B.Sbits);
+      for (int64_t w = ctx.gtid; w < nwords; w += ctx.gnthr) B.Ubits[w] = B.Sbits[w];
+      ctx.sync();
+      if (ctx.gtid == 0 && j >= 0) B.Ubits[j >> 5] |= 1u << (j & 31);
+      ctx.sync();
+    } else {
+      detect_topk<Ctx, T>(ctx, l, B.Sbits, B.Ubits);
+      for (int64_t w = ctx.gtid; w < nwords; w += ctx.gnthr) B.Ubits[w] |= B.Sbits[w];
+      ctx.sync();
+    }
+    int nu = (int)compact_bits(ctx, B.Ubits, N, [&](int64_t k, int64_t j) { U[k] = (int)j; });
+    remap(ctx, S, x, ns, U, xU, nu);                                  // x~ on U
+    for (int i = ctx.gtid; i < nu; i += ctx.gnthr) xU[i] = xU[i] + eta * ctx.c_at(U[i]);  // z on U
+    ctx.sync();
+    const T* zc = xU;
+    topk_bits(ctx, (int64_t)nu, (int64_t)K, [&](int64_t i) { return full_key(zc[i]); }, B.Pbits);
+    int ns2 = (int)compact_bits(ctx, B.Pbits, nu, [&](int64_t k, int64_t pos) { S2[k] = U[pos]; });
+    if (same_list<Ctx, T>(ctx, S, S2, ns)) { st.term = CS_TERM_SUPPORT_FIXED; break; }
+    remap(ctx, S, x, ns, S2, x2, ns2);                                // x0 = x~[S']
+    cg_solve(ctx, S2, ns2, x2, B.r, B.d, B.q, B.b, false, P, st);
+    swap_ptr<Ctx>(S, S2);
+    swap_ptr<Ctx>(x, x2);
+    ns = ns2;
+    bits_from_list<Ctx, T>(ctx, B.Sbits, nwords, S, ns);
+    ctx.set_input_support(S, ns);
+    rn2 = ctx.RES(x);
+  }
+  B.S = S; B.S2 = S2; B.x = x; B.x2 = x2;
+  return ns;
+}
+
+// run the selected pursuit and write (support, values, report)
+template <class Ctx, typename T>
+CS_DEV void run_pursuit(Ctx& ctx, const Params& P, Bufs<T> B, T* vals, int32_t* supp,
+                        cs_report* rep, unsigned pre_status) {
+  Stats st = {0, 0, 0, 0, pre_status, 0.0};
+  double rn2 = 0;
+  int ns = 0;
+  if (P.alg == CS_OMP) ns = run_omp(ctx, P, B, st, rn2);
+  else if (P.alg == CS_SP) ns = run_sp(ctx, P, B, st, rn2);
+  else ns = run_ompr(ctx, P, B, st, rn2);
+  for (int i = ctx.gtid; i < P.K; i += ctx.gnthr) {
+    supp[i] = i < ns ? B.S[i] : -1;
+    vals[i] = i < ns ? B.x[i] : T(0);
+  }
+  if (ctx.gtid == 0) {
+    rep->outer_iters = st.outer;
+    rep->cg_iters_total = st.cg_iters;
+    rep->cg_solves = st.cg_solves;
+    rep->applies = ctx.applies;
+    rep->termination = st.term;
+    rep->status = st.status;
+    rep->resid_norm = sqrt(rn2);
+    rep->cg_rel_resid = st.rel_max;
+  }
+}
+
+}  // namespace cs

@@ -1,0 +1,180 @@
+// select.cuh — support detection and support bookkeeping, written once against
+// the context interface (ctx_cta.cuh / ctx_grid.cuh).
+//
+//  * topk_bits   — radix top-K select (b2): the K largest keys, ties to the
+//                  lowest index (R12/R32), MSB-first
+//                  8-bit digits over order-preserving magnitude keys, result
+//                  written as a bitmask over the index range.
+//  * argmax_excl — OMP / OMPR(1) detection (Eq.(6)).
+//  * compact     — bitmask -> ascending index list (support merge / prune, b3).
+//  * remap       — carry coefficients from one sorted support to another
+//                  (warm start, cg1; zeros for new indices).
+#pragma once
+#include "cs_common.cuh"
+
+namespace cs {
+
+// ---------------------------------------------------------------- top-K ----
+// Warp 0 finds, scanning the 256-bin histogram from the top, the digit at which
+// the running count reaches `need`; (digit, count above it, count at it) are
+// broadcast through pick[0..2].  All threads of the block must call.
+CS_DEV void hist_pick(const unsigned* h, int64_t* pick, int64_t need, int64_t& dsel, int64_t& cum,
+                      int64_t& hsel) {
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+    unsigned c[8];
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { c[i] = h[255 - 8 * l - i]; s += c[i]; }
+    int64_t inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (l >= o) inc += t;
+    }
+    const int64_t total = __shfl_sync(0xffffffffu, inc, 31);
+    unsigned ball = __ballot_sync(0xffffffffu, inc >= need);
+    int fl = ball ? __ffs(ball) - 1 : -1;
+    if (l == fl) {
+      int64_t cu = inc - s;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (cu + c[i] >= need) { pick[0] = 255 - 8 * l - i; pick[1] = cu; pick[2] = c[i]; break; }
+        cu += c[i];
+      }
+    }
+    if (fl < 0 && l == 0) {  // fewer candidates than need: take everything
+      pick[0] = 0; pick[1] = total - h[0]; pick[2] = h[0];
+    }
+  }
+  __syncthreads();
+  dsel = pick[0];
+  cum = pick[1];
+  hsel = pick[2];
+  __syncthreads();
+}
+
+// key(i) for i in [0, n); key 0 means "never select".  Requires at least K
+// non-zero keys.  out_bits must hold ceil(n/32) words; fully overwritten.
+template <class Ctx, class KeyFn>
+CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_bits) {
+  using Key = decltype(key(int64_t(0)));
+  constexpr int NB = (int)sizeof(Key) * 8;
+  Key prefix = 0, pmask = 0;
+  int64_t need = K;
+  int64_t n_eq = 0;
+  for (int shift = NB - 8; shift >= 0; shift -= 8) {
+    ctx.hist_clear();
+    for (int64_t i = ctx.gtid; i < n; i += ctx.gnthr) {
+      Key k = key(i);
+      if ((k & pmask) == prefix) ctx.hist_add((unsigned)((k >> shift) & 255));
+    }
+    ctx.hist_done();  // merged counts now in ctx.hist_smem()
+    int64_t dsel, cum, hsel;
+    hist_pick(ctx.hist_smem(), ctx.pick, need, dsel, cum, hsel);
+    need -= cum;
+    n_eq = hsel;
+    prefix |= (Key)dsel << shift;
+    pmask |= (Key)255 << shift;
+  }
+  const Key thr = prefix;  // the K-th largest key; take `need` of the n_eq equal ones
+  const int64_t nwords = (n + 31) >> 5;
+  if (n_eq == need) {
+    // common case: every key >= thr is selected
+    for (int64_t w = ctx.gwarp; w < nwords; w += ctx.gnwarps) {
+      int64_t i = w * 32 + ctx.lane;
+      bool s = (i < n) && (key(i) >= thr);
+      uint32_t b = __ballot_sync(0xffffffffu, s);
+      if (ctx.lane == 0) out_bits[w] = b;
+    }
+    ctx.sync();
+    return;
+  }
+  // ties at the threshold: the lowest-index `need` equal keys win.
+  // warp-contiguous chunks of words, chunk order == index order
+  const int64_t per = (nwords + ctx.gnwarps - 1) / ctx.gnwarps;
+  const int64_t w0 = ctx.gwarp * per, w1 = min(nwords, w0 + per);
+  int64_t cnt = 0;
+  for (int64_t w = w0; w < w1; ++w) {
+    int64_t i = w * 32 + ctx.lane;
+    bool e = (i < n) && (key(i) == thr);
+    cnt += __popc(__ballot_sync(0xffffffffu, e));
+  }
+  int64_t tot;
+  int64_t base = ctx.excl_scan(ctx.lane == 0 ? cnt : 0, &tot);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int64_t w = w0; w < w1; ++w) {
+    int64_t i = w * 32 + ctx.lane;
+    Key k = (i < n) ? key(i) : Key(0);
+    bool e = (i < n) && (k == thr);
+    uint32_t em = __ballot_sync(0xffffffffu, e);
+    int64_t rank = base + __popc(em & ((1u << ctx.lane) - 1u));
+    bool s = (i < n) && ((k > thr) || (e && rank < need));
+    uint32_t b = __ballot_sync(0xffffffffu, s);
+    if (ctx.lane == 0) out_bits[w] = b;
+    base += __popc(em);
+  }
+  ctx.sync();
+}
+
+// ---------------------------------------------------------------- argmax ---
+// index of the largest key(i) over i in [0, n), ties -> lowest i; -1 if none.
+template <class Ctx, class KeyFn>
+CS_DEV int64_t argmax_key(Ctx& ctx, int64_t n, KeyFn key) {
+  using Key = decltype(key(int64_t(0)));
+  Key bk = 0;
+  int64_t bi = -1;
+  for (int64_t i = ctx.gtid; i < n; i += ctx.gnthr) {
+    Key k = key(i);
+    if (k > bk) { bk = k; bi = i; }  // increasing i per thread: first max kept
+  }
+  return ctx.argmax(bk, bi);
+}
+
+// -------------------------------------------------------------- compaction --
+// For every set bit i of bits[0..n) in ascending order, call emit(rank, i).
+// Returns the number of set bits (uniform).
+template <class Ctx, class Emit>
+CS_DEV int64_t compact_bits(Ctx& ctx, const uint32_t* bits, int64_t n, Emit emit) {
+  const int64_t nwords = (n + 31) >> 5;
+  const int64_t per = (nwords + ctx.gnthr - 1) / ctx.gnthr;
+  const int64_t w0 = (int64_t)ctx.gtid * per, w1 = min(nwords, w0 + per);
+  int64_t cnt = 0;
+  for (int64_t w = w0; w < w1; ++w) {
+    uint32_t b = bits[w];
+    if (w == nwords - 1 && (n & 31)) b &= (1u << (n & 31)) - 1u;
+    cnt += __popc(b);
+  }
+  int64_t tot;
+  int64_t pos = ctx.excl_scan(cnt, &tot);
+  for (int64_t w = w0; w < w1; ++w) {
+    uint32_t b = bits[w];
+    if (w == nwords - 1 && (n & 31)) b &= (1u << (n & 31)) - 1u;
+    while (b) {
+      int t = __ffs(b) - 1;
+      b &= b - 1;
+      emit(pos++, w * 32 + t);
+    }
+  }
+  ctx.sync();
+  return tot;
+}
+
+// ---------------------------------------------------------------- remap ----
+// new_vals[i] = old_vals[pos of new_list[i] in old_list] or 0 (both lists ascending)
+template <class Ctx, typename T>
+CS_DEV void remap(Ctx& ctx, const int* old_list, const T* old_vals, int n_old,
+                  const int* new_list, T* new_vals, int n_new) {
+  for (int i = ctx.gtid; i < n_new; i += ctx.gnthr) {
+    int e = new_list[i];
+    int lo = 0, hi = n_old;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (old_list[mid] < e) lo = mid + 1; else hi = mid;
+    }
+    new_vals[i] = (lo < n_old && old_list[lo] == e) ? old_vals[lo] : T(0);
+  }
+  ctx.sync();
+}
+
+}  // namespace cs

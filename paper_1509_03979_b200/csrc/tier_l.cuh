@@ -1,0 +1,364 @@
+// tier_l.cuh — Tier L: one cooperative persistent grid per problem (N >= 32768).
+// Used for configs 2 (SP, N = 2^16), 3 (OMPR, N = 2^20) and 5 (SP, N = 2^24), and
+// for operator apply / adjoint at those sizes.  See ctx_grid.cuh for the passes.
+#pragma once
+#include <atomic>
+#include <string>
+
+#include "ctx_grid.cuh"
+#include "pursuit.cuh"
+#include "tier_s.cuh"
+
+namespace cs {
+
+constexpr int TL_THREADS = 512;
+constexpr int TL_TILE = FFT_E * TL_THREADS;  // 8192 complex per CTA tile
+
+struct LGeom {
+  int64_t N, L, L1, L2;
+  int CT, shF, sh4;
+};
+
+CS_HD int ilog2(int64_t v) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return l;
+}
+
+CS_HD LGeom l_geom(int64_t N) {
+  LGeom g;
+  g.N = N;
+  g.L = N / 2;
+  const int l = ilog2(g.L);
+  g.L2 = int64_t(1) << ((l + 1) / 2);
+  g.L1 = int64_t(1) << (l / 2);
+  int64_t ct = TL_TILE / g.L1;
+  g.CT = (int)(ct < 4 ? ct : 4);
+  g.shF = (l + 1) / 2;
+  g.sh4 = (l + 1) / 2;
+  return g;
+}
+
+// Workspace layout (byte offsets) — identical on host and device.
+struct LLayout {
+  int64_t U, Wk, Cb, c0, twFlo, twFhi, tw4lo, tw4hi, in_pos;
+  int64_t S, S2, Ul, x, x2, xU, r, d, q, b, Sbits, Ubits, Pbits;
+  int64_t ctl, bar, pd, pi, pk, ghist, ctl_end;
+  int64_t bytes;
+  int maxgrid;
+};
+
+template <typename T>
+CS_HD LLayout l_layout(int64_t N, int K, int ucap, bool pursuit, int maxgrid) {
+  LLayout s;
+  LGeom g = l_geom(N);
+  const int64_t ts = sizeof(T), cs2 = 2 * sizeof(T), nw = (N + 31) / 32;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) { int64_t r = o; o = align_up(o + bytes, 256); return r; };
+  s.U = take(N * ts);
+  s.Wk = take(g.L * cs2);
+  s.Cb = take(N * ts);
+  s.c0 = pursuit ? take(N * ts) : 0;
+  s.twFlo = take((int64_t(1) << g.shF) * cs2);
+  s.twFhi = take(((g.L >> g.shF) + 1) * cs2);
+  s.tw4lo = take((int64_t(1) << g.sh4) * cs2);
+  s.tw4hi = take(((g.L >> g.sh4) + 1) * cs2);
+  if (pursuit) {
+    s.in_pos = take((int64_t)ucap * 8);
+    s.S = take((int64_t)K * 4);
+    s.S2 = take((int64_t)K * 4);
+    s.Ul = take((int64_t)ucap * 4);
+    s.x = take((int64_t)K * ts);
+    s.x2 = take((int64_t)K * ts);
+    s.xU = take((int64_t)ucap * ts);
+    s.r = take((int64_t)ucap * ts);
+    s.d = take((int64_t)ucap * ts);
+    s.q = take((int64_t)ucap * ts);
+    s.b = take((int64_t)ucap * ts);
+    s.Sbits = take(nw * 4);
+    s.Ubits = take(nw * 4);
+    s.Pbits = take(((ucap + 31) / 32) * 4);
+  } else {
+    s.in_pos = s.S = s.S2 = s.Ul = s.x = s.x2 = s.xU = s.r = s.d = s.q = s.b = 0;
+    s.Sbits = s.Ubits = s.Pbits = 0;
+  }
+  // control block (zeroed before every launch)
+  s.ctl = o;
+  s.bar = take(256);
+  s.pd = take(2 * (int64_t)maxgrid * 8);
+  s.pi = take(2 * (int64_t)maxgrid * 8);
+  s.pk = take(2 * (int64_t)maxgrid * 8);
+  s.ghist = take(3 * 256 * 4);
+  s.ctl_end = o;
+  s.bytes = o;
+  s.maxgrid = maxgrid;
+  return s;
+}
+
+template <typename T> CS_HD int64_t l_smem_bytes(int64_t N) {
+  LGeom g = l_geom(N);
+  const int64_t cs2 = 2 * sizeof(T);
+  int64_t o = 0;
+  auto take = [&](int64_t b) { o = align_up(o + b, 16); };
+  take(TL_TILE * cs2);                                    // buf
+  take(64 * cs2); take((g.L1 >= 64 ? g.L1 / 64 : 1) * cs2);   // tw1
+  take(64 * cs2); take((g.L2 >= 64 ? g.L2 / 64 : 1) * cs2);   // tw2
+  take(34 * 8); take(34 * 8); take(32 * 8); take(256 * 4); take(4 * 8);
+  return o;
+}
+
+template <typename T> struct LArgs {
+  OpMeta meta;
+  LLayout lay;
+  Params P;
+  int64_t B;
+  const T* Y;   // recover: [B][M];  apply: x [B][N];  adjoint: y [B][M]
+  T* out;       // apply: y [B][M];  adjoint: x [B][N]
+  T* vals;
+  int32_t* supp;
+  cs_report* reps;
+  char* ws;
+};
+
+template <typename T>
+CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
+  GridCtx<T> c;
+  LGeom g = l_geom(a.meta.N);
+  const LLayout& s = a.lay;
+  c.gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  c.gnthr = gridDim.x * blockDim.x;
+  c.lane = threadIdx.x & 31;
+  c.gwarp = c.gtid >> 5;
+  c.gnwarps = c.gnthr >> 5;
+  c.N = a.meta.N;
+  c.M = a.meta.M;
+  c.L = g.L;
+  c.L1 = g.L1;
+  c.L2 = g.L2;
+  c.CT = g.CT;
+  char* ws = a.ws;
+  c.U = reinterpret_cast<T*>(ws + s.U);
+  c.Wk = reinterpret_cast<C2<T>*>(ws + s.Wk);
+  c.Cb = reinterpret_cast<T*>(ws + s.Cb);
+  c.c0 = reinterpret_cast<T*>(ws + s.c0);
+  c.in_pos = reinterpret_cast<int64_t*>(ws + s.in_pos);
+  c.twF.lo = reinterpret_cast<const C2<T>*>(ws + s.twFlo);
+  c.twF.hi = reinterpret_cast<const C2<T>*>(ws + s.twFhi);
+  c.twF.sh = g.shF;
+  c.tw4.lo = reinterpret_cast<const C2<T>*>(ws + s.tw4lo);
+  c.tw4.hi = reinterpret_cast<const C2<T>*>(ws + s.tw4hi);
+  c.tw4.sh = g.sh4;
+  c.g.bar = reinterpret_cast<GridBar*>(ws + s.bar);
+  c.g.pd = reinterpret_cast<double*>(ws + s.pd);
+  c.g.pi = reinterpret_cast<int64_t*>(ws + s.pi);
+  c.g.pk = reinterpret_cast<uint64_t*>(ws + s.pk);
+  c.g.ghist = reinterpret_cast<unsigned*>(ws + s.ghist);
+  c.g.maxgrid = s.maxgrid;
+  // shared memory
+  const int64_t cs2 = 2 * sizeof(T);
+  int64_t o = 0;
+  auto take = [&](int64_t b) { int64_t r = o; o = align_up(o + b, 16); return smem + r; };
+  c.buf = reinterpret_cast<C2<T>*>(take(TL_TILE * cs2));
+  C2<T>* t1lo = reinterpret_cast<C2<T>*>(take(64 * cs2));
+  const int n1 = (int)(g.L1 >= 64 ? g.L1 / 64 : 1);
+  C2<T>* t1hi = reinterpret_cast<C2<T>*>(take(n1 * cs2));
+  C2<T>* t2lo = reinterpret_cast<C2<T>*>(take(64 * cs2));
+  const int n2 = (int)(g.L2 >= 64 ? g.L2 / 64 : 1);
+  C2<T>* t2hi = reinterpret_cast<C2<T>*>(take(n2 * cs2));
+  c.sd = reinterpret_cast<double*>(take(34 * 8));
+  c.si = reinterpret_cast<int64_t*>(take(34 * 8));
+  c.sk = reinterpret_cast<typename GridCtx<T>::Key*>(take(32 * 8));
+  c.shist = reinterpret_cast<unsigned*>(take(256 * 4));
+  c.pick = reinterpret_cast<int64_t*>(take(4 * 8));
+  tw_init<T>(t1lo, t1hi, g.L1, n1, threadIdx.x, blockDim.x);
+  tw_init<T>(t2lo, t2hi, g.L2, n2, threadIdx.x, blockDim.x);
+  c.tw1.lo = t1lo; c.tw1.hi = t1hi;
+  c.tw2.lo = t2lo; c.tw2.hi = t2hi;
+  c.bank = 0;
+  c.hpass = 0;
+  c.in_supp = nullptr;
+  c.in_ns = 0;
+  c.applies = 0;
+  c.y = nullptr;
+  __syncthreads();
+  return c;
+}
+
+template <typename T> CS_DEV void set_instance(GridCtx<T>& c, const OpMeta& m, int64_t b) {
+  c.sign = m.sign(b);
+  c.rowmask = m.rmask(b);
+  c.prefix = m.prefix(b);
+}
+
+// Global twiddle tables (plain launch before the cooperative kernel).
+template <typename T>
+__global__ void k_l_tables(LLayout s, int64_t N, char* ws) {
+  LGeom g = l_geom(N);
+  C2<T>* Flo = reinterpret_cast<C2<T>*>(ws + s.twFlo);
+  C2<T>* Fhi = reinterpret_cast<C2<T>*>(ws + s.twFhi);
+  C2<T>* Qlo = reinterpret_cast<C2<T>*>(ws + s.tw4lo);
+  C2<T>* Qhi = reinterpret_cast<C2<T>*>(ws + s.tw4hi);
+  const int64_t nlo = int64_t(1) << g.shF, nhi = (g.L >> g.shF) + 1;
+  const int64_t total = 2 * (nlo + nhi);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t which = i / (nlo + nhi), r = i % (nlo + nhi);
+    int64_t den = which ? 4 * N : g.L;
+    int64_t m = r < nlo ? r : (r - nlo) << g.shF;
+    double sn, cn;
+    sincospi(-2.0 * (double)(m % den) / (double)den, &sn, &cn);
+    C2<T> w = mk<T>((T)cn, (T)sn);
+    if (which == 0) { if (r < nlo) Flo[r] = w; else Fhi[r - nlo] = w; }
+    else { if (r < nlo) Qlo[r] = w; else Qhi[r - nlo] = w; }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TL_THREADS) k_l_apply(LArgs<T> a) {
+  extern __shared__ __align__(16) char smem[];
+  GridCtx<T> c = make_grid_ctx<T>(smem, a);
+  const int64_t N = c.N;
+  for (int64_t b = 0; b < a.B; ++b) {
+    set_instance(c, a.meta, b);
+    const T* x = a.Y + b * N;
+    for (int64_t j = c.gtid; j < N; j += c.gnthr) c.U[mk_pos(j, N)] = apply_sign<T>(c.sign, j, x[j]);
+    c.sync();
+    c.passA();
+    c.sync();
+    c.template passB<MID_FWD>(false, a.out + b * c.M);
+    c.sync();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TL_THREADS) k_l_adjoint(LArgs<T> a) {
+  extern __shared__ __align__(16) char smem[];
+  GridCtx<T> c = make_grid_ctx<T>(smem, a);
+  const int64_t N = c.N;
+  for (int64_t b = 0; b < a.B; ++b) {
+    set_instance(c, a.meta, b);
+    c.y = a.Y + b * c.M;
+    c.RES(nullptr);
+    T* x = a.out + b * N;
+    for (int64_t j = c.gtid; j < N; j += c.gnthr) x[j] = c.c_at(j);
+    c.sync();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TL_THREADS) k_l_recover(LArgs<T> a) {
+  extern __shared__ __align__(16) char smem[];
+  GridCtx<T> c = make_grid_ctx<T>(smem, a);
+  const LLayout& s = a.lay;
+  char* ws = a.ws;
+  for (int64_t b = 0; b < a.B; ++b) {
+    set_instance(c, a.meta, b);
+    c.y = a.Y + b * c.M;
+    c.applies = 0;
+    double bad = 0;
+    for (int64_t m = c.gtid; m < c.M; m += c.gnthr) bad += isfinite((double)c.y[m]) ? 0.0 : 1.0;
+    unsigned pre = c.sum(bad) > 0 ? CS_DEV_NONFINITE_Y : 0u;
+    Bufs<T> B;
+    B.S = reinterpret_cast<int*>(ws + s.S);
+    B.S2 = reinterpret_cast<int*>(ws + s.S2);
+    B.U = reinterpret_cast<int*>(ws + s.Ul);
+    B.x = reinterpret_cast<T*>(ws + s.x);
+    B.x2 = reinterpret_cast<T*>(ws + s.x2);
+    B.xU = reinterpret_cast<T*>(ws + s.xU);
+    B.r = reinterpret_cast<T*>(ws + s.r);
+    B.d = reinterpret_cast<T*>(ws + s.d);
+    B.q = reinterpret_cast<T*>(ws + s.q);
+    B.b = reinterpret_cast<T*>(ws + s.b);
+    B.Sbits = reinterpret_cast<uint32_t*>(ws + s.Sbits);
+    B.Ubits = reinterpret_cast<uint32_t*>(ws + s.Ubits);
+    B.Pbits = reinterpret_cast<uint32_t*>(ws + s.Pbits);
+    run_pursuit<GridCtx<T>, T>(c, a.P, B, a.vals + b * a.P.K, a.supp + b * a.P.K, a.reps + b, pre);
+    c.set_input_support(nullptr, 0);  // leave U all-zero for the next problem
+    c.sync();
+  }
+}
+
+// ------------------------------------------------------------ host side ----
+template <typename T> inline int l_maxgrid(const void* fn, int64_t smem) {
+  int dev = 0, nsm = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TL_THREADS, (size_t)smem);
+  if (occ < 1) occ = 1;
+  return nsm * occ;
+}
+
+template <typename T> inline int l_grid_upper() {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) {
+    cudaGetLastError();
+    nsm = 148;
+  }
+  return nsm * 4;  // generous upper bound for workspace sizing
+}
+
+template <typename T> inline size_t tier_l_apply_ws_bytes(int64_t N) {
+  return (size_t)l_layout<T>(N, 0, 0, false, l_grid_upper<T>()).bytes;
+}
+template <typename T> inline size_t tier_l_recover_ws_bytes(int64_t N, int64_t M, int K, int ucap) {
+  (void)M;
+  return (size_t)l_layout<T>(N, K, ucap, true, l_grid_upper<T>()).bytes;
+}
+
+template <typename T>
+inline cs_status l_launch(const void* fn, LArgs<T>& a, int64_t N, cudaStream_t st,
+                          std::atomic<uint64_t>& launches, std::string& err) {
+  const int64_t smem = l_smem_bytes<T>(N);
+  int grid = l_maxgrid<T>(fn, smem);
+  if (grid > a.lay.maxgrid) grid = a.lay.maxgrid;
+  cudaError_t e = cudaMemsetAsync(a.ws + a.lay.ctl, 0, (size_t)(a.lay.ctl_end - a.lay.ctl), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a.ws + a.lay.U, 0, (size_t)(N * sizeof(T)), st);
+  if (e != cudaSuccess) { err = std::string("memset: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  k_l_tables<T><<<64, 256, 0, st>>>(a.lay, N, a.ws);
+  launches.fetch_add(1);
+  void* args[] = {&a};
+  e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(TL_THREADS), args, (size_t)smem, st);
+  launches.fetch_add(1);
+  if (e != cudaSuccess) { err = std::string("cooperative launch: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  return CS_OK;
+}
+
+template <typename T>
+inline cs_status tier_l_apply(OpMeta meta, int64_t B, const T* in, T* out, void* ws, size_t ws_bytes,
+                              cudaStream_t st, bool adjoint, std::atomic<uint64_t>& launches,
+                              std::string& err) {
+  LArgs<T> a;
+  a.meta = meta;
+  a.lay = l_layout<T>(meta.N, 0, 0, false, l_grid_upper<T>());
+  if (!ws || ws_bytes < (size_t)a.lay.bytes) { err = "workspace too small"; return CS_ERR_WORKSPACE; }
+  a.B = B;
+  a.Y = in;
+  a.out = out;
+  a.ws = reinterpret_cast<char*>(ws);
+  a.vals = nullptr; a.supp = nullptr; a.reps = nullptr;
+  const void* fn = adjoint ? (const void*)k_l_adjoint<T> : (const void*)k_l_apply<T>;
+  return l_launch<T>(fn, a, meta.N, st, launches, err);
+}
+
+template <typename T>
+inline cs_status tier_l_recover(OpMeta meta, Params P, int ucap, const T* Y, int64_t B, T* vals,
+                                int32_t* supp, cs_report* reps, void* ws, size_t ws_bytes,
+                                cudaStream_t st, std::atomic<uint64_t>& launches, std::string& err) {
+  LArgs<T> a;
+  a.meta = meta;
+  a.lay = l_layout<T>(meta.N, P.K, ucap, true, l_grid_upper<T>());
+  if (!ws || ws_bytes < (size_t)a.lay.bytes) { err = "workspace too small"; return CS_ERR_WORKSPACE; }
+  a.P = P;
+  a.B = B;
+  a.Y = Y;
+  a.out = nullptr;
+  a.vals = vals;
+  a.supp = supp;
+  a.reps = reps;
+  a.ws = reinterpret_cast<char*>(ws);
+  return l_launch<T>((const void*)k_l_recover<T>, a, meta.N, st, launches, err);
+}
+
+}  // namespace cs

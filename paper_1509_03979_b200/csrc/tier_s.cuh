@@ -1,0 +1,194 @@
+// tier_s.cuh — Tier S: one thread block per problem, the whole pursuit resident in
+// shared memory (N <= 16384, i.e. the half-length FFT of <= 8192 points fits).
+// Used for config 1 (OMP, N = 4096) and config 4 (4096 batched SP problems,
+// N = 16384), and for batched operator apply / adjoint at those sizes.
+#pragma once
+#include "ctx_cta.cuh"
+#include "pursuit.cuh"
+
+namespace cs {
+
+constexpr int64_t TIER_S_MAX_N = 16384;
+
+CS_HD int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Shared-memory layout of a Tier S block (computed identically on host and device).
+struct SLayout {
+  int64_t Z, twLlo, twLhi, tw4lo, tw4hi, sign, rmask, prefix, redd, redi, redk, hist, pick;
+  int64_t S, S2, U, x, x2, xU, r, d, q, b, Sbits, Ubits, Pbits;
+  int64_t bytes;
+  int nthreads;
+};
+
+template <typename T>
+CS_HD SLayout s_layout(int64_t N, int K, int ucap, bool pursuit) {
+  SLayout s;
+  const int64_t L = N / 2, nw = (N + 31) / 32, cs2 = sizeof(T) * 2, ts = sizeof(T);
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) { int64_t r = o; o = align_up(o + bytes, 16); return r; };
+  s.Z = take(L * cs2);
+  s.twLlo = take(64 * cs2);
+  s.twLhi = take((L >= 64 ? L / 64 : 1) * cs2);
+  s.tw4lo = take(64 * cs2);
+  s.tw4hi = take((L / 128 + 1) * cs2);
+  s.sign = take(nw * 4);
+  s.rmask = take(nw * 4);
+  s.prefix = take(nw * 4);
+  s.redd = take(32 * 8);
+  s.redi = take(33 * 8);
+  s.redk = take(32 * 8);
+  s.hist = take(256 * 4);
+  s.pick = take(4 * 8);
+  if (pursuit) {
+    s.S = take((int64_t)K * 4);
+    s.S2 = take((int64_t)K * 4);
+    s.U = take((int64_t)ucap * 4);
+    s.x = take((int64_t)K * ts);
+    s.x2 = take((int64_t)K * ts);
+    s.xU = take((int64_t)ucap * ts);
+    s.r = take((int64_t)ucap * ts);
+    s.d = take((int64_t)ucap * ts);
+    s.q = take((int64_t)ucap * ts);
+    s.b = take((int64_t)ucap * ts);
+    s.Sbits = take(nw * 4);
+    s.Ubits = take(nw * 4);
+    s.Pbits = take(((ucap + 31) / 32) * 4);
+  } else {
+    s.S = s.S2 = s.U = s.x = s.x2 = s.xU = s.r = s.d = s.q = s.b = s.Sbits = s.Ubits = s.Pbits = 0;
+  }
+  s.bytes = o;
+  int64_t nt = L / FFT_E;
+  if (nt < 32) nt = 32;
+  if (nt > 512) nt = 512;
+  s.nthreads = (int)nt;
+  return s;
+}
+
+// per-instance metadata: [sign nw][rowmask nw][prefix nw]
+struct OpMeta {
+  const uint32_t* base;
+  int64_t N, M;
+  int64_t nw;
+  CS_HD const uint32_t* sign(int64_t b) const { return base + b * 3 * nw; }
+  CS_HD const uint32_t* rmask(int64_t b) const { return base + b * 3 * nw + nw; }
+  CS_HD const int32_t* prefix(int64_t b) const {
+    return reinterpret_cast<const int32_t*>(base + b * 3 * nw + 2 * nw);
+  }
+};
+
+template <typename T>
+CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta, int64_t b) {
+  CtaCtx<T> c;
+  c.gtid = threadIdx.x;
+  c.gnthr = blockDim.x;
+  c.lane = threadIdx.x & 31;
+  c.gwarp = threadIdx.x >> 5;
+  c.gnwarps = blockDim.x >> 5;
+  c.N = meta.N;
+  c.M = meta.M;
+  c.L = meta.N / 2;
+  c.Z = reinterpret_cast<C2<T>*>(smem + lay.Z);
+  c.sign = reinterpret_cast<uint32_t*>(smem + lay.sign);
+  c.rowmask = reinterpret_cast<uint32_t*>(smem + lay.rmask);
+  c.prefix = reinterpret_cast<int32_t*>(smem + lay.prefix);
+  c.twL.lo = reinterpret_cast<C2<T>*>(smem + lay.twLlo);
+  c.twL.hi = reinterpret_cast<C2<T>*>(smem + lay.twLhi);
+  c.tw4.lo = reinterpret_cast<C2<T>*>(smem + lay.tw4lo);
+  c.tw4.hi = reinterpret_cast<C2<T>*>(smem + lay.tw4hi);
+  c.redd = reinterpret_cast<double*>(smem + lay.redd);
+  c.redi = reinterpret_cast<int64_t*>(smem + lay.redi);
+  c.redk = reinterpret_cast<typename CtaCtx<T>::Key*>(smem + lay.redk);
+  c.hist = reinterpret_cast<unsigned*>(smem + lay.hist);
+  c.pick = reinterpret_cast<int64_t*>(smem + lay.pick);
+  c.in_supp = nullptr;
+  c.in_ns = 0;
+  c.applies = 0;
+  // twiddles and this instance's metadata into shared memory
+  const int64_t L = c.L, nw = meta.nw;
+  tw_init<T>(const_cast<C2<T>*>(c.twL.lo), const_cast<C2<T>*>(c.twL.hi), L,
+             (int)(L >= 64 ? L / 64 : 1), c.gtid, c.gnthr);
+  tw_init<T>(const_cast<C2<T>*>(c.tw4.lo), const_cast<C2<T>*>(c.tw4.hi), 8 * L,
+             (int)(L / 128 + 1), c.gtid, c.gnthr);
+  const uint32_t* gs = meta.sign(b);
+  const uint32_t* gm = meta.rmask(b);
+  const int32_t* gp = meta.prefix(b);
+  for (int64_t w = c.gtid; w < nw; w += c.gnthr) {
+    c.sign[w] = gs[w];
+    c.rowmask[w] = gm[w];
+    c.prefix[w] = gp[w];
+  }
+  __syncthreads();
+  return c;
+}
+
+// ---------------------------------------------------------------- kernels ---
+template <typename T>
+__global__ void __launch_bounds__(512) k_s_apply(OpMeta meta, SLayout lay, const T* __restrict__ X,
+                                                 T* __restrict__ Y) {
+  extern __shared__ __align__(16) char smem[];
+  const int64_t b = blockIdx.x;
+  CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, b);
+  const int64_t N = c.N;
+  const T* x = X + b * N;
+  T* zb = reinterpret_cast<T*>(c.Z);
+  for (int64_t j = c.gtid; j < N; j += c.gnthr) zb[mk_pos(j, N)] = apply_sign<T>(c.sign, j, x[j]);
+  __syncthreads();
+  fft_cta<T, false>(c.Z, (int)c.L, 1, c.twL);
+  c.template middle<MID_FWD>(Y + b * c.M);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_s_adjoint(OpMeta meta, SLayout lay, const T* __restrict__ Yin,
+                                                   T* __restrict__ X) {
+  extern __shared__ __align__(16) char smem[];
+  const int64_t b = blockIdx.x;
+  CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, b);
+  c.y = Yin + b * c.M;
+  c.RES(nullptr);  // A^T y (x = 0)
+  const int64_t N = c.N;
+  T* x = X + b * N;
+  for (int64_t j = c.gtid; j < N; j += c.gnthr) x[j] = c.c_at(j);
+}
+
+template <typename T> struct SRecArgs {
+  OpMeta meta;
+  SLayout lay;
+  Params P;
+  int ucap;
+  const T* Y;
+  T* vals;
+  int32_t* supp;
+  cs_report* reps;
+  T* c0ws;  // [B][N]
+};
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_s_recover(SRecArgs<T> a) {
+  extern __shared__ __align__(16) char smem[];
+  const int64_t b = blockIdx.x;
+  CtaCtx<T> c = make_cta_ctx<T>(smem, a.lay, a.meta, b);
+  c.y = a.Y + b * c.M;
+  c.c0 = a.c0ws + b * c.N;
+  // non-finite y check
+  int bad = 0;
+  for (int64_t m = c.gtid; m < c.M; m += c.gnthr) bad |= !isfinite((double)c.y[m]);
+  unsigned pre = __syncthreads_or(bad) ? CS_DEV_NONFINITE_Y : 0u;
+  Bufs<T> B;
+  const SLayout& L = a.lay;
+  B.S = reinterpret_cast<int*>(smem + L.S);
+  B.S2 = reinterpret_cast<int*>(smem + L.S2);
+  B.U = reinterpret_cast<int*>(smem + L.U);
+  B.x = reinterpret_cast<T*>(smem + L.x);
+  B.x2 = reinterpret_cast<T*>(smem + L.x2);
+  B.xU = reinterpret_cast<T*>(smem + L.xU);
+  B.r = reinterpret_cast<T*>(smem + L.r);
+  B.d = reinterpret_cast<T*>(smem + L.d);
+  B.q = reinterpret_cast<T*>(smem + L.q);
+  B.b = reinterpret_cast<T*>(smem + L.b);
+  B.Sbits = reinterpret_cast<uint32_t*>(smem + L.Sbits);
+  B.Ubits = reinterpret_cast<uint32_t*>(smem + L.Ubits);
+  B.Pbits = reinterpret_cast<uint32_t*>(smem + L.Pbits);
+  run_pursuit<CtaCtx<T>, T>(c, a.P, B, a.vals + b * a.P.K, a.supp + b * a.P.K, a.reps + b, pre);
+}
+
+}  // namespace cs

@@ -1,0 +1,68 @@
+"""Host-only checks of the C ABI (no GPU needed): the library loads, exports every
+symbol include/cs.h declares, and host-side validation returns the documented codes."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__ as g
+    g.build()
+    import paper_1509_03979_b200 as cs
+    return cs.load_library()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "cs.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(cs_[a-z0-9_]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = declared_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_binding_declares_every_export():
+    import paper_1509_03979_b200 as cs
+    assert sorted(cs.EXPORTS) == declared_functions()
+
+
+def test_status_strings_and_version(lib):
+    assert lib.cs_status_string(0) == b"CS_OK"
+    assert lib.cs_status_string(3) == b"CS_ERR_WORKSPACE"
+    assert b"sm_100a" in lib.cs_version()
+
+
+def test_meta_bytes_formula(lib):
+    # 3 words-arrays of ceil(N/32) uint32 per instance, 256-aligned, + 256 flag tail
+    assert lib.cs_operator_meta_bytes(16384, 4096, 4096) == ((4096 * 3 * 512 * 4 + 255) // 256) * 256 + 256
+    assert lib.cs_operator_meta_bytes(8, 4, 1) == 256 + 256
+
+
+def test_host_validation_codes(lib):
+    import paper_1509_03979_b200 as cs
+    n = ctypes.c_size_t()
+    # N not a power of two / out of range -> UNSUPPORTED
+    assert lib.cs_workspace_bytes(1, 100, 25, 4, 1, 0, None, ctypes.byref(n)) == 2
+    assert lib.cs_workspace_bytes(1, 1 << 26, 1 << 24, 4, 1, 0, None, ctypes.byref(n)) == 2
+    # bad K -> INVALID_ARG
+    assert lib.cs_workspace_bytes(1, 1024, 256, 0, 1, 0, None, ctypes.byref(n)) == 1
+    # null out pointer -> INVALID_ARG
+    h = ctypes.c_void_p()
+    assert lib.cs_operator_create(1024, 256, 1, None, None, None, 0, None, ctypes.byref(h)) == 1
+    assert lib.cs_operator_create(1024, 2048, 1, None, None, None, 0, None, ctypes.byref(h)) == 1
+    # workspace sizes: Tier S = B*N*sizeof(T); Tier L larger than the dense scratch
+    assert lib.cs_workspace_bytes(1, 16384, 4096, 256, 4096, 0, None, ctypes.byref(n)) == 0
+    assert n.value == 4096 * 16384 * 4
+    assert lib.cs_workspace_bytes(1, 1 << 24, 1 << 22, 65536, 1, 0, None, ctypes.byref(n)) == 0
+    assert n.value >= 4 * (1 << 24) * 4
+    assert cs.REPORT_DTYPE.itemsize == 40

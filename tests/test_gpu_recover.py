@@ -1,0 +1,111 @@
+"""GPU parity of cs_recover / cs_recover_batched (OMP, SP, OMPR with the CG-solved
+weighted LS) against the fp64 oracle on the same seeded inputs, through the C ABI.
+
+Bar (BASELINE.json north_star): identical supports and
+||s_gpu - s_oracle|| / ||s_oracle|| <= 1e-4 (fp32 GPU vs fp64 oracle)."""
+import numpy as np
+import pytest
+
+import cs_inputs
+from cs_inputs import CONFIGS
+from gpu_helpers import to_dev, measured, oracle_results, compare
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def cs():
+    import __graft_entry__ as g
+    g.build()
+    import paper_1509_03979_b200 as m
+    return m
+
+
+def _run(cs, cfg, count, dtype="float32", tol=None, b0=0, opts=None):
+    dev = torch.device("cuda:0")
+    probs = cs_inputs.make_batch(cfg, b0=b0, count=count)
+    ys = measured(probs)
+    bits, rows = to_dev(probs, dev)
+    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=count)
+    td = getattr(torch, dtype)
+    if tol is None:
+        tol = 1e-6 if dtype == "float32" else 1e-12
+    Y = torch.from_numpy(ys).to(dev, td)
+    res = cs.cs_recover_batched(A, cfg.alg, Y, cfg.K, tol, opts=opts)
+    torch.cuda.synchronize()
+    return probs, ys, res.support.cpu().numpy(), res.values.cpu().numpy(), res.reports()
+
+
+def test_c1_omp_full_size(cs):
+    cfg = CONFIGS[1]
+    probs, ys, supp, vals, reps = _run(cs, cfg, 1)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals)
+    assert not bad, bad
+    assert reps[0]["outer_iters"] == cfg.K
+    assert reps[0]["termination"] == 0
+    # noiseless: exact recovery of the planted signal as well
+    assert np.array_equal(np.sort(supp[0]), probs[0].support)
+
+
+def test_c4_sp_batched_full_size_sample(cs):
+    cfg = CONFIGS[4]
+    probs, ys, supp, vals, reps = _run(cs, cfg, 48)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals)
+    assert not bad, bad
+    assert all(r["termination"] in (3, 4) for r in reps)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_small_ragged_batch_all_algs(cs, dtype):
+    for alg in ["omp", "sp", "ompr"]:
+        cfg = cs_inputs.Config(60, alg, 512, 128, 12, "gauss", 0.0)
+        probs, ys, supp, vals, reps = _run(cs, cfg, 7, dtype)
+        refs = oracle_results(probs, ys)
+        bad, worst = compare(probs, refs, supp, vals, rtol=1e-4 if dtype == "float32" else 1e-9)
+        assert not bad, (alg, bad)
+
+
+def test_tiny_sizes(cs):
+    for N, M, K, alg in [(8, 4, 1, "omp"), (16, 8, 2, "sp"), (32, 16, 3, "ompr"), (64, 32, 4, "sp")]:
+        cfg = cs_inputs.Config(61, alg, N, M, K, "pm1", 0.0)
+        probs, ys, supp, vals, reps = _run(cs, cfg, 3, "float64")
+        refs = oracle_results(probs, ys)
+        bad, _ = compare(probs, refs, supp, vals, rtol=1e-9)
+        assert not bad, (N, alg, bad)
+
+
+def test_c2_sp_tier_l_scaled_fp64(cs):
+    cfg = CONFIGS[2].scaled(2)          # N = 32768: Tier L (cooperative grid)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 1, "float64", tol=1e-12)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals, rtol=1e-8)
+    assert not bad, bad
+
+
+def test_c3_ompr_tier_l_scaled(cs):
+    cfg = CONFIGS[3].scaled(16)         # N = 65536, K = 512
+    probs, ys, supp, vals, reps = _run(cs, cfg, 1)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals)
+    assert not bad, bad
+    assert np.array_equal(np.sort(supp[0]), probs[0].support)
+
+
+def test_c5_sp_tier_l_scaled_fp64(cs):
+    cfg = CONFIGS[5].scaled(64)         # N = 2^18, K = 1024, compressible + noise
+    probs, ys, supp, vals, reps = _run(cs, cfg, 1, "float64", tol=1e-12)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals, rtol=1e-8)
+    assert not bad, bad
+
+
+def test_deterministic_rerun(cs):
+    cfg = CONFIGS[4].scaled(4, batch=8)
+    a = _run(cs, cfg, 8)
+    b = _run(cs, cfg, 8)
+    assert np.array_equal(a[2], b[2])
+    assert np.array_equal(a[3], b[3])
