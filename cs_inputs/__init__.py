@@ -75,8 +75,6 @@ def unpack_sign_bits(bits: np.ndarray, N: int) -> np.ndarray:
 
 
 def draw_sign_bits(N: int, g: np.random.Generator) -> np.ndarray:
-    if N % 32:
-        raise ValueError("N must be a multiple of 32 for packed sign bits")
     return pack_sign_bits(g.integers(0, 2, N).astype(bool))
 
 
