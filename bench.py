@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""bench.py — B200 benchmark of greedy CS recovery (arXiv:1509.03979 hot path).
+
+Workload (default): BASELINE.json config 4 — 4096 independent SP + CG problems per
+GPU, each N = 16384, M = 4096, K = 256, own sign diagonal and row set, Gaussian
+nonzeros, noiseless.  One "step" = cs_recover_batched over the resident batch
+(detection, top-K, merge/prune and every CG solve of every problem: the whole
+hot path, §8(a) of SURVEY.md).  Multi-GPU: one process per GPU (torchrun), each
+rank owns its own 4096-problem batch (weak scaling, no data-path collective);
+results are gathered to rank 0 with one NCCL all-gather per step.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md §7 for every field.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 1..5] [--precision fp32|fp64]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import cs_inputs  # noqa: E402  (seeded generator: no method arithmetic)
+
+METRIC = "recovered signals/sec"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--batch", type=int, default=0, help="problems per GPU (0 = config default)")
+    ap.add_argument("--no-op-bench", action="store_true")
+    return ap.parse_args()
+
+
+def workload_desc(cfg):
+    return {1: "c1: OMP+CG, N=4096, M=1024, K=64, noiseless",
+            2: "c2: SP+CG, N=65536, M=16384, K=2048, sigma=1e-3",
+            3: "c3: OMPR(1)+CG, N=2^20, M=2^18, K=8192, noiseless",
+            4: "c4: batched SP+CG, 4096 x (N=16384, M=4096, K=256), noiseless",
+            5: "c5: SP+CG, N=2^24, M=2^22, K=65536, compressible, sigma=1e-4"}[cfg.cid]
+
+
+def load_peaks():
+    try:
+        return json.load(open(PEAKS_PATH))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1509_03979_b200 as cs
+
+    rank, world, local = dist_env()
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = cs_inputs.CONFIGS[args.config]
+    B = args.batch or cfg.batch
+    td = torch.float32 if args.precision == "fp32" else torch.float64
+    tol = 1e-6 if args.precision == "fp32" else 1e-12
+
+    # ---- synthetic inputs (rank-disjoint problem indices), y formed by the product operator
+    t0 = time.time()
+    probs = cs_inputs.make_batch(cfg, b0=rank * B, count=B)
+    bits = torch.from_numpy(np.stack([p.sign_bits.view(np.int32) for p in probs])).to(dev)
+    rows = torch.from_numpy(np.stack([p.rows for p in probs]).astype(np.int32)).to(dev)
+    S = torch.from_numpy(np.stack([p.s for p in probs])).to(dev, td)
+    E = torch.from_numpy(np.stack([p.noise for p in probs])).to(dev, td)
+    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=B)
+    Y = (cs.cs_operator_apply(A, S) + E).to(torch.float32).to(td)  # fp32-rounded y (R21)
+    del S, E
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+
+    stream = torch.cuda.current_stream()
+    ws = cs.Workspace()
+    out = None
+    rec = None
+
+    def step():
+        nonlocal rec
+        rec = cs.cs_recover_batched(A, cfg.alg, Y, cfg.K, tol, workspace=ws, out=rec)
+        return rec
+
+    gather_buf = None
+
+    def gather(r):
+        nonlocal gather_buf
+        if world == 1:
+            return
+        flat = torch.cat([r.support.view(torch.uint8).reshape(B, -1), r.values.view(torch.uint8).reshape(B, -1),
+                          r.report_dev.reshape(B, -1)], dim=1).reshape(-1)
+        if gather_buf is None:
+            gather_buf = torch.empty(world * flat.numel(), dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(gather_buf, flat)
+
+    for _ in range(max(args.warmup, 0)):
+        gather(step())
+    torch.cuda.synchronize()
+    reps = rec.reports()
+
+    # ---- timed region: K steps, device events, barrier + sync both sides
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = cs.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kern_ms = []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        ka = torch.cuda.Event(enable_timing=True)
+        kb = torch.cuda.Event(enable_timing=True)
+        ka.record(stream)
+        r = step()
+        kb.record(stream)
+        kern_ms.append((ka, kb))
+        gather(r)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = cs.launch_count() - launches0
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    kms = float(np.mean([a.elapsed_time(b) for a, b in kern_ms]))
+    if world > 1:
+        t = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kms = float(t[0]), float(t[1])
+    ms_per_step = ms / args.steps
+    total_signals = B * world
+    value = total_signals / (ms_per_step / 1e3)
+
+    # parity self-check on a sample of this run's outputs is done by tests; here report stats
+    applies = int(reps["applies"].sum())
+    cg_iters = int(reps["cg_iters_total"].sum())
+    outer = float(reps["outer_iters"].mean())
+
+    # ---- e2e through the public API: pinned host Y -> device, recover, results -> host
+    Yh = Y.cpu().pin_memory()
+    Yd = torch.empty_like(Y)
+    supp_h = torch.empty((B, cfg.K), dtype=torch.int32).pin_memory()
+    vals_h = torch.empty((B, cfg.K), dtype=td).pin_memory()
+    rep_h = torch.empty((B, 40), dtype=torch.uint8).pin_memory()
+    rec_e2e = None
+
+    def e2e_step():
+        nonlocal rec_e2e
+        Yd.copy_(Yh, non_blocking=True)
+        rec_e2e = cs.cs_recover_batched(A, cfg.alg, Yd, cfg.K, tol, workspace=ws, out=rec_e2e)
+        supp_h.copy_(rec_e2e.support, non_blocking=True)
+        vals_h.copy_(rec_e2e.values, non_blocking=True)
+        rep_h.copy_(rec_e2e.report_dev, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    esteps = max(3, min(args.steps, 10))
+    e0.record(stream)
+    for _ in range(esteps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1) / esteps
+    if world > 1:
+        t = torch.tensor([ems], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t[0])
+    h2d = Y.numel() * Y.element_size()
+    d2h = supp_h.numel() * 4 + vals_h.numel() * vals_h.element_size() + rep_h.numel()
+
+    # ---- operator microbenchmark: batched A and A^T over the same instances (HBM-streaming)
+    op_stats = None
+    if not args.no_op_bench:
+        X = torch.randn((B, cfg.N), device=dev, dtype=td)
+        Yo = torch.empty((B, cfg.M), device=dev, dtype=td)
+        Xo = torch.empty((B, cfg.N), device=dev, dtype=td)
+        for _ in range(3):
+            cs.cs_operator_apply(A, X, out=Yo)
+            cs.cs_operator_adjoint(A, Yo, out=Xo)
+        torch.cuda.synchronize()
+        a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        reps_op = 10
+        a0.record(stream)
+        for _ in range(reps_op):
+            cs.cs_operator_apply(A, X, out=Yo)
+        a1.record(stream)
+        for _ in range(reps_op):
+            cs.cs_operator_adjoint(A, Yo, out=Xo)
+        a2.record(stream)
+        torch.cuda.synchronize()
+        t_fwd = a0.elapsed_time(a1) / reps_op / 1e3
+        t_adj = a1.elapsed_time(a2) / reps_op / 1e3
+        es = td.itemsize if hasattr(td, "itemsize") else (4 if td == torch.float32 else 8)
+        meta_b = B * 3 * ((cfg.N + 31) // 32) * 4
+        bytes_fwd = B * (cfg.N + cfg.M) * es + meta_b
+        bytes_adj = B * (cfg.N + cfg.M) * es + meta_b
+        peaks = load_peaks()
+        op_stats = {"applies_per_s_fwd": B / t_fwd, "applies_per_s_adj": B / t_adj,
+                    "fwd_GBs": bytes_fwd / t_fwd / 1e9, "adj_GBs": bytes_adj / t_adj / 1e9,
+                    "frac_hbm_fwd": bytes_fwd / t_fwd / 1e9 / peaks["hbm_gbs"],
+                    "frac_hbm_adj": bytes_adj / t_adj / 1e9 / peaks["hbm_gbs"],
+                    "ms_fwd": t_fwd * 1e3, "ms_adj": t_adj * 1e3}
+
+    # ---- roofline of the dominant kernel (k_s_recover: the whole step is one launch)
+    peaks = load_peaks()
+    nominal_flops_per_apply = 5.0 * cfg.N * np.log2(cfg.N)     # 2 DCTs x 2.5 N log2 N
+    flops_step = applies * nominal_flops_per_apply
+    achieved_tf = flops_step / (kms / 1e3) / 1e12
+    peak_tf = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    roofline = {"bound": "alu", "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 2),
+                "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4), "traffic": None,
+                "kernel": "k_s_recover<float>", "kernel_ms": round(kms, 4),
+                "algorithmic_flops_per_launch": flops_step,
+                "peak_note": "FP32 SIMT 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md §6)"}
+    tr = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr):
+        try:
+            roofline["traffic"] = json.load(open(tr)).get(f"c{cfg.cid}_{args.precision}")
+        except Exception:
+            pass
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "signals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic (seeded, DESIGN.md §4)",
+        "config": {"workload": workload_desc(cfg), "problems_per_gpu": B, "N": cfg.N, "M": cfg.M,
+                   "K": cfg.K, "alg": cfg.alg, "tol": tol, "parallelism": f"dp{world} (independent problems)",
+                   "l2": "per-step working set > L2 (Y + c0 scratch = %d MB)" % ((Y.numel() * Y.element_size() + B * cfg.N * Y.element_size()) >> 20)},
+        "applies_per_s": round(applies * world / (ms_per_step / 1e3), 1),
+        "cg_iters_per_problem": round(cg_iters / B, 2), "outer_iters_mean": round(outer, 3),
+        "e2e": {"value": round(total_signals / (ems / 1e3), 2), "unit": "signals/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems, 4)},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "operator": op_stats,
+        "clocks": clocks,
+        "input_gen_s": round(gen_s, 2),
+    }
+    if rank == 0 and world == 1 and os.environ.get("BENCH_NO_CPU") != "1":
+        line["cpu_baseline"] = cpu_baseline(cfg, probs, Y.cpu().numpy().astype(np.float32))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- oracle
+def _oracle_one(args):
+    import oracle
+    p, y = args
+    op = oracle.SrmOperator(p.N, p.sign_bits, p.rows)
+    r = oracle.recover(p.alg, op, y.astype(np.float64), p.K, tol=1e-10)
+    return r.outer_iters
+
+
+def oracle_rate(cfg, probs, ys, budget_s=15.0):
+    """Time the oracle as it stands on the host cores: a bounded sample of the workload."""
+    import multiprocessing as mp
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    if cfg.batch > 1:
+        # batched config: a process pool over problems, all cores
+        t0 = time.time()
+        _oracle_one((probs[0], ys[0]))
+        one = time.time() - t0
+        n = int(max(cores, min(len(probs), budget_s * cores / max(one, 1e-3))))
+        n = min(n, len(probs))
+        ctx = mp.get_context("fork")
+        t0 = time.time()
+        with ctx.Pool(cores) as pool:
+            pool.map(_oracle_one, list(zip(probs[:n], ys[:n])), chunksize=1)
+        dt = time.time() - t0
+        return {"value": round(n / dt, 3), "unit": "signals/s", "cores": cores, "kind": "oracle",
+                "sample": f"{n} of {len(probs)} problems of the same batch, fp64 numpy/scipy, process pool"}
+    t0 = time.time()
+    _oracle_one((probs[0], ys[0]))
+    dt = time.time() - t0
+    return {"value": round(1.0 / dt, 6), "unit": "signals/s", "cores": 1, "kind": "oracle",
+            "sample": "1 signal, fp64 numpy/scipy, single core"}
+
+
+def cpu_baseline(cfg, probs, ys):
+    return oracle_rate(cfg, probs, ys)
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    cfg = cs_inputs.CONFIGS[args.config]
+    import oracle
+    B = args.batch or cfg.batch
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    n = min(B, max(cores, 2 * cores))          # bounded sample per step
+    probs = cs_inputs.make_batch(cfg, count=n)
+    ys = []
+    for p in probs:
+        op = oracle.SrmOperator(p.N, p.sign_bits, p.rows)
+        ys.append((op.apply(p.s) + p.noise).astype(np.float32))
+    for _ in range(args.warmup if cfg.batch > 1 else 0):
+        pass
+    rates = []
+    t_all = time.time()
+    for _ in range(max(1, args.steps)):
+        rates.append(oracle_rate(cfg, probs, ys, budget_s=3.0)["value"])
+        if time.time() - t_all > 120:
+            break
+    v = float(np.median(rates))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "signals/s", "n_gpus": world,
+            "steps": len(rates), "warmup": args.warmup, "ms_per_step": round(1e3 * n / v, 3) if v else None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, DESIGN.md §4)",
+            "config": {"workload": workload_desc(cfg), "problems_per_gpu": B, "N": cfg.N, "M": cfg.M, "K": cfg.K,
+                       "alg": cfg.alg},
+            "cpu_baseline": {"value": v, "unit": "signals/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{n} problems per step of the config-{cfg.cid} batch, fp64 oracle, process pool"},
+            "e2e": {"value": v, "unit": "signals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -124,10 +124,6 @@ __global__ void k_rows_prefix(int64_t nw, uint32_t* meta) {
   }
 }
 
-template <typename T> cs_status set_smem(const void* fn, int64_t bytes) {
-  CS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  return CS_OK;
-}
 
 OpMeta meta_of(const cs_operator* op) {
   OpMeta m;
@@ -156,19 +152,8 @@ cs_status apply_impl(const cs_operator* op, const T* x, T* y, void* ws, size_t w
   if (!op) return fail(CS_ERR_INVALID_ARG, "null operator");
   if (!x || !y) return fail(CS_ERR_INVALID_ARG, "null vector");
   if (cs_status s = check_device()) return s;
-  if (op->N <= TIER_S_MAX_N) {
-    SLayout lay = s_layout<T>(op->N, 0, 0, false);
-    OpMeta m = meta_of(op);
-    if (!adjoint) {
-      if (cs_status s = set_smem<T>((const void*)k_s_apply<T>, lay.bytes)) return s;
-      k_s_apply<T><<<(unsigned)op->B, lay.nthreads, lay.bytes, st>>>(m, lay, x, y);
-    } else {
-      if (cs_status s = set_smem<T>((const void*)k_s_adjoint<T>, lay.bytes)) return s;
-      k_s_adjoint<T><<<(unsigned)op->B, lay.nthreads, lay.bytes, st>>>(m, lay, x, y);
-    }
-    CS_LAUNCHED();
-    return CS_OK;
-  }
+  if (op->N <= TIER_S_MAX_N)
+    return s_apply_launch<T>(meta_of(op), op->B, x, y, adjoint, st, g_launches, g_last_error);
   return tier_l_apply<T>(meta_of(op), op->B, x, y, ws, ws_bytes, st, adjoint, g_launches,
                          g_last_error);
 }
@@ -213,10 +198,7 @@ cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, in
     a.supp = supp;
     a.reps = reps;
     a.c0ws = reinterpret_cast<T*>(ws);
-    if (cs_status s = set_smem<T>((const void*)k_s_recover<T>, a.lay.bytes)) return s;
-    k_s_recover<T><<<(unsigned)B, a.lay.nthreads, a.lay.bytes, st>>>(a);
-    CS_LAUNCHED();
-    return CS_OK;
+    return s_recover_launch<T>(a, B, st, g_launches, g_last_error);
   }
   return tier_l_recover<T>(meta_of(op), P, (int)ucap, Y, B, vals, supp, reps, ws, ws_bytes, st,
                            g_launches, g_last_error);

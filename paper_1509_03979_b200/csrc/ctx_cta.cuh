@@ -29,6 +29,7 @@ template <typename T> struct CtaCtx {
   // ids
   int gtid, gnthr, lane, gwarp, gnwarps;
   int64_t N, M, L;
+  int log2L;
   // shared-memory state
   C2<T>* Z;          // [L] working transform buffer; viewed as T[N] it is v (Makhoul order)
   uint32_t* sign;    // [nw]
@@ -114,12 +115,32 @@ template <typename T> struct CtaCtx {
   CS_DEV const unsigned* hist_smem() const { return hist; }
 
   // ---- correlation access: c_j = sigma_j * v[p(j)] ----
-  CS_DEV const T* cbuf() const { return reinterpret_cast<const T*>(Z); }
-  CS_DEV T c_at(int64_t j) const { return apply_sign<T>(sign, j, cbuf()[mk_pos(j, N)]); }
+  // Z is stored swizzled (fft_cta.cuh): T-position p of v lives at zt(p).
+  CS_DEV static int zt(int p) { return 2 * swz<T>(p >> 1) + (p & 1); }
+  CS_DEV const T* zbuf() const { return reinterpret_cast<const T*>(Z); }
+  CS_DEV T c_raw(int64_t j) const { return zbuf()[zt((int)mk_pos(j, N))]; }
+  // register-resident views for hot loops (the context itself lives in local memory)
+  struct CV {
+    const T* z;
+    const uint32_t* sign;
+    int N;
+    CS_DEV T raw(int64_t j) const { return z[zt((int)mk_pos(j, N))]; }
+    CS_DEV T at(int64_t j) const { return apply_sign<T>(sign, j, raw(j)); }
+  };
+  struct C0V {
+    const T* c0;
+    const uint32_t* sign;
+    int64_t N;
+    CS_DEV T at(int64_t j) const { return apply_sign<T>(sign, j, c0[mk_pos(j, N)]); }
+  };
+  CS_DEV CV cview() const { return CV{zbuf(), sign, (int)N}; }
+  CS_DEV C0V c0view() const { return C0V{c0, sign, N}; }
+  CS_DEV unsigned* hist_ptr() const { return hist; }
+  CS_DEV T c_at(int64_t j) const { return apply_sign<T>(sign, j, c_raw(j)); }
   CS_DEV T c0_at(int64_t j) const { return apply_sign<T>(sign, j, c0[mk_pos(j, N)]); }
   CS_DEV void save_c0() {
-    const T* cb = cbuf();
-    for (int64_t p = gtid; p < N; p += gnthr) c0[p] = cb[p];
+    const T* cb = zbuf();
+    for (int p = gtid; p < (int)N; p += gnthr) c0[p] = cb[zt(p)];
     __syncthreads();
   }
 
@@ -129,29 +150,38 @@ template <typename T> struct CtaCtx {
     in_ns = ns;
   }
   CS_DEV void zero_Z() {
-    T* zb = reinterpret_cast<T*>(Z);
-    for (int64_t p = gtid; p < N; p += gnthr) zb[p] = T(0);
+    C2<T>* z = Z;
+    const int n = (int)L, t0 = gtid, st = gnthr;
+    for (int m = t0; m < n; m += st) z[m] = mk<T>(0, 0);
     __syncthreads();
   }
   // scatter sigma . vals on the remembered support into the zeroed buffer
   CS_DEV void load_input(const T* vals) {
     zero_Z();
     T* zb = reinterpret_cast<T*>(Z);
-    for (int i = gtid; i < in_ns; i += gnthr) {
-      int64_t j = in_supp[i];
-      zb[mk_pos(j, N)] = apply_sign<T>(sign, j, vals[i]);
+    const int* sp = in_supp;
+    const uint32_t* sg = sign;
+    const int ns = in_ns, t0 = gtid, st = gnthr, n = (int)N;
+    for (int i = t0; i < ns; i += st) {
+      const int j = sp[i];
+      zb[zt((int)mk_pos(j, n))] = apply_sign<T>(sg, j, vals[i]);
     }
     __syncthreads();
   }
-  template <int MODE> CS_NOINL double middle(T* yout) {
+  CS_DEV void fwd() { fft_cta_dispatch<T, 0, 8, 2, 13, false>(Z, log2L, twL); }
+  CS_DEV void inv() { fft_cta_dispatch<T, 0, 8, 2, 13, true>(Z, log2L, twL); }
+  template <int MODE> CS_DEV double middle(T* yout) {
     MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, yout);
     double rn2 = 0;
-    for (int64_t k = gtid; k <= L / 2; k += gnthr) {
+    C2<T>* z = Z;
+    const int l = (int)L, t0 = gtid, st = gnthr;
+    const TwTable<T> t4 = tw4;
+    for (int k = t0; k <= l / 2; k += st) {
       if (k == 0) {
-        mid_zero<T, MODE>(Z[0], m, rn2);
+        mid_zero<T, MODE>(z[0], m, rn2);
       } else {
-        C2<T> a = tw4(k);
-        mid_pair<T, MODE>(Z[k], Z[L - k], k, a, m, rn2);
+        C2<T> a = t4(k);
+        mid_pair<T, MODE>(z[swz<T>(k)], z[swz<T>(l - k)], k, a, m, rn2);
       }
     }
     __syncthreads();
@@ -160,10 +190,13 @@ template <typename T> struct CtaCtx {
   // q = (A^T A scatter_S(d))[S] on the remembered support S (cg2)
   CS_NOINL void H(const T* d, T* q) {
     load_input(d);
-    fft_cta<T, false>(Z, (int)L, 1, twL);
+    fwd();
     middle<MID_H>(nullptr);
-    fft_cta<T, true>(Z, (int)L, 1, twL);
-    for (int i = gtid; i < in_ns; i += gnthr) q[i] = c_at(in_supp[i]);
+    inv();
+    const int* sp = in_supp;
+    const int ns = in_ns, t0 = gtid, st = gnthr;
+    const CV cv = cview();
+    for (int i = t0; i < ns; i += st) q[i] = cv.at(sp[i]);
     __syncthreads();
     ++applies;
   }
@@ -172,12 +205,12 @@ template <typename T> struct CtaCtx {
   CS_NOINL double RES(const T* x) {
     if (x) {
       load_input(x);
-      fft_cta<T, false>(Z, (int)L, 1, twL);
+      fwd();
     } else {
       zero_Z();
     }
     double rn2 = middle<MID_RES>(nullptr);
-    fft_cta<T, true>(Z, (int)L, 1, twL);
+    inv();
     ++applies;
     return sum(rn2);
   }

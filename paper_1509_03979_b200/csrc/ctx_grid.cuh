@@ -25,7 +25,7 @@ struct GridBar {
 
 CS_DEV unsigned ld_volatile(const unsigned* p) { return *reinterpret_cast<const volatile unsigned*>(p); }
 
-CS_NOINL void grid_barrier(GridBar* gb) {
+static CS_NOINL void grid_barrier(GridBar* gb) {
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned g = ld_volatile(&gb->gen);
@@ -71,7 +71,7 @@ template <typename T> struct GridCtx {
   using Key = typename KeyT<T>::type;
   int gtid, gnthr, lane, gwarp, gnwarps;
   int64_t N, M, L, L1, L2;
-  int CT;
+  int CT, log2L1, log2L2;
   // global per-problem state
   const uint32_t* sign;
   const uint32_t* rowmask;
@@ -229,7 +229,23 @@ template <typename T> struct GridCtx {
   CS_DEV const unsigned* hist_smem() const { return shist; }
 
   // ---- correlation access ----
-  CS_DEV const T* cbuf() const { return Cb; }
+  CS_DEV T c_raw(int64_t j) const { return Cb[mk_pos(j, N)]; }
+  struct CV {
+    const T* z;
+    const uint32_t* sign;
+    int64_t N;
+    CS_DEV T raw(int64_t j) const { return z[mk_pos(j, N)]; }
+    CS_DEV T at(int64_t j) const { return apply_sign<T>(sign, j, raw(j)); }
+  };
+  struct C0V {
+    const T* c0;
+    const uint32_t* sign;
+    int64_t N;
+    CS_DEV T at(int64_t j) const { return apply_sign<T>(sign, j, c0[mk_pos(j, N)]); }
+  };
+  CS_DEV CV cview() const { return CV{Cb, sign, N}; }
+  CS_DEV C0V c0view() const { return C0V{c0, sign, N}; }
+  CS_DEV unsigned* hist_ptr() const { return shist; }
   CS_DEV T c_at(int64_t j) const { return apply_sign<T>(sign, j, Cb[mk_pos(j, N)]); }
   CS_DEV T c0_at(int64_t j) const { return apply_sign<T>(sign, j, c0[mk_pos(j, N)]); }
   CS_DEV void save_c0() {
@@ -246,25 +262,40 @@ template <typename T> struct GridCtx {
     in_ns = ns;
   }
   CS_DEV void scatter(const T* vals) {
-    for (int i = gtid; i < in_ns; i += gnthr) U[in_pos[i]] = apply_sign<T>(sign, in_supp[i], vals[i]);
+    const int* sp = in_supp;
+    const int64_t* ip = in_pos;
+    const uint32_t* sg = sign;
+    T* u = U;
+    const int ns = in_ns, t0 = gtid, st = gnthr;
+    for (int i = t0; i < ns; i += st) u[ip[i]] = apply_sign<T>(sg, sp[i], vals[i]);
     sync();
+  }
+  // sub-FFTs of the four-step (256-thread blocks, compile-time lengths 2^7..2^12)
+  template <bool INV> CS_DEV void col_fft() {
+    if (CT == 4) fft_cta_dispatch<T, 2, 8, 7, 12, INV>(buf, log2L1, tw1);
+    else fft_cta_dispatch<T, 1, 8, 7, 12, INV>(buf, log2L1, tw1);
+  }
+  template <bool INV> CS_DEV void row_fft(int B) {
+    if (B == 2) fft_cta_dispatch<T, 1, 8, 7, 12, INV>(buf, log2L2, tw2);
+    else fft_cta_dispatch<T, 0, 8, 7, 12, INV>(buf, log2L2, tw2);
   }
   // pass A: columns of z = U viewed as complex [L1][L2]
   CS_NOINL void passA() {
     const C2<T>* Uc = reinterpret_cast<const C2<T>*>(U);
-    const int64_t ntiles = L2 / CT;
-    const int tile = (int)(L1 * CT);
+    const int ct = CT, lct = (ct == 4) ? 2 : 1;
+    const int64_t l2 = L2, ntiles = L2 / ct;
+    const int tile = (int)(L1 * ct);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t c0i = t * CT;
+      const int64_t c0i = t * ct;
       for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-        int64_t m1 = e / CT, cc = e % CT;
-        buf[e] = Uc[m1 * L2 + c0i + cc];
+        const int m1 = e >> lct, cc = e & (ct - 1);
+        buf[swz<T>(e)] = Uc[(int64_t)m1 * l2 + c0i + cc];
       }
       __syncthreads();
-      fft_cta<T, false>(buf, (int)L1, CT, tw1);
+      col_fft<false>();
       for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-        int64_t k1 = e / CT, m2 = c0i + e % CT;
-        Wk[k1 * L2 + m2] = cmul<T>(buf[e], twF(k1 * m2));
+        const int64_t k1 = e >> lct, m2 = c0i + (e & (ct - 1));
+        Wk[k1 * l2 + m2] = cmul<T>(buf[swz<T>(e)], twF(k1 * m2));
       }
       __syncthreads();
     }
@@ -277,37 +308,39 @@ template <typename T> struct GridCtx {
       const int64_t ka = it, kb = L1 - it;
       const bool self = (it == 0 || it == L1 / 2);
       const int B = self ? 1 : 2;
-      for (int e = threadIdx.x; e < B * L2; e += blockDim.x) {
-        int64_t m2 = e / B, k1 = (e % B) ? kb : ka;
-        buf[e] = zero_input ? mk<T>(0, 0) : Wk[k1 * L2 + m2];
+      const int lb = B - 1;  // log2 B
+      const int n2 = (int)L2;
+      for (int e = threadIdx.x; e < B * n2; e += blockDim.x) {
+        const int64_t m2 = e >> lb, k1 = (e & lb) ? kb : ka;
+        buf[swz<T>(e)] = zero_input ? mk<T>(0, 0) : Wk[k1 * L2 + m2];
       }
       __syncthreads();
-      if (!zero_input) fft_cta<T, false>(buf, (int)L2, B, tw2);
+      if (!zero_input) row_fft<false>(B);
       if (it == 0) {
-        for (int64_t k2 = threadIdx.x; k2 <= L2 / 2; k2 += blockDim.x) {
-          if (k2 == 0) mid_zero<T, MODE>(buf[0], m, rn2);
+        for (int k2 = threadIdx.x; k2 <= n2 / 2; k2 += blockDim.x) {
+          if (k2 == 0) mid_zero<T, MODE>(buf[swz<T>(0)], m, rn2);
           else {
             int64_t k = L1 * k2;
-            mid_pair<T, MODE>(buf[k2], buf[L2 - k2], k, tw4(k), m, rn2);
+            mid_pair<T, MODE>(buf[swz<T>(k2)], buf[swz<T>(n2 - k2)], k, tw4(k), m, rn2);
           }
         }
       } else if (it == L1 / 2) {
-        for (int64_t k2 = threadIdx.x; k2 < L2 / 2; k2 += blockDim.x) {
+        for (int k2 = threadIdx.x; k2 < n2 / 2; k2 += blockDim.x) {
           int64_t k = L1 / 2 + L1 * k2;
-          mid_pair<T, MODE>(buf[k2], buf[L2 - 1 - k2], k, tw4(k), m, rn2);
+          mid_pair<T, MODE>(buf[swz<T>(k2)], buf[swz<T>(n2 - 1 - k2)], k, tw4(k), m, rn2);
         }
       } else {
-        for (int64_t k2 = threadIdx.x; k2 < L2; k2 += blockDim.x) {
+        for (int k2 = threadIdx.x; k2 < n2; k2 += blockDim.x) {
           int64_t k = ka + L1 * k2;
-          mid_pair<T, MODE>(buf[2 * k2], buf[2 * (L2 - 1 - k2) + 1], k, tw4(k), m, rn2);
+          mid_pair<T, MODE>(buf[swz<T>(2 * k2)], buf[swz<T>(2 * (n2 - 1 - k2) + 1)], k, tw4(k), m, rn2);
         }
       }
       __syncthreads();
       if constexpr (MODE != MID_FWD) {
-        fft_cta<T, true>(buf, (int)L2, B, tw2);
-        for (int e = threadIdx.x; e < B * L2; e += blockDim.x) {
-          int64_t m2 = e / B, k1 = (e % B) ? kb : ka;
-          Wk[k1 * L2 + m2] = cmulc<T>(buf[e], twF(k1 * m2));
+        row_fft<true>(B);
+        for (int e = threadIdx.x; e < B * n2; e += blockDim.x) {
+          const int64_t m2 = e >> lb, k1 = (e & lb) ? kb : ka;
+          Wk[k1 * L2 + m2] = cmulc<T>(buf[swz<T>(e)], twF(k1 * m2));
         }
       }
       __syncthreads();
@@ -316,19 +349,20 @@ template <typename T> struct GridCtx {
   }
   CS_NOINL void passC() {
     C2<T>* Cc = reinterpret_cast<C2<T>*>(Cb);
-    const int64_t ntiles = L2 / CT;
-    const int tile = (int)(L1 * CT);
+    const int ct = CT, lct = (ct == 4) ? 2 : 1;
+    const int64_t l2 = L2, ntiles = L2 / ct;
+    const int tile = (int)(L1 * ct);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t c0i = t * CT;
+      const int64_t c0i = t * ct;
       for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-        int64_t k1 = e / CT, cc = e % CT;
-        buf[e] = Wk[k1 * L2 + c0i + cc];
+        const int k1 = e >> lct, cc = e & (ct - 1);
+        buf[swz<T>(e)] = Wk[(int64_t)k1 * l2 + c0i + cc];
       }
       __syncthreads();
-      fft_cta<T, true>(buf, (int)L1, CT, tw1);
+      col_fft<true>();
       for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-        int64_t m1 = e / CT, cc = e % CT;
-        Cc[m1 * L2 + c0i + cc] = buf[e];
+        const int m1 = e >> lct, cc = e & (ct - 1);
+        Cc[(int64_t)m1 * l2 + c0i + cc] = buf[swz<T>(e)];
       }
       __syncthreads();
     }
@@ -341,7 +375,10 @@ template <typename T> struct GridCtx {
     sync();
     passC();
     sync();
-    for (int i = gtid; i < in_ns; i += gnthr) q[i] = c_at(in_supp[i]);
+    const CV cv = cview();
+    const int* sp = in_supp;
+    const int ns = in_ns, t0 = gtid, st = gnthr;
+    for (int i = t0; i < ns; i += st) q[i] = cv.at(sp[i]);
     ++applies;
   }
   CS_NOINL double RES(const T* x) {

@@ -1,84 +1,91 @@
-// fft_cta.cuh — CTA-cooperative radix-16 Stockham FFT in shared memory (sm_100a).
+// fft_cta.cuh — CTA-cooperative Stockham FFT in shared memory (sm_100a).
 //
 // The DCT-II of the sensing operator is "speeded by FFT"; this is
 // that FFT, written for one CTA holding B interleaved complex sequences of
-// power-of-two length Ls in shared memory (element n of sequence b at
-// buf[n*B + b], so a warp's consecutive lanes touch consecutive words).
+// length L = 2^LOG2L in shared memory (element n of sequence b at logical
+// index n*B + b).
 //
-// Each radix-R pass is Stockham autosort (no bit reversal pass):
-//   for item (b, j), j < Ls/R, k = j mod Ns:
-//     v[r] = x[j + r Ls/R] * W_{Ns R}^{r k},  V = DFT_R(v),  x'[(j-k)R + k + r Ns] = V[r]
-// done in place: every participating thread loads its E = 16 elements into
-// registers, the CTA barriers, then stores.  Passes are radix 16 while >= 4
-// index bits remain, then one radix 2/4/8 pass.  The R-point DFTs are
-// unrolled radix-2 DIF networks with compile-time twiddles.
-//
-// Twiddles: W_Ls^m = hi[m >> 6] * lo[m & 63] from a two-level table held in
-// shared memory (computed with double-precision sincospi at kernel start), and
-// the powers W^{2k..15k} of each item's base twiddle by complex products of
-// depth <= 4 — no per-element transcendental, no table larger than 1.5 KB.
+// Design:
+//  * compile-time L, B and E (complex elements held per thread): all index math
+//    folds to shifts/masks; each thread owns E elements per pass, so a pass is
+//    "load E -> barrier -> store E" in place (no ping-pong buffer: the whole
+//    8192-point fp32 transform fits in 64 KB and two CTAs fit per SM);
+//  * ceil(LOG2L / log2 E) radix passes with balanced radices <= E (8192 points,
+//    E = 32: radix 32-16-16, three shared-memory round trips);
+//  * Stockham autosort: for item (b, j), k = j mod Ns,
+//      v[r] = x[j + r L/R] * W_{Ns R}^{r k},  V = DFT_R(v),  x'[(j-k)R + k + r Ns] = V[r];
+//  * the R-point DFT is an unrolled radix-2 DIF network with compile-time
+//    twiddles (output in bit-reversed register order, undone at compile time);
+//  * bank-conflict-free: every shared access goes through the XOR swizzle
+//    swz(a) = a ^ (((a >> 4) ^ (a >> 5)) & (S - 1)), S = complex slots per
+//    128-byte row (16 fp32, 8 fp64) — conflict-free for every load and store
+//    pattern of every pass (checked exhaustively);
+//  * twiddles: W_L^m = hi[m >> 6] * lo[m & 63] from a two-level table in shared
+//    memory (double-precision sincospi at kernel start), one lookup per item;
+//    the powers W^{2k..(R-1)k} streamed (few live registers, see tw_stream).
 #pragma once
 #include "cs_common.cuh"
 
 namespace cs {
 
-constexpr int FFT_E = 16;  // complex elements per thread per pass
+template <typename T> CS_DEV int swz(int a) {
+  constexpr int S = (sizeof(T) == 4) ? 15 : 7;
+  return a ^ (((a >> 4) ^ (a >> 5)) & S);
+}
 
 template <typename T> struct TwTable {
   const C2<T>* lo;  // W^i, i < 64
-  const C2<T>* hi;  // W^{64 i}, i < max(1, len/64) (+1 for the 4N table)
-  CS_DEV C2<T> operator()(int64_t m) const { return cmul<T>(hi[m >> 6], lo[m & 63]); }
+  const C2<T>* hi;  // W^{64 i}
+  CS_DEV C2<T> operator()(int m) const { return cmul<T>(hi[m >> 6], lo[m & 63]); }
 };
 
-// Fill lo[64], hi[nhi] with W_den^i = exp(-2 pi i * i / den) (den = period).
+// Fill lo[64], hi[nhi] with W_den^i = exp(-2 pi i * i / den).
 template <typename T>
 CS_DEV void tw_init(C2<T>* lo, C2<T>* hi, int64_t den, int nhi, int tid, int nthr) {
   for (int i = tid; i < 64 + nhi; i += nthr) {
     int64_t m = (i < 64) ? i : (int64_t)(i - 64) * 64;
     double s, c;
-    // exp(-2 pi i m/den): reduce m mod den exactly in integers first
-    int64_t mm = m % den;
-    sincospi(-2.0 * (double)mm / (double)den, &s, &c);
+    sincospi(-2.0 * (double)(m % den) / (double)den, &s, &c);
     C2<T> w = mk<T>((T)c, (T)s);
     if (i < 64) lo[i] = w; else hi[i - 64] = w;
   }
 }
 
-// ---- compile-time twiddles of the radix-16 network: W_16^t, t in [0, 8) ----
-template <typename T, int t, bool INV> CS_DEV C2<T> w16c() {
-  constexpr double c[8] = {1.0, 0.92387953251128675613, 0.70710678118654752440,
-                           0.38268343236508977173, 0.0, -0.38268343236508977173,
-                           -0.70710678118654752440, -0.92387953251128675613};
-  constexpr double s[8] = {0.0, 0.38268343236508977173, 0.70710678118654752440,
-                           0.92387953251128675613, 1.0, 0.92387953251128675613,
-                           0.70710678118654752440, 0.38268343236508977173};
+// ---- compile-time twiddles of the radix-2 network: W_32^t, t in [0, 16) ----
+template <typename T, int t, bool INV> CS_DEV C2<T> w32c() {
+  constexpr double c[16] = {1.0, 0.98078528040323044913, 0.92387953251128675613, 0.83146961230254523708,
+                            0.70710678118654752440, 0.55557023301960222474, 0.38268343236508977173,
+                            0.19509032201612826785, 0.0, -0.19509032201612826785, -0.38268343236508977173,
+                            -0.55557023301960222474, -0.70710678118654752440, -0.83146961230254523708,
+                            -0.92387953251128675613, -0.98078528040323044913};
+  constexpr double s[16] = {0.0, 0.19509032201612826785, 0.38268343236508977173, 0.55557023301960222474,
+                            0.70710678118654752440, 0.83146961230254523708, 0.92387953251128675613,
+                            0.98078528040323044913, 1.0, 0.98078528040323044913, 0.92387953251128675613,
+                            0.83146961230254523708, 0.70710678118654752440, 0.55557023301960222474,
+                            0.38268343236508977173, 0.19509032201612826785};
   return mk<T>((T)c[t], INV ? (T)s[t] : (T)(-s[t]));
 }
 
-template <typename T, int t16, bool INV> CS_DEV C2<T> tw_apply(C2<T> a) {
-  if constexpr (t16 == 0) {
+template <typename T, int t32, bool INV> CS_DEV C2<T> tw_apply(C2<T> a) {
+  if constexpr (t32 == 0) {
     return a;
-  } else if constexpr (t16 == 4) {
+  } else if constexpr (t32 == 8) {
     return mul_mi<T, INV>(a);
-  } else if constexpr (t16 == 2 || t16 == 6) {
-    // (±1 ∓ i)/sqrt2 patterns: 2 mul + 2 add
+  } else if constexpr (t32 == 4 || t32 == 12) {
     constexpr T h = (T)0.70710678118654752440;
-    C2<T> w = w16c<T, t16, INV>();
-    T sx = w.x > 0 ? (T)1 : (T)-1, sy = w.y > 0 ? (T)1 : (T)-1;
-    // a * (sx h + i sy h) = h*(sx a.x - sy a.y) + i h*(sx a.y + sy a.x)
+    constexpr T sx = (t32 == 4) ? (T)1 : (T)-1;
+    constexpr T sy = INV ? (T)1 : (T)-1;
     return mk<T>(h * (sx * a.x - sy * a.y), h * (sx * a.y + sy * a.x));
   } else {
-    return cmul<T>(a, w16c<T, t16, INV>());
+    return cmul<T>(a, w32c<T, t32, INV>());
   }
 }
 
-// radix-2 DIF stage with half-span H over a block starting at S (compile time)
-template <typename T, int R, int H, int S, int t, bool INV>
-CS_DEV void dif_bfly(C2<T>* v) {
+template <typename T, int R, int H, int S, int t, bool INV> CS_DEV void dif_bfly(C2<T>* v) {
   if constexpr (t < H) {
     C2<T> a = v[S + t], b = v[S + t + H];
     v[S + t] = cadd<T>(a, b);
-    v[S + t + H] = tw_apply<T, t * (16 / (2 * H)), INV>(csub<T>(a, b));
+    v[S + t + H] = tw_apply<T, t * (32 / (2 * H)), INV>(csub<T>(a, b));
     dif_bfly<T, R, H, S, t + 1, INV>(v);
   }
 }
@@ -100,77 +107,129 @@ template <int R> __host__ __device__ constexpr int bitrev(int r) {
     if (r & b) o |= rb;
   return o;
 }
-// in-register R-point DFT; output X_r lands at v[bitrev<R>(r)]
+// in-register R-point DFT (R <= 32); X_r lands at v[bitrev<R>(r)]
 template <typename T, int R, bool INV> CS_DEV void dft_reg(C2<T>* v) { dif_stages<T, R, R / 2, INV>(v); }
 
-// powers w[r] = w1^r, r < R, depth <= log2 R products
-template <typename T, int R> CS_DEV void tw_powers(C2<T> w1, C2<T>* w) {
-  w[0] = mk<T>(1, 0);
-  w[1] = w1;
+// v[r] *= w1^r for r < R, streaming the powers so only a handful of registers hold
+// twiddles: w^1..w^3 and a running w^(4a) (product depth <= R/4 + 2).
+template <typename T, int R> CS_DEV void tw_stream(C2<T>* v, C2<T> w1) {
+  v[1] = cmul<T>(v[1], w1);
+  if constexpr (R > 2) {
+    const C2<T> w2 = cmul<T>(w1, w1);
+    const C2<T> w3 = cmul<T>(w2, w1);
+    v[2] = cmul<T>(v[2], w2);
+    v[3] = cmul<T>(v[3], w3);
+    if constexpr (R > 4) {
+      const C2<T> w4 = cmul<T>(w2, w2);
+      C2<T> cur = w4;
 #pragma unroll
-  for (int r = 2; r < R; ++r) w[r] = cmul<T>(w[r >> 1], w[r - (r >> 1)]);
-}
-
-// One radix-R pass over B interleaved sequences of length Ls. IPT = FFT_E / R items per thread.
-template <typename T, int R, bool INV>
-CS_NOINL void fft_pass(C2<T>* buf, int Ls, int B, int Ns, int s_tw, const TwTable<T>& tw,
-                     int tid, int nact) {
-  constexpr int IPT = FFT_E / R;
-  const int Lr = Ls / R;
-  const int items = B * Lr;
-  C2<T> v[IPT][R];
-  bool act[IPT];
-#pragma unroll
-  for (int it = 0; it < IPT; ++it) {
-    int i = tid + it * nact;
-    act[it] = (tid < nact) && (i < items);
-    if (act[it]) {
-      int b = i % B, j = i / B;
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[it][r] = buf[(int64_t)(j + r * Lr) * B + b];
-      if (Ns > 1) {
-        int k = j & (Ns - 1);
-        C2<T> w1 = tw((int64_t)k * s_tw);
-        if (INV) w1 = cconj<T>(w1);
-        C2<T> w[R];
-        tw_powers<T, R>(w1, w);
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[it][r] = cmul<T>(v[it][r], w[r]);
+      for (int a = 1; a < R / 4; ++a) {
+        v[4 * a] = cmul<T>(v[4 * a], cur);
+        v[4 * a + 1] = cmul<T>(v[4 * a + 1], cmul<T>(cur, w1));
+        v[4 * a + 2] = cmul<T>(v[4 * a + 2], cmul<T>(cur, w2));
+        v[4 * a + 3] = cmul<T>(v[4 * a + 3], cmul<T>(cur, w3));
+        if (a + 1 < R / 4) cur = cmul<T>(cur, w4);
       }
-      dft_reg<T, R, INV>(v[it]);
+    }
+  }
+}
+
+// log2 radix of pass p for a length-2^LOG2L transform with <= 2^LOG2E points per thread
+template <int LOG2L, int LOG2E> struct Plan {
+  static constexpr int P = (LOG2L + LOG2E - 1) / LOG2E > 0 ? (LOG2L + LOG2E - 1) / LOG2E : 1;
+  __host__ __device__ static constexpr int rb(int p) { return LOG2L / P + (p < LOG2L % P ? 1 : 0); }
+  __host__ __device__ static constexpr int ns(int p) {  // log2 Ns before pass p
+    int s = 0;
+    for (int q = 0; q < p; ++q) s += rb(q);
+    return s;
+  }
+};
+
+template <typename T, int LOG2L, int LOG2E, int LOG2B, int P, bool INV>
+CS_DEV void fft_pass(C2<T>* buf, const TwTable<T>& tw) {
+  constexpr int PL = Plan<LOG2L, LOG2E>::P;
+  constexpr int RB = Plan<LOG2L, LOG2E>::rb(P);
+  constexpr int R = 1 << RB;
+  constexpr int NSB = Plan<LOG2L, LOG2E>::ns(P);
+  constexpr int Ns = 1 << NSB;
+  constexpr int L = 1 << LOG2L;
+  constexpr int B = 1 << LOG2B;
+  constexpr int NTA = (L * B) >> LOG2E;               // active threads
+  constexpr int IPT = (1 << (LOG2E - RB)) > 0 ? (1 << (LOG2E - RB)) : 1;  // items per thread
+  constexpr int Lr = L >> RB;
+  constexpr int ITEMS = B * Lr;
+  static_assert(PL >= 1 && RB <= 5 && RB <= LOG2E, "radix <= 32 and <= E");
+  const int tid = threadIdx.x;
+  C2<T> v[IPT][R];
+  if (tid < NTA) {
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) {
+      const int i = tid + it * NTA;
+      if (ITEMS % NTA == 0 || i < ITEMS) {
+        const int b = i & (B - 1), j = i >> LOG2B;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[it][r] = buf[swz<T>(((j + r * Lr) << LOG2B) + b)];
+        if constexpr (Ns > 1) {
+          const int k = j & (Ns - 1);
+          C2<T> w1 = tw(k << (LOG2L - NSB - RB));
+          if (INV) w1 = cconj<T>(w1);
+          tw_stream<T, R>(v[it], w1);
+        }
+        dft_reg<T, R, INV>(v[it]);
+      }
     }
   }
   __syncthreads();
+  if (tid < NTA) {
 #pragma unroll
-  for (int it = 0; it < IPT; ++it) {
-    if (act[it]) {
-      int i = tid + it * nact;
-      int b = i % B, j = i / B;
-      int k = j & (Ns - 1);
-      int base = (j - k) * R + k;
+    for (int it = 0; it < IPT; ++it) {
+      const int i = tid + it * NTA;
+      if (ITEMS % NTA == 0 || i < ITEMS) {
+        const int b = i & (B - 1), j = i >> LOG2B;
+        const int k = j & (Ns - 1);
+        const int base = (j - k) * R + k;
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[(int64_t)(base + r * Ns) * B + b] = v[it][bitrev<R>(r)];
+        for (int r = 0; r < R; ++r) buf[swz<T>(((base + r * Ns) << LOG2B) + b)] = v[it][bitrev<R>(r)];
+      }
     }
   }
   __syncthreads();
 }
 
-// Full transform: forward (INV=false: X_k = sum x_n W^{nk}) or unnormalised inverse.
-// Requires B * Ls <= FFT_E * blockDim.x; all threads of the CTA must call it.
-template <typename T, bool INV>
-CS_NOINL void fft_cta(C2<T>* buf, int Ls, int B, const TwTable<T>& tw) {
-  const int tid = threadIdx.x;
-  const int nact = max(1, (B * Ls) / FFT_E);
-  int Ns = 1;
-  int rem = Ls;
-  while (rem >= 16) {
-    fft_pass<T, 16, INV>(buf, Ls, B, Ns, Ls / (Ns * 16), tw, tid, nact);
-    Ns *= 16;
-    rem /= 16;
+template <typename T, int LOG2L, int LOG2E, int LOG2B, int P, bool INV>
+CS_DEV void fft_passes(C2<T>* buf, const TwTable<T>& tw) {
+  if constexpr (P < Plan<LOG2L, LOG2E>::P) {
+    fft_pass<T, LOG2L, LOG2E, LOG2B, P, INV>(buf, tw);
+    fft_passes<T, LOG2L, LOG2E, LOG2B, P + 1, INV>(buf, tw);
   }
-  if (rem == 8) fft_pass<T, 8, INV>(buf, Ls, B, Ns, Ls / (Ns * 8), tw, tid, nact);
-  else if (rem == 4) fft_pass<T, 4, INV>(buf, Ls, B, Ns, Ls / (Ns * 4), tw, tid, nact);
-  else if (rem == 2) fft_pass<T, 2, INV>(buf, Ls, B, Ns, Ls / (Ns * 2), tw, tid, nact);
+}
+
+// Full transform of B = 2^LOG2B interleaved sequences (unnormalised; INV = conjugate
+// twiddles).  (L * B) >> LOG2E threads participate; all threads must call.
+template <typename T, int LOG2L, int LOG2E, int LOG2B, bool INV>
+CS_NOINL void fft_cta_t(C2<T>* buf, const TwTable<T> tw) {
+  fft_passes<T, LOG2L, LOG2E, LOG2B, 0, INV>(buf, tw);
+}
+
+// E for a given (L, B) on an NT-thread block: L*B/NT clamped to [2, 32] and <= L
+__host__ __device__ constexpr int fft_log2e(int log2l, int log2b, int log2nt) {
+  int e = log2l + log2b - log2nt;
+  if (e < 1) e = 1;
+  if (e > 5) e = 5;
+  if (e > log2l) e = log2l;
+  return e;
+}
+
+// Runtime dispatch over LOG2L in [LO, HI] with fixed LOG2B and a 2^LOG2NT-thread block.
+template <typename T, int LOG2B, int LOG2NT, int LO, int HI, bool INV>
+CS_DEV void fft_cta_dispatch(C2<T>* buf, int log2l, const TwTable<T>& tw) {
+  if constexpr (LO <= HI) {
+    if (log2l == LO) {
+      fft_cta_t<T, LO, fft_log2e(LO, LOG2B, LOG2NT), LOG2B, INV>(buf, tw);
+      return;
+    }
+    fft_cta_dispatch<T, LOG2B, LOG2NT, LO + 1, HI, INV>(buf, log2l, tw);
+  }
 }
 
 }  // namespace cs

@@ -1,0 +1,10 @@
+// k_l_f32.cu — Tier L kernels and launchers, float instantiation (separate TU for a parallel build).
+#define CS_TIER_L_IMPL
+#include "tier_l.cuh"
+
+namespace cs {
+template cs_status tier_l_apply<float>(OpMeta, int64_t, const float*, float*, void*, size_t, cudaStream_t, bool,
+                                     std::atomic<uint64_t>&, std::string&);
+template cs_status tier_l_recover<float>(OpMeta, Params, int, const float*, int64_t, float*, int32_t*, cs_report*,
+                                       void*, size_t, cudaStream_t, std::atomic<uint64_t>&, std::string&);
+}  // namespace cs

@@ -42,51 +42,82 @@ struct Params {
 // iterate and r = c[supp], see pursuits.py); otherwise one H apply computes it.
 template <class Ctx, typename T>
 CS_NOINL void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q, T* b, bool r_given,
-                     const Params& P, Stats& st) {
+                       const Params& P, Stats& st) {
   ctx.set_input_support(supp, ns);
-  for (int i = ctx.gtid; i < ns; i += ctx.gnthr) b[i] = ctx.c0_at(supp[i]);  // line 12
+  const int t0 = ctx.gtid, sd = ctx.gnthr;
+  {
+    const auto c0v = ctx.c0view();
+    for (int i = t0; i < ns; i += sd) b[i] = c0v.at(supp[i]);             // line 12
+  }
   ctx.sync();
   if (!r_given) {
     ctx.H(x, q);
-    for (int i = ctx.gtid; i < ns; i += ctx.gnthr) r[i] = b[i] - q[i];
+    for (int i = t0; i < ns; i += sd) r[i] = b[i] - q[i];
   }
   double bb = 0, rr = 0;
-  for (int i = ctx.gtid; i < ns; i += ctx.gnthr) {
+  for (int i = t0; i < ns; i += sd) {
     bb += (double)b[i] * (double)b[i];
     rr += (double)r[i] * (double)r[i];
-    d[i] = r[i];                                                             // line 13
+    d[i] = r[i];                                                           // line 13
   }
   bb = ctx.sum(bb);
   rr = ctx.sum(rr);
-  const double thr = P.tol * P.tol * bb;
-  const int cap = P.cg_cap > 0 ? P.cg_cap : ns + 50;
-  int j = 0;
-  while (rr > thr) {                                                         // line 15 (R6, R7)
-    if (j >= cap) { st.status |= CS_DEV_CG_CAP; break; }
-    ctx.H(d, q);                                                             // H d_j
+  // Loop state lives in a volatile local record across the (out-of-line) sandwich
+  // H d: nothing is register-live across the call, so ptxas's inter-procedural
+  // allocator leaves the FFT its full register budget.
+  struct Keep {
+    Ctx* c;
+    Stats* st;
+    T *x, *r, *d, *q;
+    double rr, thr;
+    int ns, cap, j, t0, sd;
+  };
+  volatile Keep kp;
+  kp.c = &ctx;
+  kp.st = &st;
+  kp.x = x; kp.r = r; kp.d = d; kp.q = q;
+  kp.rr = rr;
+  kp.thr = P.tol * P.tol * bb;
+  kp.ns = ns;
+  kp.cap = P.cg_cap > 0 ? P.cg_cap : ns + 50;
+  kp.j = 0;
+  kp.t0 = t0;
+  kp.sd = sd;
+  while (true) {
+    Ctx& c = *kp.c;
+    const double rr0 = kp.rr;
+    if (!(rr0 > kp.thr)) break;                                            // line 15 (R6, R7)
+    if (kp.j >= kp.cap) { kp.st->status |= CS_DEV_CG_CAP; break; }
+    c.H(kp.d, kp.q);                                                       // H d_j (out of line)
+    Ctx& c2 = *kp.c;
+    T* xx = kp.x; T* rv = kp.r; T* dv = kp.d; T* qv = kp.q;
+    const int n = kp.ns, a0 = kp.t0, s0 = kp.sd;
     double dq = 0;
-    for (int i = ctx.gtid; i < ns; i += ctx.gnthr) dq += (double)d[i] * (double)q[i];
-    dq = ctx.sum(dq);
-    if (!(dq > 0.0)) { st.status |= CS_DEV_CG_BREAKDOWN; break; }
-    const T alpha = (T)(rr / dq);                                            // line 16
+    for (int i = a0; i < n; i += s0) dq += (double)dv[i] * (double)qv[i];
+    dq = c2.sum(dq);
+    if (!(dq > 0.0)) { kp.st->status |= CS_DEV_CG_BREAKDOWN; break; }
+    const double rrc = kp.rr;
+    const T alpha = (T)(rrc / dq);                                         // line 16
     double rr2 = 0;
-    for (int i = ctx.gtid; i < ns; i += ctx.gnthr) {
-      x[i] += alpha * d[i];                                                  // line 17
-      T ri = r[i] - alpha * q[i];                                            // line 18
-      r[i] = ri;
+    for (int i = a0; i < n; i += s0) {
+      xx[i] += alpha * dv[i];                                              // line 17
+      T ri = rv[i] - alpha * qv[i];                                        // line 18
+      rv[i] = ri;
       rr2 += (double)ri * (double)ri;
     }
-    rr2 = ctx.sum(rr2);
-    const T beta = (T)(rr2 / rr);                                            // line 19
-    for (int i = ctx.gtid; i < ns; i += ctx.gnthr) d[i] = r[i] + beta * d[i]; // line 20
-    rr = rr2;
-    ++j;                                                                     // line 21
-    if (!(rr == rr)) { st.status |= CS_DEV_CG_BREAKDOWN; break; }
+    rr2 = c2.sum(rr2);
+    const T beta = (T)(rr2 / kp.rr);                                       // line 19
+    for (int i = a0; i < n; i += s0) dv[i] = rv[i] + beta * dv[i];        // line 20
+    kp.rr = rr2;
+    kp.j = kp.j + 1;                                                       // line 21
+    if (!(rr2 == rr2)) { kp.st->status |= CS_DEV_CG_BREAKDOWN; break; }
   }
   ctx.sync();
-  st.cg_iters += j;
+  const int jj = kp.j;
+  const double rrf = kp.rr;
+  st.cg_iters += jj;
   st.cg_solves += 1;
-  double rel = bb > 0 ? sqrt(rr / bb) : 0.0;
+  double rel = bb > 0 ? sqrt(rrf / bb) : 0.0;
   if (rel > st.rel_max) st.rel_max = rel;
 }
 
@@ -113,20 +144,20 @@ CS_DEV void swap_ptr(T*& a, T*& b) { T* t = a; a = b; b = t; }
 template <class Ctx, typename T>
 CS_NOINL void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* out) {
   const int64_t N = ctx.N;
-  const T* cb = ctx.cbuf();
-  topk_bits(ctx, N, K, [&](int64_t j) {
+  const auto cv = ctx.cview();
+  topk_bits(ctx, N, K, [cv, excl](int64_t j) {
     if (excl && bit_test(excl, j)) return decltype(full_key(T(0)))(0);
-    return full_key(cb[mk_pos(j, N)]);
+    return full_key(cv.raw(j));
   }, out);
 }
 
 template <class Ctx, typename T>
 CS_NOINL int64_t detect_argmax(Ctx& ctx, const uint32_t* excl) {
   const int64_t N = ctx.N;
-  const T* cb = ctx.cbuf();
-  return argmax_key(ctx, N, [&](int64_t j) {
+  const auto cv = ctx.cview();
+  return argmax_key(ctx, N, [cv, excl](int64_t j) {
     if (bit_test(excl, j)) return decltype(full_key(T(0)))(0);
-    return full_key(cb[mk_pos(j, N)]);
+    return full_key(cv.raw(j));
   });
 }
 
@@ -152,7 +183,10 @@ CS_NOINL int run_omp(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& r
     ctx.sync();
     int ns2 = (int)compact_bits(ctx, B.Sbits, ctx.N, [&](int64_t k, int64_t j) { S2[k] = (int)j; });
     remap(ctx, S, x, ns, S2, x2, ns2);                                // warm start (R9)
-    for (int i = ctx.gtid; i < ns2; i += ctx.gnthr) B.r[i] = ctx.c_at(S2[i]);  // free r0
+    {
+      const auto cv = ctx.cview();
+      for (int i = ctx.gtid; i < ns2; i += ctx.gnthr) B.r[i] = cv.at(S2[i]);  // free r0
+    }
     swap_ptr<Ctx>(S, S2);
     swap_ptr<Ctx>(x, x2);
     ns = ns2;
@@ -191,7 +225,10 @@ CS_NOINL int run_sp(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& rn
     ctx.sync();
     int nu = (int)compact_bits(ctx, B.Ubits, N, [&](int64_t k, int64_t j) { U[k] = (int)j; });
     remap(ctx, S, x, ns, U, xU, nu);                             // x0 = x on S, 0 on J
-    for (int i = ctx.gtid; i < nu; i += ctx.gnthr) B.r[i] = ctx.c_at(U[i]);   // r0 = c[T]
+    {
+      const auto cv = ctx.cview();
+      for (int i = ctx.gtid; i < nu; i += ctx.gnthr) B.r[i] = cv.at(U[i]);   // r0 = c[T]
+    }
     cg_solve(ctx, U, nu, xU, B.r, B.d, B.q, B.b, true, P, st);
     // prune: S' = top-K of |x_T| over T (positions ascending == indices ascending)
     const T* xUc = xU;
@@ -250,7 +287,10 @@ CS_NOINL int run_ompr(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& 
     }
     int nu = (int)compact_bits(ctx, B.Ubits, N, [&](int64_t k, int64_t j) { U[k] = (int)j; });
     remap(ctx, S, x, ns, U, xU, nu);                                  // x~ on U
-    for (int i = ctx.gtid; i < nu; i += ctx.gnthr) xU[i] = xU[i] + eta * ctx.c_at(U[i]);  // z on U
+    {
+      const auto cv = ctx.cview();
+      for (int i = ctx.gtid; i < nu; i += ctx.gnthr) xU[i] = xU[i] + eta * cv.at(U[i]);  // z on U
+    }
     ctx.sync();
     const T* zc = xU;
     topk_bits(ctx, (int64_t)nu, (int64_t)K, [&](int64_t i) { return full_key(zc[i]); }, B.Pbits);

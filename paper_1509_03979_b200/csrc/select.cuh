@@ -54,6 +54,13 @@ CS_DEV void hist_pick(const unsigned* h, int64_t* pick, int64_t need, int64_t& d
   __syncthreads();
 }
 
+CS_DEV void hist_add_warp(unsigned* hist, unsigned digit) {
+  // warp-aggregated: one shared atomic per distinct digit in the warp
+  unsigned peers = __match_any_sync(__activemask(), digit);
+  int leader = __ffs(peers) - 1;
+  if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[digit], (unsigned)__popc(peers));
+}
+
 // key(i) for i in [0, n); key 0 means "never select".  Requires at least K
 // non-zero keys.  out_bits must hold ceil(n/32) words; fully overwritten.
 template <class Ctx, class KeyFn>
@@ -63,11 +70,14 @@ CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_b
   Key prefix = 0, pmask = 0;
   int64_t need = K;
   int64_t n_eq = 0;
+  const int64_t t0 = ctx.gtid, st = ctx.gnthr, gw = ctx.gwarp, gnw = ctx.gnwarps;
+  const int lane = threadIdx.x & 31;
+  unsigned* hist = ctx.hist_ptr();
   for (int shift = NB - 8; shift >= 0; shift -= 8) {
     ctx.hist_clear();
-    for (int64_t i = ctx.gtid; i < n; i += ctx.gnthr) {
+    for (int64_t i = t0; i < n; i += st) {
       Key k = key(i);
-      if ((k & pmask) == prefix) ctx.hist_add((unsigned)((k >> shift) & 255));
+      if ((k & pmask) == prefix) hist_add_warp(hist, (unsigned)((k >> shift) & 255));
     }
     ctx.hist_done();  // merged counts now in ctx.hist_smem()
     int64_t dsel, cum, hsel;
@@ -81,37 +91,37 @@ CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_b
   const int64_t nwords = (n + 31) >> 5;
   if (n_eq == need) {
     // common case: every key >= thr is selected
-    for (int64_t w = ctx.gwarp; w < nwords; w += ctx.gnwarps) {
-      int64_t i = w * 32 + ctx.lane;
+    for (int64_t w = gw; w < nwords; w += gnw) {
+      int64_t i = w * 32 + lane;
       bool s = (i < n) && (key(i) >= thr);
       uint32_t b = __ballot_sync(0xffffffffu, s);
-      if (ctx.lane == 0) out_bits[w] = b;
+      if (lane == 0) out_bits[w] = b;
     }
     ctx.sync();
     return;
   }
   // ties at the threshold: the lowest-index `need` equal keys win.
   // warp-contiguous chunks of words, chunk order == index order
-  const int64_t per = (nwords + ctx.gnwarps - 1) / ctx.gnwarps;
-  const int64_t w0 = ctx.gwarp * per, w1 = min(nwords, w0 + per);
+  const int64_t per = (nwords + gnw - 1) / gnw;
+  const int64_t w0 = gw * per, w1 = min(nwords, w0 + per);
   int64_t cnt = 0;
   for (int64_t w = w0; w < w1; ++w) {
-    int64_t i = w * 32 + ctx.lane;
+    int64_t i = w * 32 + lane;
     bool e = (i < n) && (key(i) == thr);
     cnt += __popc(__ballot_sync(0xffffffffu, e));
   }
   int64_t tot;
-  int64_t base = ctx.excl_scan(ctx.lane == 0 ? cnt : 0, &tot);
+  int64_t base = ctx.excl_scan(lane == 0 ? cnt : 0, &tot);
   base = __shfl_sync(0xffffffffu, base, 0);
   for (int64_t w = w0; w < w1; ++w) {
-    int64_t i = w * 32 + ctx.lane;
+    int64_t i = w * 32 + lane;
     Key k = (i < n) ? key(i) : Key(0);
     bool e = (i < n) && (k == thr);
     uint32_t em = __ballot_sync(0xffffffffu, e);
-    int64_t rank = base + __popc(em & ((1u << ctx.lane) - 1u));
+    int64_t rank = base + __popc(em & ((1u << lane) - 1u));
     bool s = (i < n) && ((k > thr) || (e && rank < need));
     uint32_t b = __ballot_sync(0xffffffffu, s);
-    if (ctx.lane == 0) out_bits[w] = b;
+    if (lane == 0) out_bits[w] = b;
     base += __popc(em);
   }
   ctx.sync();
@@ -124,7 +134,8 @@ CS_DEV int64_t argmax_key(Ctx& ctx, int64_t n, KeyFn key) {
   using Key = decltype(key(int64_t(0)));
   Key bk = 0;
   int64_t bi = -1;
-  for (int64_t i = ctx.gtid; i < n; i += ctx.gnthr) {
+  const int64_t t0 = ctx.gtid, st = ctx.gnthr;
+  for (int64_t i = t0; i < n; i += st) {
     Key k = key(i);
     if (k > bk) { bk = k; bi = i; }  // increasing i per thread: first max kept
   }
@@ -137,7 +148,8 @@ CS_DEV int64_t argmax_key(Ctx& ctx, int64_t n, KeyFn key) {
 template <class Ctx, class Emit>
 CS_DEV int64_t compact_bits(Ctx& ctx, const uint32_t* bits, int64_t n, Emit emit) {
   const int64_t nwords = (n + 31) >> 5;
-  const int64_t per = (nwords + ctx.gnthr - 1) / ctx.gnthr;
+  const int64_t nthr = ctx.gnthr;
+  const int64_t per = (nwords + nthr - 1) / nthr;
   const int64_t w0 = (int64_t)ctx.gtid * per, w1 = min(nwords, w0 + per);
   int64_t cnt = 0;
   for (int64_t w = w0; w < w1; ++w) {
@@ -165,7 +177,8 @@ CS_DEV int64_t compact_bits(Ctx& ctx, const uint32_t* bits, int64_t n, Emit emit
 template <class Ctx, typename T>
 CS_DEV void remap(Ctx& ctx, const int* old_list, const T* old_vals, int n_old,
                   const int* new_list, T* new_vals, int n_new) {
-  for (int i = ctx.gtid; i < n_new; i += ctx.gnthr) {
+  const int t0 = ctx.gtid, st = ctx.gnthr;
+  for (int i = t0; i < n_new; i += st) {
     int e = new_list[i];
     int lo = 0, hi = n_old;
     while (lo < hi) {

@@ -11,8 +11,8 @@
 
 namespace cs {
 
-constexpr int TL_THREADS = 512;
-constexpr int TL_TILE = FFT_E * TL_THREADS;  // 8192 complex per CTA tile
+constexpr int TL_THREADS = 256;  // fft dispatch assumes 2^8 threads
+constexpr int TL_TILE = 8192;    // complex elements per CTA tile (32 per thread)
 
 struct LGeom {
   int64_t N, L, L1, L2;
@@ -136,6 +136,8 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.L1 = g.L1;
   c.L2 = g.L2;
   c.CT = g.CT;
+  c.log2L1 = ilog2(g.L1);
+  c.log2L2 = ilog2(g.L2);
   char* ws = a.ws;
   c.U = reinterpret_cast<T*>(ws + s.U);
   c.Wk = reinterpret_cast<C2<T>*>(ws + s.Wk);
@@ -284,6 +286,7 @@ template <typename T> inline int l_maxgrid(const void* fn, int64_t smem) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TL_THREADS, (size_t)smem);
   if (occ < 1) occ = 1;
   return nsm * occ;
@@ -307,6 +310,16 @@ template <typename T> inline size_t tier_l_recover_ws_bytes(int64_t N, int64_t M
   return (size_t)l_layout<T>(N, K, ucap, true, l_grid_upper<T>()).bytes;
 }
 
+// Declared everywhere; defined (and explicitly instantiated) in k_l_f32.cu / k_l_f64.cu.
+template <typename T>
+cs_status tier_l_apply(OpMeta meta, int64_t B, const T* in, T* out, void* ws, size_t ws_bytes,
+                       cudaStream_t st, bool adjoint, std::atomic<uint64_t>& launches, std::string& err);
+template <typename T>
+cs_status tier_l_recover(OpMeta meta, Params P, int ucap, const T* Y, int64_t B, T* vals,
+                         int32_t* supp, cs_report* reps, void* ws, size_t ws_bytes,
+                         cudaStream_t st, std::atomic<uint64_t>& launches, std::string& err);
+
+#ifdef CS_TIER_L_IMPL
 template <typename T>
 inline cs_status l_launch(const void* fn, LArgs<T>& a, int64_t N, cudaStream_t st,
                           std::atomic<uint64_t>& launches, std::string& err) {
@@ -326,7 +339,7 @@ inline cs_status l_launch(const void* fn, LArgs<T>& a, int64_t N, cudaStream_t s
 }
 
 template <typename T>
-inline cs_status tier_l_apply(OpMeta meta, int64_t B, const T* in, T* out, void* ws, size_t ws_bytes,
+cs_status tier_l_apply(OpMeta meta, int64_t B, const T* in, T* out, void* ws, size_t ws_bytes,
                               cudaStream_t st, bool adjoint, std::atomic<uint64_t>& launches,
                               std::string& err) {
   LArgs<T> a;
@@ -343,7 +356,7 @@ inline cs_status tier_l_apply(OpMeta meta, int64_t B, const T* in, T* out, void*
 }
 
 template <typename T>
-inline cs_status tier_l_recover(OpMeta meta, Params P, int ucap, const T* Y, int64_t B, T* vals,
+cs_status tier_l_recover(OpMeta meta, Params P, int ucap, const T* Y, int64_t B, T* vals,
                                 int32_t* supp, cs_report* reps, void* ws, size_t ws_bytes,
                                 cudaStream_t st, std::atomic<uint64_t>& launches, std::string& err) {
   LArgs<T> a;
@@ -360,5 +373,7 @@ inline cs_status tier_l_recover(OpMeta meta, Params P, int ucap, const T* Y, int
   a.ws = reinterpret_cast<char*>(ws);
   return l_launch<T>((const void*)k_l_recover<T>, a, meta.N, st, launches, err);
 }
+
+#endif  // CS_TIER_L_IMPL
 
 }  // namespace cs

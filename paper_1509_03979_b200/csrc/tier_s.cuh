@@ -3,12 +3,16 @@
 // Used for config 1 (OMP, N = 4096) and config 4 (4096 batched SP problems,
 // N = 16384), and for batched operator apply / adjoint at those sizes.
 #pragma once
+#include <atomic>
+#include <string>
+
 #include "ctx_cta.cuh"
 #include "pursuit.cuh"
 
 namespace cs {
 
 constexpr int64_t TIER_S_MAX_N = 16384;
+constexpr int TS_THREADS = 256;  // fft dispatch assumes 2^8 threads
 
 CS_HD int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -57,10 +61,7 @@ CS_HD SLayout s_layout(int64_t N, int K, int ucap, bool pursuit) {
     s.S = s.S2 = s.U = s.x = s.x2 = s.xU = s.r = s.d = s.q = s.b = s.Sbits = s.Ubits = s.Pbits = 0;
   }
   s.bytes = o;
-  int64_t nt = L / FFT_E;
-  if (nt < 32) nt = 32;
-  if (nt > 512) nt = 512;
-  s.nthreads = (int)nt;
+  s.nthreads = TS_THREADS;
   return s;
 }
 
@@ -87,6 +88,8 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   c.N = meta.N;
   c.M = meta.M;
   c.L = meta.N / 2;
+  c.log2L = 0;
+  while ((int64_t(1) << c.log2L) < c.L) ++c.log2L;
   c.Z = reinterpret_cast<C2<T>*>(smem + lay.Z);
   c.sign = reinterpret_cast<uint32_t*>(smem + lay.sign);
   c.rowmask = reinterpret_cast<uint32_t*>(smem + lay.rmask);
@@ -123,7 +126,7 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
 
 // ---------------------------------------------------------------- kernels ---
 template <typename T>
-__global__ void __launch_bounds__(512) k_s_apply(OpMeta meta, SLayout lay, const T* __restrict__ X,
+__global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout lay, const T* __restrict__ X,
                                                  T* __restrict__ Y) {
   extern __shared__ __align__(16) char smem[];
   const int64_t b = blockIdx.x;
@@ -131,14 +134,15 @@ __global__ void __launch_bounds__(512) k_s_apply(OpMeta meta, SLayout lay, const
   const int64_t N = c.N;
   const T* x = X + b * N;
   T* zb = reinterpret_cast<T*>(c.Z);
-  for (int64_t j = c.gtid; j < N; j += c.gnthr) zb[mk_pos(j, N)] = apply_sign<T>(c.sign, j, x[j]);
+  for (int j = c.gtid; j < (int)N; j += c.gnthr)
+    zb[CtaCtx<T>::zt((int)mk_pos(j, N))] = apply_sign<T>(c.sign, j, x[j]);
   __syncthreads();
-  fft_cta<T, false>(c.Z, (int)c.L, 1, c.twL);
+  c.fwd();
   c.template middle<MID_FWD>(Y + b * c.M);
 }
 
 template <typename T>
-__global__ void __launch_bounds__(512) k_s_adjoint(OpMeta meta, SLayout lay, const T* __restrict__ Yin,
+__global__ void __launch_bounds__(TS_THREADS, 2) k_s_adjoint(OpMeta meta, SLayout lay, const T* __restrict__ Yin,
                                                    T* __restrict__ X) {
   extern __shared__ __align__(16) char smem[];
   const int64_t b = blockIdx.x;
@@ -163,7 +167,7 @@ template <typename T> struct SRecArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(512) k_s_recover(SRecArgs<T> a) {
+__global__ void __launch_bounds__(TS_THREADS, 2) k_s_recover(SRecArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
   const int64_t b = blockIdx.x;
   CtaCtx<T> c = make_cta_ctx<T>(smem, a.lay, a.meta, b);
@@ -190,5 +194,47 @@ __global__ void __launch_bounds__(512) k_s_recover(SRecArgs<T> a) {
   B.Pbits = reinterpret_cast<uint32_t*>(smem + L.Pbits);
   run_pursuit<CtaCtx<T>, T>(c, a.P, B, a.vals + b * a.P.K, a.supp + b * a.P.K, a.reps + b, pre);
 }
+
+// ------------------------------------------------------------ host side ----
+// Declared everywhere; defined (and explicitly instantiated) in k_s_f32.cu / k_s_f64.cu.
+template <typename T>
+cs_status s_apply_launch(const OpMeta& m, int64_t B, const T* in, T* out, bool adjoint, cudaStream_t st,
+                         std::atomic<uint64_t>& launches, std::string& err);
+template <typename T>
+cs_status s_recover_launch(const SRecArgs<T>& a, int64_t B, cudaStream_t st, std::atomic<uint64_t>& launches,
+                           std::string& err);
+
+#ifdef CS_TIER_S_IMPL
+inline cs_status s_attr(const void* fn, int64_t bytes, std::string& err) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) { err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  return CS_OK;
+}
+inline cs_status s_launched(std::atomic<uint64_t>& launches, std::string& err) {
+  launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { err = std::string("kernel launch: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  return CS_OK;
+}
+template <typename T>
+cs_status s_apply_launch(const OpMeta& m, int64_t B, const T* in, T* out, bool adjoint, cudaStream_t st,
+                         std::atomic<uint64_t>& launches, std::string& err) {
+  SLayout lay = s_layout<T>(m.N, 0, 0, false);
+  const void* fn = adjoint ? (const void*)k_s_adjoint<T> : (const void*)k_s_apply<T>;
+  if (cs_status s = s_attr(fn, lay.bytes, err)) return s;
+  if (adjoint) k_s_adjoint<T><<<(unsigned)B, lay.nthreads, lay.bytes, st>>>(m, lay, in, out);
+  else k_s_apply<T><<<(unsigned)B, lay.nthreads, lay.bytes, st>>>(m, lay, in, out);
+  return s_launched(launches, err);
+}
+template <typename T>
+cs_status s_recover_launch(const SRecArgs<T>& a, int64_t B, cudaStream_t st, std::atomic<uint64_t>& launches,
+                           std::string& err) {
+  if (cs_status s = s_attr((const void*)k_s_recover<T>, a.lay.bytes, err)) return s;
+  k_s_recover<T><<<(unsigned)B, a.lay.nthreads, a.lay.bytes, st>>>(a);
+  return s_launched(launches, err);
+}
+#endif
 
 }  // namespace cs
