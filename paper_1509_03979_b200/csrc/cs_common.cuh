@@ -15,6 +15,17 @@
 
 namespace cs {
 
+// Dynamic shared memory of the running kernel (every unsized extern __shared__ array
+// aliases its base).  shp(p) re-derives a generic pointer that is known to point
+// into shared memory from this base, so that out-of-line device functions (which
+// only see generic pointers) get 32-bit LDS/STS instead of generic LD/ST.
+extern __shared__ __align__(16) char cs_smem_base[];
+template <typename P> CS_DEV P* shp(P* p) {
+  const uint32_t off = (uint32_t)__cvta_generic_to_shared((const void*)p) -
+                       (uint32_t)__cvta_generic_to_shared((const void*)cs_smem_base);
+  return reinterpret_cast<P*>(cs_smem_base + off);
+}
+
 template <typename T> struct cplx_t;
 template <> struct cplx_t<float> { using type = float2; };
 template <> struct cplx_t<double> { using type = double2; };

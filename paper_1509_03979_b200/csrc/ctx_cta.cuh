@@ -15,6 +15,7 @@
 #include "cs_common.cuh"
 #include "dct_mid.cuh"
 #include "fft_cta.cuh"
+#include "sandwich_cta.cuh"
 
 namespace cs {
 
@@ -149,68 +150,21 @@ template <typename T> struct CtaCtx {
     in_supp = supp;
     in_ns = ns;
   }
-  CS_DEV void zero_Z() {
-    C2<T>* z = Z;
-    const int n = (int)L, t0 = gtid, st = gnthr;
-    for (int m = t0; m < n; m += st) z[m] = mk<T>(0, 0);
-    __syncthreads();
-  }
-  // scatter sigma . vals on the remembered support into the zeroed buffer
-  CS_DEV void load_input(const T* vals) {
-    zero_Z();
-    T* zb = reinterpret_cast<T*>(Z);
-    const int* sp = in_supp;
-    const uint32_t* sg = sign;
-    const int ns = in_ns, t0 = gtid, st = gnthr, n = (int)N;
-    for (int i = t0; i < ns; i += st) {
-      const int j = sp[i];
-      zb[zt((int)mk_pos(j, n))] = apply_sign<T>(sg, j, vals[i]);
-    }
-    __syncthreads();
-  }
-  CS_DEV void fwd() { fft_cta_dispatch<T, 0, 8, 2, 13, false>(Z, log2L, twL); }
-  CS_DEV void inv() { fft_cta_dispatch<T, 0, 8, 2, 13, true>(Z, log2L, twL); }
-  template <int MODE> CS_DEV double middle(T* yout) {
-    MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, yout);
-    double rn2 = 0;
-    C2<T>* z = Z;
-    const int l = (int)L, t0 = gtid, st = gnthr;
-    const TwTable<T> t4 = tw4;
-    for (int k = t0; k <= l / 2; k += st) {
-      if (k == 0) {
-        mid_zero<T, MODE>(z[0], m, rn2);
-      } else {
-        C2<T> a = t4(k);
-        mid_pair<T, MODE>(z[swz<T>(k)], z[swz<T>(l - k)], k, a, m, rn2);
-      }
-    }
-    __syncthreads();
-    return rn2;
+  // fused sandwich (sandwich_cta.cuh): scatter, forward FFT, DCT middle, inverse FFT, gather
+  template <int MODE, bool ZERO> CS_DEV double sandwich(const T* vin, T* vout, T* yout) {
+    const MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, yout);
+    const SwIO<T> io{in_supp, in_ns, sign, vin, vout};
+    return sw_dispatch<T, 2, 13, MODE, ZERO>(Z, log2L, twL, tw4, m, io);
   }
   // q = (A^T A scatter_S(d))[S] on the remembered support S (cg2)
-  CS_NOINL void H(const T* d, T* q) {
-    load_input(d);
-    fwd();
-    middle<MID_H>(nullptr);
-    inv();
-    const int* sp = in_supp;
-    const int ns = in_ns, t0 = gtid, st = gnthr;
-    const CV cv = cview();
-    for (int i = t0; i < ns; i += st) q[i] = cv.at(sp[i]);
-    __syncthreads();
+  CS_DEV void H(const T* d, T* q) {
+    sandwich<MID_H, false>(d, q, nullptr);
     ++applies;
   }
   // c = A^T (y - A scatter_S(x)) into the buffer (b1 + cg5); returns ||y - A x||^2.
   // x == nullptr means x = 0 (c = A^T y).
   CS_NOINL double RES(const T* x) {
-    if (x) {
-      load_input(x);
-      fwd();
-    } else {
-      zero_Z();
-    }
-    double rn2 = middle<MID_RES>(nullptr);
-    inv();
+    const double rn2 = x ? sandwich<MID_RES, false>(x, nullptr, nullptr) : sandwich<MID_RES, true>(nullptr, nullptr, nullptr);
     ++applies;
     return sum(rn2);
   }

@@ -104,6 +104,73 @@ CS_DEV void mid_pair(C2<T>& Zk, C2<T>& Zkk, int64_t k, C2<T> a, const MidCtx<T>&
   }
 }
 
+// ---- the same pair operation with the constant factors folded (Tier S) ----
+// Forward split without the two 1/2 factors: raw_k = 2 X_k, raw_{N-k} = 2 X_{N-k},
+// and for the kk pair the e^{-i pi/4} rotation split into (1 - i) and a factor
+// r2 = 1/sqrt 2: raw_kk = 2 X_kk / r2, raw_{N-kk} = 2 X_{N-kk} / r2.  mid_op2 works
+// on raw values with per-type constants (MidK<T>) and returns the value the
+// inverse split needs with its own 1/2 (and, for the kk pair, r2) folded in.
+// Requires k != L - k (the self pair n = L/2 goes through mid_pair).
+template <typename T> struct MidK {
+  T scx[2];  // s_k * (1/2, r2/2): X = scx * raw
+  T cout[2]; // (1/2, r2/2) / s_k / L * 2: returned = cout * (y - s X)          (RES)
+  T hH[2];   // invL * (1/4, 1/8): returned = [sel] raw * hH                     (H)
+};
+template <typename T> CS_DEV MidK<T> make_midk(int N) {
+  MidK<T> c;
+  const double r2 = 0.70710678118654752440, sk = sqrt(2.0 / (double)N), invL = 2.0 / (double)N;
+  c.scx[0] = (T)(sk * 0.5);
+  c.scx[1] = (T)(sk * r2 * 0.5);
+  c.cout[0] = (T)(invL / sk * 0.5);
+  c.cout[1] = (T)(invL / sk * r2 * 0.5);
+  c.hH[0] = (T)(invL * 0.25);
+  c.hH[1] = (T)(invL * 0.125);
+  return c;
+}
+CS_DEV bool bit_test32(const uint32_t* bits, int j) { return (bits[j >> 5] >> (j & 31)) & 1u; }
+CS_DEV int row_rank32(const uint32_t* mask, const int32_t* prefix, int k) {
+  return prefix[k >> 5] + __popc(mask[k >> 5] & ((1u << (k & 31)) - 1u));
+}
+template <typename T, int MODE, int TY>
+CS_DEV T mid_op2(const MidCtx<T>& m, const MidK<T>& c, int idx, T raw, double& rn2) {
+  const bool sel = bit_test32(m.rowmask, idx);
+  if constexpr (MODE == MID_H) {
+    return sel ? raw * c.hH[TY] : T(0);
+  } else if constexpr (MODE == MID_RES) {
+    if (!sel) return T(0);
+    const T d = m.y[row_rank32(m.rowmask, m.prefix, idx)] - c.scx[TY] * raw;
+    rn2 += (double)d * (double)d;
+    return d * c.cout[TY];
+  } else {
+    if (sel) m.yout[row_rank32(m.rowmask, m.prefix, idx)] = c.scx[TY] * raw;
+    return T(0);
+  }
+}
+// a = W_4N^k, w = W_N^k = a^4 (precomputed by the caller)
+template <typename T, int MODE>
+CS_DEV void mid_pair2(C2<T>& Zk, C2<T>& Zkk, int k, C2<T> a, C2<T> w, const MidCtx<T>& m, const MidK<T>& c,
+                      double& rn2) {
+  const int N = (int)m.N, kk = (N >> 1) - k;
+  const C2<T> P2 = mk<T>(Zk.x + Zkk.x, Zk.y - Zkk.y);   // Zk + conj Zkk
+  const C2<T> O2 = mk<T>(Zk.y + Zkk.y, Zkk.x - Zk.x);   // -i (Zk - conj Zkk)
+  const C2<T> Q2 = cmul<T>(w, O2);
+  const C2<T> ck = cmul<T>(a, cadd<T>(P2, Q2));        // 2 (X_k - i X_{N-k})
+  const C2<T> u = cmul<T>(a, csub<T>(P2, Q2));         // e4 conj(u) = 2 (X_kk - i X_{N-kk}) / r2 ... (see above)
+  const T gk = mid_op2<T, MODE, 0>(m, c, k, ck.x, rn2);
+  const T gnk = mid_op2<T, MODE, 0>(m, c, N - k, -ck.y, rn2);
+  const T gkk = mid_op2<T, MODE, 1>(m, c, kk, u.x - u.y, rn2);
+  const T gnkk = mid_op2<T, MODE, 1>(m, c, N - kk, u.x + u.y, rn2);
+  if constexpr (MODE != MID_FWD) {
+    const C2<T> Vk = cmulc<T>(mk<T>(gk, -gnk), a);                // conj(a) c'_k
+    const C2<T> t = cmul<T>(a, mk<T>(gkk, -gnkk));
+    const C2<T> cVkk = mk<T>(t.x - t.y, -(t.x + t.y));            // conj((1 + i) t)
+    const C2<T> E = cadd<T>(Vk, cVkk);
+    const C2<T> Od = cmulc<T>(csub<T>(Vk, cVkk), w);              // conj(w)(Vk - conj Vkk)
+    Zk = mk<T>(E.x - Od.y, E.y + Od.x);                           // E + i Od
+    Zkk = mk<T>(E.x + Od.y, Od.x - E.y);                          // conj(E - i Od)
+  }
+}
+
 template <typename T> CS_DEV MidCtx<T> make_mid(int64_t N, const uint32_t* rowmask,
                                                const int32_t* prefix, const T* y, T* yout) {
   MidCtx<T> m;

@@ -33,6 +33,14 @@ template <typename T> CS_DEV int swz(int a) {
   return a ^ (((a >> 4) ^ (a >> 5)) & S);
 }
 
+// swz as a constexpr (compile-time offsets).  swz is linear over GF(2): for
+// bit-disjoint a and c, swz(a | c) = swz(a) ^ swz(c) — so a per-thread swz(base)
+// plus a compile-time swz(c) addresses every element of a pass (one XOR, or none
+// when c has no bits in 4..8).
+template <typename T> __host__ __device__ constexpr int swz_c(int a) {
+  return a ^ (((a >> 4) ^ (a >> 5)) & ((sizeof(T) == 4) ? 15 : 7));
+}
+
 template <typename T> struct TwTable {
   const C2<T>* lo;  // W^i, i < 64
   const C2<T>* hi;  // W^{64 i}

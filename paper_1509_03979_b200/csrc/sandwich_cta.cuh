@@ -1,0 +1,240 @@
+// sandwich_cta.cuh — the fused operator sandwich of Tier S: A^T (mid) A on one CTA.
+//
+// Every CG iteration applies H d = (A^T A scatter_S d)[S] ("the operation
+// Hd_j dominates the whole computation cost"), and every detection applies
+// A^T (y - A x) (Algorithm 1 lines 03/07).  Both are
+//     forward L-point FFT (L = N/2) -> DCT split, row select / residual, inverse
+//     split -> inverse L-point FFT
+// held in one CTA's shared memory.  Design:
+//
+//  * 512 threads, two CTAs per SM, <= 64 registers: every pass keeps <= 16 points
+//    per thread;
+//  * small code (the CG loop must fit the 32 KB instruction cache): the radix-16
+//    passes are ONE loop body with a runtime stride Ns, run (log2 L - 1) / 4 times
+//    forward and inverse; a remainder pass of radix 2/4/8 covers the other bits;
+//  * the forward FFT ends with a radix-2 pass (Ns = L/2), after which item k holds
+//    Z_k and Z_{k+L/2}; the DCT real split pairs Z_n with Z_{L-n}, and the mirror
+//    of {k, k+L/2} is item L/2-k — one thread owns the unit (k, L/2-k), i.e. four
+//    points, and runs last forward pass, split, middle, inverse split and the
+//    first inverse pass (radix 2, Ns = 1, same point set) in registers;
+//  * DCT twiddles a_n = W_4N^n: one table lookup per unit (a_{k+L/2} = a_k W_16);
+//    w_n = a_n^4.
+//
+// Stockham pass (radix R, stride Ns before the pass), item j < L/R, k = j mod Ns:
+//    v_r = x[j + r L/R] * W_{Ns R}^{r k},  V = DFT_R(v),  x'[(j-k) R + k + r Ns] = V_r.
+// Shared addresses use the XOR swizzle of fft_cta.cuh; swz is linear over GF(2),
+// so swz(base | r Ns) = swz(base) ^ (XOR of swz(Ns << b) over the bits b of r).
+#pragma once
+#include "cs_common.cuh"
+#include "dct_mid.cuh"
+#include "fft_cta.cuh"
+
+namespace cs {
+
+constexpr int SW_NT = 512;  // threads per Tier S block (two blocks per SM)
+constexpr int SW_LOG2NT = 9;
+
+// ---- one Stockham pass of radix 2^RB at runtime stride Ns = 2^nsb; L = 2^LOG2L ----
+template <typename T, int LOG2L, int RB, bool INV>
+CS_DEV void sw_pass(C2<T>* buf, const TwTable<T>& tw, int nsb) {
+  constexpr int R = 1 << RB, Lr = (1 << LOG2L) >> RB;
+  static_assert(Lr <= SW_NT, "one item per thread");
+  const int j = threadIdx.x;
+  C2<T> v[R];
+  const bool act = (Lr == SW_NT) || j < Lr;
+  const int Ns = 1 << nsb, k = j & (Ns - 1);
+  if (act) {
+    const int sj = swz<T>(j);  // j < Lr: bit-disjoint from r Lr
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = buf[sj ^ swz_c<T>(r * Lr)];
+    if (Ns > 1) {
+      C2<T> w1 = tw(k << (LOG2L - nsb - RB));
+      if (INV) w1 = cconj<T>(w1);
+      tw_stream<T, R>(v, w1);
+    }
+    dft_reg<T, R, INV>(v);
+  }
+  __syncthreads();
+  if (act) {
+    const int sb = swz<T>((j - k) * R + k);  // bit-disjoint from r Ns
+    int e[RB];                                 // swz(Ns << b)
+#pragma unroll
+    for (int b = 0; b < RB; ++b) e[b] = swz<T>(Ns << b);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      int o = sb;
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+        if (r & (1 << b)) o ^= e[b];
+      buf[o] = v[bitrev<R>(r)];
+    }
+  }
+  __syncthreads();
+}
+
+template <int LOG2L> struct SwPlan {
+  // forward radices: [remainder 2^M if M > 0] [16] x Q [2 (fused)]; inverse reversed
+  static constexpr int M = (LOG2L - 1) % 4;
+  static constexpr int Q = (LOG2L - 1) / 4;
+  static constexpr int NS_R16_FWD0 = M;                                  // log2 Ns, first fwd radix-16 pass
+  static constexpr int U = (1 << LOG2L) / 4 > 0 ? (1 << LOG2L) / 4 : 1;  // fused units
+  static constexpr int UPT = (U + SW_NT - 1) / SW_NT;                     // units per thread
+  static_assert(UPT <= 4, "L <= 8192");
+};
+
+// W_16^1 (a_{k + L/2} = a_k W_16)
+template <typename T> CS_DEV C2<T> w16c() {
+  return mk<T>((T)0.92387953251128675613, (T)-0.38268343236508977173);
+}
+
+// ---- the fused unit: last forward pass (radix 2), DCT middle, first inverse pass ----
+// Unit k (1 <= k < L/4) owns items k and L/2 - k of the radix-2 pass, i.e.
+//   A0 = Z_k, A1 = Z_{k+L/2}, B0 = Z_{L/2-k}, B1 = Z_{L-k};
+// mirror pairs: (A0, B1) at n = k and (A1, B0) at n = k + L/2.
+// Unit 0 (items 0 and L/4): Z_0 (alone), Z_{L/2} (self pair), (Z_{L/4}, Z_{3L/4}).
+template <typename T, int LOG2L, int MODE, bool ZERO>
+CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, const MidCtx<T>& m) {
+  using SP = SwPlan<LOG2L>;
+  constexpr int L = 1 << LOG2L, H = L / 2, U = SP::U, UPT = SP::UPT;
+  static_assert(L >= 4, "N >= 8");
+  const int tid = threadIdx.x;
+  const MidK<T> cst = make_midk<T>(2 * L);
+  double rn2 = 0;
+  C2<T> A0[UPT], A1[UPT], B0[UPT], B1[UPT];
+#pragma unroll
+  for (int it = 0; it < UPT; ++it) {
+    const int k = tid + it * SW_NT;
+    if ((U % SW_NT == 0) || k < U) {
+      const int kb = (k == 0) ? L / 4 : H - k;
+      if constexpr (ZERO) {
+        A0[it] = A1[it] = B0[it] = B1[it] = mk<T>(0, 0);
+      } else {
+        // radix-2 pass, Ns = L/2: item j reads x[j], x[j + L/2]; twiddle W_L^j
+        C2<T> a0 = buf[swz<T>(k)], a1 = buf[swz<T>(k + H)];
+        C2<T> b0 = buf[swz<T>(kb)], b1 = buf[swz<T>(kb + H)];
+        a1 = cmul<T>(a1, tw(k));
+        b1 = cmul<T>(b1, tw(kb));
+        A0[it] = cadd<T>(a0, a1);
+        A1[it] = csub<T>(a0, a1);
+        B0[it] = cadd<T>(b0, b1);
+        B1[it] = csub<T>(b0, b1);
+      }
+      if (k != 0) {
+        const C2<T> a = tw4(k);
+        const C2<T> a2 = cmul<T>(a, a);
+        const C2<T> w = cmul<T>(a2, a2);                       // W_N^k
+        mid_pair2<T, MODE>(A0[it], B1[it], k, a, w, m, cst, rn2);
+        const C2<T> ah = cmul<T>(a, w16c<T>());                // W_4N^{k + L/2}
+        const C2<T> wh = mk<T>(w.y, -w.x);                     // W_N^{k + L/2} = -i W_N^k
+        mid_pair2<T, MODE>(A1[it], B0[it], k + H, ah, wh, m, cst, rn2);
+      } else {
+        mid_zero<T, MODE>(A0[it], m, rn2);
+        mid_pair<T, MODE>(A1[it], A1[it], H, tw4(H), m, rn2);  // self pair n = L/2
+        mid_pair<T, MODE>(B0[it], B1[it], L / 4, tw4(L / 4), m, rn2);
+      }
+    }
+  }
+  if constexpr (MODE == MID_FWD) {
+    return rn2;
+  } else {
+    __syncthreads();  // every load of the pass precedes every store (in place)
+#pragma unroll
+    for (int it = 0; it < UPT; ++it) {
+      const int k = tid + it * SW_NT;
+      if ((U % SW_NT == 0) || k < U) {
+        const int kb = (k == 0) ? L / 4 : H - k;
+        // inverse radix-2 pass, Ns = 1: item j reads x[j], x[j + L/2], writes x'[2j], x'[2j+1]
+        const int sa = swz<T>(2 * k), sb = swz<T>(2 * kb);
+        buf[sa] = cadd<T>(A0[it], A1[it]);
+        buf[sa ^ 1] = csub<T>(A0[it], A1[it]);
+        buf[sb] = cadd<T>(B0[it], B1[it]);
+        buf[sb ^ 1] = csub<T>(B0[it], B1[it]);
+      }
+    }
+    __syncthreads();
+    return rn2;
+  }
+}
+
+template <typename T, int LOG2L, bool INV>
+CS_DEV void sw_remainder(C2<T>* buf, const TwTable<T>& tw, int nsb) {
+  constexpr int M = SwPlan<LOG2L>::M;
+  if constexpr (M > 0) sw_pass<T, LOG2L, M, INV>(buf, tw, nsb);
+}
+
+// The whole sandwich as ONE out-of-line unit (one ABI register save/restore per
+// sandwich):
+//   vin != nullptr : zero the buffer and scatter sigma . vin on supp (Makhoul order)
+//   vin == nullptr : the buffer already holds the forward input (ZERO: it is 0)
+//   forward FFT, fused last pass / middle / first inverse pass, inverse FFT,
+//   vout != nullptr: gather vout[i] = sigma . buf[supp[i]] (H d restricted to S).
+template <typename T> struct SwIO {
+  const int* supp;
+  int ns;
+  const uint32_t* sign;
+  const T* vin;
+  T* vout;
+};
+
+template <typename T, int LOG2L, int MODE, bool ZERO>
+CS_NOINL double sw_sandwich_t(C2<T>* gbuf, const TwTable<T> gtw, const TwTable<T> gtw4, const MidCtx<T> gm,
+                              const SwIO<T> gio) {
+  using SP = SwPlan<LOG2L>;
+  constexpr int L = 1 << LOG2L, N = 2 * L;
+  // every pointer except m.y / m.yout is shared memory in Tier S
+  C2<T>* buf = shp(gbuf);
+  const TwTable<T> tw{shp(gtw.lo), shp(gtw.hi)}, tw4{shp(gtw4.lo), shp(gtw4.hi)};
+  MidCtx<T> m = gm;
+  m.rowmask = shp(gm.rowmask);
+  m.prefix = shp(gm.prefix);
+  const int tid = threadIdx.x;
+  T* zb = reinterpret_cast<T*>(buf);
+  auto zt = [](int p) { return 2 * swz<T>(p >> 1) + (p & 1); };
+  if constexpr (!ZERO) {
+    if (gio.vin) {
+      const int* supp = shp(gio.supp);
+      const uint32_t* sign = shp(gio.sign);
+      const T* vin = shp(gio.vin);
+      for (int i = tid; i < L; i += SW_NT) buf[i] = mk<T>(0, 0);
+      __syncthreads();
+      for (int i = tid; i < gio.ns; i += SW_NT) {
+        const int j = supp[i];
+        zb[zt((int)mk_pos(j, N))] = apply_sign<T>(sign, j, vin[i]);
+      }
+      __syncthreads();
+    }
+    sw_remainder<T, LOG2L, false>(buf, tw, 0);
+#pragma unroll 1
+    for (int q = 0; q < SP::Q; ++q) sw_pass<T, LOG2L, 4, false>(buf, tw, SP::NS_R16_FWD0 + 4 * q);
+  }
+  const double rn2 = sw_fused<T, LOG2L, MODE, ZERO>(buf, tw, tw4, m);
+  if constexpr (MODE != MID_FWD) {
+#pragma unroll 1
+    for (int q = 0; q < SP::Q; ++q) sw_pass<T, LOG2L, 4, true>(buf, tw, 1 + 4 * q);
+    sw_remainder<T, LOG2L, true>(buf, tw, 1 + 4 * SP::Q);
+    if (gio.vout) {
+      const int* supp = shp(gio.supp);
+      const uint32_t* sign = shp(gio.sign);
+      T* vout = shp(gio.vout);
+      for (int i = tid; i < gio.ns; i += SW_NT) {
+        const int j = supp[i];
+        vout[i] = apply_sign<T>(sign, j, zb[zt((int)mk_pos(j, N))]);
+      }
+      __syncthreads();
+    }
+  }
+  return rn2;
+}
+
+// runtime dispatch over log2 L in [LO, HI]
+template <typename T, int LO, int HI, int MODE, bool ZERO>
+CS_DEV double sw_dispatch(C2<T>* buf, int log2l, const TwTable<T>& tw, const TwTable<T>& tw4, const MidCtx<T>& m,
+                          const SwIO<T>& io) {
+  if constexpr (LO <= HI) {
+    if (log2l == LO) return sw_sandwich_t<T, LO, MODE, ZERO>(buf, tw, tw4, m, io);
+    return sw_dispatch<T, LO + 1, HI, MODE, ZERO>(buf, log2l, tw, tw4, m, io);
+  }
+  return 0.0;
+}
+
+}  // namespace cs

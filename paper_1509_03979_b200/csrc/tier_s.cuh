@@ -12,7 +12,7 @@
 namespace cs {
 
 constexpr int64_t TIER_S_MAX_N = 16384;
-constexpr int TS_THREADS = 256;  // fft dispatch assumes 2^8 threads
+constexpr int TS_THREADS = SW_NT;  // 512: <= 16 points per thread per FFT pass
 
 CS_HD int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -137,8 +137,7 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout 
   for (int j = c.gtid; j < (int)N; j += c.gnthr)
     zb[CtaCtx<T>::zt((int)mk_pos(j, N))] = apply_sign<T>(c.sign, j, x[j]);
   __syncthreads();
-  c.fwd();
-  c.template middle<MID_FWD>(Y + b * c.M);
+  c.template sandwich<MID_FWD, false>(nullptr, nullptr, Y + b * c.M);
 }
 
 template <typename T>
