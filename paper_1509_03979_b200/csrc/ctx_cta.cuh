@@ -52,7 +52,7 @@ template <typename T> struct CtaCtx {
 
   CS_DEV void sync() { __syncthreads(); }
 
-  CS_NOINL double sum(double v) {
+  CS_DEV double sum(double v) {
     v = warp_sum(v);
     if (lane == 0) redd[gwarp] = v;
     __syncthreads();
@@ -156,6 +156,28 @@ template <typename T> struct CtaCtx {
     const SwIO<T> io{in_supp, in_ns, sign, vin, vout};
     return sw_dispatch<T, 2, 13, MODE, ZERO>(Z, log2L, twL, tw4, m, io);
   }
+  // CG iterations with the sandwich of one compile-time length inlined: no call
+  // (and no ABI register save/restore) inside the loop.
+  template <int LOG2L, class S> CS_NOINL void cg_iterate_t(S& s) {
+    const MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, nullptr);
+    s.x = shp(s.x); s.r = shp(s.r); s.d = shp(s.d); s.q = shp(s.q);  // Tier S: all in shared memory
+    C2<T>* z = Z;
+    const TwTable<T> tl = twL, t4 = tw4;
+    const int* sp = in_supp;
+    const uint32_t* sg = sign;
+    const int ns = in_ns;
+    cg_loop(*this, s, [&](const T* d, T* q) {
+      sw_body<T, LOG2L, MID_H, false>(z, tl, t4, m, SwIO<T>{sp, ns, sg, d, q});
+    });
+    applies += s.j;
+  }
+  template <int LO, int HI, class S> CS_DEV void cg_dispatch(S& s) {
+    if constexpr (LO <= HI) {
+      if (log2L == LO) { cg_iterate_t<LO>(s); return; }
+      cg_dispatch<LO + 1, HI>(s);
+    }
+  }
+  template <class S> CS_DEV void cg_iterate(S& s) { cg_dispatch<2, 13>(s); }
   // q = (A^T A scatter_S(d))[S] on the remembered support S (cg2)
   CS_DEV void H(const T* d, T* q) {
     sandwich<MID_H, false>(d, q, nullptr);

@@ -381,6 +381,9 @@ template <typename T> struct GridCtx {
     for (int i = t0; i < ns; i += st) q[i] = cv.at(sp[i]);
     ++applies;
   }
+  template <class S> CS_NOINL void cg_iterate(S& s) {
+    cg_loop(*this, s, [this](const T* d, T* q) { H(d, q); });
+  }
   CS_NOINL double RES(const T* x) {
     if (x) {
       scatter(x);

@@ -37,6 +37,48 @@ struct Params {
 };
 
 // ------------------------------------------------------------------ CG ------
+// State of one CG solve (Algorithm 1 lines 13-22) while it iterates.
+template <typename T> struct CgState {
+  T *x, *r, *d, *q;
+  double rr, thr;  // r.r and the stopping threshold tol^2 ||b||^2 (R6, R7)
+  int ns, cap, j;
+  unsigned status;
+};
+
+// The CG iteration loop, generic over the context; Hf(d, q) applies
+// q = H d on the context's remembered support.  Each context runs it from its
+// cg_iterate(): the grid context directly, the CTA context from an out-of-line
+// instance per transform length with the sandwich inlined.
+template <class Ctx, typename T, class HFn>
+CS_DEV void cg_loop(Ctx& c, CgState<T>& s, HFn&& Hf) {
+  const int a0 = c.gtid, s0 = c.gnthr;
+  T *xx = s.x, *rv = s.r, *dv = s.d, *qv = s.q;
+  const int n = s.ns;
+  while (true) {
+    if (!(s.rr > s.thr)) break;                                            // line 15 (R6, R7)
+    if (s.j >= s.cap) { s.status |= CS_DEV_CG_CAP; break; }
+    Hf(dv, qv);                                                            // H d_j
+    double dq = 0;
+    for (int i = a0; i < n; i += s0) dq += (double)dv[i] * (double)qv[i];
+    dq = c.sum(dq);
+    if (!(dq > 0.0)) { s.status |= CS_DEV_CG_BREAKDOWN; break; }
+    const T alpha = (T)(s.rr / dq);                                        // line 16
+    double rr2 = 0;
+    for (int i = a0; i < n; i += s0) {
+      xx[i] += alpha * dv[i];                                              // line 17
+      const T ri = rv[i] - alpha * qv[i];                                  // line 18
+      rv[i] = ri;
+      rr2 += (double)ri * (double)ri;
+    }
+    rr2 = c.sum(rr2);
+    const T beta = (T)(rr2 / s.rr);                                        // line 19
+    for (int i = a0; i < n; i += s0) dv[i] = rv[i] + beta * dv[i];        // line 20
+    s.rr = rr2;
+    s.j += 1;                                                              // line 21
+    if (!(rr2 == rr2)) { s.status |= CS_DEV_CG_BREAKDOWN; break; }
+  }
+}
+
 // Solves H x = b on supp (b = c0[supp]).  x holds the warm start on entry.
 // If r_given, r holds r0 = b - H x0 on entry (free when x0 is the previous LS
 // iterate and r = c[supp], see pursuits.py); otherwise one H apply computes it.
@@ -62,62 +104,13 @@ CS_NOINL void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q
   }
   bb = ctx.sum(bb);
   rr = ctx.sum(rr);
-  // Loop state lives in a volatile local record across the (out-of-line) sandwich
-  // H d: nothing is register-live across the call, so ptxas's inter-procedural
-  // allocator leaves the FFT its full register budget.
-  struct Keep {
-    Ctx* c;
-    Stats* st;
-    T *x, *r, *d, *q;
-    double rr, thr;
-    int ns, cap, j, t0, sd;
-  };
-  volatile Keep kp;
-  kp.c = &ctx;
-  kp.st = &st;
-  kp.x = x; kp.r = r; kp.d = d; kp.q = q;
-  kp.rr = rr;
-  kp.thr = P.tol * P.tol * bb;
-  kp.ns = ns;
-  kp.cap = P.cg_cap > 0 ? P.cg_cap : ns + 50;
-  kp.j = 0;
-  kp.t0 = t0;
-  kp.sd = sd;
-  while (true) {
-    Ctx& c = *kp.c;
-    const double rr0 = kp.rr;
-    if (!(rr0 > kp.thr)) break;                                            // line 15 (R6, R7)
-    if (kp.j >= kp.cap) { kp.st->status |= CS_DEV_CG_CAP; break; }
-    c.H(kp.d, kp.q);                                                       // H d_j (out of line)
-    Ctx& c2 = *kp.c;
-    T* xx = kp.x; T* rv = kp.r; T* dv = kp.d; T* qv = kp.q;
-    const int n = kp.ns, a0 = kp.t0, s0 = kp.sd;
-    double dq = 0;
-    for (int i = a0; i < n; i += s0) dq += (double)dv[i] * (double)qv[i];
-    dq = c2.sum(dq);
-    if (!(dq > 0.0)) { kp.st->status |= CS_DEV_CG_BREAKDOWN; break; }
-    const double rrc = kp.rr;
-    const T alpha = (T)(rrc / dq);                                         // line 16
-    double rr2 = 0;
-    for (int i = a0; i < n; i += s0) {
-      xx[i] += alpha * dv[i];                                              // line 17
-      T ri = rv[i] - alpha * qv[i];                                        // line 18
-      rv[i] = ri;
-      rr2 += (double)ri * (double)ri;
-    }
-    rr2 = c2.sum(rr2);
-    const T beta = (T)(rr2 / kp.rr);                                       // line 19
-    for (int i = a0; i < n; i += s0) dv[i] = rv[i] + beta * dv[i];        // line 20
-    kp.rr = rr2;
-    kp.j = kp.j + 1;                                                       // line 21
-    if (!(rr2 == rr2)) { kp.st->status |= CS_DEV_CG_BREAKDOWN; break; }
-  }
+  CgState<T> cs_{x, r, d, q, rr, P.tol * P.tol * bb, ns, P.cg_cap > 0 ? P.cg_cap : ns + 50, 0, 0u};
+  ctx.cg_iterate(cs_);                                                     // lines 14-22
+  st.status |= cs_.status;
   ctx.sync();
-  const int jj = kp.j;
-  const double rrf = kp.rr;
-  st.cg_iters += jj;
+  st.cg_iters += cs_.j;
   st.cg_solves += 1;
-  double rel = bb > 0 ? sqrt(rrf / bb) : 0.0;
+  double rel = bb > 0 ? sqrt(cs_.rr / bb) : 0.0;
   if (rel > st.rel_max) st.rel_max = rel;
 }
 

@@ -177,8 +177,8 @@ template <typename T> struct SwIO {
 };
 
 template <typename T, int LOG2L, int MODE, bool ZERO>
-CS_NOINL double sw_sandwich_t(C2<T>* gbuf, const TwTable<T> gtw, const TwTable<T> gtw4, const MidCtx<T> gm,
-                              const SwIO<T> gio) {
+CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4, const MidCtx<T>& gm,
+                      const SwIO<T>& gio) {
   using SP = SwPlan<LOG2L>;
   constexpr int L = 1 << LOG2L, N = 2 * L;
   // every pointer except m.y / m.yout is shared memory in Tier S
@@ -224,6 +224,12 @@ CS_NOINL double sw_sandwich_t(C2<T>* gbuf, const TwTable<T> gtw, const TwTable<T
     }
   }
   return rn2;
+}
+
+template <typename T, int LOG2L, int MODE, bool ZERO>
+CS_NOINL double sw_sandwich_t(C2<T>* gbuf, const TwTable<T> gtw, const TwTable<T> gtw4, const MidCtx<T> gm,
+                              const SwIO<T> gio) {
+  return sw_body<T, LOG2L, MODE, ZERO>(gbuf, gtw, gtw4, gm, gio);
 }
 
 // runtime dispatch over log2 L in [LO, HI]
