@@ -70,6 +70,10 @@ CS_DEV int64_t row_rank(const uint32_t* mask, const int32_t* prefix, int64_t k) 
   return (int64_t)prefix[k >> 5] + __popc(below);
 }
 
+// Two-pass top-K of the CTA context (select.cuh): first-digit bins, candidate cap.
+constexpr int TOPK_BINS = 1024;
+constexpr int TOPK_CAP = 1024;
+
 // Order-preserving keys of |v| (sign cleared, +1 so that key 0 means "excluded";
 // NaN sorts above +inf).  64-bit keys for double keep the full order.
 template <typename T> struct KeyT;
@@ -79,6 +83,15 @@ template <> struct KeyT<double> { using type = uint64_t; };
 CS_DEV uint32_t full_key(float v) { return (__float_as_uint(v) & 0x7fffffffu) + 1u; }
 CS_DEV uint64_t full_key(double v) {
   return ((uint64_t)__double_as_longlong(v) & 0x7fffffffffffffffull) + 1ull;
+}
+// A 10-bit digit that is monotone non-decreasing in the key (0 for key 0): the
+// exponent and two mantissa bits of |v| as a float (double: rounded to float,
+// which preserves order up to ties).
+CS_DEV unsigned key_digit10(uint32_t k) { return k >> 21; }
+CS_DEV unsigned key_digit10(uint64_t k) {
+  if (k == 0) return 0;
+  const float f = (float)__longlong_as_double((long long)(k - 1ull));
+  return (__float_as_uint(f) + 1u) >> 21;
 }
 
 }  // namespace cs

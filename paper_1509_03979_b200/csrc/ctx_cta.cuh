@@ -41,6 +41,11 @@ template <typename T> struct CtaCtx {
   int64_t* redi;     // [33]
   Key* redk;         // [32]
   unsigned* hist;    // [256]
+  unsigned* h1;      // [TOPK_BINS]  first-digit histogram of the two-pass top-K
+  Key* ckey;         // [TOPK_CAP]   boundary-bucket candidates
+  int* cidx;         // [TOPK_CAP]
+  int* ccnt;         // [1]
+  static constexpr bool kTopkFast = true;
   int64_t* pick;     // [4]
   // global state of this problem
   const T* y;        // [M]

@@ -99,6 +99,7 @@ template <typename T> struct GridCtx {
   int applies;
 
   CS_DEV void sync() { grid_barrier(g.bar); }
+  static constexpr bool kTopkFast = false;
 
   // block-level deterministic sum; result valid in thread 0
   CS_DEV double block_sum(double v) {

@@ -61,10 +61,107 @@ CS_DEV void hist_add_warp(unsigned* hist, unsigned digit) {
   if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[digit], (unsigned)__popc(peers));
 }
 
+// ---- two-pass top-K for the CTA context ----
+// pass 1: 1024-bin histogram of a 10-bit digit that is monotone in the key;
+//         the boundary bin b1 has count(> b1) < K <= count(>= b1);
+// pass 2: indices with digit > b1 are selected (ballot -> bitmask), those with
+//         digit == b1 are appended to a candidate list;
+// then the `need` = K - count(> b1) largest candidates by (key, lowest index)
+// are found by counting, per candidate, the candidates that beat it.
+// Returns false (nothing written) if the boundary bin holds > TOPK_CAP entries
+// or fewer than K keys are non-zero; the caller then runs the radix path.
+template <class Ctx, class KeyFn>
+CS_DEV bool topk_cta_fast(Ctx& ctx, int n, int K, KeyFn key, uint32_t* out_bits) {
+  using Key = decltype(key(int64_t(0)));
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  unsigned* h = shp(ctx.h1);
+  Key* ck = shp(ctx.ckey);
+  int* ci = shp(ctx.cidx);
+  int* cc = shp(ctx.ccnt);
+  int64_t* pk = shp(ctx.pick);
+  for (int i = tid; i < TOPK_BINS; i += nt) h[i] = 0;
+  if (tid == 0) cc[0] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += nt) {
+    const Key k = key(i);
+    if (k) hist_add_warp(h, key_digit10(k));
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // lane l owns bins [1023 - 32 l - 31, 1023 - 32 l], scanned from the top
+    int s = 0;
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) s += (int)h[TOPK_BINS - 1 - 32 * lane - i];
+    int inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const unsigned ball = __ballot_sync(0xffffffffu, inc >= K);
+    const int fl = ball ? __ffs(ball) - 1 : -1;
+    if (lane == 0 && fl < 0) { pk[0] = -1; pk[1] = 0; pk[2] = 0; }
+    if (lane == fl) {
+      int cu = inc - s;
+      for (int i = 0; i < 32; ++i) {
+        const int b = TOPK_BINS - 1 - 32 * lane - i;
+        const int c = (int)h[b];
+        if (cu + c >= K) { pk[0] = b; pk[1] = cu; pk[2] = c; break; }
+        cu += c;
+      }
+    }
+  }
+  __syncthreads();
+  const int b1 = (int)pk[0], above = (int)pk[1], inb = (int)pk[2];
+  __syncthreads();  // pick[] is reused by later collectives
+  if (b1 < 0 || inb > TOPK_CAP) return false;
+  const int need = K - above;
+  const int nwords = (n + 31) >> 5;
+  for (int w = warp; w < nwords; w += nwarp) {
+    const int i = w * 32 + lane;
+    const Key k = (i < n) ? key(i) : Key(0);
+    const int d = k ? (int)key_digit10(k) : -1;
+    const unsigned sel = __ballot_sync(0xffffffffu, d > b1);
+    const unsigned cnd = __ballot_sync(0xffffffffu, d == b1);
+    if (lane == 0) out_bits[w] = sel;
+    if (cnd) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(cc, __popc(cnd));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (d == b1) {
+        const int at = base + __popc(cnd & ((1u << lane) - 1u));
+        ck[at] = k;
+        ci[at] = i;
+      }
+    }
+  }
+  __syncthreads();
+  const int C = cc[0];
+  for (int c = tid; c < C; c += nt) {
+    const Key kc = ck[c];
+    const int ic = ci[c];
+    bool take = (need >= C);
+    if (!take) {
+      int beat = 0;
+      for (int j = 0; j < C; ++j) {
+        const Key kj = ck[j];
+        beat += (kj > kc) || (kj == kc && ci[j] < ic);
+      }
+      take = beat < need;
+    }
+    if (take) atomicOr(&out_bits[ic >> 5], 1u << (ic & 31));
+  }
+  __syncthreads();
+  return true;
+}
+
 // key(i) for i in [0, n); key 0 means "never select".  Requires at least K
 // non-zero keys.  out_bits must hold ceil(n/32) words; fully overwritten.
 template <class Ctx, class KeyFn>
 CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_bits) {
+  if constexpr (Ctx::kTopkFast) {
+    if (topk_cta_fast(ctx, (int)n, (int)K, key, out_bits)) return;
+  }
   using Key = decltype(key(int64_t(0)));
   constexpr int NB = (int)sizeof(Key) * 8;
   Key prefix = 0, pmask = 0;

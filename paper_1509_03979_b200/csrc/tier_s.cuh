@@ -18,7 +18,7 @@ CS_HD int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 // Shared-memory layout of a Tier S block (computed identically on host and device).
 struct SLayout {
-  int64_t Z, twLlo, twLhi, tw4lo, tw4hi, sign, rmask, prefix, redd, redi, redk, hist, pick;
+  int64_t Z, twLlo, twLhi, tw4lo, tw4hi, sign, rmask, prefix, redd, redi, redk, hist, pick, h1, ckey, cidx, ccnt;
   int64_t S, S2, U, x, x2, xU, r, d, q, b, Sbits, Ubits, Pbits;
   int64_t bytes;
   int nthreads;
@@ -43,6 +43,12 @@ CS_HD SLayout s_layout(int64_t N, int K, int ucap, bool pursuit) {
   s.redk = take(32 * 8);
   s.hist = take(256 * 4);
   s.pick = take(4 * 8);
+  // two-pass top-K (select.cuh topk_cta_fast): 1024-bin first-digit histogram and
+  // the boundary-bucket candidates (key, index)
+  s.h1 = take(TOPK_BINS * 4);
+  s.ckey = take((int64_t)TOPK_CAP * sizeof(typename KeyT<T>::type));
+  s.cidx = take((int64_t)TOPK_CAP * 4);
+  s.ccnt = take(16);
   if (pursuit) {
     s.S = take((int64_t)K * 4);
     s.S2 = take((int64_t)K * 4);
@@ -103,6 +109,10 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   c.redk = reinterpret_cast<typename CtaCtx<T>::Key*>(smem + lay.redk);
   c.hist = reinterpret_cast<unsigned*>(smem + lay.hist);
   c.pick = reinterpret_cast<int64_t*>(smem + lay.pick);
+  c.h1 = reinterpret_cast<unsigned*>(smem + lay.h1);
+  c.ckey = reinterpret_cast<typename CtaCtx<T>::Key*>(smem + lay.ckey);
+  c.cidx = reinterpret_cast<int*>(smem + lay.cidx);
+  c.ccnt = reinterpret_cast<int*>(smem + lay.ccnt);
   c.in_supp = nullptr;
   c.in_ns = 0;
   c.applies = 0;
