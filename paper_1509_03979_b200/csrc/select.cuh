@@ -67,7 +67,7 @@ CS_DEV void hist_add_warp(unsigned* hist, unsigned digit) {
 // pass 2: indices with digit > b1 are selected (ballot -> bitmask), those with
 //         digit == b1 are appended to a candidate list;
 // then the `need` = K - count(> b1) largest candidates by (key, lowest index)
-// are found by counting, per candidate, the candidates that beat it.
+// are found by a byte radix select over the candidate list only.
 // Returns false (nothing written) if the boundary bin holds > TOPK_CAP entries
 // or fewer than K keys are non-zero; the caller then runs the radix path.
 template <class Ctx, class KeyFn>
@@ -137,19 +137,46 @@ CS_DEV bool topk_cta_fast(Ctx& ctx, int n, int K, KeyFn key, uint32_t* out_bits)
   }
   __syncthreads();
   const int C = cc[0];
+  if (need >= C) {
+    for (int c = tid; c < C; c += nt) atomicOr(&out_bits[ci[c] >> 5], 1u << (ci[c] & 31));
+    __syncthreads();
+    return true;
+  }
+  // MSB-first byte radix select of the `need` largest candidate keys
+  unsigned* hist = shp(ctx.hist);
+  constexpr int NB = (int)sizeof(Key) * 8;
+  Key prefix = 0, pmask = 0;
+  int64_t needr = need, n_eq = 0;
+  for (int shift = NB - 8; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += nt) hist[i] = 0;
+    __syncthreads();
+    for (int c = tid; c < C; c += nt) {
+      const Key k = ck[c];
+      if ((k & pmask) == prefix) hist_add_warp(hist, (unsigned)((k >> shift) & 255));
+    }
+    __syncthreads();
+    int64_t dsel, cum, hsel;
+    hist_pick(hist, pk, needr, dsel, cum, hsel);
+    needr -= cum;
+    n_eq = hsel;
+    prefix |= (Key)dsel << shift;
+    pmask |= (Key)255 << shift;
+  }
+  const Key thr = prefix;  // the need-th largest candidate key
   for (int c = tid; c < C; c += nt) {
     const Key kc = ck[c];
-    const int ic = ci[c];
-    bool take = (need >= C);
-    if (!take) {
-      int beat = 0;
-      for (int j = 0; j < C; ++j) {
-        const Key kj = ck[j];
-        beat += (kj > kc) || (kj == kc && ci[j] < ic);
+    bool take = kc > thr;
+    if (kc == thr) {
+      if (n_eq == needr) {
+        take = true;
+      } else {  // ties: the lowest indices win (R12, R32)
+        const int ic = ci[c];
+        int below = 0;
+        for (int j = 0; j < C; ++j) below += (ck[j] == thr) && (ci[j] < ic);
+        take = below < needr;
       }
-      take = beat < need;
     }
-    if (take) atomicOr(&out_bits[ic >> 5], 1u << (ic & 31));
+    if (take) atomicOr(&out_bits[ci[c] >> 5], 1u << (ci[c] & 31));
   }
   __syncthreads();
   return true;
