@@ -57,13 +57,18 @@ template <typename T> struct CtaCtx {
 
   CS_DEV void sync() { __syncthreads(); }
 
+  int rbank;  // alternating reduction bank (sum)
+  // Deterministic block sum (fixed order).  Two alternating banks of partials: the
+  // next sum writes the other bank, and the one after that is ordered behind this
+  // sum's readers by the next sum's barrier — so one barrier per reduction.
   CS_DEV double sum(double v) {
     v = warp_sum(v);
-    if (lane == 0) redd[gwarp] = v;
+    double* rb = shp(redd) + 32 * rbank;
+    rbank ^= 1;
+    if (lane == 0) rb[gwarp] = v;
     __syncthreads();
     double t = 0;
-    for (int w = 0; w < gnwarps; ++w) t += redd[w];
-    __syncthreads();
+    for (int w = 0; w < gnwarps; ++w) t += rb[w];
     return t;
   }
   // argmax of (key, idx): larger key wins, ties -> smaller idx.  Returns idx (-1 if all keys 0).
@@ -171,9 +176,26 @@ template <typename T> struct CtaCtx {
     const int* sp = in_supp;
     const uint32_t* sg = sign;
     const int ns = in_ns;
-    cg_loop(*this, s, [&](const T* d, T* q) {
+    // register copy of the fields the loop touches (the context itself lives in
+    // local memory behind a generic pointer)
+    struct Lc {
+      int gtid, gnthr, lane, gwarp, gnwarps, rbank;
+      double* redd;
+      CS_DEV double sum(double v) {
+        v = warp_sum(v);
+        double* rb = redd + 32 * rbank;
+        rbank ^= 1;
+        if (lane == 0) rb[gwarp] = v;
+        __syncthreads();
+        double t = 0;
+        for (int w = 0; w < gnwarps; ++w) t += rb[w];
+        return t;
+      }
+    } lc{gtid, gnthr, lane, gwarp, gnwarps, rbank, shp(redd)};
+    cg_loop(lc, s, [&](const T* d, T* q) {
       sw_body<T, LOG2L, MID_H, false>(z, tl, t4, m, SwIO<T>{sp, ns, sg, d, q});
     });
+    rbank = lc.rbank;
     applies += s.j;
   }
   template <int LO, int HI, class S> CS_DEV void cg_dispatch(S& s) {

@@ -38,7 +38,7 @@ CS_HD SLayout s_layout(int64_t N, int K, int ucap, bool pursuit) {
   s.sign = take(nw * 4);
   s.rmask = take(nw * 4);
   s.prefix = take(nw * 4);
-  s.redd = take(32 * 8);
+  s.redd = take(2 * 32 * 8);  // two banks: one barrier per reduction
   s.redi = take(33 * 8);
   s.redk = take(32 * 8);
   s.hist = take(256 * 4);
@@ -113,6 +113,7 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   c.ckey = reinterpret_cast<typename CtaCtx<T>::Key*>(smem + lay.ckey);
   c.cidx = reinterpret_cast<int*>(smem + lay.cidx);
   c.ccnt = reinterpret_cast<int*>(smem + lay.ccnt);
+  c.rbank = 0;
   c.in_supp = nullptr;
   c.in_ns = 0;
   c.applies = 0;
