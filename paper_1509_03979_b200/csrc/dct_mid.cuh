@@ -21,6 +21,7 @@
 #pragma once
 #include "cs_common.cuh"
 #include "fft_cta.cuh"
+#include "layout_s.cuh"
 
 namespace cs {
 
@@ -116,6 +117,18 @@ template <typename T> struct MidK {
   T cout[2]; // (1/2, r2/2) / s_k / L * 2: returned = cout * (y - s X)          (RES)
   T hH[2];   // invL * (1/4, 1/8): returned = [sel] raw * hH                     (H)
 };
+// compile-time constants for N = 2^LOG2N
+template <typename T, int LOG2N> CS_DEV MidK<T> make_midk_c() {
+  constexpr double r2 = 0.70710678118654752440, sk = sqrt_pow2(1 - LOG2N), invL = 2.0 / (double)(1ll << LOG2N);
+  MidK<T> c;
+  c.scx[0] = (T)(sk * 0.5);
+  c.scx[1] = (T)(sk * r2 * 0.5);
+  c.cout[0] = (T)(invL / sk * 0.5);
+  c.cout[1] = (T)(invL / sk * r2 * 0.5);
+  c.hH[0] = (T)(invL * 0.25);
+  c.hH[1] = (T)(invL * 0.125);
+  return c;
+}
 template <typename T> CS_DEV MidK<T> make_midk(int N) {
   MidK<T> c;
   const double r2 = 0.70710678118654752440, sk = sqrt(2.0 / (double)N), invL = 2.0 / (double)N;
@@ -169,6 +182,22 @@ CS_DEV void mid_pair2(C2<T>& Zk, C2<T>& Zkk, int k, C2<T> a, C2<T> w, const MidC
     Zk = mk<T>(E.x - Od.y, E.y + Od.x);                           // E + i Od
     Zkk = mk<T>(E.x + Od.y, Od.x - E.y);                          // conj(E - i Od)
   }
+}
+
+template <typename T, int LOG2N> CS_DEV MidCtx<T> make_mid_c(const uint32_t* rowmask, const int32_t* prefix,
+                                                           const T* y, T* yout) {
+  MidCtx<T> m;
+  m.rowmask = rowmask;
+  m.prefix = prefix;
+  m.y = y;
+  m.yout = yout;
+  m.N = 1ll << LOG2N;
+  m.s0 = (T)sqrt_pow2(-LOG2N);
+  m.sk = (T)sqrt_pow2(1 - LOG2N);
+  m.inv_s0 = (T)sqrt_pow2(LOG2N);
+  m.inv_sk = (T)sqrt_pow2(LOG2N - 1);
+  m.invL = (T)(2.0 / (double)(1ll << LOG2N));
+  return m;
 }
 
 template <typename T> CS_DEV MidCtx<T> make_mid(int64_t N, const uint32_t* rowmask,

@@ -28,6 +28,7 @@
 #include "cs_common.cuh"
 #include "dct_mid.cuh"
 #include "fft_cta.cuh"
+#include "layout_s.cuh"
 
 namespace cs {
 
@@ -98,7 +99,7 @@ CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, 
   constexpr int L = 1 << LOG2L, H = L / 2, U = SP::U, UPT = SP::UPT;
   static_assert(L >= 4, "N >= 8");
   const int tid = threadIdx.x;
-  const MidK<T> cst = make_midk<T>(2 * L);
+  const MidK<T> cst = make_midk_c<T, LOG2L + 1>();
   double rn2 = 0;
   C2<T> A0[UPT], A1[UPT], B0[UPT], B1[UPT];
 #pragma unroll
@@ -181,19 +182,26 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
                       const SwIO<T>& gio) {
   using SP = SwPlan<LOG2L>;
   constexpr int L = 1 << LOG2L, N = 2 * L;
-  // every pointer except m.y / m.yout is shared memory in Tier S
-  C2<T>* buf = shp(gbuf);
-  const TwTable<T> tw{shp(gtw.lo), shp(gtw.hi)}, tw4{shp(gtw4.lo), shp(gtw4.hi)};
-  MidCtx<T> m = gm;
-  m.rowmask = shp(gm.rowmask);
-  m.prefix = shp(gm.prefix);
+  // The FFT buffer, twiddle tables and operator metadata sit at compile-time offsets
+  // of the Tier S layout (layout_s.cuh); gbuf / gtw / gtw4 / gm name the same objects.
+  constexpr SFix F = s_fixed<T>(N);
+  (void)gbuf; (void)gtw; (void)gtw4;
+  C2<T>* buf = reinterpret_cast<C2<T>*>(cs_smem_base + F.Z);
+  const TwTable<T> tw{reinterpret_cast<const C2<T>*>(cs_smem_base + F.twLlo),
+                      reinterpret_cast<const C2<T>*>(cs_smem_base + F.twLhi)};
+  const TwTable<T> tw4{reinterpret_cast<const C2<T>*>(cs_smem_base + F.tw4lo),
+                       reinterpret_cast<const C2<T>*>(cs_smem_base + F.tw4hi)};
+  const MidCtx<T> m = make_mid_c<T, LOG2L + 1>(reinterpret_cast<const uint32_t*>(cs_smem_base + F.rmask),
+                                                reinterpret_cast<const int32_t*>(cs_smem_base + F.prefix),
+                                                gm.y, gm.yout);
+  const uint32_t* signs = reinterpret_cast<const uint32_t*>(cs_smem_base + F.sign);
   const int tid = threadIdx.x;
   T* zb = reinterpret_cast<T*>(buf);
   auto zt = [](int p) { return 2 * swz<T>(p >> 1) + (p & 1); };
   if constexpr (!ZERO) {
     if (gio.vin) {
       const int* supp = shp(gio.supp);
-      const uint32_t* sign = shp(gio.sign);
+      const uint32_t* sign = signs;
       const T* vin = shp(gio.vin);
       for (int i = tid; i < L; i += SW_NT) buf[i] = mk<T>(0, 0);
       __syncthreads();
@@ -214,7 +222,7 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
     sw_remainder<T, LOG2L, true>(buf, tw, 1 + 4 * SP::Q);
     if (gio.vout) {
       const int* supp = shp(gio.supp);
-      const uint32_t* sign = shp(gio.sign);
+      const uint32_t* sign = signs;
       T* vout = shp(gio.vout);
       for (int i = tid; i < gio.ns; i += SW_NT) {
         const int j = supp[i];

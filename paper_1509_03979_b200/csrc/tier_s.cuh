@@ -7,6 +7,7 @@
 #include <string>
 
 #include "ctx_cta.cuh"
+#include "layout_s.cuh"
 #include "pursuit.cuh"
 
 namespace cs {
@@ -27,28 +28,14 @@ struct SLayout {
 template <typename T>
 CS_HD SLayout s_layout(int64_t N, int K, int ucap, bool pursuit) {
   SLayout s;
-  const int64_t L = N / 2, nw = (N + 31) / 32, cs2 = sizeof(T) * 2, ts = sizeof(T);
-  int64_t o = 0;
+  const int64_t nw = (N + 31) / 32, ts = sizeof(T);
+  const SFix f = s_fixed<T>(N);
+  s.Z = f.Z; s.twLlo = f.twLlo; s.twLhi = f.twLhi; s.tw4lo = f.tw4lo; s.tw4hi = f.tw4hi;
+  s.sign = f.sign; s.rmask = f.rmask; s.prefix = f.prefix; s.redd = f.redd; s.redi = f.redi;
+  s.redk = f.redk; s.hist = f.hist; s.pick = f.pick; s.h1 = f.h1; s.ckey = f.ckey; s.cidx = f.cidx;
+  s.ccnt = f.ccnt;
+  int64_t o = f.end;
   auto take = [&](int64_t bytes) { int64_t r = o; o = align_up(o + bytes, 16); return r; };
-  s.Z = take(L * cs2);
-  s.twLlo = take(64 * cs2);
-  s.twLhi = take((L >= 64 ? L / 64 : 1) * cs2);
-  s.tw4lo = take(64 * cs2);
-  s.tw4hi = take((L / 128 + 1) * cs2);
-  s.sign = take(nw * 4);
-  s.rmask = take(nw * 4);
-  s.prefix = take(nw * 4);
-  s.redd = take(2 * 32 * 8);  // two banks: one barrier per reduction
-  s.redi = take(33 * 8);
-  s.redk = take(32 * 8);
-  s.hist = take(256 * 4);
-  s.pick = take(4 * 8);
-  // two-pass top-K (select.cuh topk_cta_fast): 1024-bin first-digit histogram and
-  // the boundary-bucket candidates (key, index)
-  s.h1 = take(TOPK_BINS * 4);
-  s.ckey = take((int64_t)TOPK_CAP * sizeof(typename KeyT<T>::type));
-  s.cidx = take((int64_t)TOPK_CAP * 4);
-  s.ccnt = take(16);
   if (pursuit) {
     s.S = take((int64_t)K * 4);
     s.S2 = take((int64_t)K * 4);
