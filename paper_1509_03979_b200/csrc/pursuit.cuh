@@ -50,7 +50,8 @@ template <typename T> struct CgState {
 // cg_iterate(): the grid context directly, the CTA context from an out-of-line
 // instance per transform length with the sandwich inlined.
 template <class Ctx, typename T, class HFn>
-CS_DEV void cg_loop(Ctx& c, CgState<T>& s, HFn&& Hf) {
+CS_DEV void cg_loop(Ctx& c, CgState<T>& s_io, HFn&& Hf) {
+  CgState<T> s = s_io;  // register copy (s_io lives in the caller's frame)
   const int a0 = c.gtid, s0 = c.gnthr;
   T *xx = s.x, *rv = s.r, *dv = s.d, *qv = s.q;
   const int n = s.ns;
@@ -77,6 +78,7 @@ CS_DEV void cg_loop(Ctx& c, CgState<T>& s, HFn&& Hf) {
     s.j += 1;                                                              // line 21
     if (!(rr2 == rr2)) { s.status |= CS_DEV_CG_BREAKDOWN; break; }
   }
+  s_io = s;
 }
 
 // Solves H x = b on supp (b = c0[supp]).  x holds the warm start on entry.
