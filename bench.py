@@ -130,6 +130,7 @@ def run_ours(args):
     import __graft_entry__
     __graft_entry__.build()
     import paper_1509_03979_b200 as cs
+    from paper_1509_03979_b200 import dist as csd
 
     rank, world, local = dist_env()
     if world > 1:
@@ -144,7 +145,8 @@ def run_ours(args):
 
     # ---- synthetic inputs (rank-disjoint problem indices), y formed by the product operator
     t0 = time.time()
-    probs = cs_inputs.make_batch(cfg, b0=rank * B, count=B)
+    b0, B = csd.shard(B * world, rank, world)          # contiguous block of problem indices
+    probs = cs_inputs.make_batch(cfg, b0=b0, count=B)
     bits = torch.from_numpy(np.stack([p.sign_bits.view(np.int32) for p in probs])).to(dev)
     rows = torch.from_numpy(np.stack([p.rows for p in probs]).astype(np.int32)).to(dev)
     S = torch.from_numpy(np.stack([p.s for p in probs])).to(dev, td)
@@ -168,14 +170,12 @@ def run_ours(args):
     gather_buf = None
 
     def gather(r):
+        # the only collective: one all-gather of fixed-size result records
         nonlocal gather_buf
         if world == 1:
             return
-        flat = torch.cat([r.support.view(torch.uint8).reshape(B, -1), r.values.view(torch.uint8).reshape(B, -1),
-                          r.report_dev.reshape(B, -1)], dim=1).reshape(-1)
-        if gather_buf is None:
-            gather_buf = torch.empty(world * flat.numel(), dtype=torch.uint8, device=dev)
-        dist.all_gather_into_tensor(gather_buf, flat)
+        rec = csd.pack_records(r.support, r.values, r.report_dev)
+        gather_buf = csd.gather_records(rec, world, out=gather_buf.reshape(-1) if gather_buf is not None else None)
 
     for _ in range(max(args.warmup, 0)):
         gather(step())
