@@ -76,28 +76,63 @@ template <typename T> bool tier_s_fits(int64_t N, int K, int64_t ucap, bool purs
   return s.bytes <= 227 * 1024;
 }
 
-__global__ void k_rows_mask(int64_t N, int64_t M, int64_t B, int64_t nw, const int32_t* rows,
-                            const uint32_t* sign_in, uint32_t* meta, int* err) {
+// bit position of DCT index k in the stored row mask: natural for Tier S, the
+// four-step transposed order for Tier L (tier_s.cuh OpMeta)
+struct TPos {
+  int s1, tsh;
+  __host__ __device__ int64_t operator()(int64_t k) const {
+    return ((k & ((int64_t(1) << s1) - 1)) << tsh) | (k >> s1);
+  }
+};
+TPos tpos_of(int64_t N) {
+  TPos t{0, 0};
+  if (N > TIER_S_MAX_N) {
+    const LGeom g = l_geom(N);
+    t.s1 = ilog2(g.L1);
+    t.tsh = ilog2(2 * g.L2);
+  }
+  return t;
+}
+
+__global__ void k_rows_mask(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t stride, TPos tp,
+                            const int32_t* rows, const uint32_t* sign_in, uint32_t* meta, int* err) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < B * nw) {  // copy sign words
     int64_t b = i / nw, w = i % nw;
-    meta[b * 3 * nw + w] = sign_in[b * nw + w];
+    meta[b * stride + w] = sign_in[b * nw + w];
   }
   if (i >= B * M) return;
   int64_t b = i / M, m = i % M;
   int32_t r = rows[i];
   bool ok = (r >= 0) && (r < N) && (m == 0 || rows[i - 1] < r);
   if (!ok) { atomicOr(err, 1); return; }
-  atomicOr(&meta[b * 3 * nw + nw + (r >> 5)], 1u << (r & 31));
+  const int64_t t = tp(r);
+  atomicOr(&meta[b * stride + nw + (t >> 5)], 1u << (t & 31));
+}
+
+// Tier L: tperm[rank of row m in the transposed order] = m
+__global__ void k_rows_tperm(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t stride, TPos tp, const int32_t* rows,
+                             uint32_t* meta) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= B * M) return;
+  int64_t b = i / M, m = i % M;
+  if (rows[i] < 0 || rows[i] >= N) return;  // invalid rows: reported by k_rows_mask
+  const uint32_t* mask = meta + b * stride + nw;
+  const int32_t* pre = reinterpret_cast<const int32_t*>(meta + b * stride + 2 * nw);
+  int32_t* perm = reinterpret_cast<int32_t*>(meta + b * stride + 3 * nw);
+  const int64_t t = tp(rows[i]);
+  const uint32_t w = mask[t >> 5];
+  const int32_t rank = pre[t >> 5] + __popc((t & 31) ? (w & ((1u << (t & 31)) - 1u)) : 0u);
+  perm[rank] = (int32_t)m;
 }
 
 // exclusive prefix of popcounts per instance: one block per instance
-__global__ void k_rows_prefix(int64_t nw, uint32_t* meta) {
+__global__ void k_rows_prefix(int64_t nw, int64_t stride, uint32_t* meta) {
   __shared__ int32_t wsum[32];
   __shared__ int32_t carry;
   const int64_t b = blockIdx.x;
-  const uint32_t* mask = meta + b * 3 * nw + nw;
-  int32_t* pre = reinterpret_cast<int32_t*>(meta + b * 3 * nw + 2 * nw);
+  const uint32_t* mask = meta + b * stride + nw;
+  int32_t* pre = reinterpret_cast<int32_t*>(meta + b * stride + 2 * nw);
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
@@ -125,12 +160,18 @@ __global__ void k_rows_prefix(int64_t nw, uint32_t* meta) {
 }
 
 
+int64_t meta_stride(int64_t N, int64_t M) {
+  const int64_t nw = (N + 31) / 32;
+  return 3 * nw + (N > TIER_S_MAX_N ? M : 0);
+}
+
 OpMeta meta_of(const cs_operator* op) {
   OpMeta m;
   m.base = op->meta;
   m.N = op->N;
   m.M = op->M;
   m.nw = op->nw;
+  m.stride = meta_stride(op->N, op->M);
   return m;
 }
 
@@ -212,7 +253,8 @@ size_t cs_operator_meta_bytes(int64_t N, int64_t M, int64_t batch) {
   (void)M;
   if (N <= 0 || batch <= 0) return 0;
   int64_t nw = (N + 31) / 32;
-  return (size_t)(align_up(batch * 3 * nw * 4, 256) + 256);
+  (void)nw;
+  return (size_t)(align_up(batch * meta_stride(N, M) * 4, 256) + 256);
 }
 
 cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
@@ -229,14 +271,20 @@ cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t nw = (N + 31) / 32;
   uint32_t* meta = reinterpret_cast<uint32_t*>(d_meta);
-  int* err = reinterpret_cast<int*>(reinterpret_cast<char*>(d_meta) + align_up(batch * 3 * nw * 4, 256));
+  const int64_t stride = meta_stride(N, M);
+  const TPos tp = tpos_of(N);
+  int* err = reinterpret_cast<int*>(reinterpret_cast<char*>(d_meta) + align_up(batch * stride * 4, 256));
   CS_CUDA(cudaMemsetAsync(d_meta, 0, meta_bytes, st));
   int64_t nthr = std::max(batch * M, batch * nw);
-  k_rows_mask<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(N, M, batch, nw, d_rows, d_sign_bits,
-                                                           meta, err);
+  k_rows_mask<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(N, M, batch, nw, stride, tp, d_rows,
+                                                           d_sign_bits, meta, err);
   CS_LAUNCHED();
-  k_rows_prefix<<<(unsigned)batch, 1024, 0, st>>>(nw, meta);
+  k_rows_prefix<<<(unsigned)batch, 1024, 0, st>>>(nw, stride, meta);
   CS_LAUNCHED();
+  if (N > TIER_S_MAX_N) {
+    k_rows_tperm<<<(unsigned)((batch * M + 255) / 256), 256, 0, st>>>(N, M, batch, nw, stride, tp, d_rows, meta);
+    CS_LAUNCHED();
+  }
   int herr = 0;
   CS_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   CS_CUDA(cudaStreamSynchronize(st));
@@ -268,7 +316,7 @@ cs_status cs_operator_info(const cs_operator* op, int64_t* N, int64_t* M, int64_
 
 size_t cs_operator_ws_bytes(const cs_operator* op, int precision) {
   if (!op || op->N <= TIER_S_MAX_N) return 0;
-  return precision ? tier_l_apply_ws_bytes<double>(op->N) : tier_l_apply_ws_bytes<float>(op->N);
+  return precision ? tier_l_apply_ws_bytes<double>(op->N, op->M) : tier_l_apply_ws_bytes<float>(op->N, op->M);
 }
 
 cs_status cs_operator_apply(const cs_operator* op, const float* d_x, float* d_y, void* d_ws,

@@ -67,6 +67,27 @@ template <typename T> struct GridScratch {
   int maxgrid;
 };
 
+// Tile copies with UNR independent loads in flight per thread before any store
+// (memory-level parallelism: one outstanding 8-byte load per thread caps a
+// persistent grid near 0.6 TB/s).
+template <int UNR, typename V, class LD, class ST>
+CS_DEV void staged(int n, LD&& ld, ST&& st) {
+  for (int e0 = threadIdx.x; e0 < n; e0 += UNR * (int)blockDim.x) {
+    V v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int e = e0 + u * (int)blockDim.x;
+      if (e < n) v[u] = ld(e);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int e = e0 + u * (int)blockDim.x;
+      if (e < n) st(e, v[u]);
+    }
+  }
+}
+constexpr int TL_UNR = 8;
+
 template <typename T> struct GridCtx {
   using Key = typename KeyT<T>::type;
   int gtid, gnthr, lane, gwarp, gnwarps;
@@ -76,7 +97,10 @@ template <typename T> struct GridCtx {
   const uint32_t* sign;
   const uint32_t* rowmask;
   const int32_t* prefix;
-  const T* y;
+  const T* y;        // measurements in the transposed row order (= yT during a recovery)
+  const int32_t* tperm;  // [M] y index of the t-th selected row in the transposed order
+  T* yT;             // [M] workspace
+  int s1, tsh;       // transposed mask position: t = (k mod 2^s1) << tsh | k >> s1
   T* c0;        // [N] Makhoul order
   T* U;         // [N] dense input (Makhoul order, sign applied)
   C2<T>* Wk;    // [L] four-step intermediate
@@ -286,23 +310,26 @@ template <typename T> struct GridCtx {
     const int ct = CT, lct = (ct == 4) ? 2 : 1;
     const int64_t l2 = L2, ntiles = L2 / ct;
     const int tile = (int)(L1 * ct);
+    C2<T>* sb = shp(buf);
+    C2<T>* wk = Wk;
+    const GTw<T> tf = twF;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t c0i = t * ct;
-      for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-        const int m1 = e >> lct, cc = e & (ct - 1);
-        buf[swz<T>(e)] = Uc[(int64_t)m1 * l2 + c0i + cc];
-      }
+      staged<TL_UNR, C2<T>>(tile, [&](int e) { return Uc[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]; },
+                            [&](int e, C2<T> v) { sb[swz<T>(e)] = v; });
       __syncthreads();
       col_fft<false>();
-      for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+      staged<TL_UNR, C2<T>>(tile, [&](int e) {
         const int64_t k1 = e >> lct, m2 = c0i + (e & (ct - 1));
-        Wk[k1 * l2 + m2] = cmul<T>(buf[swz<T>(e)], twF(k1 * m2));
-      }
+        return cmul<T>(sb[swz<T>(e)], tf(k1 * m2));
+      }, [&](int e, C2<T> v) { wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))] = v; });
       __syncthreads();
     }
   }
   template <int MODE> CS_NOINL double passB(bool zero_input, T* yout) {
     MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, yout);
+    m.s1 = s1;
+    m.tsh = tsh;
     double rn2 = 0;
     const int64_t nitems = L1 / 2 + 1;
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
@@ -311,38 +338,50 @@ template <typename T> struct GridCtx {
       const int B = self ? 1 : 2;
       const int lb = B - 1;  // log2 B
       const int n2 = (int)L2;
-      for (int e = threadIdx.x; e < B * n2; e += blockDim.x) {
-        const int64_t m2 = e >> lb, k1 = (e & lb) ? kb : ka;
-        buf[swz<T>(e)] = zero_input ? mk<T>(0, 0) : Wk[k1 * L2 + m2];
+      {
+        C2<T>* sb = shp(buf);
+        const C2<T>* wk = Wk;
+        const int64_t l2 = L2;
+        if (zero_input) {
+          for (int e = threadIdx.x; e < B * n2; e += blockDim.x) sb[swz<T>(e)] = mk<T>(0, 0);
+        } else {
+          staged<TL_UNR, C2<T>>(B * n2, [&](int e) { return wk[((e & lb) ? kb : ka) * l2 + (e >> lb)]; },
+                                [&](int e, C2<T> v) { sb[swz<T>(e)] = v; });
+        }
       }
       __syncthreads();
       if (!zero_input) row_fft<false>(B);
+      C2<T>* zb = shp(buf);
       if (it == 0) {
         for (int k2 = threadIdx.x; k2 <= n2 / 2; k2 += blockDim.x) {
-          if (k2 == 0) mid_zero<T, MODE>(buf[swz<T>(0)], m, rn2);
+          if (k2 == 0) mid_zero<T, MODE>(zb[swz<T>(0)], m, rn2);
           else {
             int64_t k = L1 * k2;
-            mid_pair<T, MODE>(buf[swz<T>(k2)], buf[swz<T>(n2 - k2)], k, tw4(k), m, rn2);
+            mid_pair<T, MODE>(zb[swz<T>(k2)], zb[swz<T>(n2 - k2)], k, tw4(k), m, rn2);
           }
         }
       } else if (it == L1 / 2) {
         for (int k2 = threadIdx.x; k2 < n2 / 2; k2 += blockDim.x) {
           int64_t k = L1 / 2 + L1 * k2;
-          mid_pair<T, MODE>(buf[swz<T>(k2)], buf[swz<T>(n2 - 1 - k2)], k, tw4(k), m, rn2);
+          mid_pair<T, MODE>(zb[swz<T>(k2)], zb[swz<T>(n2 - 1 - k2)], k, tw4(k), m, rn2);
         }
       } else {
         for (int k2 = threadIdx.x; k2 < n2; k2 += blockDim.x) {
           int64_t k = ka + L1 * k2;
-          mid_pair<T, MODE>(buf[swz<T>(2 * k2)], buf[swz<T>(2 * (n2 - 1 - k2) + 1)], k, tw4(k), m, rn2);
+          mid_pair<T, MODE>(zb[swz<T>(2 * k2)], zb[swz<T>(2 * (n2 - 1 - k2) + 1)], k, tw4(k), m, rn2);
         }
       }
       __syncthreads();
       if constexpr (MODE != MID_FWD) {
         row_fft<true>(B);
-        for (int e = threadIdx.x; e < B * n2; e += blockDim.x) {
+        C2<T>* sb = shp(buf);
+        C2<T>* wk = Wk;
+        const GTw<T> tf = twF;
+        const int64_t l2 = L2;
+        staged<TL_UNR, C2<T>>(B * n2, [&](int e) {
           const int64_t m2 = e >> lb, k1 = (e & lb) ? kb : ka;
-          Wk[k1 * L2 + m2] = cmulc<T>(buf[swz<T>(e)], twF(k1 * m2));
-        }
+          return cmulc<T>(sb[swz<T>(e)], tf(k1 * m2));
+        }, [&](int e, C2<T> v) { wk[((e & lb) ? kb : ka) * l2 + (e >> lb)] = v; });
       }
       __syncthreads();
     }
@@ -353,18 +392,16 @@ template <typename T> struct GridCtx {
     const int ct = CT, lct = (ct == 4) ? 2 : 1;
     const int64_t l2 = L2, ntiles = L2 / ct;
     const int tile = (int)(L1 * ct);
+    C2<T>* sb = shp(buf);
+    const C2<T>* wk = Wk;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t c0i = t * ct;
-      for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-        const int k1 = e >> lct, cc = e & (ct - 1);
-        buf[swz<T>(e)] = Wk[(int64_t)k1 * l2 + c0i + cc];
-      }
+      staged<TL_UNR, C2<T>>(tile, [&](int e) { return wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]; },
+                            [&](int e, C2<T> v) { sb[swz<T>(e)] = v; });
       __syncthreads();
       col_fft<true>();
-      for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-        const int m1 = e >> lct, cc = e & (ct - 1);
-        Cc[(int64_t)m1 * l2 + c0i + cc] = buf[swz<T>(e)];
-      }
+      staged<TL_UNR, C2<T>>(tile, [&](int e) { return sb[swz<T>(e)]; },
+                            [&](int e, C2<T> v) { Cc[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))] = v; });
       __syncthreads();
     }
   }

@@ -34,19 +34,26 @@ template <typename T> struct MidCtx {
   T* yout;                  // [M] forward output (FWD)
   int64_t N;
   T s0, sk, inv_s0, inv_sk, invL;
+  // bit position of DCT index k in rowmask/prefix: t = (k mod 2^s1) << tsh | k >> s1
+  // (s1 = 0: natural order, Tier S; s1 = log2 L1, tsh = log2(2 L2): Tier L transposed)
+  int s1, tsh;
+  CS_DEV int64_t tpos(int64_t k) const {
+    return ((k & ((int64_t(1) << s1) - 1)) << tsh) | (k >> s1);
+  }
 };
 
 template <typename T, int MODE>
-CS_DEV T mid_op(const MidCtx<T>& m, int64_t k, T X, double& rn2) {
+CS_DEV T mid_op(const MidCtx<T>& m, int64_t kn, T X, double& rn2) {
+  const int64_t k = m.tpos(kn);
   const bool sel = bit_test(m.rowmask, k);
-  const T s = (k == 0) ? m.s0 : m.sk;
+  const T s = (kn == 0) ? m.s0 : m.sk;
   if constexpr (MODE == MID_H) {
     return sel ? X * m.invL : T(0);
   } else if constexpr (MODE == MID_RES) {
     if (!sel) return T(0);
     const T d = m.y[row_rank(m.rowmask, m.prefix, k)] - s * X;
     rn2 += (double)d * (double)d;
-    const T is = (k == 0) ? m.inv_s0 : m.inv_sk;
+    const T is = (kn == 0) ? m.inv_s0 : m.inv_sk;
     return d * is * m.invL;
   } else {
     if (sel) m.yout[row_rank(m.rowmask, m.prefix, k)] = s * X;
@@ -197,6 +204,8 @@ template <typename T, int LOG2N> CS_DEV MidCtx<T> make_mid_c(const uint32_t* row
   m.inv_s0 = (T)sqrt_pow2(LOG2N);
   m.inv_sk = (T)sqrt_pow2(LOG2N - 1);
   m.invL = (T)(2.0 / (double)(1ll << LOG2N));
+  m.s1 = 0;
+  m.tsh = 0;
   return m;
 }
 
@@ -213,6 +222,8 @@ template <typename T> CS_DEV MidCtx<T> make_mid(int64_t N, const uint32_t* rowma
   m.inv_s0 = (T)sqrt((double)N);
   m.inv_sk = (T)sqrt((double)N / 2.0);
   m.invL = (T)(2.0 / (double)N);
+  m.s1 = 0;
+  m.tsh = 0;
   return m;
 }
 

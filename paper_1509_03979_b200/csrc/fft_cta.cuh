@@ -216,7 +216,9 @@ CS_DEV void fft_passes(C2<T>* buf, const TwTable<T>& tw) {
 // twiddles).  (L * B) >> LOG2E threads participate; all threads must call.
 template <typename T, int LOG2L, int LOG2E, int LOG2B, bool INV>
 CS_NOINL void fft_cta_t(C2<T>* buf, const TwTable<T> tw) {
-  fft_passes<T, LOG2L, LOG2E, LOG2B, 0, INV>(buf, tw);
+  // buffer and tables are shared memory: re-derive them in the shared window (LDS/STS)
+  const TwTable<T> ts{shp(tw.lo), shp(tw.hi)};
+  fft_passes<T, LOG2L, LOG2E, LOG2B, 0, INV>(shp(buf), ts);
 }
 
 // E for a given (L, B) on an NT-thread block: L*B/NT clamped to [2, 32] and <= L

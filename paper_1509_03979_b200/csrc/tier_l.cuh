@@ -41,7 +41,7 @@ CS_HD LGeom l_geom(int64_t N) {
 
 // Workspace layout (byte offsets) — identical on host and device.
 struct LLayout {
-  int64_t U, Wk, Cb, c0, twFlo, twFhi, tw4lo, tw4hi, in_pos;
+  int64_t U, Wk, Cb, c0, yT, twFlo, twFhi, tw4lo, tw4hi, in_pos;
   int64_t S, S2, Ul, x, x2, xU, r, d, q, b, Sbits, Ubits, Pbits;
   int64_t ctl, bar, pd, pi, pk, ghist, ctl_end;
   int64_t bytes;
@@ -49,13 +49,14 @@ struct LLayout {
 };
 
 template <typename T>
-CS_HD LLayout l_layout(int64_t N, int K, int ucap, bool pursuit, int maxgrid) {
+CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int maxgrid) {
   LLayout s;
   LGeom g = l_geom(N);
   const int64_t ts = sizeof(T), cs2 = 2 * sizeof(T), nw = (N + 31) / 32;
   int64_t o = 0;
   auto take = [&](int64_t bytes) { int64_t r = o; o = align_up(o + bytes, 256); return r; };
   s.U = take(N * ts);
+  s.yT = take(M * ts);  // y in the transposed row order (OpMeta)
   s.Wk = take(g.L * cs2);
   s.Cb = take(N * ts);
   s.c0 = pursuit ? take(N * ts) : 0;
@@ -142,6 +143,9 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.U = reinterpret_cast<T*>(ws + s.U);
   c.Wk = reinterpret_cast<C2<T>*>(ws + s.Wk);
   c.Cb = reinterpret_cast<T*>(ws + s.Cb);
+  c.yT = reinterpret_cast<T*>(ws + s.yT);
+  c.s1 = ilog2(g.L1);
+  c.tsh = ilog2(2 * g.L2);
   c.c0 = reinterpret_cast<T*>(ws + s.c0);
   c.in_pos = reinterpret_cast<int64_t*>(ws + s.in_pos);
   c.twF.lo = reinterpret_cast<const C2<T>*>(ws + s.twFlo);
@@ -190,6 +194,14 @@ template <typename T> CS_DEV void set_instance(GridCtx<T>& c, const OpMeta& m, i
   c.sign = m.sign(b);
   c.rowmask = m.rmask(b);
   c.prefix = m.prefix(b);
+  c.tperm = m.tperm(b);
+}
+
+// y (row order) -> yT (transposed row order of the stored mask); ends with a grid barrier
+template <typename T> CS_DEV void load_yT(GridCtx<T>& c, const T* y) {
+  for (int64_t t = c.gtid; t < c.M; t += c.gnthr) c.yT[t] = y[c.tperm[t]];
+  c.sync();
+  c.y = c.yT;
 }
 
 // Global twiddle tables (plain launch before the cooperative kernel).
@@ -227,8 +239,10 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_apply(LArgs<T> a) {
     c.sync();
     c.passA();
     c.sync();
-    c.template passB<MID_FWD>(false, a.out + b * c.M);
+    c.template passB<MID_FWD>(false, c.yT);
     c.sync();
+    T* y = a.out + b * c.M;
+    for (int64_t t = c.gtid; t < c.M; t += c.gnthr) y[c.tperm[t]] = c.yT[t];
   }
 }
 
@@ -239,7 +253,7 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_adjoint(LArgs<T> a) {
   const int64_t N = c.N;
   for (int64_t b = 0; b < a.B; ++b) {
     set_instance(c, a.meta, b);
-    c.y = a.Y + b * c.M;
+    load_yT(c, a.Y + b * c.M);
     c.RES(nullptr);
     T* x = a.out + b * N;
     for (int64_t j = c.gtid; j < N; j += c.gnthr) x[j] = c.c_at(j);
@@ -255,10 +269,11 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_recover(LArgs<T> a) {
   char* ws = a.ws;
   for (int64_t b = 0; b < a.B; ++b) {
     set_instance(c, a.meta, b);
-    c.y = a.Y + b * c.M;
+    const T* yb = a.Y + b * c.M;
     c.applies = 0;
     double bad = 0;
-    for (int64_t m = c.gtid; m < c.M; m += c.gnthr) bad += isfinite((double)c.y[m]) ? 0.0 : 1.0;
+    for (int64_t m = c.gtid; m < c.M; m += c.gnthr) bad += isfinite((double)yb[m]) ? 0.0 : 1.0;
+    load_yT(c, yb);
     unsigned pre = c.sum(bad) > 0 ? CS_DEV_NONFINITE_Y : 0u;
     Bufs<T> B;
     B.S = reinterpret_cast<int*>(ws + s.S);
@@ -302,12 +317,12 @@ template <typename T> inline int l_grid_upper() {
   return nsm * 4;  // generous upper bound for workspace sizing
 }
 
-template <typename T> inline size_t tier_l_apply_ws_bytes(int64_t N) {
-  return (size_t)l_layout<T>(N, 0, 0, false, l_grid_upper<T>()).bytes;
+template <typename T> inline size_t tier_l_apply_ws_bytes(int64_t N, int64_t M) {
+  return (size_t)l_layout<T>(N, M, 0, 0, false, l_grid_upper<T>()).bytes;
 }
 template <typename T> inline size_t tier_l_recover_ws_bytes(int64_t N, int64_t M, int K, int ucap) {
   (void)M;
-  return (size_t)l_layout<T>(N, K, ucap, true, l_grid_upper<T>()).bytes;
+  return (size_t)l_layout<T>(N, M, K, ucap, true, l_grid_upper<T>()).bytes;
 }
 
 // Declared everywhere; defined (and explicitly instantiated) in k_l_f32.cu / k_l_f64.cu.
@@ -344,7 +359,7 @@ cs_status tier_l_apply(OpMeta meta, int64_t B, const T* in, T* out, void* ws, si
                               std::string& err) {
   LArgs<T> a;
   a.meta = meta;
-  a.lay = l_layout<T>(meta.N, 0, 0, false, l_grid_upper<T>());
+  a.lay = l_layout<T>(meta.N, meta.M, 0, 0, false, l_grid_upper<T>());
   if (!ws || ws_bytes < (size_t)a.lay.bytes) { err = "workspace too small"; return CS_ERR_WORKSPACE; }
   a.B = B;
   a.Y = in;
@@ -361,7 +376,7 @@ cs_status tier_l_recover(OpMeta meta, Params P, int ucap, const T* Y, int64_t B,
                                 cudaStream_t st, std::atomic<uint64_t>& launches, std::string& err) {
   LArgs<T> a;
   a.meta = meta;
-  a.lay = l_layout<T>(meta.N, P.K, ucap, true, l_grid_upper<T>());
+  a.lay = l_layout<T>(meta.N, meta.M, P.K, ucap, true, l_grid_upper<T>());
   if (!ws || ws_bytes < (size_t)a.lay.bytes) { err = "workspace too small"; return CS_ERR_WORKSPACE; }
   a.P = P;
   a.B = B;

@@ -46,6 +46,9 @@ def test_meta_bytes_formula(lib):
     # 3 words-arrays of ceil(N/32) uint32 per instance, 256-aligned, + 256 flag tail
     assert lib.cs_operator_meta_bytes(16384, 4096, 4096) == ((4096 * 3 * 512 * 4 + 255) // 256) * 256 + 256
     assert lib.cs_operator_meta_bytes(8, 4, 1) == 256 + 256
+    # N > 16384 (Tier L): + an M-entry int32 row permutation per instance (transposed mask)
+    N, M = 1 << 20, 1 << 18
+    assert lib.cs_operator_meta_bytes(N, M, 1) == ((3 * (N // 32) * 4 + M * 4 + 255) // 256) * 256 + 256
 
 
 def test_host_validation_codes(lib):
