@@ -87,6 +87,41 @@ CS_DEV void staged(int n, LD&& ld, ST&& st) {
   }
 }
 constexpr int TL_UNR = 8;
+// two consecutive complex values moved with one 16-byte access (fp32)
+template <typename T> struct CP { C2<T> a, b; };
+template <typename T> CS_DEV CP<T> ldp(const C2<T>* p) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    return CP<T>{mk<T>(v.x, v.y), mk<T>(v.z, v.w)};
+  } else {
+    return CP<T>{p[0], p[1]};
+  }
+}
+template <typename T> CS_DEV void stp(C2<T>* p, const CP<T>& v) {
+  if constexpr (sizeof(T) == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.a.x, v.a.y, v.b.x, v.b.y);
+  } else {
+    p[0] = v.a;
+    p[1] = v.b;
+  }
+}
+// the same over the whole grid (index range [0, n), thread gtid of gnthr)
+template <int UNR, typename V, class LD, class ST>
+CS_DEV void gstaged(int64_t n, int64_t gtid, int64_t gnthr, LD&& ld, ST&& st) {
+  for (int64_t e0 = gtid; e0 < n; e0 += UNR * gnthr) {
+    V v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t e = e0 + u * gnthr;
+      if (e < n) v[u] = ld(e);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t e = e0 + u * gnthr;
+      if (e < n) st(e, v[u]);
+    }
+  }
+}
 
 template <typename T> struct GridCtx {
   using Key = typename KeyT<T>::type;
@@ -115,6 +150,7 @@ template <typename T> struct GridCtx {
   int64_t* si;  // [34]
   Key* sk;      // [32]
   unsigned* shist;  // [256]
+  uint32_t* msm;    // [4][2 L2 / 32] staged pass-B row metadata (mask x2, prefix x2)
   int64_t* pick;    // [4]
   GridScratch<T> g;
   int bank, hpass;
@@ -315,14 +351,24 @@ template <typename T> struct GridCtx {
     const GTw<T> tf = twF;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t c0i = t * ct;
-      staged<TL_UNR, C2<T>>(tile, [&](int e) { return Uc[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]; },
-                            [&](int e, C2<T> v) { sb[swz<T>(e)] = v; });
+      // element e = (m1, cc), pairs (cc, cc + 1) with cc even move as one 16-byte access
+      staged<TL_UNR, CP<T>>(tile / 2, [&](int p) {
+        const int e = 2 * p;
+        return ldp<T>(&Uc[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);
+      }, [&](int p, const CP<T>& v) {
+        sb[swz<T>(2 * p)] = v.a;
+        sb[swz<T>(2 * p + 1)] = v.b;
+      });
       __syncthreads();
       col_fft<false>();
-      staged<TL_UNR, C2<T>>(tile, [&](int e) {
+      staged<TL_UNR, CP<T>>(tile / 2, [&](int p) {
+        const int e = 2 * p;
         const int64_t k1 = e >> lct, m2 = c0i + (e & (ct - 1));
-        return cmul<T>(sb[swz<T>(e)], tf(k1 * m2));
-      }, [&](int e, C2<T> v) { wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))] = v; });
+        return CP<T>{cmul<T>(sb[swz<T>(e)], tf(k1 * m2)), cmul<T>(sb[swz<T>(e + 1)], tf(k1 * (m2 + 1)))};
+      }, [&](int p, const CP<T>& v) {
+        const int e = 2 * p;
+        stp<T>(&wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))], v);
+      });
       __syncthreads();
     }
   }
@@ -345,13 +391,40 @@ template <typename T> struct GridCtx {
         if (zero_input) {
           for (int e = threadIdx.x; e < B * n2; e += blockDim.x) sb[swz<T>(e)] = mk<T>(0, 0);
         } else {
-          staged<TL_UNR, C2<T>>(B * n2, [&](int e) { return wk[((e & lb) ? kb : ka) * l2 + (e >> lb)]; },
-                                [&](int e, C2<T> v) { sb[swz<T>(e)] = v; });
+          // pair q: row r = q & lb, m2 = 2 (q >> lb); smem element e = (m2 << lb) | r
+          staged<TL_UNR, CP<T>>(B * n2 / 2, [&](int q) {
+            const int r = q & lb, m2 = 2 * (q >> lb);
+            return ldp<T>(&wk[(r ? kb : ka) * l2 + m2]);
+          }, [&](int q, const CP<T>& v) {
+            const int r = q & lb, m2 = 2 * (q >> lb);
+            sb[swz<T>((m2 << lb) | r)] = v.a;
+            sb[swz<T>(((m2 + 1) << lb) | r)] = v.b;
+          });
         }
+      }
+      {
+        // stage the transposed-mask and prefix words of rows ka, kb
+        const int W = (int)((2 * L2) >> 5);
+        uint32_t* ms = shp(msm);
+        const int32_t* pg = prefix;
+        const uint32_t* mg = rowmask;
+        const int64_t r0 = ka * (int64_t)W, r1 = (kb & (L1 - 1)) * (int64_t)W;
+        staged<TL_UNR, uint32_t>(4 * W, [&](int e) {
+          const int q = e / W, w = e - q * W;
+          const int64_t at = ((q & 1) ? r1 : r0) + w;
+          return (q < 2) ? mg[at] : (uint32_t)pg[at];
+        }, [&](int e, uint32_t v) { ms[e] = v; });
       }
       __syncthreads();
       if (!zero_input) row_fft<false>(B);
       C2<T>* zb = shp(buf);
+      {
+        const int W = (int)((2 * L2) >> 5);
+        m.rowmask = shp(msm);
+        m.prefix = reinterpret_cast<const int32_t*>(shp(msm) + 2 * W);
+        m.staged = 1;
+        m.ra = (int)ka;
+      }
       if (it == 0) {
         for (int k2 = threadIdx.x; k2 <= n2 / 2; k2 += blockDim.x) {
           if (k2 == 0) mid_zero<T, MODE>(zb[swz<T>(0)], m, rn2);
@@ -378,10 +451,15 @@ template <typename T> struct GridCtx {
         C2<T>* wk = Wk;
         const GTw<T> tf = twF;
         const int64_t l2 = L2;
-        staged<TL_UNR, C2<T>>(B * n2, [&](int e) {
-          const int64_t m2 = e >> lb, k1 = (e & lb) ? kb : ka;
-          return cmulc<T>(sb[swz<T>(e)], tf(k1 * m2));
-        }, [&](int e, C2<T> v) { wk[((e & lb) ? kb : ka) * l2 + (e >> lb)] = v; });
+        staged<TL_UNR, CP<T>>(B * n2 / 2, [&](int q) {
+          const int r = q & lb, m2 = 2 * (q >> lb);
+          const int64_t k1 = r ? kb : ka;
+          return CP<T>{cmulc<T>(sb[swz<T>((m2 << lb) | r)], tf(k1 * m2)),
+                       cmulc<T>(sb[swz<T>(((m2 + 1) << lb) | r)], tf(k1 * (m2 + 1)))};
+        }, [&](int q, const CP<T>& v) {
+          const int r = q & lb, m2 = 2 * (q >> lb);
+          stp<T>(&wk[(r ? kb : ka) * l2 + m2], v);
+        });
       }
       __syncthreads();
     }
@@ -396,12 +474,21 @@ template <typename T> struct GridCtx {
     const C2<T>* wk = Wk;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t c0i = t * ct;
-      staged<TL_UNR, C2<T>>(tile, [&](int e) { return wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]; },
-                            [&](int e, C2<T> v) { sb[swz<T>(e)] = v; });
+      staged<TL_UNR, CP<T>>(tile / 2, [&](int p) {
+        const int e = 2 * p;
+        return ldp<T>(&wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);
+      }, [&](int p, const CP<T>& v) {
+        sb[swz<T>(2 * p)] = v.a;
+        sb[swz<T>(2 * p + 1)] = v.b;
+      });
       __syncthreads();
       col_fft<true>();
-      staged<TL_UNR, C2<T>>(tile, [&](int e) { return sb[swz<T>(e)]; },
-                            [&](int e, C2<T> v) { Cc[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))] = v; });
+      staged<TL_UNR, CP<T>>(tile / 2, [&](int p) {
+        return CP<T>{sb[swz<T>(2 * p)], sb[swz<T>(2 * p + 1)]};
+      }, [&](int p, const CP<T>& v) {
+        const int e = 2 * p;
+        stp<T>(&Cc[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))], v);
+      });
       __syncthreads();
     }
   }

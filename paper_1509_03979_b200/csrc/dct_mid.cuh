@@ -37,26 +37,41 @@ template <typename T> struct MidCtx {
   // bit position of DCT index k in rowmask/prefix: t = (k mod 2^s1) << tsh | k >> s1
   // (s1 = 0: natural order, Tier S; s1 = log2 L1, tsh = log2(2 L2): Tier L transposed)
   int s1, tsh;
+  // Tier L pass B: the mask / prefix words of the (at most two) transposed rows an
+  // item touches are staged in shared memory: row `ra` -> slot 0, any other -> slot 1,
+  // rowmask = staged mask [2][W], prefix = staged prefix [2][W] (W = 2^tsh / 32).
+  int staged, ra;
   CS_DEV int64_t tpos(int64_t k) const {
     return ((k & ((int64_t(1) << s1) - 1)) << tsh) | (k >> s1);
+  }
+  CS_DEV int64_t word(int64_t t) const {
+    if (!staged) return t >> 5;
+    const int64_t a = t >> tsh, W = (int64_t(1) << tsh) >> 5;
+    return (a == ra ? 0 : W) + ((t >> 5) & (W - 1));
+  }
+  CS_DEV bool sel(int64_t t) const { return (rowmask[word(t)] >> (t & 31)) & 1u; }
+  CS_DEV int64_t rank(int64_t t) const {
+    const int64_t w = word(t);
+    const uint32_t below = (t & 31) ? (rowmask[w] & ((1u << (t & 31)) - 1u)) : 0u;
+    return (int64_t)prefix[w] + __popc(below);
   }
 };
 
 template <typename T, int MODE>
 CS_DEV T mid_op(const MidCtx<T>& m, int64_t kn, T X, double& rn2) {
   const int64_t k = m.tpos(kn);
-  const bool sel = bit_test(m.rowmask, k);
+  const bool sel = m.sel(k);
   const T s = (kn == 0) ? m.s0 : m.sk;
   if constexpr (MODE == MID_H) {
     return sel ? X * m.invL : T(0);
   } else if constexpr (MODE == MID_RES) {
     if (!sel) return T(0);
-    const T d = m.y[row_rank(m.rowmask, m.prefix, k)] - s * X;
+    const T d = m.y[m.rank(k)] - s * X;
     rn2 += (double)d * (double)d;
     const T is = (kn == 0) ? m.inv_s0 : m.inv_sk;
     return d * is * m.invL;
   } else {
-    if (sel) m.yout[row_rank(m.rowmask, m.prefix, k)] = s * X;
+    if (sel) m.yout[m.rank(k)] = s * X;
     return T(0);
   }
 }
@@ -206,6 +221,8 @@ template <typename T, int LOG2N> CS_DEV MidCtx<T> make_mid_c(const uint32_t* row
   m.invL = (T)(2.0 / (double)(1ll << LOG2N));
   m.s1 = 0;
   m.tsh = 0;
+  m.staged = 0;
+  m.ra = 0;
   return m;
 }
 
@@ -224,6 +241,8 @@ template <typename T> CS_DEV MidCtx<T> make_mid(int64_t N, const uint32_t* rowma
   m.invL = (T)(2.0 / (double)N);
   m.s1 = 0;
   m.tsh = 0;
+  m.staged = 0;
+  m.ra = 0;
   return m;
 }
 

@@ -43,7 +43,7 @@ CS_HD LGeom l_geom(int64_t N) {
 struct LLayout {
   int64_t U, Wk, Cb, c0, yT, twFlo, twFhi, tw4lo, tw4hi, in_pos;
   int64_t S, S2, Ul, x, x2, xU, r, d, q, b, Sbits, Ubits, Pbits;
-  int64_t ctl, bar, pd, pi, pk, ghist, ctl_end;
+  int64_t ctl, bar, pd, pi, pk, ghist, ts, ctl_end;
   int64_t bytes;
   int maxgrid;
 };
@@ -90,6 +90,7 @@ CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int 
   s.pi = take(2 * (int64_t)maxgrid * 8);
   s.pk = take(2 * (int64_t)maxgrid * 8);
   s.ghist = take(3 * 256 * 4);
+  s.ts = take(64 * 8);  // diagnostics: %globaltimer at phase boundaries (block 0)
   s.ctl_end = o;
   s.bytes = o;
   s.maxgrid = maxgrid;
@@ -105,6 +106,7 @@ template <typename T> CS_HD int64_t l_smem_bytes(int64_t N) {
   take(64 * cs2); take((g.L1 >= 64 ? g.L1 / 64 : 1) * cs2);   // tw1
   take(64 * cs2); take((g.L2 >= 64 ? g.L2 / 64 : 1) * cs2);   // tw2
   take(34 * 8); take(34 * 8); take(32 * 8); take(256 * 4); take(4 * 8);
+  take(4 * ((2 * g.L2) / 32) * 4);                        // staged row metadata of pass B
   return o;
 }
 
@@ -176,6 +178,7 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.sk = reinterpret_cast<typename GridCtx<T>::Key*>(take(32 * 8));
   c.shist = reinterpret_cast<unsigned*>(take(256 * 4));
   c.pick = reinterpret_cast<int64_t*>(take(4 * 8));
+  c.msm = reinterpret_cast<uint32_t*>(take(4 * ((2 * g.L2) / 32) * 4));
   tw_init<T>(t1lo, t1hi, g.L1, n1, threadIdx.x, blockDim.x);
   tw_init<T>(t2lo, t2hi, g.L2, n2, threadIdx.x, blockDim.x);
   c.tw1.lo = t1lo; c.tw1.hi = t1hi;
@@ -199,7 +202,9 @@ template <typename T> CS_DEV void set_instance(GridCtx<T>& c, const OpMeta& m, i
 
 // y (row order) -> yT (transposed row order of the stored mask); ends with a grid barrier
 template <typename T> CS_DEV void load_yT(GridCtx<T>& c, const T* y) {
-  for (int64_t t = c.gtid; t < c.M; t += c.gnthr) c.yT[t] = y[c.tperm[t]];
+  const int32_t* tp = c.tperm;
+  T* yT = c.yT;
+  gstaged<TL_UNR, T>(c.M, c.gtid, c.gnthr, [&](int64_t t) { return y[tp[t]]; }, [&](int64_t t, T v) { yT[t] = v; });
   c.sync();
   c.y = c.yT;
 }
@@ -235,14 +240,55 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_apply(LArgs<T> a) {
   for (int64_t b = 0; b < a.B; ++b) {
     set_instance(c, a.meta, b);
     const T* x = a.Y + b * N;
-    for (int64_t j = c.gtid; j < N; j += c.gnthr) c.U[mk_pos(j, N)] = apply_sign<T>(c.sign, j, x[j]);
+    const uint32_t* sg = c.sign;
+    T* U = c.U;
+    uint64_t* ts = reinterpret_cast<uint64_t*>(a.ws + a.lay.ts);
+    auto stamp = [&](int i) {
+      if (blockIdx.x == 0 && threadIdx.x == 0 && b == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        ts[i] = t;
+      }
+    };
+    stamp(0);
+    // four consecutive j per unit: x[j..j+3] -> U[j/2], U[j/2+1] (even j) and
+    // U[N-2-j/2], U[N-1-j/2] (odd j, descending) — Makhoul order, sign applied
+    gstaged<TL_UNR, float4>(N / 4, c.gtid, c.gnthr, [&](int64_t q) {
+      const int64_t j = 4 * q;
+      float4 v;
+      if constexpr (sizeof(T) == 4) {
+        v = *reinterpret_cast<const float4*>(x + j);
+      } else {
+        v = make_float4(0, 0, 0, 0);
+      }
+      return v;
+    }, [&](int64_t q, float4 v) {
+      const int64_t j = 4 * q;
+      if constexpr (sizeof(T) == 4) {
+        const uint32_t w = sg[j >> 5] >> (j & 31);
+        const float a0 = (w & 1u) ? -v.x : v.x, a1 = (w & 2u) ? -v.y : v.y;
+        const float a2 = (w & 4u) ? -v.z : v.z, a3 = (w & 8u) ? -v.w : v.w;
+        *reinterpret_cast<float2*>(U + j / 2) = make_float2(a0, a2);
+        *reinterpret_cast<float2*>(U + N - 2 - j / 2) = make_float2(a3, a1);
+      } else {
+        for (int u = 0; u < 4; ++u) U[mk_pos(j + u, N)] = apply_sign<T>(sg, j + u, x[j + u]);
+      }
+    });
     c.sync();
+    stamp(1);
     c.passA();
     c.sync();
+    stamp(2);
     c.template passB<MID_FWD>(false, c.yT);
     c.sync();
+    stamp(3);
     T* y = a.out + b * c.M;
-    for (int64_t t = c.gtid; t < c.M; t += c.gnthr) y[c.tperm[t]] = c.yT[t];
+    const int32_t* tp = c.tperm;
+    const T* yT = c.yT;
+    gstaged<TL_UNR, T>(c.M, c.gtid, c.gnthr, [&](int64_t t) { return yT[t]; },
+                       [&](int64_t t, T v) { y[tp[t]] = v; });
+    c.sync();
+    stamp(4);
   }
 }
 
@@ -256,7 +302,10 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_adjoint(LArgs<T> a) {
     load_yT(c, a.Y + b * c.M);
     c.RES(nullptr);
     T* x = a.out + b * N;
-    for (int64_t j = c.gtid; j < N; j += c.gnthr) x[j] = c.c_at(j);
+    const uint32_t* sg = c.sign;
+    const T* Cb = c.Cb;
+    gstaged<TL_UNR, T>(N, c.gtid, c.gnthr, [&](int64_t j) { return apply_sign<T>(sg, j, Cb[mk_pos(j, N)]); },
+                       [&](int64_t j, T v) { x[j] = v; });
     c.sync();
   }
 }

@@ -140,9 +140,38 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout 
   CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, b);
   const int64_t N = c.N;
   const T* x = X + b * N;
-  T* zb = reinterpret_cast<T*>(c.Z);
-  for (int j = c.gtid; j < (int)N; j += c.gnthr)
-    zb[CtaCtx<T>::zt((int)mk_pos(j, N))] = apply_sign<T>(c.sign, j, x[j]);
+  if constexpr (sizeof(T) == 4) {
+    // x[4q..4q+3] -> complex slots q (x_{4q}, x_{4q+2}) and L-1-q (x_{4q+3}, x_{4q+1})
+    // of the Makhoul sequence (cs_common.cuh mk_pos), sign applied; 16-byte loads,
+    // all of a thread's loads in flight before its stores
+    const int L = (int)(N >> 1), nq = (int)(N >> 2);
+    C2<T>* z = shp(c.Z);
+    const uint32_t* sg = shp(c.sign);
+    constexpr int UQ = 8;
+    for (int q0 = threadIdx.x; q0 < nq; q0 += UQ * TS_THREADS) {
+      float4 v[UQ];
+#pragma unroll
+      for (int u = 0; u < UQ; ++u) {
+        const int q = q0 + u * TS_THREADS;
+        if (q < nq) v[u] = *reinterpret_cast<const float4*>(x + 4 * q);
+      }
+#pragma unroll
+      for (int u = 0; u < UQ; ++u) {
+        const int q = q0 + u * TS_THREADS;
+        if (q < nq) {
+          const uint32_t w = sg[q >> 3] >> ((4 * q) & 31);
+          const float a0 = (w & 1u) ? -v[u].x : v[u].x, a1 = (w & 2u) ? -v[u].y : v[u].y;
+          const float a2 = (w & 4u) ? -v[u].z : v[u].z, a3 = (w & 8u) ? -v[u].w : v[u].w;
+          z[swz<T>(q)] = mk<T>(a0, a2);
+          z[swz<T>(L - 1 - q)] = mk<T>(a3, a1);
+        }
+      }
+    }
+  } else {
+    T* zb = reinterpret_cast<T*>(c.Z);
+    for (int j = c.gtid; j < (int)N; j += c.gnthr)
+      zb[CtaCtx<T>::zt((int)mk_pos(j, N))] = apply_sign<T>(c.sign, j, x[j]);
+  }
   __syncthreads();
   c.template sandwich<MID_FWD, false>(nullptr, nullptr, Y + b * c.M);
 }
