@@ -20,6 +20,14 @@ namespace cs {
 // into shared memory from this base, so that out-of-line device functions (which
 // only see generic pointers) get 32-bit LDS/STS instead of generic LD/ST.
 extern __shared__ __align__(16) char cs_smem_base[];
+// threadIdx.x read through volatile asm: the read cannot be hoisted out of a loop, so
+// per-pass address arithmetic derived from it is recomputed (a few ALU ops) instead of
+// being hoisted and spilled to local memory under a 64-register budget.
+CS_DEV int tid_fresh() {
+  int t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return t;
+}
 template <typename P> CS_DEV P* shp(P* p) {
   const uint32_t off = (uint32_t)__cvta_generic_to_shared((const void*)p) -
                        (uint32_t)__cvta_generic_to_shared((const void*)cs_smem_base);

@@ -46,8 +46,14 @@ CS_DEV void sw_pass(C2<T>* buf, const TwTable<T>& tw, int nsb) {
   const int Ns = 1 << nsb, k = j & (Ns - 1);
   if (act) {
     const int sj = swz<T>(j);  // j < Lr: bit-disjoint from r Lr
+    if constexpr (Lr % 512 == 0) {
+      // swz(r Lr) = r Lr and sj < Lr: plain offsets (immediate-addressed LDS, no registers)
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = buf[sj ^ swz_c<T>(r * Lr)];
+      for (int r = 0; r < R; ++r) v[r] = buf[sj + r * Lr];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = buf[sj ^ swz_c<T>(r * Lr)];
+    }
     if (Ns > 1) {
       C2<T> w1 = tw(k << (LOG2L - nsb - RB));
       if (INV) w1 = cconj<T>(w1);
