@@ -283,7 +283,7 @@ def run_ours(args):
         t_fwd = a0.elapsed_time(a1) / reps_op / 1e3
         t_adj = a1.elapsed_time(a2) / reps_op / 1e3
         es = td.itemsize if hasattr(td, "itemsize") else (4 if td == torch.float32 else 8)
-        meta_b = B * 3 * ((cfg.N + 31) // 32) * 4
+        meta_b = B * (3 * ((cfg.N + 31) // 32) * 4 + (cfg.M * 4 if cfg.N > 16384 else 0))
         bytes_fwd = B * (cfg.N + cfg.M) * es + meta_b
         bytes_adj = B * (cfg.N + cfg.M) * es + meta_b
         peaks = load_peaks()
@@ -293,17 +293,36 @@ def run_ours(args):
                     "frac_hbm_adj": bytes_adj / t_adj / 1e9 / peaks["hbm_gbs"],
                     "ms_fwd": t_fwd * 1e3, "ms_adj": t_adj * 1e3}
 
-    # ---- roofline of the dominant kernel (k_s_recover: the whole step is one launch)
+    # ---- roofline of the dominant kernel: the whole step is one launch of the recovery
+    # kernel (k_s_recover for N <= 16384, k_l_recover above), timed with CUDA events on
+    # the launching stream (kms, per launch).  DESIGN.md §6 derives both models.
     peaks = load_peaks()
-    nominal_flops_per_apply = 5.0 * cfg.N * np.log2(cfg.N)     # 2 DCTs x 2.5 N log2 N
-    flops_step = applies * nominal_flops_per_apply
-    achieved_tf = flops_step / (kms / 1e3) / 1e12
-    peak_tf = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    roofline = {"bound": "alu", "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 2),
-                "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4), "traffic": None,
-                "kernel": "k_s_recover<float>", "kernel_ms": round(kms, 4),
-                "algorithmic_flops_per_launch": flops_step,
-                "peak_note": "FP32 SIMT 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md §6)"}
+    es = 4 if args.precision == "fp32" else 8
+    tier_s = cfg.N <= 16384
+    if tier_s:
+        # FP32-ALU bound: nominal DCT flops 2.5 N log2 N per transform, 2 per sandwich,
+        # sandwiches counted on the device (cs_report.applies); peak = 148 SM x 128 FP32
+        # lanes x 2 flop x sm_max_mhz (fp64: the fp64 pipe is half rate on B200)
+        nominal_flops_per_apply = 5.0 * cfg.N * np.log2(cfg.N)
+        flops_step = applies * nominal_flops_per_apply
+        achieved = flops_step / (kms / 1e3) / 1e12
+        peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12 / (1 if es == 4 else 2)
+        roofline = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "kernel": f"k_s_recover<{'float' if es == 4 else 'double'}>", "kernel_ms": round(kms, 4),
+                    "algorithmic_flops_per_launch": flops_step,
+                    "peak_note": "derived: FP32 SIMT 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md §6)"}
+    else:
+        # HBM/L2-streaming four-step: each sandwich moves 3 passes x (read + write) of the
+        # N-real (N/2-complex) vector = 24 N bytes (fp32); peak = measured copy bandwidth
+        bytes_step = applies * 6.0 * cfg.N * es
+        achieved = bytes_step / (kms / 1e3) / 1e9
+        peak = peaks["hbm_gbs"]
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": None,
+                    "kernel": f"k_l_recover<{'float' if es == 4 else 'double'}>", "kernel_ms": round(kms, 4),
+                    "algorithmic_bytes_per_launch": bytes_step,
+                    "peak_note": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
     tr = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr):
         try:
