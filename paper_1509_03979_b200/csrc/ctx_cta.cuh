@@ -168,35 +168,68 @@ template <typename T> struct CtaCtx {
   }
   // CG iterations with the sandwich of one compile-time length inlined: no call
   // (and no ABI register save/restore) inside the loop.
-  template <int LOG2L, class S> CS_NOINL void cg_iterate_t(S& s) {
-    const MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, nullptr);
-    s.x = shp(s.x); s.r = shp(s.r); s.d = shp(s.d); s.q = shp(s.q);  // Tier S: all in shared memory
-    C2<T>* z = Z;
-    const TwTable<T> tl = twL, t4 = tw4;
-    const int* sp = in_supp;
-    const uint32_t* sg = sign;
-    const int ns = in_ns;
-    // register copy of the fields the loop touches (the context itself lives in
-    // local memory behind a generic pointer)
-    struct Lc {
-      int gtid, gnthr, lane, gwarp, gnwarps, rbank;
-      double* redd;
-      CS_DEV double sum(double v) {
-        v = warp_sum(v);
-        double* rb = redd + 32 * rbank;
-        rbank ^= 1;
-        if (lane == 0) rb[gwarp] = v;
-        __syncthreads();
-        double t = 0;
-        for (int w = 0; w < gnwarps; ++w) t += rb[w];
-        return t;
+  template <int LOG2L, class S> CS_NOINL void cg_iterate_t(S& s_io) {
+    // Algorithm 1 lines 14-22 for one compile-time transform length, the
+    // sandwich inlined.  Only ~12 uniform scalars stay live across the sandwich (shared
+    // offsets of the four vectors, rr, thr, ns, cap, j, status, bank): everything else
+    // (ids, reduction slots, layout) is recomputed from threadIdx / compile-time offsets,
+    // so the 64-register budget holds the FFT without spilling loop state.
+    constexpr int NT = SW_NT, NWARP = SW_NT / 32;
+    constexpr SFix F = s_fixed<T>(int64_t(2) << LOG2L);
+    T* const xv = shp(s_io.x);
+    T* const rv = shp(s_io.r);
+    T* const dv = shp(s_io.d);
+    T* const qv = shp(s_io.q);
+    const int* const sp = shp(in_supp);
+    const int n = s_io.ns;
+    const double thr = s_io.thr;
+    const int cap = s_io.cap;
+    double rr = s_io.rr;
+    int j = s_io.j;
+    unsigned status = s_io.status;
+    int rb = rbank;
+    const MidCtx<T> m0 = make_mid_c<T, LOG2L + 1>(nullptr, nullptr, nullptr, nullptr);
+    constexpr int64_t REDD = F.redd;
+    auto bsum = [&rb](double v) {
+      v = warp_sum(v);
+      double* slots = reinterpret_cast<double*>(cs_smem_base + REDD) + 32 * rb;
+      rb ^= 1;
+      if ((threadIdx.x & 31) == 0) slots[threadIdx.x >> 5] = v;
+      __syncthreads();
+      double t = 0;
+#pragma unroll
+      for (int w = 0; w < NWARP; ++w) t += slots[w];
+      return t;
+    };
+    while (true) {
+      if (!(rr > thr)) break;                                              // line 15 (R6, R7)
+      if (j >= cap) { status |= CS_DEV_CG_CAP; break; }
+      sw_body<T, LOG2L, MID_H, false>(nullptr, TwTable<T>{}, TwTable<T>{}, m0,
+                                      SwIO<T>{sp, n, nullptr, dv, qv});    // q = H d_j
+      double dq = 0;
+      for (int i = threadIdx.x; i < n; i += NT) dq += (double)dv[i] * (double)qv[i];
+      dq = bsum(dq);
+      if (!(dq > 0.0)) { status |= CS_DEV_CG_BREAKDOWN; break; }
+      const T alpha = (T)(rr / dq);                                        // line 16
+      double rr2 = 0;
+      for (int i = threadIdx.x; i < n; i += NT) {
+        xv[i] += alpha * dv[i];                                            // line 17
+        const T ri = rv[i] - alpha * qv[i];                                // line 18
+        rv[i] = ri;
+        rr2 += (double)ri * (double)ri;
       }
-    } lc{gtid, gnthr, lane, gwarp, gnwarps, rbank, shp(redd)};
-    cg_loop(lc, s, [&](const T* d, T* q) {
-      sw_body<T, LOG2L, MID_H, false>(z, tl, t4, m, SwIO<T>{sp, ns, sg, d, q});
-    });
-    rbank = lc.rbank;
-    applies += s.j;
+      rr2 = bsum(rr2);
+      const T beta = (T)(rr2 / rr);                                        // line 19
+      for (int i = threadIdx.x; i < n; i += NT) dv[i] = rv[i] + beta * dv[i];  // line 20
+      rr = rr2;
+      ++j;                                                                 // line 21
+      if (!(rr2 == rr2)) { status |= CS_DEV_CG_BREAKDOWN; break; }
+    }
+    applies += j - s_io.j;
+    s_io.rr = rr;
+    s_io.j = j;
+    s_io.status = status;
+    rbank = rb;
   }
   template <int LO, int HI, class S> CS_DEV void cg_dispatch(S& s) {
     if constexpr (LO <= HI) {

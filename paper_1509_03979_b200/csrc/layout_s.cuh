@@ -8,7 +8,7 @@
 namespace cs {
 
 struct SFix {
-  int64_t Z, twLlo, twLhi, tw4lo, tw4hi, sign, rmask, prefix, redd, redi, redk, hist, pick, h1, ckey, cidx, ccnt, end;
+  int64_t Z, twLlo, twLhi, tw4lo, tw4hi, sign, rmask, prefix, redd, redi, redk, hist, pick, h1, ckey, cidx, ccnt, zero, end;
 };
 
 __host__ __device__ constexpr int64_t al16(int64_t x) { return (x + 15) / 16 * 16; }
@@ -35,6 +35,7 @@ template <typename T> __host__ __device__ constexpr SFix s_fixed(int64_t N) {
   s.ckey = o;   o = al16(o + (int64_t)TOPK_CAP * sizeof(typename KeyT<T>::type));
   s.cidx = o;   o = al16(o + (int64_t)TOPK_CAP * 4);
   s.ccnt = o;   o = al16(o + 16);
+  s.zero = o;   o = al16(o + 16);  // an int 0 read through volatile (sandwich_cta.cuh opaque_tid)
   s.end = o;
   return s;
 }

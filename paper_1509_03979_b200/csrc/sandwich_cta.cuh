@@ -35,12 +35,20 @@ namespace cs {
 constexpr int SW_NT = 512;  // threads per Tier S block (two blocks per SM)
 constexpr int SW_LOG2NT = 9;
 
+// threadIdx.x plus a 0 read through a volatile shared load: address arithmetic derived
+// from it cannot be hoisted out of the CG loop (where, under the 64-register budget,
+// ptxas would otherwise precompute and spill it), so it is recomputed each pass.
+template <typename T, int LOG2L> CS_DEV int opaque_tid() {
+  constexpr SFix F = s_fixed<T>(int64_t(2) << LOG2L);
+  return (int)threadIdx.x + *reinterpret_cast<volatile int*>(cs_smem_base + F.zero);
+}
+
 // ---- one Stockham pass of radix 2^RB at runtime stride Ns = 2^nsb; L = 2^LOG2L ----
 template <typename T, int LOG2L, int RB, bool INV>
 CS_DEV void sw_pass(C2<T>* buf, const TwTable<T>& tw, int nsb) {
   constexpr int R = 1 << RB, Lr = (1 << LOG2L) >> RB;
   static_assert(Lr <= SW_NT, "one item per thread");
-  const int j = threadIdx.x;
+  const int j = opaque_tid<T, LOG2L>();
   C2<T> v[R];
   const bool act = (Lr == SW_NT) || j < Lr;
   const int Ns = 1 << nsb, k = j & (Ns - 1);
@@ -104,7 +112,7 @@ CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, 
   using SP = SwPlan<LOG2L>;
   constexpr int L = 1 << LOG2L, H = L / 2, U = SP::U, UPT = SP::UPT;
   static_assert(L >= 4, "N >= 8");
-  const int tid = threadIdx.x;
+  const int tid = opaque_tid<T, LOG2L>();
   const MidK<T> cst = make_midk_c<T, LOG2L + 1>();
   double rn2 = 0;
   C2<T> A0[UPT], A1[UPT], B0[UPT], B1[UPT];

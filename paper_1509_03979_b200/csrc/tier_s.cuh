@@ -110,6 +110,7 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   c.cidx = reinterpret_cast<int*>(smem + lay.cidx);
   c.ccnt = reinterpret_cast<int*>(smem + lay.ccnt);
   c.rbank = 0;
+  if (threadIdx.x == 0) *reinterpret_cast<int*>(smem + s_fixed<T>(meta.N).zero) = 0;
   c.in_supp = nullptr;
   c.in_ns = 0;
   c.applies = 0;
