@@ -56,6 +56,8 @@ template <typename T> struct CtaCtx {
   int applies;
 
   CS_DEV void sync() { __syncthreads(); }
+  // pointer into this context's working set as the compiler should see it: shared (Tier S)
+  template <typename P> CS_DEV P* loc(P* p) const { return shp(p); }
 
   int rbank;  // alternating reduction bank (sum)
   // Deterministic block sum (fixed order).  Two alternating banks of partials: the

@@ -160,6 +160,7 @@ template <typename T> struct GridCtx {
 
   CS_DEV void sync() { grid_barrier(g.bar); }
   static constexpr bool kTopkFast = false;
+  template <typename P> CS_DEV P* loc(P* p) const { return p; }  // global (Tier L)
 
   // block-level deterministic sum; result valid in thread 0
   CS_DEV double block_sum(double v) {

@@ -88,6 +88,12 @@ template <class Ctx, typename T>
 CS_NOINL void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q, T* b, bool r_given,
                        const Params& P, Stats& st) {
   ctx.set_input_support(supp, ns);
+  supp = ctx.loc(supp);
+  x = ctx.loc(x);
+  r = ctx.loc(r);
+  d = ctx.loc(d);
+  q = ctx.loc(q);
+  b = ctx.loc(b);
   const int t0 = ctx.gtid, sd = ctx.gnthr;
   {
     const auto c0v = ctx.c0view();
@@ -139,7 +145,10 @@ CS_DEV void swap_ptr(T*& a, T*& b) { T* t = a; a = b; b = t; }
 template <class Ctx, typename T>
 CS_NOINL void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* out) {
   const int64_t N = ctx.N;
-  const auto cv = ctx.cview();
+  auto cv = ctx.cview();
+  cv.z = ctx.loc(cv.z);
+  cv.sign = ctx.loc(cv.sign);
+  excl = excl ? ctx.loc(excl) : nullptr;
   topk_bits(ctx, N, K, [cv, excl](int64_t j) {
     if (excl && bit_test(excl, j)) return decltype(full_key(T(0)))(0);
     return full_key(cv.raw(j));
@@ -149,7 +158,10 @@ CS_NOINL void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* o
 template <class Ctx, typename T>
 CS_NOINL int64_t detect_argmax(Ctx& ctx, const uint32_t* excl) {
   const int64_t N = ctx.N;
-  const auto cv = ctx.cview();
+  auto cv = ctx.cview();
+  cv.z = ctx.loc(cv.z);
+  cv.sign = ctx.loc(cv.sign);
+  excl = ctx.loc(excl);
   return argmax_key(ctx, N, [cv, excl](int64_t j) {
     if (bit_test(excl, j)) return decltype(full_key(T(0)))(0);
     return full_key(cv.raw(j));
