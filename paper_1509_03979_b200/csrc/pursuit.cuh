@@ -149,10 +149,27 @@ CS_NOINL void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* o
   cv.z = ctx.loc(cv.z);
   cv.sign = ctx.loc(cv.sign);
   excl = excl ? ctx.loc(excl) : nullptr;
+  using Key = decltype(full_key(T(0)));
+  if constexpr (Ctx::kTopkFast) {
+    // CTA: visit the correlation buffer in its own (Makhoul, swizzled) order, two
+    // positions per complex slot, instead of gathering it in natural index order
+    const int n = (int)N, L = n / 2;
+    const C2<T>* zs = reinterpret_cast<const C2<T>*>(cv.z);
+    auto visit = [&](auto&& f) {
+      for (int q = threadIdx.x; q < L; q += blockDim.x) {
+        const C2<T> z = zs[swz<T>(q)];
+        const int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;        // mk_nat(2q)
+        const int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;  // mk_nat(2q+1)
+        f(j0, (excl && bit_test(excl, j0)) ? Key(0) : full_key(z.x));
+        f(j1, (excl && bit_test(excl, j1)) ? Key(0) : full_key(z.y));
+      }
+    };
+    if (topk_cta_fast_v<Ctx, Key>(ctx, n, (int)K, visit, out)) return;
+  }
   topk_bits(ctx, N, K, [cv, excl](int64_t j) {
-    if (excl && bit_test(excl, j)) return decltype(full_key(T(0)))(0);
+    if (excl && bit_test(excl, j)) return Key(0);
     return full_key(cv.raw(j));
-  }, out);
+  }, out, false);
 }
 
 template <class Ctx, typename T>
@@ -162,8 +179,26 @@ CS_NOINL int64_t detect_argmax(Ctx& ctx, const uint32_t* excl) {
   cv.z = ctx.loc(cv.z);
   cv.sign = ctx.loc(cv.sign);
   excl = ctx.loc(excl);
+  using Key = decltype(full_key(T(0)));
+  if constexpr (Ctx::kTopkFast) {
+    const int n = (int)N, L = n / 2;
+    const C2<T>* zs = reinterpret_cast<const C2<T>*>(cv.z);
+    Key bk = 0;
+    int64_t bi = -1;
+    auto take = [&](int j, Key k) {  // larger key wins, ties -> lower index (R12)
+      if (k > bk || (k == bk && k != 0 && j < bi)) { bk = k; bi = j; }
+    };
+    for (int q = threadIdx.x; q < L; q += blockDim.x) {
+      const C2<T> z = zs[swz<T>(q)];
+      const int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;
+      const int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;
+      take(j0, bit_test(excl, j0) ? Key(0) : full_key(z.x));
+      take(j1, bit_test(excl, j1) ? Key(0) : full_key(z.y));
+    }
+    return ctx.argmax(bk, bi);
+  }
   return argmax_key(ctx, N, [cv, excl](int64_t j) {
-    if (bit_test(excl, j)) return decltype(full_key(T(0)))(0);
+    if (bit_test(excl, j)) return Key(0);
     return full_key(cv.raw(j));
   });
 }

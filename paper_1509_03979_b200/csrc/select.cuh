@@ -70,22 +70,23 @@ CS_DEV void hist_add_warp(unsigned* hist, unsigned digit) {
 // are found by a byte radix select over the candidate list only.
 // Returns false (nothing written) if the boundary bin holds > TOPK_CAP entries
 // or fewer than K keys are non-zero; the caller then runs the radix path.
-template <class Ctx, class KeyFn>
-CS_DEV bool topk_cta_fast(Ctx& ctx, int n, int K, KeyFn key, uint32_t* out_bits) {
-  using Key = decltype(key(int64_t(0)));
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+// `visit(f)` calls f(index, key) once for every element, in any order and from any
+// thread (key 0 = never select); `nbits` = size of the index range of out_bits.
+template <class Ctx, typename Key, class Visit>
+CS_DEV bool topk_cta_fast_v(Ctx& ctx, int nbits, int K, Visit&& visit, uint32_t* out_bits) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   unsigned* h = shp(ctx.h1);
-  Key* ck = shp(ctx.ckey);
+  Key* ck = reinterpret_cast<Key*>(shp(ctx.ckey));
   int* ci = shp(ctx.cidx);
   int* cc = shp(ctx.ccnt);
   int64_t* pk = shp(ctx.pick);
   for (int i = tid; i < TOPK_BINS; i += nt) h[i] = 0;
   if (tid == 0) cc[0] = 0;
   __syncthreads();
-  for (int i = tid; i < n; i += nt) {
-    const Key k = key(i);
+  visit([&](int i, Key k) {
+    (void)i;
     if (k) hist_add_warp(h, key_digit10(k));
-  }
+  });
   __syncthreads();
   if (warp == 0) {
     // lane l owns bins [1023 - 32 l - 31, 1023 - 32 l], scanned from the top
@@ -111,30 +112,24 @@ CS_DEV bool topk_cta_fast(Ctx& ctx, int n, int K, KeyFn key, uint32_t* out_bits)
       }
     }
   }
+  const int nwords = (nbits + 31) >> 5;
+  for (int w = tid; w < nwords; w += nt) out_bits[w] = 0u;
   __syncthreads();
   const int b1 = (int)pk[0], above = (int)pk[1], inb = (int)pk[2];
   __syncthreads();  // pick[] is reused by later collectives
   if (b1 < 0 || inb > TOPK_CAP) return false;
   const int need = K - above;
-  const int nwords = (n + 31) >> 5;
-  for (int w = warp; w < nwords; w += nwarp) {
-    const int i = w * 32 + lane;
-    const Key k = (i < n) ? key(i) : Key(0);
-    const int d = k ? (int)key_digit10(k) : -1;
-    const unsigned sel = __ballot_sync(0xffffffffu, d > b1);
-    const unsigned cnd = __ballot_sync(0xffffffffu, d == b1);
-    if (lane == 0) out_bits[w] = sel;
-    if (cnd) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(cc, __popc(cnd));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (d == b1) {
-        const int at = base + __popc(cnd & ((1u << lane) - 1u));
-        ck[at] = k;
-        ci[at] = i;
-      }
+  visit([&](int i, Key k) {
+    if (!k) return;
+    const int d = (int)key_digit10(k);
+    if (d > b1) {
+      atomicOr(&out_bits[i >> 5], 1u << (i & 31));
+    } else if (d == b1) {
+      const int at = atomicAdd(cc, 1);
+      ck[at] = k;
+      ci[at] = i;
     }
-  }
+  });
   __syncthreads();
   const int C = cc[0];
   if (need >= C) {
@@ -143,6 +138,8 @@ CS_DEV bool topk_cta_fast(Ctx& ctx, int n, int K, KeyFn key, uint32_t* out_bits)
     return true;
   }
   // MSB-first byte radix select of the `need` largest candidate keys
+  const int nwarp = nt >> 5;
+  (void)nwarp;
   unsigned* hist = shp(ctx.hist);
   constexpr int NB = (int)sizeof(Key) * 8;
   Key prefix = 0, pmask = 0;
@@ -182,12 +179,20 @@ CS_DEV bool topk_cta_fast(Ctx& ctx, int n, int K, KeyFn key, uint32_t* out_bits)
   return true;
 }
 
+template <class Ctx, class KeyFn>
+CS_DEV bool topk_cta_fast(Ctx& ctx, int n, int K, KeyFn key, uint32_t* out_bits) {
+  using Key = decltype(key(int64_t(0)));
+  return topk_cta_fast_v<Ctx, Key>(ctx, n, K, [&](auto&& f) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) f(i, key(i));
+  }, out_bits);
+}
+
 // key(i) for i in [0, n); key 0 means "never select".  Requires at least K
 // non-zero keys.  out_bits must hold ceil(n/32) words; fully overwritten.
 template <class Ctx, class KeyFn>
-CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_bits) {
+CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_bits, bool try_fast = true) {
   if constexpr (Ctx::kTopkFast) {
-    if (topk_cta_fast(ctx, (int)n, (int)K, key, out_bits)) return;
+    if (try_fast && topk_cta_fast(ctx, (int)n, (int)K, key, out_bits)) return;
   }
   using Key = decltype(key(int64_t(0)));
   constexpr int NB = (int)sizeof(Key) * 8;
