@@ -109,3 +109,24 @@ def test_deterministic_rerun(cs):
     b = _run(cs, cfg, 8)
     assert np.array_equal(a[2], b[2])
     assert np.array_equal(a[3], b[3])
+
+
+@pytest.mark.parametrize("alg,N,M,K", [("omp", 1024, 256, 8), ("sp", 16384, 4096, 256),
+                                       ("ompr", 2048, 512, 16), ("sp", 65536, 16384, 64)])
+def test_all_ties_zero_measurements(cs, alg, N, M, K):
+    """y = 0: every correlation is exactly 0, so every selection is a full tie and must
+    go to the lowest indices (SURVEY §8c.7 #12, #32); the oracle gives the same."""
+    cfg = cs_inputs.Config(62, alg, N, M, K, "gauss", 0.0)
+    probs = cs_inputs.make_batch(cfg, count=2)
+    ys = np.zeros((2, M), dtype=np.float32)
+    dev = torch.device("cuda:0")
+    bits, rows = to_dev(probs, dev)
+    A = cs.Operator(N, M, bits, rows, batch=2)
+    res = cs.cs_recover_batched(A, alg, torch.from_numpy(ys).to(dev), K, 1e-6)
+    torch.cuda.synchronize()
+    supp = res.support.cpu().numpy()
+    refs = oracle_results(probs, ys)
+    for b in range(2):
+        assert np.array_equal(np.sort(supp[b]), refs[b].support), (alg, b)
+        assert np.array_equal(np.sort(supp[b]), np.arange(K))
+    assert np.all(res.values.cpu().numpy() == 0)
