@@ -87,6 +87,18 @@ CS_DEV void staged(int n, LD&& ld, ST&& st) {
   }
 }
 constexpr int TL_UNR = 8;
+constexpr int TL_LOG2NT = 8;  // Tier L blocks: 256 threads (two per SM, 128 registers)
+// Asynchronous global -> shared copies of one complex element (cp.async, LDGSTS): a
+// whole tile's loads are in flight at once without staging registers.
+template <typename T> CS_DEV void cp_async_c(C2<T>* sdst, const C2<T>* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  if constexpr (sizeof(T) == 4) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+  } else {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+  }
+}
+CS_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 // two consecutive complex values moved with one 16-byte access (fp32)
 template <typename T> struct CP { C2<T> a, b; };
 template <typename T> CS_DEV CP<T> ldp(const C2<T>* p) {
@@ -334,12 +346,18 @@ template <typename T> struct GridCtx {
   }
   // sub-FFTs of the four-step (256-thread blocks, compile-time lengths 2^7..2^12)
   template <bool INV> CS_DEV void col_fft() {
-    if (CT == 4) fft_cta_dispatch<T, 2, 8, 7, 12, INV>(buf, log2L1, tw1);
-    else fft_cta_dispatch<T, 1, 8, 7, 12, INV>(buf, log2L1, tw1);
+#ifdef CS_DIAG_NOFFT
+    return;  // diagnostics build only: memory-phase timing without the sub-FFTs
+#endif
+    if (CT == 4) fft_cta_dispatch<T, 2, TL_LOG2NT, 7, 12, INV>(buf, log2L1, tw1);
+    else fft_cta_dispatch<T, 1, TL_LOG2NT, 7, 12, INV>(buf, log2L1, tw1);
   }
   template <bool INV> CS_DEV void row_fft(int B) {
-    if (B == 2) fft_cta_dispatch<T, 1, 8, 7, 12, INV>(buf, log2L2, tw2);
-    else fft_cta_dispatch<T, 0, 8, 7, 12, INV>(buf, log2L2, tw2);
+#ifdef CS_DIAG_NOFFT
+    return;
+#endif
+    if (B == 2) fft_cta_dispatch<T, 1, TL_LOG2NT, 7, 12, INV>(buf, log2L2, tw2);
+    else fft_cta_dispatch<T, 0, TL_LOG2NT, 7, 12, INV>(buf, log2L2, tw2);
   }
   // pass A: columns of z = U viewed as complex [L1][L2]
   CS_NOINL void passA() {
@@ -352,14 +370,10 @@ template <typename T> struct GridCtx {
     const GTw<T> tf = twF;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t c0i = t * ct;
-      // element e = (m1, cc), pairs (cc, cc + 1) with cc even move as one 16-byte access
-      staged<TL_UNR, CP<T>>(tile / 2, [&](int p) {
-        const int e = 2 * p;
-        return ldp<T>(&Uc[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);
-      }, [&](int p, const CP<T>& v) {
-        sb[swz<T>(2 * p)] = v.a;
-        sb[swz<T>(2 * p + 1)] = v.b;
-      });
+      // element e = (m1, cc): the whole tile in flight as cp.async
+      for (int e = threadIdx.x; e < tile; e += blockDim.x)
+        cp_async_c<T>(&sb[swz<T>(e)], &Uc[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);
+      cp_async_wait_all();
       __syncthreads();
       col_fft<false>();
       staged<TL_UNR, CP<T>>(tile / 2, [&](int p) {
@@ -393,14 +407,9 @@ template <typename T> struct GridCtx {
           for (int e = threadIdx.x; e < B * n2; e += blockDim.x) sb[swz<T>(e)] = mk<T>(0, 0);
         } else {
           // pair q: row r = q & lb, m2 = 2 (q >> lb); smem element e = (m2 << lb) | r
-          staged<TL_UNR, CP<T>>(B * n2 / 2, [&](int q) {
-            const int r = q & lb, m2 = 2 * (q >> lb);
-            return ldp<T>(&wk[(r ? kb : ka) * l2 + m2]);
-          }, [&](int q, const CP<T>& v) {
-            const int r = q & lb, m2 = 2 * (q >> lb);
-            sb[swz<T>((m2 << lb) | r)] = v.a;
-            sb[swz<T>(((m2 + 1) << lb) | r)] = v.b;
-          });
+          for (int e = threadIdx.x; e < B * n2; e += blockDim.x)
+            cp_async_c<T>(&sb[swz<T>(e)], &wk[((e & lb) ? kb : ka) * l2 + (e >> lb)]);
+          cp_async_wait_all();
         }
       }
       {
@@ -475,13 +484,9 @@ template <typename T> struct GridCtx {
     const C2<T>* wk = Wk;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t c0i = t * ct;
-      staged<TL_UNR, CP<T>>(tile / 2, [&](int p) {
-        const int e = 2 * p;
-        return ldp<T>(&wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);
-      }, [&](int p, const CP<T>& v) {
-        sb[swz<T>(2 * p)] = v.a;
-        sb[swz<T>(2 * p + 1)] = v.b;
-      });
+      for (int e = threadIdx.x; e < tile; e += blockDim.x)
+        cp_async_c<T>(&sb[swz<T>(e)], &wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);
+      cp_async_wait_all();
       __syncthreads();
       col_fft<true>();
       staged<TL_UNR, CP<T>>(tile / 2, [&](int p) {

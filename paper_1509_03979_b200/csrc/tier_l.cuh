@@ -11,7 +11,7 @@
 
 namespace cs {
 
-constexpr int TL_THREADS = 256;  // fft dispatch assumes 2^8 threads
+constexpr int TL_THREADS = 1 << TL_LOG2NT;  // 256 (measured: 512-thread blocks at 64 registers were slower for c2/c3)
 constexpr int TL_TILE = 8192;    // complex elements per CTA tile (32 per thread)
 
 struct LGeom {
