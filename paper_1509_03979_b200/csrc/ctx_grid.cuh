@@ -53,6 +53,9 @@ template <typename T> struct GTw {
   const C2<T>* hi;
   int sh;
   CS_DEV C2<T> operator()(int64_t m) const {
+#ifdef CS_DIAG_NOTW
+    return mk<T>(T(1), T(0));  // diagnostics build only
+#endif
     return cmul<T>(__ldg(&hi[m >> sh]), __ldg(&lo[m & ((1ll << sh) - 1)]));
   }
 };
@@ -87,6 +90,7 @@ CS_DEV void staged(int n, LD&& ld, ST&& st) {
   }
 }
 constexpr int TL_UNR = 8;
+constexpr int TW_ANCHOR = 4;  // twiddle recurrence re-anchored from the table every 4 steps
 constexpr int TL_LOG2NT = 8;  // Tier L blocks: 256 threads (two per SM, 128 registers)
 // Asynchronous global -> shared copies of one complex element (cp.async, LDGSTS): a
 // whole tile's loads are in flight at once without staging registers.
@@ -376,14 +380,29 @@ template <typename T> struct GridCtx {
       cp_async_wait_all();
       __syncthreads();
       col_fft<false>();
-      staged<TL_UNR, CP<T>>(tile / 2, [&](int p) {
-        const int e = 2 * p;
-        const int64_t k1 = e >> lct, m2 = c0i + (e & (ct - 1));
-        return CP<T>{cmul<T>(sb[swz<T>(e)], tf(k1 * m2)), cmul<T>(sb[swz<T>(e + 1)], tf(k1 * (m2 + 1)))};
-      }, [&](int p, const CP<T>& v) {
-        const int e = 2 * p;
-        stp<T>(&wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))], v);
-      });
+      // thread's pairs p = tid + u NT: fixed columns (m2, m2 + 1), rows k1 = k10 + u dk.
+      // Twiddles W_L^{k1 m2}: a table lookup every TW_ANCHOR steps, a multiplication by
+      // W_L^{dk m2} in between (<= TW_ANCHOR - 1 roundings of drift)
+      {
+        const int NT = blockDim.x, np = tile / 2;
+        const int e0 = 2 * (int)threadIdx.x;
+        const int64_t k10 = e0 >> lct, dk = (2 * NT) >> lct;
+        const int64_t m2 = c0i + (e0 & (ct - 1));
+        const C2<T> sa = tf(dk * m2), sbb = tf(dk * (m2 + 1));
+        C2<T> wa = mk<T>(1, 0), wb = mk<T>(1, 0);
+        for (int u = 0, p = threadIdx.x; p < np; ++u, p += NT) {
+          const int64_t k1 = k10 + u * dk;
+          if ((u & (TW_ANCHOR - 1)) == 0) {
+            wa = tf(k1 * m2);
+            wb = tf(k1 * (m2 + 1));
+          } else {
+            wa = cmul<T>(wa, sa);
+            wb = cmul<T>(wb, sbb);
+          }
+          const int e = 2 * p;
+          stp<T>(&wk[k1 * l2 + m2], CP<T>{cmul<T>(sb[swz<T>(e)], wa), cmul<T>(sb[swz<T>(e + 1)], wb)});
+        }
+      }
       __syncthreads();
     }
   }
@@ -461,15 +480,28 @@ template <typename T> struct GridCtx {
         C2<T>* wk = Wk;
         const GTw<T> tf = twF;
         const int64_t l2 = L2;
-        staged<TL_UNR, CP<T>>(B * n2 / 2, [&](int q) {
-          const int r = q & lb, m2 = 2 * (q >> lb);
+        // pairs q = tid + u NT: fixed row r, columns m2 = m20 + u dm (anchored recurrence
+        // of W_L^{-k1 m2} as in pass A)
+        {
+          const int NT = blockDim.x, nq = B * n2 / 2;
+          const int r = (int)threadIdx.x & lb;
           const int64_t k1 = r ? kb : ka;
-          return CP<T>{cmulc<T>(sb[swz<T>((m2 << lb) | r)], tf(k1 * m2)),
-                       cmulc<T>(sb[swz<T>(((m2 + 1) << lb) | r)], tf(k1 * (m2 + 1)))};
-        }, [&](int q, const CP<T>& v) {
-          const int r = q & lb, m2 = 2 * (q >> lb);
-          stp<T>(&wk[(r ? kb : ka) * l2 + m2], v);
-        });
+          const int64_t m20 = 2 * ((int)threadIdx.x >> lb), dm = 2 * (NT >> lb);
+          const C2<T> st = tf(k1 * dm);  // W^{k1 dm}
+          C2<T> wa = mk<T>(1, 0), wb = mk<T>(1, 0);
+          for (int u = 0, q = threadIdx.x; q < nq; ++u, q += NT) {
+            const int64_t m2 = m20 + u * dm;
+            if ((u & (TW_ANCHOR - 1)) == 0) {
+              wa = tf(k1 * m2);
+              wb = tf(k1 * (m2 + 1));
+            } else {
+              wa = cmul<T>(wa, st);
+              wb = cmul<T>(wb, st);
+            }
+            stp<T>(&wk[k1 * l2 + m2], CP<T>{cmulc<T>(sb[swz<T>((int)(m2 << lb) | r)], wa),
+                                             cmulc<T>(sb[swz<T>((int)((m2 + 1) << lb) | r)], wb)});
+          }
+        }
       }
       __syncthreads();
     }
