@@ -25,24 +25,38 @@ struct GridBar {
 
 CS_DEV unsigned ld_volatile(const unsigned* p) { return *reinterpret_cast<const volatile unsigned*>(p); }
 
+CS_DEV unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+CS_DEV void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+CS_DEV unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Grid-wide barrier: block-level barrier, then thread 0 arrives with an acq_rel atomic and
+// spins on the generation word with acquire loads (release/acquire make every block's
+// writes before the barrier visible after it); bounded spin with a watchdog trap (~15 s).
 static CS_NOINL void grid_barrier(GridBar* gb) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned g = ld_volatile(&gb->gen);
-    __threadfence();
-    unsigned arrived = atomicAdd(&gb->count, 1u) + 1u;
+    const unsigned g = ld_acquire_gpu(&gb->gen);
+    const unsigned arrived = atom_add_acq_rel_gpu(&gb->count, 1u) + 1u;
     if (arrived == gridDim.x) {
-      atomicExch(&gb->count, 0u);
-      __threadfence();
-      atomicAdd(&gb->gen, 1u);
+      gb->count = 0u;                 // ordered before the release below
+      st_release_gpu(&gb->gen, g + 1u);
     } else {
       long long t0 = clock64();
-      while (ld_volatile(&gb->gen) == g) {
-        __nanosleep(32);
-        if (clock64() - t0 > (1ll << 35)) __trap();  // ~15 s watchdog: never hang the GPU
+      unsigned spins = 0;
+      while (ld_acquire_gpu(&gb->gen) == g) {
+        if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 35)) __trap();  // never hang the GPU
       }
     }
-    __threadfence();
   }
   __syncthreads();
 }
