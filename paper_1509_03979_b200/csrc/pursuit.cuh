@@ -315,6 +315,62 @@ CS_NOINL int run_ompr(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& 
   st.term = CS_TERM_ITER_CAP;
   for (int it = 1; it <= max_outer; ++it) {
     st.outer = it;
+    if (l == 1) {
+      // OMPR(1): J = {j}, j = argmax |c| off S (z = x~ + eta c = eta c off S); S u J has
+      // K + 1 entries, so S' = top-K of |z| over it drops exactly the entry with the
+      // smallest |z| (ties: the lowest indices are kept, the highest such one drops).
+      // Done as a sorted insert / delete and one argmin — no bitmask compaction or
+      // radix select (each costs several grid barriers in the grid context).
+      const int64_t j = detect_argmax<Ctx, T>(ctx, B.Sbits);
+      if (j < 0) { st.term = CS_TERM_SUPPORT_FIXED; break; }
+      const int* Sl = ctx.loc(S);
+      int lo = 0, hi = ns;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (Sl[mid] < j) lo = mid + 1; else hi = mid;
+      }
+      const int pos = lo;                                             // j's place in S u J
+      {
+        auto cv = ctx.cview();
+        cv.z = ctx.loc(cv.z);
+        cv.sign = ctx.loc(cv.sign);
+        for (int i = ctx.gtid; i <= ns; i += ctx.gnthr) {
+          const int u = (i < pos) ? S[i] : (i == pos ? (int)j : S[i - 1]);
+          const T xv = (i < pos) ? x[i] : (i == pos ? T(0) : x[i - 1]);
+          U[i] = u;
+          xU[i] = xv + eta * cv.at(u);                                // z on S u J
+        }
+      }
+      ctx.sync();
+      using Key = decltype(full_key(T(0)));
+      const Key kmax = Key(1) << (sizeof(Key) * 8 - 1);              // above every key
+      Key bk = 0;
+      int64_t bi = -1;
+      for (int i = ctx.gtid; i <= ns; i += ctx.gnthr) {
+        const Key kk = kmax - full_key(xU[i]) + 1;                    // larger = smaller |z|
+        const int64_t id = ns - i;                                    // smaller = higher position
+        if (kk > bk || (kk == bk && id < bi)) { bk = kk; bi = id; }
+      }
+      const int drop = (int)(ns - ctx.argmax(bk, bi));
+      if (drop == pos) { st.term = CS_TERM_SUPPORT_FIXED; break; }    // S' == S
+      for (int i = ctx.gtid; i < ns; i += ctx.gnthr) {
+        const int src = (i < drop) ? i : i + 1;
+        S2[i] = U[src];
+        x2[i] = (src < pos) ? x[src] : (src == pos ? T(0) : x[src - 1]);  // x0 = x~[S']
+      }
+      if (ctx.gtid == 0) {
+        const int d = U[drop];
+        B.Sbits[d >> 5] &= ~(1u << (d & 31));
+        B.Sbits[j >> 5] |= 1u << (j & 31);
+      }
+      ctx.sync();
+      cg_solve(ctx, S2, ns, x2, B.r, B.d, B.q, B.b, false, P, st);
+      swap_ptr<Ctx>(S, S2);
+      swap_ptr<Ctx>(x, x2);
+      ctx.set_input_support(S, ns);
+      rn2 = ctx.RES(x);
+      continue;
+    }
     // J = top-l of |z| = |x~ + eta c| off S (x~ = 0 there)
     if (l == 1) {
       int64_t j = detect_argmax<Ctx, T>(ctx, B.Sbits);
