@@ -171,6 +171,11 @@ template <typename T> struct GridCtx {
   C2<T>* Wk;    // [L] four-step intermediate
   T* Cb;        // [N] output (Makhoul order)
   int64_t* in_pos;  // [cap] positions of the remembered input support
+  // the support bucketed by pass-A / pass-C column tile (CSR): tile t owns the entries
+  // tlist[tstart[t] .. tstart[t+1]) (indices into the support list)
+  int* tcnt;        // [ntiles + 1] counts, then exclusive starts
+  int* tfill;       // [ntiles]
+  int* tlist;       // [cap]
   GTw<T> twF;   // W_L
   GTw<T> tw4;   // W_4N
   // shared memory
@@ -346,12 +351,55 @@ template <typename T> struct GridCtx {
   }
 
   // ---- sandwich ----
+  CS_DEV int ntiles() const { return (int)(L2 / CT); }
+  // column tile of Makhoul position p: complex index p/2 = m1 L2 + m2, tile m2 / CT
+  CS_DEV int tile_of(int64_t p) const { return (int)(((p >> 1) & (L2 - 1)) / CT); }
   CS_DEV void set_input_support(const int* supp, int ns) {
     for (int i = gtid; i < in_ns; i += gnthr) U[in_pos[i]] = T(0);
+    const int nt = ntiles();
+    for (int t = gtid; t <= nt; t += gnthr) { tcnt[t] = 0; if (t < nt) tfill[t] = 0; }
     sync();
-    for (int i = gtid; i < ns; i += gnthr) in_pos[i] = mk_pos(supp[i], N);
+    for (int i = gtid; i < ns; i += gnthr) {
+      const int64_t p = mk_pos(supp[i], N);
+      in_pos[i] = p;
+      atomicAdd(&tcnt[tile_of(p)], 1);
+    }
+    sync();
+    if (blockIdx.x == 0) {  // exclusive scan of the tile counts (one block; nt <= 4096)
+      __shared__ int carry;
+      if (threadIdx.x == 0) carry = 0;
+      __syncthreads();
+      for (int base = 0; base <= nt; base += blockDim.x) {
+        const int t = base + threadIdx.x;
+        const int v = (t < nt) ? tcnt[t] : 0;
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += u;
+        }
+        if (lane == 31) si[threadIdx.x >> 5] = inc;
+        __syncthreads();
+        int off = carry, tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+          if (w < (int)(threadIdx.x >> 5)) off += (int)si[w];
+          tot += (int)si[w];
+        }
+        __syncthreads();
+        if (t <= nt) tcnt[t] = off + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+      }
+    }
+    sync();
+    for (int i = gtid; i < ns; i += gnthr) {
+      const int t = tile_of(in_pos[i]);
+      tlist[tcnt[t] + atomicAdd(&tfill[t], 1)] = i;
+    }
     in_supp = supp;
     in_ns = ns;
+    sync();
   }
   CS_DEV void scatter(const T* vals) {
     const int* sp = in_supp;
@@ -416,6 +464,84 @@ template <typename T> struct GridCtx {
           const int e = 2 * p;
           stp<T>(&wk[k1 * l2 + m2], CP<T>{cmul<T>(sb[swz<T>(e)], wa), cmul<T>(sb[swz<T>(e + 1)], wb)});
         }
+      }
+      __syncthreads();
+    }
+  }
+  // pass A with a sparse input (H d, RES x on a support): each tile's few nonzeros are
+  // scattered from the bucketed support list into a zeroed tile — U is never read
+  CS_NOINL void passA_sparse(const T* vals) {
+    const int ct = CT, lct = (ct == 4) ? 2 : 1;
+    const int64_t l2 = L2, ntl = L2 / ct;
+    const int tile = (int)(L1 * ct);
+    C2<T>* sb = shp(buf);
+    T* sbt = reinterpret_cast<T*>(sb);
+    C2<T>* wk = Wk;
+    const GTw<T> tf = twF;
+    const int* sp = in_supp;
+    const int64_t* ip = in_pos;
+    const uint32_t* sg = sign;
+    for (int64_t t = blockIdx.x; t < ntl; t += gridDim.x) {
+      const int64_t c0i = t * ct;
+      for (int e = threadIdx.x; e < tile; e += blockDim.x) sb[e] = mk<T>(0, 0);
+      __syncthreads();
+      for (int q = tcnt[t] + threadIdx.x; q < tcnt[t + 1]; q += blockDim.x) {
+        const int i = tlist[q];
+        const int64_t p = ip[i], c = p >> 1;
+        const int e = (int)(((c / l2) << lct) | (c - (c / l2) * l2 - c0i));
+        sbt[2 * swz<T>(e) + (int)(p & 1)] = apply_sign<T>(sg, sp[i], vals[i]);
+      }
+      __syncthreads();
+      col_fft<false>();
+      {
+        const int NT = blockDim.x, np = tile / 2;
+        const int e0 = 2 * (int)threadIdx.x;
+        const int64_t k10 = e0 >> lct, dk = (2 * NT) >> lct;
+        const int64_t m2 = c0i + (e0 & (ct - 1));
+        const C2<T> sa = tf(dk * m2), sbb = tf(dk * (m2 + 1));
+        C2<T> wa = mk<T>(1, 0), wb = mk<T>(1, 0);
+        for (int u = 0, pp = threadIdx.x; pp < np; ++u, pp += NT) {
+          const int64_t k1 = k10 + u * dk;
+          if ((u & (TW_ANCHOR - 1)) == 0) {
+            wa = tf(k1 * m2);
+            wb = tf(k1 * (m2 + 1));
+          } else {
+            wa = cmul<T>(wa, sa);
+            wb = cmul<T>(wb, sbb);
+          }
+          const int e = 2 * pp;
+          stp<T>(&wk[k1 * l2 + m2], CP<T>{cmul<T>(sb[swz<T>(e)], wa), cmul<T>(sb[swz<T>(e + 1)], wb)});
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // pass C with a sparse output (H d restricted to the support): after the inverse column
+  // FFT each tile writes only its support entries, q_i = sigma_j . buf[p_i] — Cb is never
+  // written and no separate gather runs
+  CS_NOINL void passC_sparse(T* outv) {
+    const int ct = CT, lct = (ct == 4) ? 2 : 1;
+    const int64_t l2 = L2, ntl = L2 / ct;
+    const int tile = (int)(L1 * ct);
+    C2<T>* sb = shp(buf);
+    const T* sbt = reinterpret_cast<const T*>(sb);
+    const C2<T>* wk = Wk;
+    const int* sp = in_supp;
+    const int64_t* ip = in_pos;
+    const uint32_t* sg = sign;
+    for (int64_t t = blockIdx.x; t < ntl; t += gridDim.x) {
+      if (tcnt[t + 1] == tcnt[t]) continue;  // no support entry in this tile: skip it
+      const int64_t c0i = t * ct;
+      for (int e = threadIdx.x; e < tile; e += blockDim.x)
+        cp_async_c<T>(&sb[swz<T>(e)], &wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);
+      cp_async_wait_all();
+      __syncthreads();
+      col_fft<true>();
+      for (int q = tcnt[t] + threadIdx.x; q < tcnt[t + 1]; q += blockDim.x) {
+        const int i = tlist[q];
+        const int64_t p = ip[i], c = p >> 1;
+        const int e = (int)(((c / l2) << lct) | (c - (c / l2) * l2 - c0i));
+        outv[i] = apply_sign<T>(sg, sp[i], sbt[2 * swz<T>(e) + (int)(p & 1)]);
       }
       __syncthreads();
     }
@@ -545,17 +671,12 @@ template <typename T> struct GridCtx {
     }
   }
   CS_NOINL void H(const T* d, T* q) {
-    scatter(d);
-    passA();
+    passA_sparse(d);
     sync();
     passB<MID_H>(false, nullptr);
     sync();
-    passC();
+    passC_sparse(q);
     sync();
-    const CV cv = cview();
-    const int* sp = in_supp;
-    const int ns = in_ns, t0 = gtid, st = gnthr;
-    for (int i = t0; i < ns; i += st) q[i] = cv.at(sp[i]);
     ++applies;
   }
   template <class S> CS_NOINL void cg_iterate(S& s) {
@@ -563,8 +684,7 @@ template <typename T> struct GridCtx {
   }
   CS_NOINL double RES(const T* x) {
     if (x) {
-      scatter(x);
-      passA();
+      passA_sparse(x);
       sync();
     }
     double rn2 = passB<MID_RES>(x == nullptr, nullptr);

@@ -41,7 +41,7 @@ CS_HD LGeom l_geom(int64_t N) {
 
 // Workspace layout (byte offsets) — identical on host and device.
 struct LLayout {
-  int64_t U, Wk, Cb, c0, yT, twFlo, twFhi, tw4lo, tw4hi, in_pos;
+  int64_t U, Wk, Cb, c0, yT, twFlo, twFhi, tw4lo, tw4hi, in_pos, tcnt, tfill, tlist;
   int64_t S, S2, Ul, x, x2, xU, r, d, q, b, Sbits, Ubits, Pbits;
   int64_t ctl, bar, pd, pi, pk, ghist, ts, ctl_end;
   int64_t bytes;
@@ -66,6 +66,9 @@ CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int 
   s.tw4hi = take(((g.L >> g.sh4) + 1) * cs2);
   if (pursuit) {
     s.in_pos = take((int64_t)ucap * 8);
+    s.tcnt = take((g.L2 / g.CT + 1) * 4);
+    s.tfill = take((g.L2 / g.CT) * 4);
+    s.tlist = take((int64_t)ucap * 4);
     s.S = take((int64_t)K * 4);
     s.S2 = take((int64_t)K * 4);
     s.Ul = take((int64_t)ucap * 4);
@@ -81,6 +84,7 @@ CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int 
     s.Pbits = take(((ucap + 31) / 32) * 4);
   } else {
     s.in_pos = s.S = s.S2 = s.Ul = s.x = s.x2 = s.xU = s.r = s.d = s.q = s.b = 0;
+    s.tcnt = s.tfill = s.tlist = 0;
     s.Sbits = s.Ubits = s.Pbits = 0;
   }
   // control block (zeroed before every launch)
@@ -150,6 +154,9 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.tsh = ilog2(2 * g.L2);
   c.c0 = reinterpret_cast<T*>(ws + s.c0);
   c.in_pos = reinterpret_cast<int64_t*>(ws + s.in_pos);
+  c.tcnt = reinterpret_cast<int*>(ws + s.tcnt);
+  c.tfill = reinterpret_cast<int*>(ws + s.tfill);
+  c.tlist = reinterpret_cast<int*>(ws + s.tlist);
   c.twF.lo = reinterpret_cast<const C2<T>*>(ws + s.twFlo);
   c.twF.hi = reinterpret_cast<const C2<T>*>(ws + s.twFhi);
   c.twF.sh = g.shF;
