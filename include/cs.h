@@ -168,6 +168,15 @@ const char* cs_last_error(void);
 uint64_t cs_launch_count(int reset);
 const char* cs_version(void);
 
+/* Diagnostics: byte offset, in a Tier L (N > 16384) recovery workspace, of 8 uint64 phase
+ * accumulators (nanoseconds of %globaltimer seen by block 0: [0] everything between
+ * sandwiches, [1] pass A of H, [2] pass B of H, [3] pass C of H, [4] pass A of the residual,
+ * [5] its pass B, [6] its pass C + reduction), valid after the stream syncs; -1 for Tier S. */
+int64_t cs_diag_phase_offset(int alg, int64_t N, int64_t M, int32_t K, int32_t ompr_l, int precision);
+/* Diagnostics: microseconds per grid-wide barrier (with_sum: plus a grid reduction) in a
+ * cooperative launch shaped like the Tier L recovery; synchronous; -1 on error. */
+double cs_diag_grid_barrier_us(int iters, int with_sum);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,7 +54,7 @@ EXPORTS = [
     "cs_operator_ws_bytes", "cs_operator_apply", "cs_operator_apply_f64", "cs_operator_adjoint",
     "cs_operator_adjoint_f64", "cs_workspace_bytes", "cs_recover", "cs_recover_f64",
     "cs_recover_batched", "cs_recover_batched_f64", "cs_status_string", "cs_last_error",
-    "cs_launch_count", "cs_version",
+    "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
 ]
 
 
@@ -91,6 +91,8 @@ def load_library(path: str = LIB_PATH):
         "cs_last_error": (ctypes.c_char_p, []),
         "cs_launch_count": (ctypes.c_uint64, [ctypes.c_int]),
         "cs_version": (ctypes.c_char_p, []),
+        "cs_diag_phase_offset": (I64, [ctypes.c_int, I64, I64, I32, I32, ctypes.c_int]),
+        "cs_diag_grid_barrier_us": (ctypes.c_double, [ctypes.c_int, ctypes.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

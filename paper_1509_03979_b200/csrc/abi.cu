@@ -399,4 +399,30 @@ uint64_t cs_launch_count(int reset) {
 }
 const char* cs_version(void) { return "csgpu 0.1.0 (sm_100a)"; }
 
+double cs_diag_grid_barrier_us(int iters, int with_sum) {
+  const int64_t smem = l_smem_bytes<float>(1 << 20);
+  const void* fn = (const void*)k_l_recover<float>;
+  const int grid = l_maxgrid<float>(fn, smem);
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, 4096 + 2 * (size_t)grid * 8) != cudaSuccess) return -1.0;
+  cudaMemset(buf, 0, 4096 + 2 * (size_t)grid * 8);
+  GridBar* gb = reinterpret_cast<GridBar*>(buf);
+  uint64_t* out = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(buf) + 256);
+  double* pd = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + 4096);
+  void* args[] = {&gb, &pd, &iters, &with_sum, &out};
+  cudaLaunchCooperativeKernel((const void*)k_l_barrier_bench<float>, dim3(grid), dim3(TL_THREADS), args, 0, 0);
+  uint64_t h[2] = {0, 0};
+  cudaMemcpy(h, out, 16, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  return (double)h[0] / 1e3 / iters;
+}
+
+int64_t cs_diag_phase_offset(int alg, int64_t N, int64_t M, int32_t K, int32_t ompr_l, int precision) {
+  if (N <= TIER_S_MAX_N) return -1;
+  const int64_t ucap = ucap_of(alg, K, ompr_l);
+  const LLayout s = precision ? l_layout<double>(N, M, K, (int)ucap, true, l_grid_upper<double>())
+                              : l_layout<float>(N, M, K, (int)ucap, true, l_grid_upper<float>());
+  return s.ts + 8 * 8;
+}
+
 }  // extern "C"

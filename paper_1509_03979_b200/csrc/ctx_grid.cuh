@@ -189,6 +189,18 @@ template <typename T> struct GridCtx {
   int64_t* pick;    // [4]
   GridScratch<T> g;
   int bank, hpass;
+  // diagnostics: block 0 / thread 0 accumulates %globaltimer time per phase into
+  // ptime[phase] (workspace control block, zeroed per launch); tprev = last mark
+  uint64_t* ptime;
+  uint64_t tprev;
+  CS_DEV void mark(int phase) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (tprev) ptime[phase] += t - tprev;
+      tprev = t;
+    }
+  }
   const int* in_supp;
   int in_ns;
   int applies;
@@ -250,14 +262,21 @@ template <typename T> struct GridCtx {
       PI[blockIdx.x] = bi;
     }
     sync();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0 merges the per-block partials (lanes stride, then shuffle)
       Key bk = 0;
       int64_t bi = -1;
-      for (int c = 0; c < (int)gridDim.x; ++c) {
-        Key kc = (Key)PK[c];
-        if (kc > bk || (kc == bk && bk != 0 && PI[c] < bi)) { bk = kc; bi = PI[c]; }
+      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) {
+        const Key kc = (Key)PK[c];
+        const int64_t ic = PI[c];
+        if (kc > bk || (kc == bk && kc != 0 && ic < bi)) { bk = kc; bi = ic; }
       }
-      si[33] = bk ? bi : -1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const Key k2 = __shfl_down_sync(0xffffffffu, bk, o);
+        const int64_t i2 = __shfl_down_sync(0xffffffffu, bi, o);
+        if (k2 > bk || (k2 == bk && k2 != 0 && i2 < bi)) { bk = k2; bi = i2; }
+      }
+      if (threadIdx.x == 0) si[33] = bk ? bi : -1;
     }
     __syncthreads();
     int64_t r = si[33];
@@ -283,14 +302,22 @@ template <typename T> struct GridCtx {
     int64_t* P = g.pi + bank * g.maxgrid;
     if (threadIdx.x == 0) P[blockIdx.x] = ctot;
     sync();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0: lanes stride over the per-block partials, then shuffle
       int64_t before = 0, all = 0;
-      for (int c = 0; c < (int)gridDim.x; ++c) {
-        if (c < (int)blockIdx.x) before += P[c];
-        all += P[c];
+      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) {
+        const int64_t v = P[c];
+        if (c < (int)blockIdx.x) before += v;
+        all += v;
       }
-      si[32] = before;
-      si[33] = all;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        before += __shfl_down_sync(0xffffffffu, before, o);
+        all += __shfl_down_sync(0xffffffffu, all, o);
+      }
+      if (threadIdx.x == 0) {
+        si[32] = before;
+        si[33] = all;
+      }
     }
     __syncthreads();
     int64_t before = si[32];
@@ -671,27 +698,36 @@ template <typename T> struct GridCtx {
     }
   }
   CS_NOINL void H(const T* d, T* q) {
+    mark(0);
     passA_sparse(d);
     sync();
+    mark(1);
     passB<MID_H>(false, nullptr);
     sync();
+    mark(2);
     passC_sparse(q);
     sync();
+    mark(3);
     ++applies;
   }
   template <class S> CS_NOINL void cg_iterate(S& s) {
     cg_loop(*this, s, [this](const T* d, T* q) { H(d, q); });
   }
   CS_NOINL double RES(const T* x) {
+    mark(0);
     if (x) {
       passA_sparse(x);
       sync();
     }
+    mark(4);
     double rn2 = passB<MID_RES>(x == nullptr, nullptr);
     sync();
+    mark(5);
     passC();
+    const double r = sum(rn2);  // the reduction's barrier also publishes Cb
+    mark(6);
     ++applies;
-    return sum(rn2);  // the reduction's barrier also publishes Cb
+    return r;
   }
 };
 

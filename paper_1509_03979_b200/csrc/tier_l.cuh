@@ -192,6 +192,8 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.tw2.lo = t2lo; c.tw2.hi = t2hi;
   c.bank = 0;
   c.hpass = 0;
+  c.ptime = reinterpret_cast<uint64_t*>(ws + s.ts) + 8;
+  c.tprev = 0;
   c.in_supp = nullptr;
   c.in_ns = 0;
   c.applies = 0;
@@ -349,6 +351,38 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_recover(LArgs<T> a) {
     c.set_input_support(nullptr, 0);  // leave U all-zero for the next problem
     c.sync();
   }
+}
+
+// Diagnostics: `iters` grid barriers (and grid sums) in a cooperative launch of the
+// recovery's shape; block 0 / thread 0 records the elapsed %globaltimer.
+template <typename T>
+__global__ void __launch_bounds__(TL_THREADS) k_l_barrier_bench(GridBar* gb, double* pd, int iters, int with_sum,
+                                                               uint64_t* out) {
+  __shared__ double red[32];
+  uint64_t t0 = 0, t1 = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  double acc = 0;
+  for (int i = 0; i < iters; ++i) {
+    if (with_sum) {
+      double v = threadIdx.x * 1e-3;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        pd[(i & 1) * gridDim.x + blockIdx.x] = t;
+      }
+    }
+    grid_barrier(gb);
+    if (with_sum && threadIdx.x < 32) {
+      double a = 0;
+      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) a += pd[(i & 1) * gridDim.x + c];
+      acc += a;
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  if (blockIdx.x == 0 && threadIdx.x == 0) { out[0] = t1 - t0; out[1] = (uint64_t)acc; }
 }
 
 // ------------------------------------------------------------ host side ----
