@@ -175,8 +175,9 @@ CS_DEV void fft_pass(C2<T>* buf, const TwTable<T>& tw) {
       const int i = tid + it * NTA;
       if (ITEMS % NTA == 0 || i < ITEMS) {
         const int b = i & (B - 1), j = i >> LOG2B;
+        const int sj = swz<T>((j << LOG2B) | b);  // j < Lr: bit-disjoint from (r Lr) << LOG2B
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[it][r] = buf[swz<T>(((j + r * Lr) << LOG2B) + b)];
+        for (int r = 0; r < R; ++r) v[it][r] = buf[sj ^ swz_c<T>((r * Lr) << LOG2B)];
         if constexpr (Ns > 1) {
           const int k = j & (Ns - 1);
           C2<T> w1 = tw(k << (LOG2L - NSB - RB));
@@ -195,9 +196,9 @@ CS_DEV void fft_pass(C2<T>* buf, const TwTable<T>& tw) {
       if (ITEMS % NTA == 0 || i < ITEMS) {
         const int b = i & (B - 1), j = i >> LOG2B;
         const int k = j & (Ns - 1);
-        const int base = (j - k) * R + k;
+        const int sb = swz<T>((((j - k) * R + k) << LOG2B) | b);  // bit-disjoint from (r Ns) << LOG2B
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[swz<T>(((base + r * Ns) << LOG2B) + b)] = v[it][bitrev<R>(r)];
+        for (int r = 0; r < R; ++r) buf[sb ^ swz_c<T>((r * Ns) << LOG2B)] = v[it][bitrev<R>(r)];
       }
     }
   }
