@@ -78,6 +78,45 @@ CS_DEV int64_t row_rank(const uint32_t* mask, const int32_t* prefix, int64_t k) 
   return (int64_t)prefix[k >> 5] + __popc(below);
 }
 
+// Tile copies with UNR independent loads in flight per thread before any store
+// (memory-level parallelism: one outstanding 8-byte load per thread caps a
+// persistent grid near 0.6 TB/s).
+template <int UNR, typename V, class LD, class ST>
+CS_DEV void staged(int n, LD&& ld, ST&& st) {
+  for (int e0 = threadIdx.x; e0 < n; e0 += UNR * (int)blockDim.x) {
+    V v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int e = e0 + u * (int)blockDim.x;
+      if (e < n) v[u] = ld(e);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int e = e0 + u * (int)blockDim.x;
+      if (e < n) st(e, v[u]);
+    }
+  }
+}
+constexpr int TL_UNR = 8;
+constexpr int TW_ANCHOR = 4;  // twiddle recurrence re-anchored from the table every 4 steps
+// the same over the whole grid (index range [0, n), thread gtid of gnthr)
+template <int UNR, typename V, class LD, class ST>
+CS_DEV void gstaged(int64_t n, int64_t gtid, int64_t gnthr, LD&& ld, ST&& st) {
+  for (int64_t e0 = gtid; e0 < n; e0 += UNR * gnthr) {
+    V v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t e = e0 + u * gnthr;
+      if (e < n) v[u] = ld(e);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t e = e0 + u * gnthr;
+      if (e < n) st(e, v[u]);
+    }
+  }
+}
+
 // Two-pass top-K of the CTA context (select.cuh): first-digit bins, candidate cap.
 constexpr int TOPK_BINS = 1024;
 constexpr int TOPK_CAP = 1024;

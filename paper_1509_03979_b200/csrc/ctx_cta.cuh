@@ -56,6 +56,7 @@ template <typename T> struct CtaCtx {
   int applies;
 
   CS_DEV void sync() { __syncthreads(); }
+  CS_DEV void mark(int) {}  // phase accounting is a grid-context diagnostic
   // pointer into this context's working set as the compiler should see it: shared (Tier S)
   template <typename P> CS_DEV P* loc(P* p) const { return shp(p); }
 

@@ -84,27 +84,6 @@ template <typename T> struct GridScratch {
   int maxgrid;
 };
 
-// Tile copies with UNR independent loads in flight per thread before any store
-// (memory-level parallelism: one outstanding 8-byte load per thread caps a
-// persistent grid near 0.6 TB/s).
-template <int UNR, typename V, class LD, class ST>
-CS_DEV void staged(int n, LD&& ld, ST&& st) {
-  for (int e0 = threadIdx.x; e0 < n; e0 += UNR * (int)blockDim.x) {
-    V v[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int e = e0 + u * (int)blockDim.x;
-      if (e < n) v[u] = ld(e);
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int e = e0 + u * (int)blockDim.x;
-      if (e < n) st(e, v[u]);
-    }
-  }
-}
-constexpr int TL_UNR = 8;
-constexpr int TW_ANCHOR = 4;  // twiddle recurrence re-anchored from the table every 4 steps
 constexpr int TL_LOG2NT = 8;  // Tier L blocks: 256 threads (two per SM, 128 registers)
 // Asynchronous global -> shared copies of one complex element (cp.async, LDGSTS): a
 // whole tile's loads are in flight at once without staging registers.
@@ -133,23 +112,6 @@ template <typename T> CS_DEV void stp(C2<T>* p, const CP<T>& v) {
   } else {
     p[0] = v.a;
     p[1] = v.b;
-  }
-}
-// the same over the whole grid (index range [0, n), thread gtid of gnthr)
-template <int UNR, typename V, class LD, class ST>
-CS_DEV void gstaged(int64_t n, int64_t gtid, int64_t gnthr, LD&& ld, ST&& st) {
-  for (int64_t e0 = gtid; e0 < n; e0 += UNR * gnthr) {
-    V v[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int64_t e = e0 + u * gnthr;
-      if (e < n) v[u] = ld(e);
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int64_t e = e0 + u * gnthr;
-      if (e < n) st(e, v[u]);
-    }
   }
 }
 
@@ -382,7 +344,6 @@ template <typename T> struct GridCtx {
   // column tile of Makhoul position p: complex index p/2 = m1 L2 + m2, tile m2 / CT
   CS_DEV int tile_of(int64_t p) const { return (int)(((p >> 1) & (L2 - 1)) / CT); }
   CS_DEV void set_input_support(const int* supp, int ns) {
-    for (int i = gtid; i < in_ns; i += gnthr) U[in_pos[i]] = T(0);
     const int nt = ntiles();
     for (int t = gtid; t <= nt; t += gnthr) { tcnt[t] = 0; if (t < nt) tfill[t] = 0; }
     sync();

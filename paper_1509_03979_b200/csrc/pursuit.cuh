@@ -166,6 +166,17 @@ CS_NOINL void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* o
     };
     if (topk_cta_fast_v<Ctx, Key>(ctx, n, (int)K, visit, out)) return;
   }
+  if constexpr (!Ctx::kTopkFast) {
+    // grid: materialise the keys once in natural index order (the dense input buffer U
+    // is free during a recovery), so the radix passes read them contiguously
+    Key* keys = reinterpret_cast<Key*>(ctx.U);
+    gstaged<TL_UNR, Key>(N, ctx.gtid, ctx.gnthr, [&](int64_t j) {
+      return (excl && bit_test(excl, j)) ? Key(0) : full_key(cv.raw(j));
+    }, [&](int64_t j, Key k) { keys[j] = k; });
+    ctx.sync();
+    topk_bits(ctx, N, K, [keys](int64_t j) { return keys[j]; }, out, false);
+    return;
+  }
   topk_bits(ctx, N, K, [cv, excl](int64_t j) {
     if (excl && bit_test(excl, j)) return Key(0);
     return full_key(cv.raw(j));
@@ -262,7 +273,9 @@ CS_NOINL int run_sp(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& rn
   st.term = CS_TERM_ITER_CAP;
   for (int it = 1; it <= max_outer; ++it) {
     st.outer = it;
+    ctx.mark(0);
     detect_topk<Ctx, T>(ctx, K, B.Sbits, B.Ubits);               // J = top-K off S
+    ctx.mark(7);
     for (int64_t w = ctx.gtid; w < nwords; w += ctx.gnthr) B.Ubits[w] |= B.Sbits[w];  // T = S u J
     ctx.sync();
     int nu = (int)compact_bits(ctx, B.Ubits, N, [&](int64_t k, int64_t j) { U[k] = (int)j; });

@@ -204,9 +204,19 @@ CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_b
   unsigned* hist = ctx.hist_ptr();
   for (int shift = NB - 8; shift >= 0; shift -= 8) {
     ctx.hist_clear();
-    for (int64_t i = t0; i < n; i += st) {
-      Key k = key(i);
-      if ((k & pmask) == prefix) hist_add_warp(hist, (unsigned)((k >> shift) & 255));
+    constexpr int UK = 8;  // keys in flight per thread before the histogram updates
+    for (int64_t i0 = t0; i0 < n; i0 += UK * st) {
+      Key kv[UK];
+#pragma unroll
+      for (int u = 0; u < UK; ++u) {
+        const int64_t i = i0 + u * st;
+        kv[u] = (i < n) ? key(i) : Key(0);
+      }
+#pragma unroll
+      for (int u = 0; u < UK; ++u) {
+        const int64_t i = i0 + u * st;
+        if (i < n && (kv[u] & pmask) == prefix) hist_add_warp(hist, (unsigned)((kv[u] >> shift) & 255));
+      }
     }
     ctx.hist_done();  // merged counts now in ctx.hist_smem()
     int64_t dsel, cum, hsel;

@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_recover(LArgs<T> a) {
     B.Ubits = reinterpret_cast<uint32_t*>(ws + s.Ubits);
     B.Pbits = reinterpret_cast<uint32_t*>(ws + s.Pbits);
     run_pursuit<GridCtx<T>, T>(c, a.P, B, a.vals + b * a.P.K, a.supp + b * a.P.K, a.reps + b, pre);
-    c.set_input_support(nullptr, 0);  // leave U all-zero for the next problem
+    c.set_input_support(nullptr, 0);
     c.sync();
   }
 }

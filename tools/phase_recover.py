@@ -24,7 +24,7 @@ torch.cuda.synchronize()
 tot = ev0.elapsed_time(ev1)
 raw = ws.buf.cpu().numpy()
 # ptime = ts area + 8 slots; locate the ts area: search for the accumulator block (values < 1e12 ns)
-names = ["between sandwiches", "H pass A", "H pass B", "H pass C", "RES pass A", "RES pass B", "RES pass C+sum"]
+names = ["between sandwiches", "H pass A", "H pass B", "H pass C", "RES pass A", "RES pass B", "RES pass C+sum", "SP detection top-K"]
 rep = r.reports()[0]
 print("total ms", tot, "outer", rep["outer_iters"], "cg", rep["cg_iters_total"], "applies", rep["applies"])
 off = cs.load_library().cs_diag_phase_offset(cs.ALGS[cfg.alg], cfg.N, cfg.M, cfg.K, 0, 0)
