@@ -161,6 +161,28 @@ cs_status cs_recover_batched_f64(const cs_operator* op, int alg, const double* d
                                  cs_report* d_reports, void* d_ws, size_t ws_bytes,
                                  cs_stream_t stream);
 
+/* Host-buffer variants (the end-to-end entry points): h_Y [B][M] and the outputs
+ * h_vals [B][K], h_support [B][K], h_reports [B] are HOST memory (pinned for overlap).
+ * The batch is copied in, recovered and copied out in chunks of two recovery waves, on
+ * internal streams so that the copies of one chunk overlap the recovery of its
+ * neighbours; `stream` is ordered before the first copy and after the last one (results
+ * are valid once `stream` is synchronised).  d_ws: DEVICE workspace of at least
+ * cs_workspace_bytes_host bytes (the recovery workspace plus device staging of the
+ * batch).  Errors as cs_recover_batched. */
+cs_status cs_workspace_bytes_host(int alg, int64_t N, int64_t M, int32_t K, int64_t batch,
+                                  int precision /*0 fp32, 1 fp64*/, const cs_options* opts,
+                                  size_t* bytes);
+cs_status cs_recover_batched_host(const cs_operator* op, int alg, const float* h_Y, int64_t B,
+                                  int64_t M, int64_t N, int32_t K, double tol,
+                                  const cs_options* opts, float* h_vals, int32_t* h_support,
+                                  cs_report* h_reports, void* d_ws, size_t ws_bytes,
+                                  cs_stream_t stream);
+cs_status cs_recover_batched_host_f64(const cs_operator* op, int alg, const double* h_Y, int64_t B,
+                                      int64_t M, int64_t N, int32_t K, double tol,
+                                      const cs_options* opts, double* h_vals,
+                                      int32_t* h_support, cs_report* h_reports, void* d_ws,
+                                      size_t ws_bytes, cs_stream_t stream);
+
 /* ---------------------------------------------------------------- misc ------ */
 const char* cs_status_string(cs_status s);
 const char* cs_last_error(void);

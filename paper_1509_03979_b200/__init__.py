@@ -53,7 +53,8 @@ EXPORTS = [
     "cs_operator_meta_bytes", "cs_operator_create", "cs_operator_destroy", "cs_operator_info",
     "cs_operator_ws_bytes", "cs_operator_apply", "cs_operator_apply_f64", "cs_operator_adjoint",
     "cs_operator_adjoint_f64", "cs_workspace_bytes", "cs_recover", "cs_recover_f64",
-    "cs_recover_batched", "cs_recover_batched_f64", "cs_status_string", "cs_last_error",
+    "cs_recover_batched", "cs_recover_batched_f64", "cs_workspace_bytes_host", "cs_recover_batched_host",
+    "cs_recover_batched_host_f64", "cs_status_string", "cs_last_error",
     "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
 ]
 
@@ -87,6 +88,12 @@ def load_library(path: str = LIB_PATH):
                                      ctypes.POINTER(cs_options), P, P, P, P, SZ, P]),
         "cs_recover_batched_f64": (I32, [P, ctypes.c_int, P, I64, I64, I64, I32, ctypes.c_double,
                                          ctypes.POINTER(cs_options), P, P, P, P, SZ, P]),
+        "cs_workspace_bytes_host": (I32, [ctypes.c_int, I64, I64, I32, I64, ctypes.c_int,
+                                          ctypes.POINTER(cs_options), ctypes.POINTER(SZ)]),
+        "cs_recover_batched_host": (I32, [P, ctypes.c_int, P, I64, I64, I64, I32, ctypes.c_double,
+                                          ctypes.POINTER(cs_options), P, P, P, P, SZ, P]),
+        "cs_recover_batched_host_f64": (I32, [P, ctypes.c_int, P, I64, I64, I64, I32, ctypes.c_double,
+                                              ctypes.POINTER(cs_options), P, P, P, P, SZ, P]),
         "cs_status_string": (ctypes.c_char_p, [I32]),
         "cs_last_error": (ctypes.c_char_p, []),
         "cs_launch_count": (ctypes.c_uint64, [ctypes.c_int]),
@@ -248,6 +255,41 @@ def cs_recover_batched(op: Operator, alg, Y, K: int, tol: float, opts: Optional[
     _check(f(op.handle, a, _ptr(Y), B, M, op.N, K, tol,
              ctypes.byref(opts) if opts is not None else None, _ptr(out.values), _ptr(out.support),
              _ptr(out.report_dev), _ptr(ws), ws.numel(), _stream(stream)), "cs_recover_batched")
+    return out
+
+
+@dataclass
+class HostRecovery:
+    support: "object"   # torch int32 [B, K] (pinned host)
+    values: "object"    # torch float [B, K] (pinned host)
+    report_host: "object"  # torch uint8 [B, 40] (pinned host)
+
+    def reports(self):
+        return np.frombuffer(self.report_host.numpy().tobytes(), dtype=REPORT_DTYPE)
+
+
+def cs_recover_batched_host(op: Operator, alg, Y_host, K: int, tol: float, opts: Optional[cs_options] = None,
+                            workspace: Optional[Workspace] = None, out: Optional[HostRecovery] = None,
+                            stream=None) -> HostRecovery:
+    """End-to-end entry point: Y_host [B, M] in (pinned) host memory, results to pinned host
+    memory; the copies overlap the recovery inside the library (cs_recover_batched_host)."""
+    torch = _torch()
+    B, M = Y_host.shape
+    a = ALGS[alg] if isinstance(alg, str) else alg
+    prec = 1 if Y_host.dtype == torch.float64 else 0
+    n = ctypes.c_size_t()
+    _check(load_library().cs_workspace_bytes_host(a, op.N, M, K, B, prec,
+                                                  ctypes.byref(opts) if opts is not None else None,
+                                                  ctypes.byref(n)), "cs_workspace_bytes_host")
+    ws = (workspace or Workspace()).get(n.value, op.meta.device)
+    if out is None:
+        out = HostRecovery(torch.empty((B, K), dtype=torch.int32).pin_memory(),
+                           torch.empty((B, K), dtype=Y_host.dtype).pin_memory(),
+                           torch.empty((B, 40), dtype=torch.uint8).pin_memory())
+    f = _lib.cs_recover_batched_host_f64 if prec else _lib.cs_recover_batched_host
+    _check(f(op.handle, a, _ptr(Y_host), B, M, op.N, K, tol,
+             ctypes.byref(opts) if opts is not None else None, _ptr(out.values), _ptr(out.support),
+             _ptr(out.report_host), _ptr(ws), ws.numel(), _stream(stream)), "cs_recover_batched_host")
     return out
 
 

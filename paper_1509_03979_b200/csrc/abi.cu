@@ -6,9 +6,11 @@
 //     one thread block per problem (tier_s.cuh);
 //   Tier L (larger N): one cooperative persistent grid per problem with a
 //     four-step FFT over L2-resident scratch (tier_l.cuh).
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "tier_l.cuh"
@@ -245,6 +247,103 @@ cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, in
                            g_launches, g_last_error);
 }
 
+// ---------------------------------------------------------------- host-buffer pipeline
+// Streams and events of the host-buffer entry points, created once per device.
+struct HostPipe {
+  cudaStream_t s_in = nullptr, s_out = nullptr, s_comp = nullptr;
+  cudaEvent_t ev[2][64] = {};
+  cudaEvent_t fin = nullptr;
+  bool ok = false;
+};
+HostPipe& host_pipe(int dev) {
+  static std::mutex mu;
+  static HostPipe pipes[16];
+  std::lock_guard<std::mutex> lock(mu);
+  HostPipe& p = pipes[dev & 15];
+  if (!p.ok) {
+    bool good = cudaStreamCreateWithFlags(&p.s_in, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&p.s_out, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&p.s_comp, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaEventCreateWithFlags(&p.fin, cudaEventDisableTiming) == cudaSuccess;
+    for (int k = 0; k < 2 && good; ++k)
+      for (int c = 0; c < 64 && good; ++c)
+        good = cudaEventCreateWithFlags(&p.ev[k][c], cudaEventDisableTiming) == cudaSuccess;
+    p.ok = good;
+  }
+  return p;
+}
+
+size_t staging_bytes(int64_t B, int64_t M, int32_t K, size_t es) {
+  return (size_t)(align_up(B * M * (int64_t)es, 256) + align_up(B * K * (int64_t)es, 256) +
+                  align_up(B * (int64_t)K * 4, 256) + align_up(B * (int64_t)sizeof(cs_report), 256));
+}
+
+// y (pinned host) -> device -> recover -> (support, values, reports) (pinned host), in chunks
+// of whole waves on two alternating compute streams so that copies overlap recovery and a
+// chunk's last wave overlaps the next chunk.
+template <typename T>
+cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t B, int64_t M, int64_t N,
+                            int32_t K, double tol, const cs_options* opts, T* hvals, int32_t* hsupp,
+                            cs_report* hreps, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!op) return fail(CS_ERR_INVALID_ARG, "null operator");
+  if (!hY || !hvals || !hsupp || !hreps) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
+  if (B < 1 || B > op->B) return fail(CS_ERR_INVALID_ARG, "batch exceeds operator instances");
+  if (cs_status s = check_N(N)) return s;
+  if (K < 1) return fail(CS_ERR_INVALID_ARG, "K must be >= 1");
+  const int prec = sizeof(T) == 8 ? 1 : 0;
+  size_t need_rec = 0;
+  if (cs_status s = cs_workspace_bytes(alg, N, M, K, B, prec, opts, &need_rec)) return s;
+  const size_t rec_al = (size_t)align_up((int64_t)need_rec, 256);
+  if (!ws || ws_bytes < rec_al + staging_bytes(B, M, K, sizeof(T)))
+    return fail(CS_ERR_WORKSPACE, "workspace too small");
+  char* w = reinterpret_cast<char*>(ws);
+  T* dY = reinterpret_cast<T*>(w + rec_al);
+  T* dvals = reinterpret_cast<T*>(reinterpret_cast<char*>(dY) + align_up(B * M * (int64_t)sizeof(T), 256));
+  int32_t* dsupp = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dvals) + align_up(B * K * (int64_t)sizeof(T), 256));
+  cs_report* dreps = reinterpret_cast<cs_report*>(reinterpret_cast<char*>(dsupp) + align_up(B * (int64_t)K * 4, 256));
+  int dev = 0;
+  CS_CUDA(cudaGetDevice(&dev));
+  HostPipe& hp = host_pipe(dev);
+  if (!hp.ok) return fail(CS_ERR_CUDA, "could not create the host-pipeline streams");
+  const int l = (opts && opts->ompr_l > 0) ? opts->ompr_l : 1;
+  const bool tier_s = tier_s_fits<T>(N, K, ucap_of(alg, K, l), true);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // chunk = two waves of the Tier S recovery (two blocks per SM); Tier L: one chunk
+  const int64_t CH = tier_s ? std::max<int64_t>(1, (int64_t)4 * nsm) : B;
+  const int64_t nch = (B + CH - 1) / CH;
+  if (nch > 64) return fail(CS_ERR_INVALID_ARG, "batch too large for the host pipeline (64 chunks)");
+  CS_CUDA(cudaEventRecord(hp.fin, st));             // order behind earlier work on the caller's stream
+  CS_CUDA(cudaStreamWaitEvent(hp.s_in, hp.fin, 0));
+  for (int64_t c = 0; c < nch; ++c) {
+    const int64_t b0 = c * CH, cnt = std::min(CH, B - b0);
+    CS_CUDA(cudaMemcpyAsync(dY + b0 * M, hY + b0 * M, (size_t)(cnt * M) * sizeof(T), cudaMemcpyHostToDevice,
+                            hp.s_in));
+    CS_CUDA(cudaEventRecord(hp.ev[0][c], hp.s_in));
+    cudaStream_t sc = (c & 1) ? hp.s_comp : st;
+    CS_CUDA(cudaStreamWaitEvent(sc, hp.ev[0][c], 0));
+    cs_operator sub = *op;
+    sub.meta = op->meta + b0 * meta_stride(op->N, op->M);
+    sub.B = cnt;
+    char* rws = tier_s ? w + (size_t)(b0 * N) * sizeof(T) : w;
+    const size_t rws_bytes = tier_s ? (size_t)(cnt * N) * sizeof(T) : need_rec;
+    if (cs_status s = recover_impl<T>(&sub, alg, dY + b0 * M, cnt, M, N, K, tol, opts, dvals + b0 * K,
+                                      dsupp + b0 * K, dreps + b0, rws, rws_bytes, sc))
+      return s;
+    CS_CUDA(cudaEventRecord(hp.ev[1][c], sc));
+    CS_CUDA(cudaStreamWaitEvent(hp.s_out, hp.ev[1][c], 0));
+    CS_CUDA(cudaMemcpyAsync(hsupp + b0 * K, dsupp + b0 * K, (size_t)(cnt * K) * 4, cudaMemcpyDeviceToHost,
+                            hp.s_out));
+    CS_CUDA(cudaMemcpyAsync(hvals + b0 * K, dvals + b0 * K, (size_t)(cnt * K) * sizeof(T),
+                            cudaMemcpyDeviceToHost, hp.s_out));
+    CS_CUDA(cudaMemcpyAsync(hreps + b0, dreps + b0, (size_t)cnt * sizeof(cs_report), cudaMemcpyDeviceToHost,
+                            hp.s_out));
+  }
+  CS_CUDA(cudaEventRecord(hp.fin, hp.s_out));
+  CS_CUDA(cudaStreamWaitEvent(st, hp.fin, 0));      // the caller's stream completes after everything
+  return CS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -352,6 +451,28 @@ cs_status cs_workspace_bytes(int alg, int64_t N, int64_t M, int32_t K, int64_t b
                  : tier_l_recover_ws_bytes<float>(N, M, K, (int)ucap);
   }
   return CS_OK;
+}
+
+cs_status cs_workspace_bytes_host(int alg, int64_t N, int64_t M, int32_t K, int64_t batch, int precision,
+                                  const cs_options* opts, size_t* bytes) {
+  size_t rec = 0;
+  if (cs_status s = cs_workspace_bytes(alg, N, M, K, batch, precision, opts, &rec)) return s;
+  *bytes = (size_t)align_up((int64_t)rec, 256) + staging_bytes(batch, M, K, precision ? 8 : 4);
+  return CS_OK;
+}
+cs_status cs_recover_batched_host(const cs_operator* op, int alg, const float* h_Y, int64_t B, int64_t M,
+                                  int64_t N, int32_t K, double tol, const cs_options* opts, float* h_vals,
+                                  int32_t* h_support, cs_report* h_reports, void* d_ws, size_t ws_bytes,
+                                  cs_stream_t stream) {
+  return recover_host_impl<float>(op, alg, h_Y, B, M, N, K, tol, opts, h_vals, h_support, h_reports, d_ws,
+                                  ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+cs_status cs_recover_batched_host_f64(const cs_operator* op, int alg, const double* h_Y, int64_t B, int64_t M,
+                                      int64_t N, int32_t K, double tol, const cs_options* opts, double* h_vals,
+                                      int32_t* h_support, cs_report* h_reports, void* d_ws, size_t ws_bytes,
+                                      cs_stream_t stream) {
+  return recover_host_impl<double>(op, alg, h_Y, B, M, N, K, tol, opts, h_vals, h_support, h_reports, d_ws,
+                                   ws_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 cs_status cs_recover(const cs_operator* op, int alg, const float* d_y, int64_t M, int64_t N, int32_t K,

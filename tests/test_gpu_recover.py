@@ -130,3 +130,21 @@ def test_all_ties_zero_measurements(cs, alg, N, M, K):
         assert np.array_equal(np.sort(supp[b]), refs[b].support), (alg, b)
         assert np.array_equal(np.sort(supp[b]), np.arange(K))
     assert np.all(res.values.cpu().numpy() == 0)
+
+
+def test_host_buffer_entry_point_matches_device_path(cs):
+    """cs_recover_batched_host (chunked copy/compute pipeline) returns exactly what the
+    device entry point returns, for a batch spanning several chunks and a ragged tail."""
+    cfg = CONFIGS[4].scaled(4, batch=1300)     # N = 4096; chunks of 4 x #SM problems
+    probs = cs_inputs.make_batch(cfg, count=1300)
+    ys = measured(probs)
+    dev = torch.device("cuda:0")
+    bits, rows = to_dev(probs, dev)
+    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=1300)
+    Yd = torch.from_numpy(ys).to(dev)
+    ref = cs.cs_recover_batched(A, cfg.alg, Yd, cfg.K, 1e-6)
+    host = cs.cs_recover_batched_host(A, cfg.alg, torch.from_numpy(ys).pin_memory(), cfg.K, 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(host.support, ref.support.cpu())
+    assert torch.equal(host.values, ref.values.cpu())
+    assert np.array_equal(host.reports(), ref.reports())
