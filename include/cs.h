@@ -90,10 +90,11 @@ typedef struct {
  */
 typedef struct cs_operator cs_operator;
 
-/* Bytes of device metadata `cs_operator_create` needs per instance: sign words, row
- * bitmask and row-rank prefix (3 * ceil(N/32) * 4 bytes), plus for N > 16384 a row
- * permutation (M * 4 bytes: the row mask is stored in the four-step FFT's transposed
- * order there); 256-byte aligned, plus a 256-byte status tail. */
+/* Bytes of device metadata `cs_operator_create` needs per instance: sign words; for
+ * N <= 16384 the row bitmask and row-rank prefix in natural order (CTA tier); for every N
+ * the row bitmask and prefix in the four-step FFT's transposed order plus a row
+ * permutation of M int32 (grid tier) — (3 or 5) * ceil(N/32) * 4 + 4M
+ * bytes; 256-byte aligned, plus a 256-byte status tail. */
 size_t cs_operator_meta_bytes(int64_t N, int64_t M, int64_t batch);
 
 /* Build an operator.

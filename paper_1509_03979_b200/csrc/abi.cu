@@ -86,18 +86,15 @@ struct TPos {
     return ((k & ((int64_t(1) << s1) - 1)) << tsh) | (k >> s1);
   }
 };
-TPos tpos_of(int64_t N) {
-  TPos t{0, 0};
-  if (N > TIER_S_MAX_N) {
-    const LGeom g = l_geom(N);
-    t.s1 = ilog2(g.L1);
-    t.tsh = ilog2(2 * g.L2);
-  }
-  return t;
+TPos tpos_of(int64_t N) {  // the four-step's transposed order (Tier L geometry of N)
+  const LGeom g = l_geom(N);
+  return TPos{ilog2(g.L1), ilog2(2 * g.L2)};
 }
 
-__global__ void k_rows_mask(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t stride, TPos tp,
-                            const int32_t* rows, const uint32_t* sign_in, uint32_t* meta, int* err) {
+// natural_off >= 0: also set the natural-order bit (Tier S); toff: transposed mask (Tier L)
+__global__ void k_rows_mask(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t stride, int64_t natural_off,
+                            int64_t toff, TPos tp, const int32_t* rows, const uint32_t* sign_in, uint32_t* meta,
+                            int* err) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < B * nw) {  // copy sign words
     int64_t b = i / nw, w = i % nw;
@@ -108,20 +105,21 @@ __global__ void k_rows_mask(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t
   int32_t r = rows[i];
   bool ok = (r >= 0) && (r < N) && (m == 0 || rows[i - 1] < r);
   if (!ok) { atomicOr(err, 1); return; }
+  if (natural_off >= 0) atomicOr(&meta[b * stride + natural_off + (r >> 5)], 1u << (r & 31));
   const int64_t t = tp(r);
-  atomicOr(&meta[b * stride + nw + (t >> 5)], 1u << (t & 31));
+  atomicOr(&meta[b * stride + toff + (t >> 5)], 1u << (t & 31));
 }
 
 // Tier L: tperm[rank of row m in the transposed order] = m
-__global__ void k_rows_tperm(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t stride, TPos tp, const int32_t* rows,
-                             uint32_t* meta) {
+__global__ void k_rows_tperm(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t stride, int64_t toff, TPos tp,
+                             const int32_t* rows, uint32_t* meta) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= B * M) return;
   int64_t b = i / M, m = i % M;
   if (rows[i] < 0 || rows[i] >= N) return;  // invalid rows: reported by k_rows_mask
-  const uint32_t* mask = meta + b * stride + nw;
-  const int32_t* pre = reinterpret_cast<const int32_t*>(meta + b * stride + 2 * nw);
-  int32_t* perm = reinterpret_cast<int32_t*>(meta + b * stride + 3 * nw);
+  const uint32_t* mask = meta + b * stride + toff;
+  const int32_t* pre = reinterpret_cast<const int32_t*>(meta + b * stride + toff + nw);
+  int32_t* perm = reinterpret_cast<int32_t*>(meta + b * stride + toff + 2 * nw);
   const int64_t t = tp(rows[i]);
   const uint32_t w = mask[t >> 5];
   const int32_t rank = pre[t >> 5] + __popc((t & 31) ? (w & ((1u << (t & 31)) - 1u)) : 0u);
@@ -129,12 +127,12 @@ __global__ void k_rows_tperm(int64_t N, int64_t M, int64_t B, int64_t nw, int64_
 }
 
 // exclusive prefix of popcounts per instance: one block per instance
-__global__ void k_rows_prefix(int64_t nw, int64_t stride, uint32_t* meta) {
+__global__ void k_rows_prefix(int64_t nw, int64_t stride, int64_t mask_off, uint32_t* meta) {
   __shared__ int32_t wsum[32];
   __shared__ int32_t carry;
   const int64_t b = blockIdx.x;
-  const uint32_t* mask = meta + b * stride + nw;
-  int32_t* pre = reinterpret_cast<int32_t*>(meta + b * stride + 2 * nw);
+  const uint32_t* mask = meta + b * stride + mask_off;
+  int32_t* pre = reinterpret_cast<int32_t*>(meta + b * stride + mask_off + nw);
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
@@ -162,9 +160,17 @@ __global__ void k_rows_prefix(int64_t nw, int64_t stride, uint32_t* meta) {
 }
 
 
+// Per-instance metadata (words): [sign nw] then, for N <= 16384 only, the natural-order
+// [row mask nw][prefix nw] of Tier S; then for every N the Tier L transposed
+// [row mask nw][prefix nw][tperm M] (Tier L also serves small N when Tier S's shared
+// memory cannot hold the pursuit, e.g. fp64 with a large K).
+int64_t meta_toff(int64_t N) {
+  const int64_t nw = (N + 31) / 32;
+  return N > TIER_S_MAX_N ? nw : 3 * nw;
+}
 int64_t meta_stride(int64_t N, int64_t M) {
   const int64_t nw = (N + 31) / 32;
-  return 3 * nw + (N > TIER_S_MAX_N ? M : 0);
+  return meta_toff(N) + 2 * nw + M;
 }
 
 OpMeta meta_of(const cs_operator* op) {
@@ -174,6 +180,7 @@ OpMeta meta_of(const cs_operator* op) {
   m.M = op->M;
   m.nw = op->nw;
   m.stride = meta_stride(op->N, op->M);
+  m.toff = meta_toff(op->N);
   return m;
 }
 
@@ -375,15 +382,18 @@ cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t
   int* err = reinterpret_cast<int*>(reinterpret_cast<char*>(d_meta) + align_up(batch * stride * 4, 256));
   CS_CUDA(cudaMemsetAsync(d_meta, 0, meta_bytes, st));
   int64_t nthr = std::max(batch * M, batch * nw);
-  k_rows_mask<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(N, M, batch, nw, stride, tp, d_rows,
+  const int64_t toff = meta_toff(N), natural = N > TIER_S_MAX_N ? -1 : nw;
+  k_rows_mask<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(N, M, batch, nw, stride, natural, toff, tp, d_rows,
                                                            d_sign_bits, meta, err);
   CS_LAUNCHED();
-  k_rows_prefix<<<(unsigned)batch, 1024, 0, st>>>(nw, stride, meta);
-  CS_LAUNCHED();
-  if (N > TIER_S_MAX_N) {
-    k_rows_tperm<<<(unsigned)((batch * M + 255) / 256), 256, 0, st>>>(N, M, batch, nw, stride, tp, d_rows, meta);
+  if (natural >= 0) {
+    k_rows_prefix<<<(unsigned)batch, 1024, 0, st>>>(nw, stride, natural, meta);
     CS_LAUNCHED();
   }
+  k_rows_prefix<<<(unsigned)batch, 1024, 0, st>>>(nw, stride, toff, meta);
+  CS_LAUNCHED();
+  k_rows_tperm<<<(unsigned)((batch * M + 255) / 256), 256, 0, st>>>(N, M, batch, nw, stride, toff, tp, d_rows, meta);
+  CS_LAUNCHED();
   int herr = 0;
   CS_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   CS_CUDA(cudaStreamSynchronize(st));

@@ -403,15 +403,15 @@ template <typename T> struct GridCtx {
 #ifdef CS_DIAG_NOFFT
     return;  // diagnostics build only: memory-phase timing without the sub-FFTs
 #endif
-    if (CT == 4) fft_cta_dispatch<T, 2, TL_LOG2NT, 7, 12, INV>(buf, log2L1, tw1);
-    else fft_cta_dispatch<T, 1, TL_LOG2NT, 7, 12, INV>(buf, log2L1, tw1);
+    if (CT == 4) fft_cta_dispatch<T, 2, TL_LOG2NT, 1, 12, INV>(buf, log2L1, tw1);
+    else fft_cta_dispatch<T, 1, TL_LOG2NT, 1, 12, INV>(buf, log2L1, tw1);
   }
   template <bool INV> CS_DEV void row_fft(int B) {
 #ifdef CS_DIAG_NOFFT
     return;
 #endif
-    if (B == 2) fft_cta_dispatch<T, 1, TL_LOG2NT, 7, 12, INV>(buf, log2L2, tw2);
-    else fft_cta_dispatch<T, 0, TL_LOG2NT, 7, 12, INV>(buf, log2L2, tw2);
+    if (B == 2) fft_cta_dispatch<T, 1, TL_LOG2NT, 1, 12, INV>(buf, log2L2, tw2);
+    else fft_cta_dispatch<T, 0, TL_LOG2NT, 1, 12, INV>(buf, log2L2, tw2);
   }
   // pass A: columns of z = U viewed as complex [L1][L2]
   CS_NOINL void passA() {
@@ -566,7 +566,7 @@ template <typename T> struct GridCtx {
         const int32_t* pg = prefix;
         const uint32_t* mg = rowmask;
         const int64_t r0 = ka * (int64_t)W, r1 = (kb & (L1 - 1)) * (int64_t)W;
-        staged<TL_UNR, uint32_t>(4 * W, [&](int e) {
+        if (W > 0) staged<TL_UNR, uint32_t>(4 * W, [&](int e) {
           const int q = e / W, w = e - q * W;
           const int64_t at = ((q & 1) ? r1 : r0) + w;
           return (q < 2) ? mg[at] : (uint32_t)pg[at];
@@ -576,10 +576,11 @@ template <typename T> struct GridCtx {
       if (!zero_input) row_fft<false>(B);
       C2<T>* zb = shp(buf);
       {
+        // a transposed row shorter than a word (small-N fallback): read the mask in place
         const int W = (int)((2 * L2) >> 5);
-        m.rowmask = shp(msm);
-        m.prefix = reinterpret_cast<const int32_t*>(shp(msm) + 2 * W);
-        m.staged = 1;
+        m.rowmask = W > 0 ? shp(msm) : rowmask;
+        m.prefix = W > 0 ? reinterpret_cast<const int32_t*>(shp(msm) + 2 * W) : prefix;
+        m.staged = W > 0;
         m.ra = (int)ka;
       }
       if (it == 0) {

@@ -424,6 +424,11 @@ CS_NOINL int run_ompr(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& 
 template <class Ctx, typename T>
 CS_DEV void run_pursuit(Ctx& ctx, const Params& P, Bufs<T> B, T* vals, int32_t* supp,
                         cs_report* rep, unsigned pre_status) {
+  // every buffer as the context's memory space (shared for the CTA context: LDS/STS)
+  B.S = ctx.loc(B.S); B.S2 = ctx.loc(B.S2); B.U = ctx.loc(B.U);
+  B.x = ctx.loc(B.x); B.x2 = ctx.loc(B.x2); B.xU = ctx.loc(B.xU);
+  B.r = ctx.loc(B.r); B.d = ctx.loc(B.d); B.q = ctx.loc(B.q); B.b = ctx.loc(B.b);
+  B.Sbits = ctx.loc(B.Sbits); B.Ubits = ctx.loc(B.Ubits); B.Pbits = ctx.loc(B.Pbits);
   Stats st = {0, 0, 0, 0, pre_status, 0.0};
   double rn2 = 0;
   int ns = 0;

@@ -33,7 +33,8 @@ CS_HD LGeom l_geom(int64_t N) {
   g.L2 = int64_t(1) << ((l + 1) / 2);
   g.L1 = int64_t(1) << (l / 2);
   int64_t ct = TL_TILE / g.L1;
-  g.CT = (int)(ct < 4 ? ct : 4);
+  ct = ct < 4 ? ct : 4;
+  g.CT = (int)(ct < g.L2 ? ct : g.L2);  // small N (Tier L fallback): no more columns than L2
   g.shF = (l + 1) / 2;
   g.sh4 = (l + 1) / 2;
   return g;
@@ -204,8 +205,8 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
 
 template <typename T> CS_DEV void set_instance(GridCtx<T>& c, const OpMeta& m, int64_t b) {
   c.sign = m.sign(b);
-  c.rowmask = m.rmask(b);
-  c.prefix = m.prefix(b);
+  c.rowmask = m.tmask(b);
+  c.prefix = m.tprefix(b);
   c.tperm = m.tperm(b);
 }
 

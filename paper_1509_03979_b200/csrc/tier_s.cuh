@@ -58,24 +58,28 @@ CS_HD SLayout s_layout(int64_t N, int K, int ucap, bool pursuit) {
   return s;
 }
 
-// Per-instance metadata: [sign nw][rowmask nw][prefix nw] (+ [tperm M] for Tier L).
-// Tier S (N <= 16384) keeps the row mask in natural DCT-index order.  Tier L keeps
-// it TRANSPOSED to the four-step's pass-B order: DCT index
-// k = a + L1 b (a < L1, b < 2 L2) sits at bit t = a (2 L2) + b, the prefix counts
-// rows in that order, and tperm[t_rank] is the y index of the t_rank-th selected
-// row in that order.
+// Per-instance metadata (abi.cu meta_stride): [sign nw], for N <= 16384 the natural-order
+// [rowmask nw][prefix nw] of Tier S, then the Tier L [tmask nw][tprefix nw][tperm M]: the
+// row mask TRANSPOSED to the four-step's pass-B order — DCT index
+// k = a + L1 b (a < L1, b < 2 L2) at bit t = a (2 L2) + b — its rank prefix in that order,
+// and tperm[t_rank] = y index of the t_rank-th selected row in that order.
 struct OpMeta {
   const uint32_t* base;
   int64_t N, M;
   int64_t nw;
   int64_t stride;  // words per instance
+  int64_t toff;    // word offset of the transposed mask within an instance
   CS_HD const uint32_t* sign(int64_t b) const { return base + b * stride; }
   CS_HD const uint32_t* rmask(int64_t b) const { return base + b * stride + nw; }
   CS_HD const int32_t* prefix(int64_t b) const {
     return reinterpret_cast<const int32_t*>(base + b * stride + 2 * nw);
   }
+  CS_HD const uint32_t* tmask(int64_t b) const { return base + b * stride + toff; }
+  CS_HD const int32_t* tprefix(int64_t b) const {
+    return reinterpret_cast<const int32_t*>(base + b * stride + toff + nw);
+  }
   CS_HD const int32_t* tperm(int64_t b) const {
-    return reinterpret_cast<const int32_t*>(base + b * stride + 3 * nw);
+    return reinterpret_cast<const int32_t*>(base + b * stride + toff + 2 * nw);
   }
 };
 

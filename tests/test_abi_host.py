@@ -43,10 +43,12 @@ def test_status_strings_and_version(lib):
 
 
 def test_meta_bytes_formula(lib):
-    # 3 words-arrays of ceil(N/32) uint32 per instance, 256-aligned, + 256 flag tail
-    assert lib.cs_operator_meta_bytes(16384, 4096, 4096) == ((4096 * 3 * 512 * 4 + 255) // 256) * 256 + 256
+    # N <= 16384: sign + natural mask/prefix + transposed mask/prefix (5 word arrays of
+    # ceil(N/32)) + an M-entry int32 permutation per instance, 256-aligned, + 256 flag tail
+    assert lib.cs_operator_meta_bytes(16384, 4096, 4096) == \
+        ((4096 * (5 * 512 + 4096) * 4 + 255) // 256) * 256 + 256
     assert lib.cs_operator_meta_bytes(8, 4, 1) == 256 + 256
-    # N > 16384 (Tier L): + an M-entry int32 row permutation per instance (transposed mask)
+    # N > 16384 (Tier L only): sign + transposed mask/prefix + permutation
     N, M = 1 << 20, 1 << 18
     assert lib.cs_operator_meta_bytes(N, M, 1) == ((3 * (N // 32) * 4 + M * 4 + 255) // 256) * 256 + 256
 

@@ -148,3 +148,16 @@ def test_host_buffer_entry_point_matches_device_path(cs):
     assert torch.equal(host.support, ref.support.cpu())
     assert torch.equal(host.values, ref.values.cpu())
     assert np.array_equal(host.reports(), ref.reports())
+
+
+@pytest.mark.parametrize("alg,N,M,K,dtype", [("sp", 16384, 4096, 1024, "float64"),
+                                             ("omp", 8192, 2048, 512, "float64"),
+                                             ("sp", 16384, 8192, 2048, "float32")])
+def test_small_n_large_k_grid_fallback(cs, alg, N, M, K, dtype):
+    """N <= 16384 whose pursuit does not fit one CTA's shared memory (fp64 with a large K,
+    or a very large K) runs on the grid tier; it must still equal the oracle."""
+    cfg = cs_inputs.Config(63, alg, N, M, K, "gauss", 0.0)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 1, dtype)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals, rtol=1e-4 if dtype == "float32" else 1e-8)
+    assert not bad, bad
