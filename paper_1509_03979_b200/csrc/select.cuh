@@ -138,13 +138,19 @@ CS_DEV bool topk_cta_fast_v(Ctx& ctx, int nbits, int K, Visit&& visit, uint32_t*
     return true;
   }
   // MSB-first byte radix select of the `need` largest candidate keys
-  const int nwarp = nt >> 5;
-  (void)nwarp;
   unsigned* hist = shp(ctx.hist);
   constexpr int NB = (int)sizeof(Key) * 8;
   Key prefix = 0, pmask = 0;
+  int start = NB - 8;
+  if constexpr (sizeof(Key) == 4) {
+    // fp32 keys: the digit is key >> 21, so every candidate shares bits 31..21 — the
+    // top byte is common and the select starts at bits 23..16
+    pmask = (Key)0xFF000000u;
+    prefix = ck[0] & pmask;
+    start = 16;
+  }
   int64_t needr = need, n_eq = 0;
-  for (int shift = NB - 8; shift >= 0; shift -= 8) {
+  for (int shift = start; shift >= 0; shift -= 8) {
     for (int i = tid; i < 256; i += nt) hist[i] = 0;
     __syncthreads();
     for (int c = tid; c < C; c += nt) {
