@@ -196,6 +196,12 @@ const char* cs_version(void);
  * sandwiches, [1] pass A of H, [2] pass B of H, [3] pass C of H, [4] pass A of the residual,
  * [5] its pass B, [6] its pass C + reduction), valid after the stream syncs; -1 for Tier S. */
 int64_t cs_diag_phase_offset(int alg, int64_t N, int64_t M, int32_t K, int32_t ompr_l, int precision);
+/* Test hook: the CTA tier's top-K selection on d_vals [n] (fp32 or fp64 by `precision`):
+ * bit i of d_out_bits [ceil(n/32)] (device) is set iff |vals[i]| is among the K largest,
+ * ties to the lowest index.  mode 0: the two-pass path (radix fallback),
+ * mode 1: the radix path.  One CTA; asynchronous on `stream`.  1 <= K <= n <= 2^24. */
+cs_status cs_diag_topk(const void* d_vals, int64_t n, int64_t K, int precision, int mode,
+                       uint32_t* d_out_bits, cs_stream_t stream);
 /* Diagnostics: microseconds per grid-wide barrier (with_sum: plus a grid reduction) in a
  * cooperative launch shaped like the Tier L recovery; synchronous; -1 on error. */
 double cs_diag_grid_barrier_us(int iters, int with_sum);

@@ -56,6 +56,7 @@ EXPORTS = [
     "cs_recover_batched", "cs_recover_batched_f64", "cs_workspace_bytes_host", "cs_recover_batched_host",
     "cs_recover_batched_host_f64", "cs_status_string", "cs_last_error",
     "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
+    "cs_diag_topk",
 ]
 
 
@@ -100,6 +101,7 @@ def load_library(path: str = LIB_PATH):
         "cs_version": (ctypes.c_char_p, []),
         "cs_diag_phase_offset": (I64, [ctypes.c_int, I64, I64, I32, I32, ctypes.c_int]),
         "cs_diag_grid_barrier_us": (ctypes.c_double, [ctypes.c_int, ctypes.c_int]),
+        "cs_diag_topk": (I32, [P, I64, I64, ctypes.c_int, ctypes.c_int, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -530,6 +530,18 @@ uint64_t cs_launch_count(int reset) {
 }
 const char* cs_version(void) { return "csgpu 0.1.0 (sm_100a)"; }
 
+cs_status cs_diag_topk(const void* d_vals, int64_t n, int64_t K, int precision, int mode,
+                       uint32_t* d_out_bits, cs_stream_t stream) {
+  if (!d_vals || !d_out_bits) return fail(CS_ERR_INVALID_ARG, "null pointer");
+  if (n < 1 || n > (1 << 24) || K < 1 || K > n) return fail(CS_ERR_INVALID_ARG, "need 1 <= K <= n <= 2^24");
+  if (cs_status s = check_device()) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return precision ? s_diag_topk_launch<double>(reinterpret_cast<const double*>(d_vals), (int)n, (int)K, mode,
+                                               d_out_bits, st, g_launches, g_last_error)
+                   : s_diag_topk_launch<float>(reinterpret_cast<const float*>(d_vals), (int)n, (int)K, mode,
+                                              d_out_bits, st, g_launches, g_last_error);
+}
+
 double cs_diag_grid_barrier_us(int iters, int with_sum) {
   const int64_t smem = l_smem_bytes<float>(1 << 20);
   const void* fn = (const void*)k_l_recover<float>;

@@ -235,8 +235,38 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_recover(SRecArgs<T> a) {
   run_pursuit<CtaCtx<T>, T>(c, a.P, B, a.vals + b * a.P.K, a.supp + b * a.P.K, a.reps + b, pre);
 }
 
+// Diagnostics / test hook: the CTA context's top-K selection (select.cuh topk_bits) on a
+// caller's value array: out_bits = the K largest |vals| (ties -> lowest index).
+// mode 0: two-pass path (radix fallback on overflow), mode 1: radix path only.
+template <typename T>
+__global__ void __launch_bounds__(TS_THREADS, 1) k_s_diag_topk(SLayout lay, const T* vals, int n, int K, int mode,
+                                                              uint32_t* out_bits) {
+  extern __shared__ __align__(16) char smem[];
+  CtaCtx<T> c;
+  c.gtid = threadIdx.x;
+  c.gnthr = blockDim.x;
+  c.lane = threadIdx.x & 31;
+  c.gwarp = threadIdx.x >> 5;
+  c.gnwarps = blockDim.x >> 5;
+  c.redd = reinterpret_cast<double*>(smem + lay.redd);
+  c.redi = reinterpret_cast<int64_t*>(smem + lay.redi);
+  c.redk = reinterpret_cast<typename CtaCtx<T>::Key*>(smem + lay.redk);
+  c.hist = reinterpret_cast<unsigned*>(smem + lay.hist);
+  c.pick = reinterpret_cast<int64_t*>(smem + lay.pick);
+  c.h1 = reinterpret_cast<unsigned*>(smem + lay.h1);
+  c.ckey = reinterpret_cast<typename CtaCtx<T>::Key*>(smem + lay.ckey);
+  c.cidx = reinterpret_cast<int*>(smem + lay.cidx);
+  c.ccnt = reinterpret_cast<int*>(smem + lay.ccnt);
+  c.rbank = 0;
+  __syncthreads();
+  topk_bits(c, (int64_t)n, (int64_t)K, [vals](int64_t i) { return full_key(vals[i]); }, out_bits, mode == 0);
+}
+
 // ------------------------------------------------------------ host side ----
 // Declared everywhere; defined (and explicitly instantiated) in k_s_f32.cu / k_s_f64.cu.
+template <typename T>
+cs_status s_diag_topk_launch(const T* vals, int n, int K, int mode, uint32_t* out, cudaStream_t st,
+                             std::atomic<uint64_t>& launches, std::string& err);
 template <typename T>
 cs_status s_apply_launch(const OpMeta& m, int64_t B, const T* in, T* out, bool adjoint, cudaStream_t st,
                          std::atomic<uint64_t>& launches, std::string& err);
@@ -266,6 +296,14 @@ cs_status s_apply_launch(const OpMeta& m, int64_t B, const T* in, T* out, bool a
   if (cs_status s = s_attr(fn, lay.bytes, err)) return s;
   if (adjoint) k_s_adjoint<T><<<(unsigned)B, lay.nthreads, lay.bytes, st>>>(m, lay, in, out);
   else k_s_apply<T><<<(unsigned)B, lay.nthreads, lay.bytes, st>>>(m, lay, in, out);
+  return s_launched(launches, err);
+}
+template <typename T>
+cs_status s_diag_topk_launch(const T* vals, int n, int K, int mode, uint32_t* out, cudaStream_t st,
+                             std::atomic<uint64_t>& launches, std::string& err) {
+  SLayout lay = s_layout<T>(16384, 0, 0, false);
+  if (cs_status s = s_attr((const void*)k_s_diag_topk<T>, lay.bytes, err)) return s;
+  k_s_diag_topk<T><<<1, lay.nthreads, lay.bytes, st>>>(lay, vals, n, K, mode, out);
   return s_launched(launches, err);
 }
 template <typename T>
