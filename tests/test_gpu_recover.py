@@ -161,3 +161,33 @@ def test_small_n_large_k_grid_fallback(cs, alg, N, M, K, dtype):
     refs = oracle_results(probs, ys)
     bad, worst = compare(probs, refs, supp, vals, rtol=1e-4 if dtype == "float32" else 1e-8)
     assert not bad, bad
+
+
+@pytest.mark.parametrize("N,M,K", [(2048, 512, 16), (65536, 16384, 64)])
+def test_nonfinite_measurements_flagged(cs, N, M, K):
+    """y with a NaN / Inf: the report carries CS_DEV_NONFINITE_Y on both tiers,
+    and the other problems of the batch are unaffected."""
+    cfg = cs_inputs.Config(64, "sp", N, M, K, "gauss", 0.0)
+    probs = cs_inputs.make_batch(cfg, count=2)
+    ys = measured(probs)
+    ys[1, 3] = np.nan
+    dev = torch.device("cuda:0")
+    bits, rows = to_dev(probs, dev)
+    A = cs.Operator(N, M, bits, rows, batch=2)
+    res = cs.cs_recover_batched(A, "sp", torch.from_numpy(ys).to(dev), K, 1e-6)
+    torch.cuda.synchronize()
+    reps = res.reports()
+    assert reps[1]["status"] & 1
+    assert not (reps[0]["status"] & 1)
+    refs = oracle_results(probs[:1], ys[:1])
+    bad, _ = compare(probs[:1], refs, res.support.cpu().numpy()[:1], res.values.cpu().numpy()[:1])
+    assert not bad, bad
+
+
+def test_deterministic_rerun_grid_tier(cs):
+    """Fixed-order grid reductions: two runs of the grid tier agree bit for bit."""
+    cfg = CONFIGS[2].scaled(2)            # N = 32768
+    a = _run(cs, cfg, 1)
+    b = _run(cs, cfg, 1)
+    assert np.array_equal(a[2], b[2])
+    assert np.array_equal(a[3], b[3])
