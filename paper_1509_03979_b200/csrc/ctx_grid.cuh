@@ -476,7 +476,7 @@ template <typename T> struct GridCtx {
       for (int q = tcnt[t] + threadIdx.x; q < tcnt[t + 1]; q += blockDim.x) {
         const int i = tlist[q];
         const int64_t p = ip[i], c = p >> 1;
-        const int e = (int)(((c / l2) << lct) | (c - (c / l2) * l2 - c0i));
+        const int e = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
         sbt[2 * swz<T>(e) + (int)(p & 1)] = apply_sign<T>(sg, sp[i], vals[i]);
       }
       __syncthreads();
@@ -528,7 +528,7 @@ template <typename T> struct GridCtx {
       for (int q = tcnt[t] + threadIdx.x; q < tcnt[t + 1]; q += blockDim.x) {
         const int i = tlist[q];
         const int64_t p = ip[i], c = p >> 1;
-        const int e = (int)(((c / l2) << lct) | (c - (c / l2) * l2 - c0i));
+        const int e = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
         outv[i] = apply_sign<T>(sg, sp[i], sbt[2 * swz<T>(e) + (int)(p & 1)]);
       }
       __syncthreads();

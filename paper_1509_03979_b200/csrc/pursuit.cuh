@@ -87,6 +87,7 @@ CS_DEV void cg_loop(Ctx& c, CgState<T>& s_io, HFn&& Hf) {
 template <class Ctx, typename T>
 CS_NOINL void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q, T* b, bool r_given,
                        const Params& P, Stats& st) {
+  ctx.mark(0);
   ctx.set_input_support(supp, ns);
   supp = ctx.loc(supp);
   x = ctx.loc(x);
@@ -113,6 +114,7 @@ CS_NOINL void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q
   bb = ctx.sum(bb);
   rr = ctx.sum(rr);
   CgState<T> cs_{x, r, d, q, rr, P.tol * P.tol * bb, ns, P.cg_cap > 0 ? P.cg_cap : ns + 50, 0, 0u};
+  ctx.mark(8);
   ctx.cg_iterate(cs_);                                                     // lines 14-22
   st.status |= cs_.status;
   ctx.sync();
@@ -334,6 +336,7 @@ CS_NOINL int run_ompr(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& 
       // smallest |z| (ties: the lowest indices are kept, the highest such one drops).
       // Done as a sorted insert / delete and one argmin — no bitmask compaction or
       // radix select (each costs several grid barriers in the grid context).
+      ctx.mark(0);
       const int64_t j = detect_argmax<Ctx, T>(ctx, B.Sbits);
       if (j < 0) { st.term = CS_TERM_SUPPORT_FIXED; break; }
       const int* Sl = ctx.loc(S);
@@ -377,6 +380,7 @@ CS_NOINL int run_ompr(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& 
         B.Sbits[j >> 5] |= 1u << (j & 31);
       }
       ctx.sync();
+      ctx.mark(9);
       cg_solve(ctx, S2, ns, x2, B.r, B.d, B.q, B.b, false, P, st);
       swap_ptr<Ctx>(S, S2);
       swap_ptr<Ctx>(x, x2);

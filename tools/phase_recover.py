@@ -24,9 +24,9 @@ torch.cuda.synchronize()
 tot = ev0.elapsed_time(ev1)
 raw = ws.buf.cpu().numpy()
 # ptime = ts area + 8 slots; locate the ts area: search for the accumulator block (values < 1e12 ns)
-names = ["between sandwiches", "H pass A", "H pass B", "H pass C", "RES pass A", "RES pass B", "RES pass C+sum", "SP detection top-K"]
+names = ["between sandwiches", "H pass A", "H pass B", "H pass C", "RES pass A", "RES pass B", "RES pass C+sum", "SP detection top-K", "CG setup", "OMPR(1) swap"]
 rep = r.reports()[0]
 print("total ms", tot, "outer", rep["outer_iters"], "cg", rep["cg_iters_total"], "applies", rep["applies"])
 off = cs.load_library().cs_diag_phase_offset(cs.ALGS[cfg.alg], cfg.N, cfg.M, cfg.K, 0, 0)
-acc = raw[off:off + 64].view(np.uint64)
+acc = raw[off:off + 80].view(np.uint64)
 print({n: round(float(v) / 1e6, 3) for n, v in zip(names, acc)}, "ms (block 0)")
