@@ -596,6 +596,28 @@ template <typename T> struct GridCtx {
           int64_t k = L1 / 2 + L1 * k2;
           mid_pair<T, MODE>(zb[swz<T>(k2)], zb[swz<T>(n2 - 1 - k2)], k, tw4(k), m, rn2);
         }
+      } else if (m.staged) {
+        // general item (rows ka, kb = L1 - ka): the four DCT indices of the pair at column
+        // k2 sit in the staged rows at (ka, k2), (kb, 2L2-1-k2), (kb, L2-1-k2), (ka, L2+k2)
+        // (transposed order, §5.2); constants folded as in Tier S (dct_mid.cuh mid_pair2g)
+        const int W = (int)((2 * L2) >> 5), l2i = (int)L2;
+        const uint32_t* mw = m.rowmask;
+        const int32_t* pw = m.prefix;
+        const MidK<T> cst = make_midk<T>((int)N);
+        for (int k2 = threadIdx.x; k2 < n2; k2 += blockDim.x) {
+          const int k = (int)ka + (int)L1 * k2;
+          const int slot[4] = {0, W, W, 0};
+          const int bb[4] = {k2, 2 * l2i - 1 - k2, l2i - 1 - k2, l2i + k2};
+          const C2<T> a = tw4(k);
+          const C2<T> a2 = cmul<T>(a, a);
+          const C2<T> w = cmul<T>(a2, a2);
+          mid_pair2g<T, MODE>(zb[swz<T>(2 * k2)], zb[swz<T>(2 * (n2 - 1 - k2) + 1)], a, w, m, cst, rn2,
+              [&](int q) { return (bool)((mw[slot[q] + (bb[q] >> 5)] >> (bb[q] & 31)) & 1u); },
+              [&](int q) {
+                const int wi = slot[q] + (bb[q] >> 5), bit = bb[q] & 31;
+                return pw[wi] + __popc(mw[wi] & ((1u << bit) - 1u));
+              });
+        }
       } else {
         for (int k2 = threadIdx.x; k2 < n2; k2 += blockDim.x) {
           int64_t k = ka + L1 * k2;

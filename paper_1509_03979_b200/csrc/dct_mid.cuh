@@ -181,20 +181,35 @@ CS_DEV T mid_op2(const MidCtx<T>& m, const MidK<T>& c, int idx, T raw, double& r
     return T(0);
   }
 }
-// a = W_4N^k, w = W_N^k = a^4 (precomputed by the caller)
-template <typename T, int MODE>
-CS_DEV void mid_pair2(C2<T>& Zk, C2<T>& Zkk, int k, C2<T> a, C2<T> w, const MidCtx<T>& m, const MidK<T>& c,
-                      double& rn2) {
-  const int N = (int)m.N, kk = (N >> 1) - k;
+// The pair operation on raw values with a caller-supplied row lookup: sel(q) / rank(q) for
+// the four DCT indices q = 0: k, 1: N-k, 2: kk = L-k, 3: N-kk (rank only called when sel).
+// a = W_4N^k, w = W_N^k = a^4 (precomputed by the caller).
+template <typename T, int MODE, int TY, class RK>
+CS_DEV T mid_op2g(const MidCtx<T>& m, const MidK<T>& c, bool sel, RK&& rank, T raw, double& rn2) {
+  if constexpr (MODE == MID_H) {
+    return sel ? raw * c.hH[TY] : T(0);
+  } else if constexpr (MODE == MID_RES) {
+    if (!sel) return T(0);
+    const T d = m.y[rank()] - c.scx[TY] * raw;
+    rn2 += (double)d * (double)d;
+    return d * c.cout[TY];
+  } else {
+    if (sel) m.yout[rank()] = c.scx[TY] * raw;
+    return T(0);
+  }
+}
+template <typename T, int MODE, class SEL, class RANK>
+CS_DEV void mid_pair2g(C2<T>& Zk, C2<T>& Zkk, C2<T> a, C2<T> w, const MidCtx<T>& m, const MidK<T>& c,
+                       double& rn2, SEL&& sel, RANK&& rank) {
   const C2<T> P2 = mk<T>(Zk.x + Zkk.x, Zk.y - Zkk.y);   // Zk + conj Zkk
   const C2<T> O2 = mk<T>(Zk.y + Zkk.y, Zkk.x - Zk.x);   // -i (Zk - conj Zkk)
   const C2<T> Q2 = cmul<T>(w, O2);
   const C2<T> ck = cmul<T>(a, cadd<T>(P2, Q2));        // 2 (X_k - i X_{N-k})
-  const C2<T> u = cmul<T>(a, csub<T>(P2, Q2));         // e4 conj(u) = 2 (X_kk - i X_{N-kk}) / r2 ... (see above)
-  const T gk = mid_op2<T, MODE, 0>(m, c, k, ck.x, rn2);
-  const T gnk = mid_op2<T, MODE, 0>(m, c, N - k, -ck.y, rn2);
-  const T gkk = mid_op2<T, MODE, 1>(m, c, kk, u.x - u.y, rn2);
-  const T gnkk = mid_op2<T, MODE, 1>(m, c, N - kk, u.x + u.y, rn2);
+  const C2<T> u = cmul<T>(a, csub<T>(P2, Q2));         // e4 conj(u) = 2 (X_kk - i X_{N-kk}) / r2
+  const T gk = mid_op2g<T, MODE, 0>(m, c, sel(0), [&] { return rank(0); }, ck.x, rn2);
+  const T gnk = mid_op2g<T, MODE, 0>(m, c, sel(1), [&] { return rank(1); }, -ck.y, rn2);
+  const T gkk = mid_op2g<T, MODE, 1>(m, c, sel(2), [&] { return rank(2); }, u.x - u.y, rn2);
+  const T gnkk = mid_op2g<T, MODE, 1>(m, c, sel(3), [&] { return rank(3); }, u.x + u.y, rn2);
   if constexpr (MODE != MID_FWD) {
     const C2<T> Vk = cmulc<T>(mk<T>(gk, -gnk), a);                // conj(a) c'_k
     const C2<T> t = cmul<T>(a, mk<T>(gkk, -gnkk));
@@ -204,6 +219,15 @@ CS_DEV void mid_pair2(C2<T>& Zk, C2<T>& Zkk, int k, C2<T> a, C2<T> w, const MidC
     Zk = mk<T>(E.x - Od.y, E.y + Od.x);                           // E + i Od
     Zkk = mk<T>(E.x + Od.y, Od.x - E.y);                          // conj(E - i Od)
   }
+}
+// natural-order row bitmask (Tier S)
+template <typename T, int MODE>
+CS_DEV void mid_pair2(C2<T>& Zk, C2<T>& Zkk, int k, C2<T> a, C2<T> w, const MidCtx<T>& m, const MidK<T>& c,
+                      double& rn2) {
+  const int N = (int)m.N, kk = (N >> 1) - k;
+  const int idx[4] = {k, N - k, kk, N - kk};
+  mid_pair2g<T, MODE>(Zk, Zkk, a, w, m, c, rn2, [&](int q) { return bit_test32(m.rowmask, idx[q]); },
+                      [&](int q) { return row_rank32(m.rowmask, m.prefix, idx[q]); });
 }
 
 template <typename T, int LOG2N> CS_DEV MidCtx<T> make_mid_c(const uint32_t* rowmask, const int32_t* prefix,
