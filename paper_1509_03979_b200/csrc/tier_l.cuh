@@ -2,6 +2,7 @@
 // Used for configs 2 (SP, N = 2^16), 3 (OMPR, N = 2^20) and 5 (SP, N = 2^24), and
 // for operator apply / adjoint at those sizes.  See ctx_grid.cuh for the passes.
 #pragma once
+#include <algorithm>
 #include <atomic>
 #include <string>
 
@@ -432,8 +433,12 @@ inline cs_status l_launch(const void* fn, LArgs<T>& a, int64_t N, cudaStream_t s
   const int64_t smem = l_smem_bytes<T>(N);
   int grid = l_maxgrid<T>(fn, smem);
   if (grid > a.lay.maxgrid) grid = a.lay.maxgrid;
+  // no more blocks than the passes have tiles / row pairs: at mid-size N (c2: 64 tiles,
+  // 65 row pairs) extra blocks only make every grid barrier and reduction slower
+  const LGeom g = l_geom(N);
+  const int64_t work = std::max<int64_t>(g.L2 / g.CT, g.L1 / 2 + 1);
+  if (work < grid) grid = (int)work;
   cudaError_t e = cudaMemsetAsync(a.ws + a.lay.ctl, 0, (size_t)(a.lay.ctl_end - a.lay.ctl), st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(a.ws + a.lay.U, 0, (size_t)(N * sizeof(T)), st);
   if (e != cudaSuccess) { err = std::string("memset: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
   k_l_tables<T><<<64, 256, 0, st>>>(a.lay, N, a.ws);
   launches.fetch_add(1);
