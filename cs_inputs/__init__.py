@@ -34,7 +34,7 @@ def rng(cfg: int, trial: int, b: int, tag: int) -> np.random.Generator:
 class Config:
     """One BASELINE.json config."""
     cid: int
-    alg: str            # "omp" | "sp" | "ompr"
+    alg: str            # "omp" | "sp" | "ompr" | "cosamp"
     N: int
     M: int
     K: int

@@ -25,5 +25,5 @@ Pins (tests/test_oracle_*.py, `-m "not gpu"`):
 """
 from .operator import SrmOperator, DenseOperator, dct_matrix, dense_srm  # noqa: F401
 from .cg import cg, reduced_cg, CgResult  # noqa: F401
-from .pursuits import omp, sp, ompr, recover, topk, PursuitResult  # noqa: F401
+from .pursuits import omp, sp, ompr, cosamp, recover, topk, PursuitResult  # noqa: F401
 from .dense import brute_force_l0, lstsq_on_support  # noqa: F401

@@ -5,6 +5,9 @@
             paper, reconstructed per S:286-294 + SURVEY §8c.4 (reading R15).
 * OMPR(l) — named at P:574-576 (CG-OMPR); body not given, reconstructed per
             S:296-304 + SURVEY §8c.5 (reading R16).
+* CoSaMP  — named at P:84 among the greedy methods; body not
+            given in the paper: the published CoSaMP iteration (Needell & Tropp) with
+            the paper's CG as its LS step and this build's halting rule (reading R33).
 
 Every least-squares step is `oracle.cg.cg` (Eq.(11)) warm-started from
 the previous iterate (BASELINE.json; reading R9).  When the warm start is the
@@ -176,5 +179,48 @@ def ompr(op, y, K, tol=1e-10, l=1, eta=1.0, max_outer=0, solver="cg", cg_cap=0) 
                          float(np.linalg.norm(r)), term, hist)
 
 
+def cosamp(op, y, K, tol=1e-10, max_outer=30, solver="cg", cg_cap=0) -> PursuitResult:
+    """CG-CoSaMP (named P:84; iteration per Needell & Tropp, reading R33).
+
+    x = 0, S = {} ; repeat:  c = A^T (y - A x);  Omega = top-2K of |c| (all indices);
+    T = Omega u S;  b_T = LS on T (CG, warm start x, free r0 = c[T]);  S' = top-K of
+    |b_T| over T;  x' = b_T on S' (no second LS);  r' = y - A x'.
+    Halting: ||r'|| >= ||r|| after the first iteration -> keep (S, x) (T_RESID_ROSE);
+    otherwise accept (S', x') and stop if S' == S (T_SUPPORT_FIXED); max_outer -> cap."""
+    y = np.asarray(y, dtype=np.float64)
+    N = op.N
+    c0 = op.adjoint(y)
+    ls = _LS(op, y, c0, solver, tol, cg_cap)
+    S = np.zeros(0, dtype=np.int64)
+    x = np.zeros(0)
+    c = c0                                         # A^T (y - A 0)
+    rn = float(np.linalg.norm(y))
+    hist = [rn]
+    term, it = T_ITER_CAP, 0
+    for it in range(1, max_outer + 1):
+        Om = topk(np.abs(c), min(2 * K, N))
+        T = np.union1d(S, Om)
+        xT = ls(T, x0=_scatter(N, S, x)[T], r0=c[T])
+        keep = np.zeros(N, dtype=bool)
+        keep[T] = True
+        dT = np.zeros(N)
+        dT[T] = np.abs(xT)
+        S2 = topk(dT, K, allowed=keep)
+        x2 = _scatter(N, T, xT)[S2]
+        r2 = y - op.apply(_scatter(N, S2, x2))
+        rn2 = float(np.linalg.norm(r2))
+        if it > 1 and rn2 >= rn:
+            term = T_RESID_ROSE
+            break
+        fixed = np.array_equal(S2, S)
+        S, x, rn = S2, x2, rn2
+        hist.append(rn)
+        if fixed:
+            term = T_SUPPORT_FIXED
+            break
+        c = op.adjoint(r2)
+    return PursuitResult(S, x, _scatter(N, S, x), it, ls.iters, rn, term, hist)
+
+
 def recover(alg, op, y, K, **kw) -> PursuitResult:
-    return {"omp": omp, "sp": sp, "ompr": ompr}[alg](op, y, K, **kw)
+    return {"omp": omp, "sp": sp, "ompr": ompr, "cosamp": cosamp}[alg](op, y, K, **kw)

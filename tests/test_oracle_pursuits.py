@@ -8,13 +8,13 @@ import pytest
 
 import cs_inputs
 from cs_inputs import CONFIGS
-from oracle import DenseOperator, SrmOperator, omp, sp, ompr, brute_force_l0, topk
+from oracle import DenseOperator, SrmOperator, omp, sp, ompr, cosamp, brute_force_l0, topk
 from helpers import measure, oracle_recover
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
 
 
-@pytest.mark.parametrize("fn", [omp, sp, ompr])
+@pytest.mark.parametrize("fn", [omp, sp, ompr, cosamp])
 def test_identity_worked_example(fn):
     g = GOLD["pursuit_identity"]
     op = DenseOperator(np.eye(4))
@@ -39,7 +39,7 @@ def test_topk_ties_go_to_lowest_index():
     np.testing.assert_array_equal(topk(np.zeros(5), 3), [0, 1, 2])
 
 
-@pytest.mark.parametrize("fn", [omp, sp, ompr])
+@pytest.mark.parametrize("fn", [omp, sp, ompr, cosamp])
 def test_matches_brute_force_on_tiny_planted(fn):
     """l0 enumeration (Eq.(3)) on noiseless planted 2-sparse instances."""
     g = np.random.default_rng(11)
@@ -63,7 +63,7 @@ def test_matches_brute_force_on_tiny_planted(fn):
     assert hits >= 16
 
 
-@pytest.mark.parametrize("alg", ["omp", "sp", "ompr"])
+@pytest.mark.parametrize("alg", ["omp", "sp", "ompr", "cosamp"])
 def test_cg_backend_equals_dense_ls_backend(alg):
     """S:484 acceptance 4: CG_WEIGHTED == DENSE_LS, N=128, M=32, K=8."""
     for trial in range(10):
@@ -118,3 +118,30 @@ def test_sp_noisy_invariants_c2_scaled():
     assert res.support.size == p.K
     # noise floor: ||r|| is about sigma sqrt(M - K)
     assert res.resid_norm <= 2.0 * CONFIGS[2].noise * np.sqrt(p.M)
+
+
+def test_cosamp_exact_recovery_c4_shape():
+    """CoSaMP (R33) at the c4 shape (N = 16384, M = 4096, K = 256): planted support and
+    coefficients; a fixed point reached in a few iterations."""
+    cfg = cs_inputs.Config(4, "cosamp", 16384, 4096, 256, "gauss", 0.0)
+    p = cs_inputs.make_problem(cfg, 3)
+    op, y32 = measure(p)
+    res = oracle_recover(p, y32)
+    _check_exact(p, res, 1e-6)
+    assert res.termination in (3, 4) and res.outer_iters <= 6   # at the fp32-y floor either halt fires
+
+
+def test_cosamp_first_iterate_is_pruned_ls_on_top_2k():
+    """One iteration by hand with the dense-LS backend: T = top-2K |A^T y|, b = lstsq on T,
+    S' = top-K |b| — the definition of the CoSaMP step (R33)."""
+    g = np.random.default_rng(5)
+    M, N, K = 40, 64, 4
+    A = g.standard_normal((M, N)) / np.sqrt(M)
+    y = g.standard_normal(M)
+    res = cosamp(DenseOperator(A), y, K, tol=1e-13, max_outer=1, solver="lstsq")
+    T = np.argsort(-np.abs(A.T @ y), kind="stable")[: 2 * K]
+    T.sort()
+    b = np.linalg.lstsq(A[:, T], y, rcond=None)[0]
+    keep = np.sort(T[np.argsort(-np.abs(b), kind="stable")[:K]])
+    np.testing.assert_array_equal(res.support, keep)
+    np.testing.assert_allclose(res.x, b[np.searchsorted(T, keep)], rtol=1e-10)
