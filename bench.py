@@ -17,6 +17,7 @@ Prints ONE JSON line (rank 0).  See DESIGN.md §7 for every field.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -44,11 +45,24 @@ def parse():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--batch", type=int, default=0, help="problems per GPU (0 = config default)")
+    ap.add_argument("--alg", choices=["omp", "sp", "ompr", "cosamp"], default="",
+                    help="run the config's workload with another pursuit (not a BASELINE line)")
     ap.add_argument("--no-op-bench", action="store_true")
     return ap.parse_args()
 
 
+def select_config(args):
+    cfg = cs_inputs.CONFIGS[args.config]
+    if args.alg and args.alg != cfg.alg:
+        cfg = dataclasses.replace(cfg, alg=args.alg)
+    return cfg
+
+
 def workload_desc(cfg):
+    base = cs_inputs.CONFIGS[cfg.cid]
+    if cfg.alg != base.alg:
+        names = {"omp": "OMP", "sp": "SP", "ompr": "OMPR(1)", "cosamp": "CoSaMP"}
+        return f"c{cfg.cid}-shape with {names[cfg.alg]}+CG (alg override): N={cfg.N}, M={cfg.M}, K={cfg.K}"
     return {1: "c1: OMP+CG, N=4096, M=1024, K=64, noiseless",
             2: "c2: SP+CG, N=65536, M=16384, K=2048, sigma=1e-3",
             3: "c3: OMPR(1)+CG, N=2^20, M=2^18, K=8192, noiseless",
@@ -138,7 +152,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cfg = cs_inputs.CONFIGS[args.config]
+    cfg = select_config(args)
     B = args.batch or cfg.batch
     td = torch.float32 if args.precision == "fp32" else torch.float64
     tol = 1e-6 if args.precision == "fp32" else 1e-12
@@ -324,7 +338,8 @@ def run_ours(args):
     tr = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr):
         try:
-            roofline["traffic"] = json.load(open(tr)).get(f"c{cfg.cid}_{args.precision}")
+            key = f"c{cfg.cid}_{args.precision}" + ("" if cfg.alg == cs_inputs.CONFIGS[cfg.cid].alg else f"_{cfg.alg}")
+            roofline["traffic"] = json.load(open(tr)).get(key)
         except Exception:
             pass
 
@@ -399,7 +414,7 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return
-    cfg = cs_inputs.CONFIGS[args.config]
+    cfg = select_config(args)
     import oracle
     B = args.batch or cfg.batch
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()

@@ -44,15 +44,15 @@ typedef enum {
   CS_ERR_NONFINITE = 5      /* reserved for host-detected non-finite input */
 } cs_status;
 
-typedef enum { CS_OMP = 0, CS_SP = 1, CS_OMPR = 2 } cs_alg;
+typedef enum { CS_OMP = 0, CS_SP = 1, CS_OMPR = 2, CS_COSAMP = 3 } cs_alg;
 
 /* cs_report.termination — why the OUTER pursuit loop stopped. */
 typedef enum {
   CS_TERM_DONE = 0,          /* OMP ran its K iterations                 */
-  CS_TERM_ITER_CAP = 1,      /* SP/OMPR hit max_outer                                   */
+  CS_TERM_ITER_CAP = 1,      /* SP/OMPR/CoSaMP hit max_outer                            */
   CS_TERM_STAGNATION = 2,    /* a CG solve broke down (d^T H d <= 0)             */
-  CS_TERM_SUPPORT_FIXED = 3, /* SP/OMPR: new support == old support                     */
-  CS_TERM_RESID_ROSE = 4     /* SP: ||r'|| >= ||r|| — previous (S, x) kept      */
+  CS_TERM_SUPPORT_FIXED = 3, /* SP/OMPR/CoSaMP: new support == old support              */
+  CS_TERM_RESID_ROSE = 4     /* SP/CoSaMP: ||r'|| >= ||r|| — previous (S, x) kept */
 } cs_term;
 
 /* cs_report.status bits — conditions found on the device. */
@@ -72,7 +72,7 @@ typedef struct {
 } cs_report;               /* 40 bytes */
 
 typedef struct {
-  int32_t max_outer;    /* SP/OMPR outer cap; 0 -> SP 30, OMPR 2K */
+  int32_t max_outer;    /* SP/OMPR/CoSaMP outer cap; 0 -> SP 30, OMPR 2K, CoSaMP 30 */
   int32_t cg_max_iters; /* 0 -> |S| + 50 (Thm 5 bound |S| plus slack, SURVEY #29)           */
   int32_t ompr_l;       /* OMPR(l): indices swapped in per outer iteration; 0 -> 1  */
   float ompr_eta;       /* OMPR step eta; 0 -> 1.0                                   */
@@ -128,13 +128,15 @@ cs_status cs_operator_adjoint_f64(const cs_operator* op, const double* d_y, doub
  * Algorithm 1) in place of the pseudo-inverse:
  *   CS_OMP  — Algorithm 1, exactly K outer iterations;
  *   CS_SP   — CG-SP (named P:574-576; body per S:286-294, R15);
- *   CS_OMPR — CG-OMPR(l, eta) (named P:574-576; body per S:296-304, R16).
+ *   CS_OMPR — CG-OMPR(l, eta) (named P:574-576; body per S:296-304, R16);
+ *   CS_COSAMP — CG-CoSaMP (named P:84 among the greedy methods; the published CoSaMP
+ *             iteration with this CG as its LS step, halting rule DESIGN.md R33).
  * Each CG solve is warm-started from the previous iterate and stops when
  * ||r_j|| <= tol * ||b|| (relative; R6/R7), at cg_max_iters, or on breakdown.
  *
  * Outputs: d_support [K] int32 ascending, d_vals [K] the LS coefficients on it,
  * d_report one cs_report (DEVICE memory).  Requirements: 1 <= K; OMP: K <= M;
- * SP: 2K <= M; OMPR: K + l <= M; K <= N/2; 0 <= tol.
+ * SP: 2K <= M; OMPR: K + l <= M; CoSaMP: 3K <= M; K <= N/2; 0 <= tol.
  */
 cs_status cs_workspace_bytes(int alg, int64_t N, int64_t M, int32_t K, int64_t batch,
                              int precision /*0 fp32, 1 fp64*/, const cs_options* opts,

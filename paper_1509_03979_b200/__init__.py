@@ -24,7 +24,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcsgpu.so")
 
-ALGS = {"omp": 0, "sp": 1, "ompr": 2}
+ALGS = {"omp": 0, "sp": 1, "ompr": 2, "cosamp": 3}
 TERM_NAMES = {0: "done", 1: "iter_cap", 2: "stagnation", 3: "support_fixed", 4: "resid_rose"}
 STATUS = {0: "CS_OK", 1: "CS_ERR_INVALID_ARG", 2: "CS_ERR_UNSUPPORTED", 3: "CS_ERR_WORKSPACE",
           4: "CS_ERR_CUDA", 5: "CS_ERR_NONFINITE"}

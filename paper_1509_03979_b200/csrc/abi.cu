@@ -69,6 +69,7 @@ cs_status check_device() {
 int64_t ucap_of(int alg, int K, int l) {
   if (alg == CS_SP) return 2 * (int64_t)K;
   if (alg == CS_OMPR) return (int64_t)K + (l > 0 ? l : 1);
+  if (alg == CS_COSAMP) return 3 * (int64_t)K;
   return K;
 }
 
@@ -214,7 +215,7 @@ cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, in
                        cs_report* reps, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (!op) return fail(CS_ERR_INVALID_ARG, "null operator");
   if (!Y || !vals || !supp || !reps) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
-  if (alg < CS_OMP || alg > CS_OMPR) return fail(CS_ERR_INVALID_ARG, "unknown algorithm");
+  if (alg < CS_OMP || alg > CS_COSAMP) return fail(CS_ERR_INVALID_ARG, "unknown algorithm");
   if (cs_status s = check_N(N)) return s;
   if (N != op->N || M != op->M) return fail(CS_ERR_INVALID_ARG, "M/N do not match the operator");
   if (B < 1 || B > op->B) return fail(CS_ERR_INVALID_ARG, "batch exceeds operator instances");
@@ -230,6 +231,7 @@ cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, in
   if (alg == CS_OMP && K > M) return fail(CS_ERR_INVALID_ARG, "OMP needs K <= M");
   if (alg == CS_SP && 2 * (int64_t)K > M) return fail(CS_ERR_INVALID_ARG, "SP needs 2K <= M");
   if (alg == CS_OMPR && (int64_t)K + l > M) return fail(CS_ERR_INVALID_ARG, "OMPR needs K + l <= M");
+  if (alg == CS_COSAMP && 3 * (int64_t)K > M) return fail(CS_ERR_INVALID_ARG, "CoSaMP needs 3K <= M");
   if (cs_status s = check_device()) return s;
   size_t need = 0;
   const int prec = sizeof(T) == 8 ? 1 : 0;

@@ -9,6 +9,8 @@
 //  omp      : Algorithm 1 lines 01-10, exactly K iterations.
 //  sp       : CG-SP, body per S:289 / SURVEY §8c.4 (R15).
 //  ompr     : CG-OMPR(l, eta), body per S:299 / SURVEY §8c.5 (R16).
+//  cosamp   : CG-CoSaMP (named P:84), the published CoSaMP iteration with the
+//             paper's CG as its LS step; halting rule R33.
 //
 // Every thread of the context runs the same control flow; scalars come out of
 // deterministic collectives, so every branch is uniform.
@@ -424,6 +426,60 @@ CS_NOINL int run_ompr(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& 
   return ns;
 }
 
+// ------------------------------------------------------------------ CoSaMP --
+// x = 0; repeat: Omega = top-2K |c| (c = A^T r, all indices), T = Omega u S, CG on T
+// (warm start x, free r0 = c[T] since x lives on T), S' = top-K |x_T|, x' = x_T on S',
+// r' = y - A x'.  Halt (R33): ||r'|| >= ||r|| after the first pass keeps (S, x);
+// otherwise accept and stop once S' == S.
+template <class Ctx, typename T>
+CS_NOINL int run_cosamp(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& rn2) {
+  const int64_t N = ctx.N, nwords = (N + 31) >> 5;
+  const int K = P.K;
+  const int64_t K2 = (2 * (int64_t)K < N) ? 2 * (int64_t)K : N;
+  int *S = B.S, *S2 = B.S2, *U = B.U;
+  T *x = B.x, *x2 = B.x2, *xU = B.xU;
+  rn2 = ctx.RES((const T*)nullptr);                              // c = A^T y, ||r||^2 = ||y||^2
+  ctx.save_c0();
+  for (int64_t w = ctx.gtid; w < nwords; w += ctx.gnthr) B.Sbits[w] = 0u;
+  ctx.sync();
+  int ns = 0;
+  const int max_outer = P.max_outer > 0 ? P.max_outer : 30;
+  st.term = CS_TERM_ITER_CAP;
+  for (int it = 1; it <= max_outer; ++it) {
+    st.outer = it;
+    ctx.mark(0);
+    detect_topk<Ctx, T>(ctx, K2, nullptr, B.Ubits);             // Omega = top-2K |c|
+    ctx.mark(7);
+    for (int64_t w = ctx.gtid; w < nwords; w += ctx.gnthr) B.Ubits[w] |= B.Sbits[w];  // T = Omega u S
+    ctx.sync();
+    int nu = (int)compact_bits(ctx, B.Ubits, N, [&](int64_t k, int64_t j) { U[k] = (int)j; });
+    remap(ctx, S, x, ns, U, xU, nu);                             // x0 = x on S, 0 elsewhere
+    {
+      const auto cv = ctx.cview();
+      for (int i = ctx.gtid; i < nu; i += ctx.gnthr) B.r[i] = cv.at(U[i]);   // r0 = c[T]
+    }
+    cg_solve(ctx, U, nu, xU, B.r, B.d, B.q, B.b, true, P, st);
+    const T* xUc = xU;
+    topk_bits(ctx, (int64_t)nu, (int64_t)K, [&](int64_t i) { return full_key(xUc[i]); }, B.Pbits);
+    int ns2 = (int)compact_bits(ctx, B.Pbits, nu, [&](int64_t k, int64_t pos) {
+      S2[k] = U[pos];
+      x2[k] = xU[pos];
+    });
+    ctx.set_input_support(S2, ns2);
+    const double rn2new = ctx.RES(x2);                           // r' and c' = A^T r'
+    if (it > 1 && rn2new >= rn2) { st.term = CS_TERM_RESID_ROSE; break; }   // keep (S, x)
+    const bool fixed = (ns == ns2) && same_list<Ctx, T>(ctx, S, S2, ns);
+    swap_ptr<Ctx>(S, S2);
+    swap_ptr<Ctx>(x, x2);
+    ns = ns2;
+    rn2 = rn2new;
+    if (fixed) { st.term = CS_TERM_SUPPORT_FIXED; break; }
+    bits_from_list<Ctx, T>(ctx, B.Sbits, nwords, S, ns);
+  }
+  B.S = S; B.S2 = S2; B.x = x; B.x2 = x2;
+  return ns;
+}
+
 // run the selected pursuit and write (support, values, report)
 template <class Ctx, typename T>
 CS_DEV void run_pursuit(Ctx& ctx, const Params& P, Bufs<T> B, T* vals, int32_t* supp,
@@ -438,7 +494,8 @@ CS_DEV void run_pursuit(Ctx& ctx, const Params& P, Bufs<T> B, T* vals, int32_t* 
   int ns = 0;
   if (P.alg == CS_OMP) ns = run_omp(ctx, P, B, st, rn2);
   else if (P.alg == CS_SP) ns = run_sp(ctx, P, B, st, rn2);
-  else ns = run_ompr(ctx, P, B, st, rn2);
+  else if (P.alg == CS_OMPR) ns = run_ompr(ctx, P, B, st, rn2);
+  else ns = run_cosamp(ctx, P, B, st, rn2);
   for (int i = ctx.gtid; i < P.K; i += ctx.gnthr) {
     supp[i] = i < ns ? B.S[i] : -1;
     vals[i] = i < ns ? B.x[i] : T(0);

@@ -61,7 +61,7 @@ def test_c4_sp_batched_full_size_sample(cs):
 
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 def test_small_ragged_batch_all_algs(cs, dtype):
-    for alg in ["omp", "sp", "ompr"]:
+    for alg in ["omp", "sp", "ompr", "cosamp"]:
         cfg = cs_inputs.Config(60, alg, 512, 128, 12, "gauss", 0.0)
         probs, ys, supp, vals, reps = _run(cs, cfg, 7, dtype)
         refs = oracle_results(probs, ys)
@@ -70,7 +70,8 @@ def test_small_ragged_batch_all_algs(cs, dtype):
 
 
 def test_tiny_sizes(cs):
-    for N, M, K, alg in [(8, 4, 1, "omp"), (16, 8, 2, "sp"), (32, 16, 3, "ompr"), (64, 32, 4, "sp")]:
+    for N, M, K, alg in [(8, 4, 1, "omp"), (16, 8, 2, "sp"), (32, 16, 3, "ompr"), (64, 32, 4, "sp"),
+                         (16, 8, 2, "cosamp"), (64, 32, 4, "cosamp")]:
         cfg = cs_inputs.Config(61, alg, N, M, K, "pm1", 0.0)
         probs, ys, supp, vals, reps = _run(cs, cfg, 3, "float64")
         refs = oracle_results(probs, ys)
@@ -112,7 +113,8 @@ def test_deterministic_rerun(cs):
 
 
 @pytest.mark.parametrize("alg,N,M,K", [("omp", 1024, 256, 8), ("sp", 16384, 4096, 256),
-                                       ("ompr", 2048, 512, 16), ("sp", 65536, 16384, 64)])
+                                       ("ompr", 2048, 512, 16), ("sp", 65536, 16384, 64),
+                                       ("cosamp", 16384, 4096, 256), ("cosamp", 65536, 16384, 64)])
 def test_all_ties_zero_measurements(cs, alg, N, M, K):
     """y = 0: every correlation is exactly 0, so every selection is a full tie and must
     go to the lowest indices (SURVEY §8c.7 #12, #32); the oracle gives the same."""
@@ -191,3 +193,44 @@ def test_deterministic_rerun_grid_tier(cs):
     b = _run(cs, cfg, 1)
     assert np.array_equal(a[2], b[2])
     assert np.array_equal(a[3], b[3])
+
+
+# ---------------------------------------------------------------- CoSaMP (R33) ----
+def test_cosamp_c4_shape_batched(cs):
+    """CG-CoSaMP on the c4 workload shape (N = 16384, M = 4096, K = 256), CTA tier."""
+    cfg = cs_inputs.Config(4, "cosamp", 16384, 4096, 256, "gauss", 0.0, batch=48)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 48)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals)
+    assert not bad, bad
+    assert all(r["termination"] in (3, 4) for r in reps)
+    assert all(np.array_equal(np.sort(supp[b]), probs[b].support) for b in range(48))
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_cosamp_noisy_ragged(cs, dtype):
+    """Noisy K-sparse Gaussian signals, ragged batch of 5: fp64 equals the
+    oracle; fp32 too at this size (well-separated coefficients)."""
+    cfg = cs_inputs.Config(65, "cosamp", 2048, 768, 32, "gauss", 1e-3)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 5, dtype)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals, rtol=1e-4 if dtype == "float32" else 1e-9)
+    assert not bad, bad
+
+
+def test_cosamp_tier_l_fp64(cs):
+    """Grid tier (N = 2^16): noisy c2-shape problem, fp64 against the oracle."""
+    cfg = cs_inputs.Config(66, "cosamp", 65536, 16384, 1024, "gauss", 1e-2)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 1, "float64", tol=1e-12)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals, rtol=1e-8)
+    assert not bad, bad
+
+
+def test_cosamp_tier_l_fp32_exact(cs):
+    cfg = cs_inputs.Config(67, "cosamp", 1 << 18, 1 << 16, 2048, "gauss", 0.0)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 1)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals)
+    assert not bad, bad
+    assert np.array_equal(np.sort(supp[0]), probs[0].support)
