@@ -23,7 +23,7 @@ from typing import Optional
 
 import numpy as np
 
-TAG_SIGMA, TAG_ROWS, TAG_POS, TAG_VAL, TAG_NOISE, TAG_PERM = range(6)
+TAG_SIGMA, TAG_ROWS, TAG_POS, TAG_VAL, TAG_NOISE, TAG_PERM, TAG_RAND = range(7)
 
 
 def rng(cfg: int, trial: int, b: int, tag: int) -> np.random.Generator:
@@ -41,6 +41,7 @@ class Config:
     signal: str         # "gauss" | "pm1" | "power"
     noise: float        # sigma_eta
     batch: int = 1
+    randomizer: str = "sign"   # "sign": R = diag(+-1) (BASELINE); "perm": Eq.(7)'s permutation, sigma = +1
 
     def scaled(self, div: int, batch: Optional[int] = None) -> "Config":
         """Same recipe at N/div, M/div, K/div (ratios kept); used for parity tests."""
@@ -82,6 +83,11 @@ def draw_rows(N: int, M: int, g: np.random.Generator) -> np.ndarray:
     return np.sort(g.choice(N, M, replace=False)).astype(np.int32)
 
 
+def draw_perm(N: int, g: np.random.Generator) -> np.ndarray:
+    """A uniformly random permutation pi of [0, N) (the randomizer R of Eq.(7))."""
+    return g.permutation(N).astype(np.int32)
+
+
 def draw_signal(kind: str, N: int, K: int, g_pos: np.random.Generator,
                 g_val: np.random.Generator, g_perm: np.random.Generator):
     """Planted signal s (float64[N]) and its sorted support (int64)."""
@@ -116,18 +122,24 @@ class Problem:
     s: np.ndarray           # float64[N] planted signal
     support: np.ndarray     # planted support (sorted)
     noise: np.ndarray       # float64[M] eta
+    perm: Optional[np.ndarray] = None   # int32[N] pi of the randomizer R (randomizer "perm")
 
 
 def make_problem(cfg: Config, trial: int = 0, b: int = 0) -> Problem:
     c = cfg.cid
     N, M, K = cfg.N, cfg.M, cfg.K
-    bits = draw_sign_bits(N, rng(c, trial, b, TAG_SIGMA))
+    if cfg.randomizer == "perm":
+        bits = pack_sign_bits(np.zeros(N, dtype=bool))
+        perm = draw_perm(N, rng(c, trial, b, TAG_RAND))
+    else:
+        bits = draw_sign_bits(N, rng(c, trial, b, TAG_SIGMA))
+        perm = None
     rows = draw_rows(N, M, rng(c, trial, b, TAG_ROWS))
     s, supp = draw_signal(cfg.signal, N, K, rng(c, trial, b, TAG_POS),
                           rng(c, trial, b, TAG_VAL), rng(c, trial, b, TAG_PERM))
     eta = rng(c, trial, b, TAG_NOISE).standard_normal(M) * cfg.noise if cfg.noise > 0 \
         else np.zeros(M)
-    return Problem(N, M, K, cfg.alg, bits, rows, s, supp, eta)
+    return Problem(N, M, K, cfg.alg, bits, rows, s, supp, eta, perm)
 
 
 def make_batch(cfg: Config, trial: int = 0, b0: int = 0, count: Optional[int] = None):

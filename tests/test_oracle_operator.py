@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 import scipy.fft
 
-from cs_inputs import pack_sign_bits, draw_sign_bits, draw_rows, rng
+from cs_inputs import pack_sign_bits, draw_sign_bits, draw_rows, draw_perm, rng
 from oracle import SrmOperator, dct_matrix, dense_srm
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
@@ -109,3 +109,45 @@ def test_first_row_is_mean_scaled():
     op = SrmOperator(N, pack_sign_bits(np.zeros(N, bool)), np.array([0]))
     x = np.arange(N, dtype=float)
     np.testing.assert_allclose(op.apply(x), [x.sum() / np.sqrt(N)], rtol=1e-14)
+
+
+# ---------------------------------------------------------------- Eq.(7) randomizer R = pi (R34)
+@pytest.mark.parametrize("N,M", [(8, 2), (64, 16), (512, 128)])
+def test_perm_operator_matches_dense_definition(N, M):
+    """A = C_N[rows] R diag(sigma) with R the explicit permutation matrix R[i, pi(i)] = 1."""
+    bits = draw_sign_bits(max(N, 32), rng(97, 0, N, 0))
+    rows = draw_rows(N, M, rng(97, 0, N, 1))
+    perm = draw_perm(N, rng(97, 0, N, 2))
+    op = SrmOperator(N, bits, rows, perm)
+    A = dense_srm(N, bits, rows, perm)
+    g = np.random.default_rng(N + 1)
+    for _ in range(3):
+        x, w = g.standard_normal(N), g.standard_normal(M)
+        np.testing.assert_allclose(op.apply(x), A @ x, atol=1e-12 * np.linalg.norm(x))
+        np.testing.assert_allclose(op.adjoint(w), A.T @ w, atol=1e-12 * np.linalg.norm(w))
+
+
+def test_perm_columns_are_permuted_dct_columns():
+    """Column j of D F R is column pi^{-1}(j) of the row-sampled DCT (the randomizer only
+    relabels columns, Eq.(7)): A e_j = C_N[rows, pi^{-1}(j)]."""
+    N, M = 128, 32
+    perm = draw_perm(N, rng(97, 1, N, 2))
+    pinv = np.argsort(perm)
+    rows = draw_rows(N, M, rng(97, 1, N, 1))
+    op = SrmOperator(N, pack_sign_bits(np.zeros(N, bool)), rows, perm)
+    C = dct_matrix(N)
+    for j in [0, 1, 5, 77, N - 1]:
+        e = np.zeros(N)
+        e[j] = 1.0
+        np.testing.assert_allclose(op.apply(e), C[rows, pinv[j]], atol=1e-14)
+
+
+def test_perm_operator_rows_orthonormal_and_adjoint():
+    N, M = 2048, 512
+    perm = draw_perm(N, rng(97, 2, N, 2))
+    op = SrmOperator(N, draw_sign_bits(N, rng(97, 2, N, 0)), draw_rows(N, M, rng(97, 2, N, 1)), perm)
+    AAT = np.stack([op.apply(op.adjoint(e)) for e in np.eye(M)[:64]], axis=1)
+    np.testing.assert_allclose(AAT, np.eye(M)[:, :64], atol=1e-13)
+    g = np.random.default_rng(3)
+    x, w = g.standard_normal(N), g.standard_normal(M)
+    assert abs(op.apply(x) @ w - x @ op.adjoint(w)) <= 1e-12 * np.linalg.norm(x) * np.linalg.norm(w)

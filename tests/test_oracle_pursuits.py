@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import cs_inputs
+import oracle
 from cs_inputs import CONFIGS
 from oracle import DenseOperator, SrmOperator, omp, sp, ompr, cosamp, brute_force_l0, topk
 from helpers import measure, oracle_recover
@@ -145,3 +146,19 @@ def test_cosamp_first_iterate_is_pruned_ls_on_top_2k():
     keep = np.sort(T[np.argsort(-np.abs(b), kind="stable")[:K]])
     np.testing.assert_array_equal(res.support, keep)
     np.testing.assert_allclose(res.x, b[np.searchsorted(T, keep)], rtol=1e-10)
+
+
+@pytest.mark.parametrize("alg", ["omp", "sp", "ompr", "cosamp"])
+def test_perm_randomizer_is_a_column_relabelling(alg):
+    """Eq.(7)'s R (R34) relabels columns: recovering s with D F R equals recovering
+    s' = R s with D F (sigma = +1, no R) and mapping the support back through pi."""
+    cfg = cs_inputs.Config(91, alg, 1024, 256, 16, "gauss", 0.0, randomizer="perm")
+    p = cs_inputs.make_problem(cfg, 0)
+    op = SrmOperator(p.N, p.sign_bits, p.rows, p.perm)
+    y = op.apply(p.s)
+    a = oracle.recover(alg, op, y, p.K, tol=1e-13)
+    op1 = SrmOperator(p.N, p.sign_bits, p.rows)
+    b = oracle.recover(alg, op1, op1.apply(p.s[p.perm]), p.K, tol=1e-13)
+    np.testing.assert_array_equal(a.support, np.sort(p.perm[b.support]))
+    np.testing.assert_allclose(a.s_hat[p.perm], b.s_hat, atol=1e-10)
+    np.testing.assert_array_equal(a.support, p.support)
