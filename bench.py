@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="problems per GPU (0 = config default)")
     ap.add_argument("--alg", choices=["omp", "sp", "ompr", "cosamp"], default="",
                     help="run the config's workload with another pursuit (not a BASELINE line)")
+    ap.add_argument("--randomizer", choices=["sign", "perm"], default="sign",
+                    help="perm: the paper's literal Eq.(7) D F R operator (R34; not a BASELINE line)")
     ap.add_argument("--no-op-bench", action="store_true")
     return ap.parse_args()
 
@@ -55,14 +57,18 @@ def select_config(args):
     cfg = cs_inputs.CONFIGS[args.config]
     if args.alg and args.alg != cfg.alg:
         cfg = dataclasses.replace(cfg, alg=args.alg)
+    if args.randomizer != cfg.randomizer:
+        cfg = dataclasses.replace(cfg, randomizer=args.randomizer)
     return cfg
 
 
 def workload_desc(cfg):
     base = cs_inputs.CONFIGS[cfg.cid]
-    if cfg.alg != base.alg:
+    if cfg.alg != base.alg or cfg.randomizer != base.randomizer:
         names = {"omp": "OMP", "sp": "SP", "ompr": "OMPR(1)", "cosamp": "CoSaMP"}
-        return f"c{cfg.cid}-shape with {names[cfg.alg]}+CG (alg override): N={cfg.N}, M={cfg.M}, K={cfg.K}"
+        op = "D.F.R (Eq.(7) permutation randomizer)" if cfg.randomizer == "perm" else "P.DCT.diag(sigma)"
+        return (f"c{cfg.cid}-shape with {names[cfg.alg]}+CG on {op} (override): "
+                f"N={cfg.N}, M={cfg.M}, K={cfg.K}")
     return {1: "c1: OMP+CG, N=4096, M=1024, K=64, noiseless",
             2: "c2: SP+CG, N=65536, M=16384, K=2048, sigma=1e-3",
             3: "c3: OMPR(1)+CG, N=2^20, M=2^18, K=8192, noiseless",
@@ -165,7 +171,10 @@ def run_ours(args):
     rows = torch.from_numpy(np.stack([p.rows for p in probs]).astype(np.int32)).to(dev)
     S = torch.from_numpy(np.stack([p.s for p in probs])).to(dev, td)
     E = torch.from_numpy(np.stack([p.noise for p in probs])).to(dev, td)
-    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=B)
+    perm = None
+    if cfg.randomizer == "perm":
+        perm = torch.from_numpy(np.stack([p.perm for p in probs]).astype(np.int32)).to(dev)
+    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=B, perm=perm)
     Y = (cs.cs_operator_apply(A, S) + E).to(torch.float32).to(td)  # fp32-rounded y (R21)
     del S, E
     torch.cuda.synchronize()
@@ -296,6 +305,8 @@ def run_ours(args):
         t_adj = a1.elapsed_time(a2) / reps_op / 1e3
         es = td.itemsize if hasattr(td, "itemsize") else (4 if td == torch.float32 else 8)
         meta_b = B * (3 * ((cfg.N + 31) // 32) * 4 + (cfg.M * 4 if cfg.N > 16384 else 0))
+        if cfg.randomizer == "perm":
+            meta_b += B * cfg.N * 4     # pi^-1 gathered once per apply / adjoint
         bytes_fwd = B * (cfg.N + cfg.M) * es + meta_b
         bytes_adj = B * (cfg.N + cfg.M) * es + meta_b
         peaks = load_peaks()
@@ -338,7 +349,8 @@ def run_ours(args):
     tr = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr):
         try:
-            key = f"c{cfg.cid}_{args.precision}" + ("" if cfg.alg == cs_inputs.CONFIGS[cfg.cid].alg else f"_{cfg.alg}")
+            key = f"c{cfg.cid}_{args.precision}" + ("" if cfg.alg == cs_inputs.CONFIGS[cfg.cid].alg else f"_{cfg.alg}") \
+                + ("" if cfg.randomizer == "sign" else f"_{cfg.randomizer}")
             roofline["traffic"] = json.load(open(tr)).get(key)
         except Exception:
             pass

@@ -106,6 +106,22 @@ size_t cs_operator_meta_bytes(int64_t N, int64_t M, int64_t batch);
 cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
                              const int32_t* d_rows, void* d_meta, size_t meta_bytes,
                              cs_stream_t stream, cs_operator** out);
+
+/* The paper's literal Eq.(7) sensing operator Phi = D F R with the
+ * randomizer R a permutation (R34), optionally
+ * composed with the sign diagonal:  A x = (C_N R (sigma . x))[rows],  (R u)_i = u_{pi(i)}.
+ *   d_sign_bits [batch][ceil(N/32)] as above, or NULL for sigma = +1 (the paper's D F R);
+ *   d_perm      [batch][N] int32: pi, a permutation of [0, N) per instance.  Checked HERE
+ *               on the device; a non-permutation returns CS_ERR_INVALID_ARG.
+ *   d_meta      >= cs_operator_meta_bytes_perm bytes (the plain metadata, then pi and
+ *               pi^-1 per instance: + 8N bytes per instance, 256-byte aligned).
+ * Every call taking a cs_operator accepts it (apply, adjoint, all recover variants); the
+ * pursuits select over the ORIGINAL indices j (ties -> lowest j) and return supports
+ * in them.  Synchronises `stream`. */
+size_t cs_operator_meta_bytes_perm(int64_t N, int64_t M, int64_t batch);
+cs_status cs_operator_create_perm(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
+                                  const int32_t* d_perm, const int32_t* d_rows, void* d_meta,
+                                  size_t meta_bytes, cs_stream_t stream, cs_operator** out);
 cs_status cs_operator_destroy(cs_operator* op);
 cs_status cs_operator_info(const cs_operator* op, int64_t* N, int64_t* M, int64_t* batch);
 

@@ -56,7 +56,7 @@ EXPORTS = [
     "cs_recover_batched", "cs_recover_batched_f64", "cs_workspace_bytes_host", "cs_recover_batched_host",
     "cs_recover_batched_host_f64", "cs_status_string", "cs_last_error",
     "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
-    "cs_diag_topk",
+    "cs_diag_topk", "cs_operator_meta_bytes_perm", "cs_operator_create_perm",
 ]
 
 
@@ -72,6 +72,8 @@ def load_library(path: str = LIB_PATH):
     sig = {
         "cs_operator_meta_bytes": (SZ, [I64, I64, I64]),
         "cs_operator_create": (I32, [I64, I64, I64, P, P, P, SZ, P, ctypes.POINTER(P)]),
+        "cs_operator_meta_bytes_perm": (SZ, [I64, I64, I64]),
+        "cs_operator_create_perm": (I32, [I64, I64, I64, P, P, P, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_destroy": (I32, [P]),
         "cs_operator_info": (I32, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
         "cs_operator_ws_bytes": (SZ, [P, ctypes.c_int]),
@@ -141,20 +143,30 @@ def launch_count(reset: bool = False) -> int:
 
 
 class Operator:
-    """Handle for A = P . DCT-II . diag(sigma) with `batch` independent instances."""
+    """Handle for A = P . DCT-II . diag(sigma) with `batch` independent instances; with
+    `perm` ([batch][N] int32 pi), the Eq.(7) operator P . DCT-II . R . diag(sigma)
+    (cs_operator_create_perm; sign_bits may then be None for sigma = +1)."""
 
-    def __init__(self, N: int, M: int, sign_bits, rows, batch: int = 1, stream=None):
+    def __init__(self, N: int, M: int, sign_bits, rows, batch: int = 1, stream=None, perm=None):
         torch = _torch()
         L = load_library()
         self.N, self.M, self.batch = int(N), int(M), int(batch)
         dev = rows.device
-        nb = L.cs_operator_meta_bytes(N, M, batch)
-        self.meta = torch.empty(nb, dtype=torch.uint8, device=dev)
-        sb = sign_bits.to(device=dev).contiguous()
         rw = rows.to(device=dev, dtype=torch.int32).contiguous()
+        sb = None if sign_bits is None else sign_bits.to(device=dev).contiguous()
         h = ctypes.c_void_p()
-        _check(L.cs_operator_create(N, M, batch, _ptr(sb), _ptr(rw), _ptr(self.meta), nb,
-                                    _stream(stream), ctypes.byref(h)), "cs_operator_create")
+        if perm is None:
+            nb = L.cs_operator_meta_bytes(N, M, batch)
+            self.meta = torch.empty(nb, dtype=torch.uint8, device=dev)
+            _check(L.cs_operator_create(N, M, batch, _ptr(sb), _ptr(rw), _ptr(self.meta), nb,
+                                        _stream(stream), ctypes.byref(h)), "cs_operator_create")
+        else:
+            pm = perm.to(device=dev, dtype=torch.int32).contiguous()
+            nb = L.cs_operator_meta_bytes_perm(N, M, batch)
+            self.meta = torch.empty(nb, dtype=torch.uint8, device=dev)
+            _check(L.cs_operator_create_perm(N, M, batch, _ptr(sb) if sb is not None else None, _ptr(pm),
+                                             _ptr(rw), _ptr(self.meta), nb, _stream(stream),
+                                             ctypes.byref(h)), "cs_operator_create_perm")
         self.handle = h
         self._ws = {}
 

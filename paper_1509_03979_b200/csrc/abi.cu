@@ -20,8 +20,9 @@ using namespace cs;
 
 struct cs_operator {
   int64_t N, M, B, nw;
-  uint32_t* meta;   // device: [B][3][nw]
+  uint32_t* meta;   // device: [B][stride] (meta_stride)
   int* errflag;     // device int in the meta tail
+  int32_t* perm;    // device: [B][pi N][pi^-1 N] after the meta tail (Eq.(7) randomizer), or null
   int device;
 };
 
@@ -99,7 +100,7 @@ __global__ void k_rows_mask(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < B * nw) {  // copy sign words
     int64_t b = i / nw, w = i % nw;
-    meta[b * stride + w] = sign_in[b * nw + w];
+    meta[b * stride + w] = sign_in ? sign_in[b * nw + w] : 0u;
   }
   if (i >= B * M) return;
   int64_t b = i / M, m = i % M;
@@ -109,6 +110,18 @@ __global__ void k_rows_mask(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t
   if (natural_off >= 0) atomicOr(&meta[b * stride + natural_off + (r >> 5)], 1u << (r & 31));
   const int64_t t = tp(r);
   atomicOr(&meta[b * stride + toff + (t >> 5)], 1u << (t & 31));
+}
+
+// Eq.(7) randomizer: copy pi, build pi^-1 (pre-filled with -1); err |= 2 unless pi is a
+// permutation of [0, N) in every instance
+__global__ void k_perm_setup(int64_t N, int64_t B, const int32_t* pin, int32_t* perm, int* err) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= B * N) return;
+  const int64_t b = i / N, k = i % N;
+  const int32_t v = pin[i];
+  perm[b * 2 * N + k] = v;
+  if (v < 0 || v >= N) { atomicOr(err, 2); return; }
+  if (atomicExch(&perm[b * 2 * N + N + v], (int32_t)k) != -1) atomicOr(err, 2);
 }
 
 // Tier L: tperm[rank of row m in the transposed order] = m
@@ -182,6 +195,7 @@ OpMeta meta_of(const cs_operator* op) {
   m.nw = op->nw;
   m.stride = meta_stride(op->N, op->M);
   m.toff = meta_toff(op->N);
+  m.perm = op->perm;
   return m;
 }
 
@@ -333,6 +347,7 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
     CS_CUDA(cudaStreamWaitEvent(sc, hp.ev[0][c], 0));
     cs_operator sub = *op;
     sub.meta = op->meta + b0 * meta_stride(op->N, op->M);
+    if (op->perm) sub.perm = op->perm + b0 * 2 * N;
     sub.B = cnt;
     char* rws = tier_s ? w + (size_t)(b0 * N) * sizeof(T) : w;
     const size_t rws_bytes = tier_s ? (size_t)(cnt * N) * sizeof(T) : need_rec;
@@ -365,16 +380,17 @@ size_t cs_operator_meta_bytes(int64_t N, int64_t M, int64_t batch) {
   return (size_t)(align_up(batch * meta_stride(N, M) * 4, 256) + 256);
 }
 
-cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
-                             const int32_t* d_rows, void* d_meta, size_t meta_bytes,
+static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
+                             const int32_t* d_perm, const int32_t* d_rows, void* d_meta, size_t meta_bytes,
                              cs_stream_t stream, cs_operator** out) {
   if (!out) return fail(CS_ERR_INVALID_ARG, "out is null");
   *out = nullptr;
   if (cs_status s = check_N(N)) return s;
   if (M < 1 || M > N) return fail(CS_ERR_INVALID_ARG, "M must be in [1, N]");
   if (batch < 1 || batch > (1 << 30)) return fail(CS_ERR_INVALID_ARG, "bad batch");
-  if (!d_sign_bits || !d_rows || !d_meta) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
-  if (meta_bytes < cs_operator_meta_bytes(N, M, batch)) return fail(CS_ERR_WORKSPACE, "meta buffer too small");
+  if ((!d_sign_bits && !d_perm) || !d_rows || !d_meta) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
+  const size_t need = d_perm ? cs_operator_meta_bytes_perm(N, M, batch) : cs_operator_meta_bytes(N, M, batch);
+  if (meta_bytes < need) return fail(CS_ERR_WORKSPACE, "meta buffer too small");
   if (cs_status s = check_device()) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t nw = (N + 31) / 32;
@@ -382,7 +398,14 @@ cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t
   const int64_t stride = meta_stride(N, M);
   const TPos tp = tpos_of(N);
   int* err = reinterpret_cast<int*>(reinterpret_cast<char*>(d_meta) + align_up(batch * stride * 4, 256));
-  CS_CUDA(cudaMemsetAsync(d_meta, 0, meta_bytes, st));
+  const size_t base_bytes = cs_operator_meta_bytes(N, M, batch);
+  CS_CUDA(cudaMemsetAsync(d_meta, 0, base_bytes, st));
+  int32_t* perm = d_perm ? reinterpret_cast<int32_t*>(reinterpret_cast<char*>(d_meta) + base_bytes) : nullptr;
+  if (perm) {
+    CS_CUDA(cudaMemsetAsync(perm, 0xFF, (size_t)(batch * 2 * N) * 4, st));
+    k_perm_setup<<<(unsigned)((batch * N + 255) / 256), 256, 0, st>>>(N, batch, d_perm, perm, err);
+    CS_LAUNCHED();
+  }
   int64_t nthr = std::max(batch * M, batch * nw);
   const int64_t toff = meta_toff(N), natural = N > TIER_S_MAX_N ? -1 : nw;
   k_rows_mask<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(N, M, batch, nw, stride, natural, toff, tp, d_rows,
@@ -399,7 +422,8 @@ cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t
   int herr = 0;
   CS_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   CS_CUDA(cudaStreamSynchronize(st));
-  if (herr) return fail(CS_ERR_INVALID_ARG, "rows must be strictly increasing and in [0, N)");
+  if (herr & 1) return fail(CS_ERR_INVALID_ARG, "rows must be strictly increasing and in [0, N)");
+  if (herr & 2) return fail(CS_ERR_INVALID_ARG, "perm must be a permutation of [0, N)");
   cs_operator* op = new cs_operator;
   op->N = N;
   op->M = M;
@@ -407,9 +431,36 @@ cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t
   op->nw = nw;
   op->meta = meta;
   op->errflag = err;
+  op->perm = perm;
   CS_CUDA(cudaGetDevice(&op->device));
   *out = op;
   return CS_OK;
+}
+
+cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
+                             const int32_t* d_rows, void* d_meta, size_t meta_bytes,
+                             cs_stream_t stream, cs_operator** out) {
+  if (!d_sign_bits) {
+    if (out) *out = nullptr;
+    return fail(CS_ERR_INVALID_ARG, "null pointer argument");
+  }
+  return create_impl(N, M, batch, d_sign_bits, nullptr, d_rows, d_meta, meta_bytes, stream, out);
+}
+
+size_t cs_operator_meta_bytes_perm(int64_t N, int64_t M, int64_t batch) {
+  const size_t base = cs_operator_meta_bytes(N, M, batch);
+  if (!base) return 0;
+  return base + (size_t)align_up(batch * 2 * N * 4, 256);
+}
+
+cs_status cs_operator_create_perm(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
+                                  const int32_t* d_perm, const int32_t* d_rows, void* d_meta,
+                                  size_t meta_bytes, cs_stream_t stream, cs_operator** out) {
+  if (!d_perm) {
+    if (out) *out = nullptr;
+    return fail(CS_ERR_INVALID_ARG, "null pointer argument");
+  }
+  return create_impl(N, M, batch, d_sign_bits, d_perm, d_rows, d_meta, meta_bytes, stream, out);
 }
 
 cs_status cs_operator_destroy(cs_operator* op) {

@@ -36,6 +36,8 @@ template <typename T> struct CtaCtx {
   uint32_t* sign;    // [nw]
   uint32_t* rowmask; // [nw]
   int32_t* prefix;   // [nw]
+  const int32_t* pm;    // global: Eq.(7) randomizer pi (R34), or null
+  const int32_t* pinv;  // global: pi^-1, or null
   TwTable<T> twL, tw4;
   double* redd;      // [32]
   int64_t* redi;     // [33]
@@ -132,26 +134,32 @@ template <typename T> struct CtaCtx {
   // Z is stored swizzled (fft_cta.cuh): T-position p of v lives at zt(p).
   CS_DEV static int zt(int p) { return 2 * swz<T>(p >> 1) + (p & 1); }
   CS_DEV const T* zbuf() const { return reinterpret_cast<const T*>(Z); }
-  CS_DEV T c_raw(int64_t j) const { return zbuf()[zt((int)mk_pos(j, N))]; }
+  // Makhoul position of index j: mk_pos(pi^-1(j)) under the Eq.(7) randomizer (R34)
+  CS_DEV static int ppos(const int32_t* pinv, int64_t j, int64_t N) {
+    return (int)mk_pos(pinv ? (int64_t)pinv[j] : j, N);
+  }
+  CS_DEV T c_raw(int64_t j) const { return zbuf()[zt(ppos(pinv, j, N))]; }
   // register-resident views for hot loops (the context itself lives in local memory)
   struct CV {
     const T* z;
     const uint32_t* sign;
     int N;
-    CS_DEV T raw(int64_t j) const { return z[zt((int)mk_pos(j, N))]; }
+    const int32_t* pinv;
+    CS_DEV T raw(int64_t j) const { return z[zt(ppos(pinv, j, N))]; }
     CS_DEV T at(int64_t j) const { return apply_sign<T>(sign, j, raw(j)); }
   };
   struct C0V {
     const T* c0;
     const uint32_t* sign;
     int64_t N;
-    CS_DEV T at(int64_t j) const { return apply_sign<T>(sign, j, c0[mk_pos(j, N)]); }
+    const int32_t* pinv;
+    CS_DEV T at(int64_t j) const { return apply_sign<T>(sign, j, c0[ppos(pinv, j, N)]); }
   };
-  CS_DEV CV cview() const { return CV{zbuf(), sign, (int)N}; }
-  CS_DEV C0V c0view() const { return C0V{c0, sign, N}; }
+  CS_DEV CV cview() const { return CV{zbuf(), sign, (int)N, pinv}; }
+  CS_DEV C0V c0view() const { return C0V{c0, sign, N, pinv}; }
   CS_DEV unsigned* hist_ptr() const { return hist; }
   CS_DEV T c_at(int64_t j) const { return apply_sign<T>(sign, j, c_raw(j)); }
-  CS_DEV T c0_at(int64_t j) const { return apply_sign<T>(sign, j, c0[mk_pos(j, N)]); }
+  CS_DEV T c0_at(int64_t j) const { return apply_sign<T>(sign, j, c0[ppos(pinv, j, N)]); }
   CS_DEV void save_c0() {
     const T* cb = zbuf();
     for (int p = gtid; p < (int)N; p += gnthr) c0[p] = cb[zt(p)];

@@ -126,6 +126,8 @@ template <typename T> struct GridCtx {
   const int32_t* prefix;
   const T* y;        // measurements in the transposed row order (= yT during a recovery)
   const int32_t* tperm;  // [M] y index of the t-th selected row in the transposed order
+  const int32_t* pm;     // Eq.(7) randomizer pi (R34), or null
+  const int32_t* pinv;   // pi^-1, or null
   T* yT;             // [M] workspace
   int s1, tsh;       // transposed mask position: t = (k mod 2^s1) << tsh | k >> s1
   T* c0;        // [N] Makhoul order
@@ -315,25 +317,31 @@ template <typename T> struct GridCtx {
   CS_DEV const unsigned* hist_smem() const { return shist; }
 
   // ---- correlation access ----
-  CS_DEV T c_raw(int64_t j) const { return Cb[mk_pos(j, N)]; }
+  // Makhoul position of index j: mk_pos(pi^-1(j)) under the Eq.(7) randomizer (R34)
+  CS_DEV static int64_t ppos(const int32_t* pinv, int64_t j, int64_t N) {
+    return mk_pos(pinv ? (int64_t)pinv[j] : j, N);
+  }
+  CS_DEV T c_raw(int64_t j) const { return Cb[ppos(pinv, j, N)]; }
   struct CV {
     const T* z;
     const uint32_t* sign;
     int64_t N;
-    CS_DEV T raw(int64_t j) const { return z[mk_pos(j, N)]; }
+    const int32_t* pinv;
+    CS_DEV T raw(int64_t j) const { return z[ppos(pinv, j, N)]; }
     CS_DEV T at(int64_t j) const { return apply_sign<T>(sign, j, raw(j)); }
   };
   struct C0V {
     const T* c0;
     const uint32_t* sign;
     int64_t N;
-    CS_DEV T at(int64_t j) const { return apply_sign<T>(sign, j, c0[mk_pos(j, N)]); }
+    const int32_t* pinv;
+    CS_DEV T at(int64_t j) const { return apply_sign<T>(sign, j, c0[ppos(pinv, j, N)]); }
   };
-  CS_DEV CV cview() const { return CV{Cb, sign, N}; }
-  CS_DEV C0V c0view() const { return C0V{c0, sign, N}; }
+  CS_DEV CV cview() const { return CV{Cb, sign, N, pinv}; }
+  CS_DEV C0V c0view() const { return C0V{c0, sign, N, pinv}; }
   CS_DEV unsigned* hist_ptr() const { return shist; }
-  CS_DEV T c_at(int64_t j) const { return apply_sign<T>(sign, j, Cb[mk_pos(j, N)]); }
-  CS_DEV T c0_at(int64_t j) const { return apply_sign<T>(sign, j, c0[mk_pos(j, N)]); }
+  CS_DEV T c_at(int64_t j) const { return apply_sign<T>(sign, j, Cb[ppos(pinv, j, N)]); }
+  CS_DEV T c0_at(int64_t j) const { return apply_sign<T>(sign, j, c0[ppos(pinv, j, N)]); }
   CS_DEV void save_c0() {
     for (int64_t p = gtid; p < N; p += gnthr) c0[p] = Cb[p];
     sync();
@@ -348,7 +356,7 @@ template <typename T> struct GridCtx {
     for (int t = gtid; t <= nt; t += gnthr) { tcnt[t] = 0; if (t < nt) tfill[t] = 0; }
     sync();
     for (int i = gtid; i < ns; i += gnthr) {
-      const int64_t p = mk_pos(supp[i], N);
+      const int64_t p = ppos(pinv, supp[i], N);
       in_pos[i] = p;
       atomicAdd(&tcnt[tile_of(p)], 1);
     }

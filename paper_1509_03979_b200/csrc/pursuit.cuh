@@ -159,11 +159,13 @@ CS_NOINL void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* o
     // positions per complex slot, instead of gathering it in natural index order
     const int n = (int)N, L = n / 2;
     const C2<T>* zs = reinterpret_cast<const C2<T>*>(cv.z);
+    const int32_t* pm = ctx.pm;   // Eq.(7) randomizer: position i holds index pi(i) (R34)
     auto visit = [&](auto&& f) {
       for (int q = threadIdx.x; q < L; q += blockDim.x) {
         const C2<T> z = zs[swz<T>(q)];
-        const int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;        // mk_nat(2q)
-        const int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;  // mk_nat(2q+1)
+        int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;        // mk_nat(2q)
+        int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;  // mk_nat(2q+1)
+        if (pm) { j0 = pm[j0]; j1 = pm[j1]; }
         f(j0, (excl && bit_test(excl, j0)) ? Key(0) : full_key(z.x));
         f(j1, (excl && bit_test(excl, j1)) ? Key(0) : full_key(z.y));
       }
@@ -203,10 +205,12 @@ CS_NOINL int64_t detect_argmax(Ctx& ctx, const uint32_t* excl) {
     auto take = [&](int j, Key k) {  // larger key wins, ties -> lower index (R12)
       if (k > bk || (k == bk && k != 0 && j < bi)) { bk = k; bi = j; }
     };
+    const int32_t* pm = ctx.pm;
     for (int q = threadIdx.x; q < L; q += blockDim.x) {
       const C2<T> z = zs[swz<T>(q)];
-      const int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;
-      const int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;
+      int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;
+      int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;
+      if (pm) { j0 = pm[j0]; j1 = pm[j1]; }
       take(j0, bit_test(excl, j0) ? Key(0) : full_key(z.x));
       take(j1, bit_test(excl, j1) ? Key(0) : full_key(z.y));
     }

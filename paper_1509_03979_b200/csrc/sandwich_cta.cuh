@@ -219,9 +219,11 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
       const T* vin = shp(gio.vin);
       for (int i = tid; i < L; i += SW_NT) buf[i] = mk<T>(0, 0);
       __syncthreads();
+      // Eq.(7) randomizer pi^-1 (R34), parked in shared memory by make_cta_ctx
+      const int32_t* pv = *reinterpret_cast<const int32_t* const*>(cs_smem_base + F.zero + 8);
       for (int i = tid; i < gio.ns; i += SW_NT) {
         const int j = supp[i];
-        zb[zt((int)mk_pos(j, N))] = apply_sign<T>(sign, j, vin[i]);
+        zb[zt((int)mk_pos(pv ? pv[j] : j, N))] = apply_sign<T>(sign, j, vin[i]);
       }
       __syncthreads();
     }
@@ -238,9 +240,10 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
       const int* supp = shp(gio.supp);
       const uint32_t* sign = signs;
       T* vout = shp(gio.vout);
+      const int32_t* pv = *reinterpret_cast<const int32_t* const*>(cs_smem_base + F.zero + 8);
       for (int i = tid; i < gio.ns; i += SW_NT) {
         const int j = supp[i];
-        vout[i] = apply_sign<T>(sign, j, zb[zt((int)mk_pos(j, N))]);
+        vout[i] = apply_sign<T>(sign, j, zb[zt((int)mk_pos(pv ? pv[j] : j, N))]);
       }
       __syncthreads();
     }

@@ -209,6 +209,8 @@ template <typename T> CS_DEV void set_instance(GridCtx<T>& c, const OpMeta& m, i
   c.rowmask = m.tmask(b);
   c.prefix = m.tprefix(b);
   c.tperm = m.tperm(b);
+  c.pm = m.pm(b);
+  c.pinv = m.pinv(b);
 }
 
 // y (row order) -> yT (transposed row order of the stored mask); ends with a grid barrier
@@ -243,6 +245,15 @@ __global__ void k_l_tables(LLayout s, int64_t N, char* ws) {
   }
 }
 
+// Eq.(7) randomizer: x_j lands at the Makhoul position of pi^-1(j) (R34).  Out of line so
+// the plain path's register allocation is unaffected.
+template <typename T>
+CS_NOINL void l_scatter_perm(int64_t t0, int64_t nt, int64_t N, const T* x, const uint32_t* sg,
+                             const int32_t* pv, T* U) {
+  gstaged<TL_UNR, T>(N, t0, nt, [&](int64_t j) { return apply_sign<T>(sg, j, x[j]); },
+                     [&](int64_t j, T v) { U[mk_pos(pv[j], N)] = v; });
+}
+
 template <typename T>
 __global__ void __launch_bounds__(TL_THREADS) k_l_apply(LArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
@@ -264,6 +275,8 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_apply(LArgs<T> a) {
     stamp(0);
     // four consecutive j per unit: x[j..j+3] -> U[j/2], U[j/2+1] (even j) and
     // U[N-2-j/2], U[N-1-j/2] (odd j, descending) — Makhoul order, sign applied
+    if (c.pinv) l_scatter_perm<T>(c.gtid, c.gnthr, N, x, sg, c.pinv, U);
+    else
     gstaged<TL_UNR, float4>(N / 4, c.gtid, c.gnthr, [&](int64_t q) {
       const int64_t j = 4 * q;
       float4 v;
@@ -315,7 +328,9 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_adjoint(LArgs<T> a) {
     T* x = a.out + b * N;
     const uint32_t* sg = c.sign;
     const T* Cb = c.Cb;
-    gstaged<TL_UNR, T>(N, c.gtid, c.gnthr, [&](int64_t j) { return apply_sign<T>(sg, j, Cb[mk_pos(j, N)]); },
+    const int32_t* pv = c.pinv;
+    gstaged<TL_UNR, T>(N, c.gtid, c.gnthr,
+                       [&](int64_t j) { return apply_sign<T>(sg, j, Cb[GridCtx<T>::ppos(pv, j, N)]); },
                        [&](int64_t j, T v) { x[j] = v; });
     c.sync();
   }

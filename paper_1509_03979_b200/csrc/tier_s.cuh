@@ -69,6 +69,7 @@ struct OpMeta {
   int64_t nw;
   int64_t stride;  // words per instance
   int64_t toff;    // word offset of the transposed mask within an instance
+  const int32_t* perm;  // Eq.(7) randomizer R (R34): per instance [pi N][pi^-1 N], or null
   CS_HD const uint32_t* sign(int64_t b) const { return base + b * stride; }
   CS_HD const uint32_t* rmask(int64_t b) const { return base + b * stride + nw; }
   CS_HD const int32_t* prefix(int64_t b) const {
@@ -81,6 +82,8 @@ struct OpMeta {
   CS_HD const int32_t* tperm(int64_t b) const {
     return reinterpret_cast<const int32_t*>(base + b * stride + toff + 2 * nw);
   }
+  CS_HD const int32_t* pm(int64_t b) const { return perm ? perm + b * 2 * N : nullptr; }
+  CS_HD const int32_t* pinv(int64_t b) const { return perm ? perm + b * 2 * N + N : nullptr; }
 };
 
 template <typename T>
@@ -114,7 +117,12 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   c.cidx = reinterpret_cast<int*>(smem + lay.cidx);
   c.ccnt = reinterpret_cast<int*>(smem + lay.ccnt);
   c.rbank = 0;
-  if (threadIdx.x == 0) *reinterpret_cast<int*>(smem + s_fixed<T>(meta.N).zero) = 0;
+  c.pm = meta.pm(b);
+  c.pinv = meta.pinv(b);
+  if (threadIdx.x == 0) {
+    *reinterpret_cast<int*>(smem + s_fixed<T>(meta.N).zero) = 0;
+    *reinterpret_cast<const int32_t**>(smem + s_fixed<T>(meta.N).zero + 8) = c.pinv;  // sandwich_cta.cuh
+  }
   c.in_supp = nullptr;
   c.in_ns = 0;
   c.applies = 0;
@@ -145,7 +153,13 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout 
   CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, b);
   const int64_t N = c.N;
   const T* x = X + b * N;
-  if constexpr (sizeof(T) == 4) {
+  if (c.pinv) {
+    // Eq.(7) randomizer: x_j lands at the Makhoul position of pi^-1(j) (R34)
+    T* zb = reinterpret_cast<T*>(c.Z);
+    const int32_t* pv = c.pinv;
+    for (int j = c.gtid; j < (int)N; j += c.gnthr)
+      zb[CtaCtx<T>::zt((int)mk_pos(pv[j], N))] = apply_sign<T>(c.sign, j, x[j]);
+  } else if constexpr (sizeof(T) == 4) {
     // x[4q..4q+3] -> complex slots q (x_{4q}, x_{4q+2}) and L-1-q (x_{4q+3}, x_{4q+1})
     // of the Makhoul sequence (cs_common.cuh mk_pos), sign applied; 16-byte loads,
     // all of a thread's loads in flight before its stores

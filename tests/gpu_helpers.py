@@ -12,6 +12,14 @@ def to_dev(problems, dev):
     return bits, rows
 
 
+def perms_dev(problems, dev):
+    """[B][N] int32 permutations of the Eq.(7) randomizer (R34), or None."""
+    import torch
+    if problems[0].perm is None:
+        return None
+    return torch.from_numpy(np.stack([p.perm for p in problems]).astype(np.int32)).to(dev)
+
+
 def measured(problems):
     """y via the ORACLE operator, rounded to fp32 (R21)."""
     ys = []

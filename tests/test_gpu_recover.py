@@ -8,7 +8,7 @@ import pytest
 
 import cs_inputs
 from cs_inputs import CONFIGS
-from gpu_helpers import to_dev, measured, oracle_results, compare
+from gpu_helpers import to_dev, perms_dev, measured, oracle_results, compare
 
 pytestmark = pytest.mark.gpu
 
@@ -28,7 +28,7 @@ def _run(cs, cfg, count, dtype="float32", tol=None, b0=0, opts=None):
     probs = cs_inputs.make_batch(cfg, b0=b0, count=count)
     ys = measured(probs)
     bits, rows = to_dev(probs, dev)
-    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=count)
+    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=count, perm=perms_dev(probs, dev))
     td = getattr(torch, dtype)
     if tol is None:
         tol = 1e-6 if dtype == "float32" else 1e-12
