@@ -61,18 +61,31 @@ static CS_NOINL void grid_barrier(GridBar* gb) {
   __syncthreads();
 }
 
-// Global two-level twiddle table: W^m = hi[m >> sh] * lo[m & (2^sh - 1)]
+// Shared-memory three-level twiddle table of W_den for exponents m < range (range a power
+// of two): W^m = t2[m >> 16] * t1[(m >> 8) & 255] * t0[m & 255].  A few KB per table
+// instead of a global two-level table: every lookup is three shared loads (no L2 round
+// trip on the passes' critical path), one rounding more than before.
 template <typename T> struct GTw {
-  const C2<T>* lo;
-  const C2<T>* hi;
-  int sh;
+  const C2<T>* t;     // [t0: 256][t1: 256][t2: (range >> 16) + 1]
+  int64_t mask;       // range - 1 (W_L: range = den, so exponents wrap mod L)
   CS_DEV C2<T> operator()(int64_t m) const {
 #ifdef CS_DIAG_NOTW
     return mk<T>(T(1), T(0));  // diagnostics build only
 #endif
-    return cmul<T>(__ldg(&hi[m >> sh]), __ldg(&lo[m & ((1ll << sh) - 1)]));
+    m &= mask;
+    return cmul<T>(cmul<T>(t[512 + (m >> 16)], t[256 + ((m >> 8) & 255)]), t[m & 255]);
   }
 };
+CS_HD int64_t gtw_entries(int64_t range) { return 512 + (range >> 16) + 1; }
+template <typename T> CS_DEV void gtw_init(C2<T>* t, int64_t den, int64_t range, int tid, int nthr) {
+  const int64_t n = gtw_entries(range);
+  for (int64_t i = tid; i < n; i += nthr) {
+    const int64_t m = i < 256 ? i : (i < 512 ? (i - 256) << 8 : (i - 512) << 16);
+    double s, c;
+    sincospi(-2.0 * (double)(m & (den - 1)) / (double)den, &s, &c);
+    t[i] = mk<T>((T)c, (T)s);
+  }
+}
 
 // scratch for collectives (global, zeroed before launch)
 template <typename T> struct GridScratch {
@@ -603,6 +616,37 @@ template <typename T> struct GridCtx {
         for (int k2 = threadIdx.x; k2 < n2 / 2; k2 += blockDim.x) {
           int64_t k = L1 / 2 + L1 * k2;
           mid_pair<T, MODE>(zb[swz<T>(k2)], zb[swz<T>(n2 - 1 - k2)], k, tw4(k), m, rn2);
+        }
+      } else if (m.staged && L2 >= 256 && blockDim.x == 256) {
+        // general item, strength-reduced (the common case: every item of c2/c3/c5).  Thread
+        // t owns k2 = t + 256 u.  Its four mask bits sit at fixed bit positions (k2 & 31 or
+        // 31 - (k2 & 31)) of words that move by +-8 per step; its two buffer slots move by
+        // +-512 (above the swizzle's bits, so swz is computed once); the twiddle
+        // a = W_4N^(ka + L1 k2) follows the anchored recurrence of passes A/B (a table
+        // lookup every TW_ANCHOR steps).  Same arithmetic as the branch below.
+        const int W = (int)((2 * L2) >> 5), W1 = (int)(L2 >> 5);
+        const uint32_t* mw = m.rowmask;
+        const int32_t* pw = m.prefix;
+        const MidK<T> cst = make_midk<T>((int)N);
+        const int t = (int)threadIdx.x, b0 = t & 31, b1 = 31 - b0;
+        const uint32_t lm0 = (1u << b0) - 1u, lm1 = (1u << b1) - 1u;
+        const int s0 = swz<T>(2 * t), s1i = swz<T>(2 * n2 - 1 - 2 * t);
+        const int64_t l1 = L1;
+        const C2<T> astep = tw4(l1 * 256);
+        C2<T> a = mk<T>(1, 0);
+        for (int u = 0, k2 = t; k2 < n2; ++u, k2 += 256) {
+          const int q = k2 >> 5;
+          const int wi[4] = {q, W + 2 * W1 - 1 - q, W + W1 - 1 - q, W1 + q};
+          const int bi[4] = {b0, b1, b1, b0};
+          if ((u & (TW_ANCHOR - 1)) == 0) a = tw4(ka + l1 * k2);
+          else a = cmul<T>(a, astep);
+          const C2<T> a2 = cmul<T>(a, a);
+          const C2<T> w = cmul<T>(a2, a2);
+          mid_pair2g<T, MODE>(zb[s0 + 512 * u], zb[s1i - 512 * u], a, w, m, cst, rn2,
+              [&](int qq) { return (bool)((mw[wi[qq]] >> bi[qq]) & 1u); },
+              [&](int qq) {
+                return pw[wi[qq]] + __popc(mw[wi[qq]] & ((bi[qq] == b0) ? lm0 : lm1));
+              });
         }
       } else if (m.staged) {
         // general item (rows ka, kb = L1 - ka): the four DCT indices of the pair at column

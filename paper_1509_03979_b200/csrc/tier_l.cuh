@@ -43,7 +43,7 @@ CS_HD LGeom l_geom(int64_t N) {
 
 // Workspace layout (byte offsets) — identical on host and device.
 struct LLayout {
-  int64_t U, Wk, Cb, c0, yT, twFlo, twFhi, tw4lo, tw4hi, in_pos, tcnt, tfill, tlist;
+  int64_t U, Wk, Cb, c0, yT, in_pos, tcnt, tfill, tlist;
   int64_t S, S2, Ul, x, x2, xU, r, d, q, b, Sbits, Ubits, Pbits;
   int64_t ctl, bar, pd, pi, pk, ghist, ts, ctl_end;
   int64_t bytes;
@@ -62,10 +62,6 @@ CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int 
   s.Wk = take(g.L * cs2);
   s.Cb = take(N * ts);
   s.c0 = pursuit ? take(N * ts) : 0;
-  s.twFlo = take((int64_t(1) << g.shF) * cs2);
-  s.twFhi = take(((g.L >> g.shF) + 1) * cs2);
-  s.tw4lo = take((int64_t(1) << g.sh4) * cs2);
-  s.tw4hi = take(((g.L >> g.sh4) + 1) * cs2);
   if (pursuit) {
     s.in_pos = take((int64_t)ucap * 8);
     s.tcnt = take((g.L2 / g.CT + 1) * 4);
@@ -113,6 +109,8 @@ template <typename T> CS_HD int64_t l_smem_bytes(int64_t N) {
   take(64 * cs2); take((g.L2 >= 64 ? g.L2 / 64 : 1) * cs2);   // tw2
   take(34 * 8); take(34 * 8); take(32 * 8); take(256 * 4); take(4 * 8);
   take(4 * ((2 * g.L2) / 32) * 4);                        // staged row metadata of pass B
+  take(gtw_entries(g.L) * cs2);                           // W_L (three-level)
+  take(gtw_entries(N) * cs2);                             // W_4N (exponents k < N)
   return o;
 }
 
@@ -159,12 +157,6 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.tcnt = reinterpret_cast<int*>(ws + s.tcnt);
   c.tfill = reinterpret_cast<int*>(ws + s.tfill);
   c.tlist = reinterpret_cast<int*>(ws + s.tlist);
-  c.twF.lo = reinterpret_cast<const C2<T>*>(ws + s.twFlo);
-  c.twF.hi = reinterpret_cast<const C2<T>*>(ws + s.twFhi);
-  c.twF.sh = g.shF;
-  c.tw4.lo = reinterpret_cast<const C2<T>*>(ws + s.tw4lo);
-  c.tw4.hi = reinterpret_cast<const C2<T>*>(ws + s.tw4hi);
-  c.tw4.sh = g.sh4;
   c.g.bar = reinterpret_cast<GridBar*>(ws + s.bar);
   c.g.pd = reinterpret_cast<double*>(ws + s.pd);
   c.g.pi = reinterpret_cast<int64_t*>(ws + s.pi);
@@ -188,6 +180,14 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.shist = reinterpret_cast<unsigned*>(take(256 * 4));
   c.pick = reinterpret_cast<int64_t*>(take(4 * 8));
   c.msm = reinterpret_cast<uint32_t*>(take(4 * ((2 * g.L2) / 32) * 4));
+  C2<T>* tF = reinterpret_cast<C2<T>*>(take(gtw_entries(g.L) * cs2));
+  C2<T>* tQ = reinterpret_cast<C2<T>*>(take(gtw_entries(g.N) * cs2));
+  gtw_init<T>(tF, g.L, g.L, threadIdx.x, blockDim.x);
+  gtw_init<T>(tQ, 4 * g.N, g.N, threadIdx.x, blockDim.x);
+  c.twF.t = shp(tF);
+  c.twF.mask = g.L - 1;
+  c.tw4.t = shp(tQ);
+  c.tw4.mask = g.N - 1;
   tw_init<T>(t1lo, t1hi, g.L1, n1, threadIdx.x, blockDim.x);
   tw_init<T>(t2lo, t2hi, g.L2, n2, threadIdx.x, blockDim.x);
   c.tw1.lo = t1lo; c.tw1.hi = t1hi;
@@ -220,29 +220,6 @@ template <typename T> CS_DEV void load_yT(GridCtx<T>& c, const T* y) {
   gstaged<TL_UNR, T>(c.M, c.gtid, c.gnthr, [&](int64_t t) { return y[tp[t]]; }, [&](int64_t t, T v) { yT[t] = v; });
   c.sync();
   c.y = c.yT;
-}
-
-// Global twiddle tables (plain launch before the cooperative kernel).
-template <typename T>
-__global__ void k_l_tables(LLayout s, int64_t N, char* ws) {
-  LGeom g = l_geom(N);
-  C2<T>* Flo = reinterpret_cast<C2<T>*>(ws + s.twFlo);
-  C2<T>* Fhi = reinterpret_cast<C2<T>*>(ws + s.twFhi);
-  C2<T>* Qlo = reinterpret_cast<C2<T>*>(ws + s.tw4lo);
-  C2<T>* Qhi = reinterpret_cast<C2<T>*>(ws + s.tw4hi);
-  const int64_t nlo = int64_t(1) << g.shF, nhi = (g.L >> g.shF) + 1;
-  const int64_t total = 2 * (nlo + nhi);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t which = i / (nlo + nhi), r = i % (nlo + nhi);
-    int64_t den = which ? 4 * N : g.L;
-    int64_t m = r < nlo ? r : (r - nlo) << g.shF;
-    double sn, cn;
-    sincospi(-2.0 * (double)(m % den) / (double)den, &sn, &cn);
-    C2<T> w = mk<T>((T)cn, (T)sn);
-    if (which == 0) { if (r < nlo) Flo[r] = w; else Fhi[r - nlo] = w; }
-    else { if (r < nlo) Qlo[r] = w; else Qhi[r - nlo] = w; }
-  }
 }
 
 // Eq.(7) randomizer: x_j lands at the Makhoul position of pi^-1(j) (R34).  Out of line so
@@ -455,8 +432,6 @@ inline cs_status l_launch(const void* fn, LArgs<T>& a, int64_t N, cudaStream_t s
   if (work < grid) grid = (int)work;
   cudaError_t e = cudaMemsetAsync(a.ws + a.lay.ctl, 0, (size_t)(a.lay.ctl_end - a.lay.ctl), st);
   if (e != cudaSuccess) { err = std::string("memset: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
-  k_l_tables<T><<<64, 256, 0, st>>>(a.lay, N, a.ws);
-  launches.fetch_add(1);
   void* args[] = {&a};
   e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(TL_THREADS), args, (size_t)smem, st);
   launches.fetch_add(1);
