@@ -10,6 +10,8 @@ timeout 600 python bench.py > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.er
 for c in 1 2 3 5; do
   BENCH_NO_CPU=1 timeout 600 python bench.py --config $c --steps 3 --warmup 3 > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err
 done
+BENCH_NO_CPU=1 timeout 600 python bench.py --config 4 --alg cosamp --steps 5 --warmup 3 > gpurun_out/bench_c4_cosamp.json 2> gpurun_out/bench_c4_cosamp.err
+BENCH_NO_CPU=1 timeout 600 python bench.py --config 4 --randomizer perm --steps 5 --warmup 3 > gpurun_out/bench_c4_perm.json 2> gpurun_out/bench_c4_perm.err
 timeout 300 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 export PROF_B=4096
 timeout 300 python tools/prof_c4.py > gpurun_out/prof_plain.log 2>&1 && \
