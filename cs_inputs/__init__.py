@@ -42,6 +42,7 @@ class Config:
     noise: float        # sigma_eta
     batch: int = 1
     randomizer: str = "sign"   # "sign": R = diag(+-1) (BASELINE); "perm": Eq.(7)'s permutation, sigma = +1
+    psi: str = "I"             # dictionary: "I" (BASELINE) or "dct" (A = Phi C_N)
 
     def scaled(self, div: int, batch: Optional[int] = None) -> "Config":
         """Same recipe at N/div, M/div, K/div (ratios kept); used for parity tests."""
@@ -123,6 +124,7 @@ class Problem:
     support: np.ndarray     # planted support (sorted)
     noise: np.ndarray       # float64[M] eta
     perm: Optional[np.ndarray] = None   # int32[N] pi of the randomizer R (randomizer "perm")
+    psi: Optional[str] = None           # None (Psi = I) or "dct"
 
 
 def make_problem(cfg: Config, trial: int = 0, b: int = 0) -> Problem:
@@ -139,7 +141,7 @@ def make_problem(cfg: Config, trial: int = 0, b: int = 0) -> Problem:
                           rng(c, trial, b, TAG_VAL), rng(c, trial, b, TAG_PERM))
     eta = rng(c, trial, b, TAG_NOISE).standard_normal(M) * cfg.noise if cfg.noise > 0 \
         else np.zeros(M)
-    return Problem(N, M, K, cfg.alg, bits, rows, s, supp, eta, perm)
+    return Problem(N, M, K, cfg.alg, bits, rows, s, supp, eta, perm, "dct" if cfg.psi == "dct" else None)
 
 
 def make_batch(cfg: Config, trial: int = 0, b0: int = 0, count: Optional[int] = None):

@@ -151,3 +151,41 @@ def test_perm_operator_rows_orthonormal_and_adjoint():
     g = np.random.default_rng(3)
     x, w = g.standard_normal(N), g.standard_normal(M)
     assert abs(op.apply(x) @ w - x @ op.adjoint(w)) <= 1e-12 * np.linalg.norm(x) * np.linalg.norm(w)
+
+
+# ---------------------------------------------------------------- Psi = DCT (A = Phi Psi, R35)
+@pytest.mark.parametrize("N,M,use_perm", [(16, 4, False), (64, 16, True), (512, 128, True)])
+def test_psi_dct_operator_matches_dense_definition(N, M, use_perm):
+    """A = C_N[rows] R diag(sigma) C_N with explicit cosine matrices on the dense side."""
+    bits = draw_sign_bits(max(N, 32), rng(96, 0, N, 0))
+    rows = draw_rows(N, M, rng(96, 0, N, 1))
+    perm = draw_perm(N, rng(96, 0, N, 2)) if use_perm else None
+    op = SrmOperator(N, bits, rows, perm, psi="dct")
+    A = dense_srm(N, bits, rows, perm, psi="dct")
+    g = np.random.default_rng(N + 2)
+    for _ in range(3):
+        x, w = g.standard_normal(N), g.standard_normal(M)
+        np.testing.assert_allclose(op.apply(x), A @ x, atol=1e-12 * np.linalg.norm(x))
+        np.testing.assert_allclose(op.adjoint(w), A.T @ w, atol=1e-12 * np.linalg.norm(w))
+
+
+def test_psi_dct_columns_are_phi_of_dct_basis_vectors():
+    """x = Psi s: column j of A = Phi Psi is Phi applied to column j of C_N."""
+    N, M = 128, 32
+    bits = draw_sign_bits(N, rng(96, 1, N, 0))
+    rows = draw_rows(N, M, rng(96, 1, N, 1))
+    phi = SrmOperator(N, bits, rows)
+    A = SrmOperator(N, bits, rows, psi="dct")
+    C = dct_matrix(N)
+    for j in [0, 3, 64, N - 1]:
+        e = np.zeros(N)
+        e[j] = 1.0
+        np.testing.assert_allclose(A.apply(e), phi.apply(C[:, j]), atol=1e-13)
+
+
+def test_psi_dct_rows_orthonormal():
+    N, M = 1024, 256
+    op = SrmOperator(N, draw_sign_bits(N, rng(96, 2, N, 0)), draw_rows(N, M, rng(96, 2, N, 1)),
+                     draw_perm(N, rng(96, 2, N, 2)), psi="dct")
+    AAT = np.stack([op.apply(op.adjoint(e)) for e in np.eye(M)[:48]], axis=1)
+    np.testing.assert_allclose(AAT, np.eye(M)[:, :48], atol=1e-13)
