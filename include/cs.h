@@ -122,10 +122,28 @@ size_t cs_operator_meta_bytes_perm(int64_t N, int64_t M, int64_t batch);
 cs_status cs_operator_create_perm(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
                                   const int32_t* d_perm, const int32_t* d_rows, void* d_meta,
                                   size_t meta_bytes, cs_stream_t stream, cs_operator** out);
+
+/* Dictionary Psi of A = Phi Psi (x = Psi s).  The paper's experiments use a DCT
+ * ("Psi is chosen to be a discrete cosine transform"; R35): Psi = C_N,
+ * the orthonormal DCT-II, so A s = (C_N R (sigma . C_N s))[rows].  BASELINE.json fixes
+ * Psi = I. */
+typedef enum { CS_PSI_IDENTITY = 0, CS_PSI_DCT = 1 } cs_psi;
+
+/* General constructor: Phi = P C_N R diag(sigma) (d_sign_bits and/or d_perm as in
+ * cs_operator_create_perm; either may be NULL, not both) and the dictionary `psi`.
+ * d_meta: cs_operator_meta_bytes_perm bytes with d_perm, else cs_operator_meta_bytes.
+ * CS_PSI_DCT is built for N <= 16384 (the CTA tier): larger N returns CS_ERR_UNSUPPORTED
+ * here, and a recovery whose pursuit state does not fit one CTA's shared memory returns
+ * CS_ERR_UNSUPPORTED from cs_recover*.  With CS_PSI_DCT, apply/adjoint need a workspace of
+ * cs_operator_ws_bytes (batch * N elements).  Supports and values are in the s-domain. */
+cs_status cs_operator_create_ex(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
+                                const int32_t* d_perm, const int32_t* d_rows, int psi, void* d_meta,
+                                size_t meta_bytes, cs_stream_t stream, cs_operator** out);
 cs_status cs_operator_destroy(cs_operator* op);
 cs_status cs_operator_info(const cs_operator* op, int64_t* N, int64_t* M, int64_t* batch);
 
-/* Workspace bytes for apply/adjoint (0 for N <= 16384, else the four-step scratch). */
+/* Workspace bytes for apply/adjoint (0 for N <= 16384 — batch * N elements with
+ * CS_PSI_DCT — else the four-step scratch). */
 size_t cs_operator_ws_bytes(const cs_operator* op, int precision /*0 fp32, 1 fp64*/);
 
 /* y[b] = A_b x[b] for every instance b.  x [batch][N], y [batch][M]. */

@@ -56,7 +56,7 @@ EXPORTS = [
     "cs_recover_batched", "cs_recover_batched_f64", "cs_workspace_bytes_host", "cs_recover_batched_host",
     "cs_recover_batched_host_f64", "cs_status_string", "cs_last_error",
     "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
-    "cs_diag_topk", "cs_operator_meta_bytes_perm", "cs_operator_create_perm",
+    "cs_diag_topk", "cs_operator_meta_bytes_perm", "cs_operator_create_perm", "cs_operator_create_ex",
 ]
 
 
@@ -74,6 +74,7 @@ def load_library(path: str = LIB_PATH):
         "cs_operator_create": (I32, [I64, I64, I64, P, P, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_meta_bytes_perm": (SZ, [I64, I64, I64]),
         "cs_operator_create_perm": (I32, [I64, I64, I64, P, P, P, P, SZ, P, ctypes.POINTER(P)]),
+        "cs_operator_create_ex": (I32, [I64, I64, I64, P, P, P, ctypes.c_int, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_destroy": (I32, [P]),
         "cs_operator_info": (I32, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
         "cs_operator_ws_bytes": (SZ, [P, ctypes.c_int]),
@@ -147,15 +148,25 @@ class Operator:
     `perm` ([batch][N] int32 pi), the Eq.(7) operator P . DCT-II . R . diag(sigma)
     (cs_operator_create_perm; sign_bits may then be None for sigma = +1)."""
 
-    def __init__(self, N: int, M: int, sign_bits, rows, batch: int = 1, stream=None, perm=None):
+    def __init__(self, N: int, M: int, sign_bits, rows, batch: int = 1, stream=None, perm=None, psi=None):
         torch = _torch()
         L = load_library()
         self.N, self.M, self.batch = int(N), int(M), int(batch)
+        self.psi = psi
         dev = rows.device
         rw = rows.to(device=dev, dtype=torch.int32).contiguous()
         sb = None if sign_bits is None else sign_bits.to(device=dev).contiguous()
         h = ctypes.c_void_p()
-        if perm is None:
+        if psi is not None:
+            code = {"I": 0, "dct": 1}[psi]
+            pm = None if perm is None else perm.to(device=dev, dtype=torch.int32).contiguous()
+            nb = (L.cs_operator_meta_bytes_perm if pm is not None else L.cs_operator_meta_bytes)(N, M, batch)
+            self.meta = torch.empty(nb, dtype=torch.uint8, device=dev)
+            _check(L.cs_operator_create_ex(N, M, batch, _ptr(sb) if sb is not None else None,
+                                           _ptr(pm) if pm is not None else None, _ptr(rw), code,
+                                           _ptr(self.meta), nb, _stream(stream), ctypes.byref(h)),
+                   "cs_operator_create_ex")
+        elif perm is None:
             nb = L.cs_operator_meta_bytes(N, M, batch)
             self.meta = torch.empty(nb, dtype=torch.uint8, device=dev)
             _check(L.cs_operator_create(N, M, batch, _ptr(sb), _ptr(rw), _ptr(self.meta), nb,

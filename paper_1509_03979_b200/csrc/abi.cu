@@ -23,6 +23,7 @@ struct cs_operator {
   uint32_t* meta;   // device: [B][stride] (meta_stride)
   int* errflag;     // device int in the meta tail
   int32_t* perm;    // device: [B][pi N][pi^-1 N] after the meta tail (Eq.(7) randomizer), or null
+  int psi;          // dictionary Psi: 0 = I, 1 = C_N (R35)
   int device;
 };
 
@@ -196,6 +197,7 @@ OpMeta meta_of(const cs_operator* op) {
   m.stride = meta_stride(op->N, op->M);
   m.toff = meta_toff(op->N);
   m.perm = op->perm;
+  m.psi = op->psi;
   return m;
 }
 
@@ -217,8 +219,14 @@ cs_status apply_impl(const cs_operator* op, const T* x, T* y, void* ws, size_t w
   if (!op) return fail(CS_ERR_INVALID_ARG, "null operator");
   if (!x || !y) return fail(CS_ERR_INVALID_ARG, "null vector");
   if (cs_status s = check_device()) return s;
-  if (op->N <= TIER_S_MAX_N)
-    return s_apply_launch<T>(meta_of(op), op->B, x, y, adjoint, st, g_launches, g_last_error);
+  if (op->psi && op->N > TIER_S_MAX_N)
+    return fail(CS_ERR_UNSUPPORTED, "Psi = DCT operators are built for N <= 16384 (CTA tier) in this version");
+  if (op->N <= TIER_S_MAX_N) {
+    if (op->psi && (!ws || ws_bytes < (size_t)(op->B * op->N) * sizeof(T)))
+      return fail(CS_ERR_WORKSPACE, "workspace too small (Psi = DCT needs batch * N elements)");
+    return s_apply_launch<T>(meta_of(op), op->B, x, y, adjoint, reinterpret_cast<T*>(ws), st, g_launches,
+                             g_last_error);
+  }
   return tier_l_apply<T>(meta_of(op), op->B, x, y, ws, ws_bytes, st, adjoint, g_launches,
                          g_last_error);
 }
@@ -253,7 +261,10 @@ cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, in
   if (!ws || ws_bytes < need) return fail(CS_ERR_WORKSPACE, "workspace too small");
   Params P = make_params(alg, K, tol, opts);
   const int64_t ucap = ucap_of(alg, K, l);
-  if (tier_s_fits<T>(N, K, ucap, true)) {
+  const bool fits_s = tier_s_fits<T>(N, K, ucap, true);
+  if (op->psi && !fits_s)
+    return fail(CS_ERR_UNSUPPORTED, "Psi = DCT recovery runs on the CTA tier only (N <= 16384, pursuit in shared memory)");
+  if (fits_s) {
     SRecArgs<T> a;
     a.meta = meta_of(op);
     a.lay = s_layout<T>(N, K, (int)ucap, true);
@@ -349,8 +360,8 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
     sub.meta = op->meta + b0 * meta_stride(op->N, op->M);
     if (op->perm) sub.perm = op->perm + b0 * 2 * N;
     sub.B = cnt;
-    char* rws = tier_s ? w + (size_t)(b0 * N) * sizeof(T) : w;
-    const size_t rws_bytes = tier_s ? (size_t)(cnt * N) * sizeof(T) : need_rec;
+    char* rws = tier_s ? w + (size_t)(b0 * 2 * N) * sizeof(T) : w;
+    const size_t rws_bytes = tier_s ? (size_t)(cnt * 2 * N) * sizeof(T) : need_rec;
     if (cs_status s = recover_impl<T>(&sub, alg, dY + b0 * M, cnt, M, N, K, tol, opts, dvals + b0 * K,
                                       dsupp + b0 * K, dreps + b0, rws, rws_bytes, sc))
       return s;
@@ -381,8 +392,8 @@ size_t cs_operator_meta_bytes(int64_t N, int64_t M, int64_t batch) {
 }
 
 static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
-                             const int32_t* d_perm, const int32_t* d_rows, void* d_meta, size_t meta_bytes,
-                             cs_stream_t stream, cs_operator** out) {
+                             const int32_t* d_perm, const int32_t* d_rows, int psi, void* d_meta,
+                             size_t meta_bytes, cs_stream_t stream, cs_operator** out) {
   if (!out) return fail(CS_ERR_INVALID_ARG, "out is null");
   *out = nullptr;
   if (cs_status s = check_N(N)) return s;
@@ -432,6 +443,7 @@ static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t
   op->meta = meta;
   op->errflag = err;
   op->perm = perm;
+  op->psi = psi;
   CS_CUDA(cudaGetDevice(&op->device));
   *out = op;
   return CS_OK;
@@ -444,7 +456,7 @@ cs_status cs_operator_create(int64_t N, int64_t M, int64_t batch, const uint32_t
     if (out) *out = nullptr;
     return fail(CS_ERR_INVALID_ARG, "null pointer argument");
   }
-  return create_impl(N, M, batch, d_sign_bits, nullptr, d_rows, d_meta, meta_bytes, stream, out);
+  return create_impl(N, M, batch, d_sign_bits, nullptr, d_rows, 0, d_meta, meta_bytes, stream, out);
 }
 
 size_t cs_operator_meta_bytes_perm(int64_t N, int64_t M, int64_t batch) {
@@ -460,7 +472,18 @@ cs_status cs_operator_create_perm(int64_t N, int64_t M, int64_t batch, const uin
     if (out) *out = nullptr;
     return fail(CS_ERR_INVALID_ARG, "null pointer argument");
   }
-  return create_impl(N, M, batch, d_sign_bits, d_perm, d_rows, d_meta, meta_bytes, stream, out);
+  return create_impl(N, M, batch, d_sign_bits, d_perm, d_rows, 0, d_meta, meta_bytes, stream, out);
+}
+
+cs_status cs_operator_create_ex(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
+                                const int32_t* d_perm, const int32_t* d_rows, int psi, void* d_meta,
+                                size_t meta_bytes, cs_stream_t stream, cs_operator** out) {
+  if (out) *out = nullptr;
+  if (psi != CS_PSI_IDENTITY && psi != CS_PSI_DCT) return fail(CS_ERR_INVALID_ARG, "psi must be CS_PSI_IDENTITY or CS_PSI_DCT");
+  if (psi == CS_PSI_DCT && N > TIER_S_MAX_N)
+    return fail(CS_ERR_UNSUPPORTED, "Psi = DCT operators are built for N <= 16384 (CTA tier) in this version");
+  if (!d_sign_bits && !d_perm) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
+  return create_impl(N, M, batch, d_sign_bits, d_perm, d_rows, psi, d_meta, meta_bytes, stream, out);
 }
 
 cs_status cs_operator_destroy(cs_operator* op) {
@@ -477,6 +500,7 @@ cs_status cs_operator_info(const cs_operator* op, int64_t* N, int64_t* M, int64_
 }
 
 size_t cs_operator_ws_bytes(const cs_operator* op, int precision) {
+  if (op && op->psi && op->N <= TIER_S_MAX_N) return (size_t)(op->B * op->N) * (precision ? 8 : 4);
   if (!op || op->N <= TIER_S_MAX_N) return 0;
   return precision ? tier_l_apply_ws_bytes<double>(op->N, op->M) : tier_l_apply_ws_bytes<float>(op->N, op->M);
 }
@@ -508,7 +532,7 @@ cs_status cs_workspace_bytes(int alg, int64_t N, int64_t M, int32_t K, int64_t b
   const bool dbl = precision != 0;
   bool s = dbl ? tier_s_fits<double>(N, K, ucap, true) : tier_s_fits<float>(N, K, ucap, true);
   if (s) {
-    *bytes = (size_t)(batch * N * (dbl ? 8 : 4));
+    *bytes = (size_t)(batch * 2 * N * (dbl ? 8 : 4));   // A^T y and the Psi-mode scratch per problem
   } else {
     *bytes = dbl ? tier_l_recover_ws_bytes<double>(N, M, K, (int)ucap)
                  : tier_l_recover_ws_bytes<float>(N, M, K, (int)ucap);

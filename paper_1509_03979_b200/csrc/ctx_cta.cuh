@@ -56,6 +56,15 @@ template <typename T> struct CtaCtx {
   const int* in_supp;
   int in_ns;
   int applies;
+  // dictionary Psi = C_N (R35): A = Phi Psi.  The pursuit's index space is the s-domain
+  // (no sign, no permutation: `sign` holds zeros, pm/pinv are null); Phi's sign bits,
+  // pi^-1 and row mask are read from the instance metadata by the Psi-mode helpers.
+  int psi;                   // 0: Psi = I, 1: Psi = C_N
+  T* G;                      // global [N] scratch of this problem (Psi mode)
+  const uint32_t* phi_sign;  // global
+  const int32_t* phi_pinv;   // global, or null
+  const uint32_t* g_rmask;   // global natural-order row mask / prefix of the instance
+  const int32_t* g_prefix;
 
   CS_DEV void sync() { __syncthreads(); }
   CS_DEV void mark(int) {}  // phase accounting is a grid-context diagnostic
@@ -215,7 +224,7 @@ template <typename T> struct CtaCtx {
     while (true) {
       if (!(rr > thr)) break;                                              // line 15 (R6, R7)
       if (j >= cap) { status |= CS_DEV_CG_CAP; break; }
-      sw_body<T, LOG2L, MID_H, false>(nullptr, TwTable<T>{}, TwTable<T>{}, m0,
+      sw_body<T, LOG2L, MID_H, false, false>(nullptr, TwTable<T>{}, TwTable<T>{}, m0,
                                       SwIO<T>{sp, n, nullptr, dv, qv});    // q = H d_j
       double dq = 0;
       for (int i = threadIdx.x; i < n; i += NT) dq += (double)dv[i] * (double)qv[i];
@@ -248,18 +257,115 @@ template <typename T> struct CtaCtx {
       cg_dispatch<LO + 1, HI>(s);
     }
   }
-  template <class S> CS_DEV void cg_iterate(S& s) { cg_dispatch<2, 13>(s); }
+  template <class S> CS_DEV void cg_iterate(S& s) {
+    if (psi | (pinv != nullptr)) { cg_iterate_generic(s); return; }
+    cg_dispatch<2, 13>(s);  // the hot loop: sandwich inlined, no permutation
+  }
+  // Psi = DCT or the Eq.(7) permutation: the generic CG loop around the out-of-line
+  // sandwiches (kept out of line so the plain path's caller stays small)
+  template <class S> CS_NOINL void cg_iterate_generic(S& s) {
+    if (psi) {
+      cg_loop(*this, s, [this](const T* d, T* q) { H_psi(d, q); });
+      return;
+    }
+    cg_loop(*this, s, [this](const T* d, T* q) {
+      sandwich<MID_H, false>(d, q, nullptr);
+      ++applies;
+    });
+  }
   // q = (A^T A scatter_S(d))[S] on the remembered support S (cg2)
   CS_DEV void H(const T* d, T* q) {
+    if (psi) { H_psi(d, q); return; }
     sandwich<MID_H, false>(d, q, nullptr);
     ++applies;
   }
   // c = A^T (y - A scatter_S(x)) into the buffer (b1 + cg5); returns ||y - A x||^2.
   // x == nullptr means x = 0 (c = A^T y).
   CS_NOINL double RES(const T* x) {
+    if (psi) return RES_psi(x);
     const double rn2 = x ? sandwich<MID_RES, false>(x, nullptr, nullptr) : sandwich<MID_RES, true>(nullptr, nullptr, nullptr);
     ++applies;
     return sum(rn2);
+  }
+
+  // ---- Psi = C_N (R35): every A / A^T is C_N, Phi, and C_N^T composed from the same
+  // sandwich kernels.  A full DCT-II (all N outputs) is the forward sandwich with every
+  // row selected (rank(k) = k), and C_N^T of a dense vector is the adjoint sandwich with
+  // every row selected; the Eq.(7) permutation and the signs sit between them, moved
+  // through the problem's global scratch G (natural order).
+  CS_NOINL void mask_full() {
+    const int64_t nw = (N + 31) >> 5;
+    const uint32_t last = (N & 31) ? ((1u << (N & 31)) - 1u) : ~0u;
+    for (int64_t w = gtid; w < nw; w += gnthr) {
+      rowmask[w] = (w == nw - 1) ? last : ~0u;
+      prefix[w] = (int32_t)(32 * w);
+    }
+    __syncthreads();
+  }
+  CS_NOINL void mask_real() {
+    const int64_t nw = (N + 31) >> 5;
+    for (int64_t w = gtid; w < nw; w += gnthr) {
+      rowmask[w] = g_rmask[w];
+      prefix[w] = g_prefix[w];
+    }
+    __syncthreads();
+  }
+  // Z <- Makhoul order of u = R diag(sigma) G: u_{pi^-1(j)} = sigma_j G_j
+  CS_NOINL void phi_in() {
+    T* zb = reinterpret_cast<T*>(Z);
+    for (int64_t j = gtid; j < N; j += gnthr)
+      zb[zt(ppos(phi_pinv, j, N))] = apply_sign<T>(phi_sign, j, G[j]);
+    __syncthreads();
+  }
+  // G <- diag(sigma) R^T v, v in Makhoul order in Z: G_j = sigma_j v_{pi^-1(j)}
+  CS_NOINL void phi_out() {
+    const T* zb = zbuf();
+    for (int64_t j = gtid; j < N; j += gnthr) G[j] = apply_sign<T>(phi_sign, j, zb[zt(ppos(phi_pinv, j, N))]);
+    __syncthreads();
+  }
+  // G <- C_N s, s = scatter_S(vin) (vin == nullptr: s already in Z, Makhoul order)
+  CS_NOINL void psi_to_G(const T* vin) {
+    mask_full();
+    sandwich<MID_FWD, false>(vin, nullptr, G);
+    __syncthreads();
+  }
+  // Z <- C_N^T G (Makhoul order)
+  CS_NOINL void psiT_from_G() {
+    mask_full();
+    const T* ys = y;
+    y = G;
+    sandwich<MID_RES, true>(nullptr, nullptr, nullptr);
+    y = ys;
+    __syncthreads();
+  }
+  CS_NOINL void H_psi(const T* d, T* q) {
+    psi_to_G(d);                                        // C_N s
+    mask_real();
+    phi_in();                                           // R diag(sigma)
+    sandwich<MID_H, false>(nullptr, nullptr, nullptr);  // C^T P^T P C
+    phi_out();                                          // diag(sigma) R^T
+    psiT_from_G();                                      // C_N^T
+    const T* zb = zbuf();
+    for (int i = gtid; i < in_ns; i += gnthr) q[i] = zb[zt((int)mk_pos(in_supp[i], N))];
+    __syncthreads();
+    ++applies;
+  }
+  CS_NOINL double RES_psi(const T* x) {
+    double rn2;
+    if (x) {
+      psi_to_G(x);
+      mask_real();
+      phi_in();
+      rn2 = sandwich<MID_RES, false>(nullptr, nullptr, nullptr);   // Phi^T (y - Phi u)
+    } else {
+      mask_real();
+      rn2 = sandwich<MID_RES, true>(nullptr, nullptr, nullptr);    // Phi^T y
+    }
+    rn2 = sum(rn2);
+    phi_out();
+    psiT_from_G();                                                 // A^T r, s-domain
+    ++applies;
+    return rn2;
   }
 };
 

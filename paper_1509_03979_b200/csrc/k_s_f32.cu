@@ -3,7 +3,7 @@
 #include "tier_s.cuh"
 
 namespace cs {
-template cs_status s_apply_launch<float>(const OpMeta&, int64_t, const float*, float*, bool, cudaStream_t,
+template cs_status s_apply_launch<float>(const OpMeta&, int64_t, const float*, float*, bool, float*, cudaStream_t,
                                        std::atomic<uint64_t>&, std::string&);
 template cs_status s_recover_launch<float>(const SRecArgs<float>&, int64_t, cudaStream_t, std::atomic<uint64_t>&,
                                          std::string&);

@@ -3,7 +3,7 @@
 #include "tier_s.cuh"
 
 namespace cs {
-template cs_status s_apply_launch<double>(const OpMeta&, int64_t, const double*, double*, bool, cudaStream_t,
+template cs_status s_apply_launch<double>(const OpMeta&, int64_t, const double*, double*, bool, double*, cudaStream_t,
                                        std::atomic<uint64_t>&, std::string&);
 template cs_status s_recover_launch<double>(const SRecArgs<double>&, int64_t, cudaStream_t, std::atomic<uint64_t>&,
                                          std::string&);

@@ -18,6 +18,8 @@
 #include "cs_common.cuh"
 #include "select.cuh"
 
+#include <type_traits>
+
 namespace cs {
 
 template <typename T> struct Bufs {
@@ -160,17 +162,22 @@ CS_NOINL void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* o
     const int n = (int)N, L = n / 2;
     const C2<T>* zs = reinterpret_cast<const C2<T>*>(cv.z);
     const int32_t* pm = ctx.pm;   // Eq.(7) randomizer: position i holds index pi(i) (R34)
-    auto visit = [&](auto&& f) {
-      for (int q = threadIdx.x; q < L; q += blockDim.x) {
-        const C2<T> z = zs[swz<T>(q)];
-        int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;        // mk_nat(2q)
-        int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;  // mk_nat(2q+1)
-        if (pm) { j0 = pm[j0]; j1 = pm[j1]; }
-        f(j0, (excl && bit_test(excl, j0)) ? Key(0) : full_key(z.x));
-        f(j1, (excl && bit_test(excl, j1)) ? Key(0) : full_key(z.y));
-      }
+    // the permuted and the plain visitor are separate instances (no per-element branch)
+    auto run = [&](auto has_pm) -> bool {
+      constexpr bool HP = decltype(has_pm)::value;
+      auto visit = [&](auto&& f) {
+        for (int q = threadIdx.x; q < L; q += blockDim.x) {
+          const C2<T> z = zs[swz<T>(q)];
+          int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;        // mk_nat(2q)
+          int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;  // mk_nat(2q+1)
+          if constexpr (HP) { j0 = pm[j0]; j1 = pm[j1]; }
+          f(j0, (excl && bit_test(excl, j0)) ? Key(0) : full_key(z.x));
+          f(j1, (excl && bit_test(excl, j1)) ? Key(0) : full_key(z.y));
+        }
+      };
+      return topk_cta_fast_v<Ctx, Key>(ctx, n, (int)K, visit, out);
     };
-    if (topk_cta_fast_v<Ctx, Key>(ctx, n, (int)K, visit, out)) return;
+    if (pm ? run(std::true_type{}) : run(std::false_type{})) return;
   }
   if constexpr (!Ctx::kTopkFast) {
     // grid: materialise the keys once in natural index order (the dense input buffer U
@@ -206,14 +213,18 @@ CS_NOINL int64_t detect_argmax(Ctx& ctx, const uint32_t* excl) {
       if (k > bk || (k == bk && k != 0 && j < bi)) { bk = k; bi = j; }
     };
     const int32_t* pm = ctx.pm;
-    for (int q = threadIdx.x; q < L; q += blockDim.x) {
-      const C2<T> z = zs[swz<T>(q)];
-      int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;
-      int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;
-      if (pm) { j0 = pm[j0]; j1 = pm[j1]; }
-      take(j0, bit_test(excl, j0) ? Key(0) : full_key(z.x));
-      take(j1, bit_test(excl, j1) ? Key(0) : full_key(z.y));
-    }
+    auto scan = [&](auto has_pm) {
+      constexpr bool HP = decltype(has_pm)::value;
+      for (int q = threadIdx.x; q < L; q += blockDim.x) {
+        const C2<T> z = zs[swz<T>(q)];
+        int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;
+        int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;
+        if constexpr (HP) { j0 = pm[j0]; j1 = pm[j1]; }
+        take(j0, bit_test(excl, j0) ? Key(0) : full_key(z.x));
+        take(j1, bit_test(excl, j1) ? Key(0) : full_key(z.y));
+      }
+    };
+    if (pm) scan(std::true_type{}); else scan(std::false_type{});
     return ctx.argmax(bk, bi);
   }
   return argmax_key(ctx, N, [cv, excl](int64_t j) {

@@ -191,7 +191,9 @@ template <typename T> struct SwIO {
   T* vout;
 };
 
-template <typename T, int LOG2L, int MODE, bool ZERO>
+// PERM = false: the caller guarantees no Eq.(7) permutation (the CG loop of a plain
+// operator), so the scatter / gather carry no pi^-1 lookup.
+template <typename T, int LOG2L, int MODE, bool ZERO, bool PERM = true>
 CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4, const MidCtx<T>& gm,
                       const SwIO<T>& gio) {
   using SP = SwPlan<LOG2L>;
@@ -220,10 +222,10 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
       for (int i = tid; i < L; i += SW_NT) buf[i] = mk<T>(0, 0);
       __syncthreads();
       // Eq.(7) randomizer pi^-1 (R34), parked in shared memory by make_cta_ctx
-      const int32_t* pv = *reinterpret_cast<const int32_t* const*>(cs_smem_base + F.zero + 8);
+      const int32_t* pv = PERM ? *reinterpret_cast<const int32_t* const*>(cs_smem_base + F.zero + 8) : nullptr;
       for (int i = tid; i < gio.ns; i += SW_NT) {
         const int j = supp[i];
-        zb[zt((int)mk_pos(pv ? pv[j] : j, N))] = apply_sign<T>(sign, j, vin[i]);
+        zb[zt((int)mk_pos((PERM && pv) ? pv[j] : j, N))] = apply_sign<T>(sign, j, vin[i]);
       }
       __syncthreads();
     }
@@ -240,10 +242,10 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
       const int* supp = shp(gio.supp);
       const uint32_t* sign = signs;
       T* vout = shp(gio.vout);
-      const int32_t* pv = *reinterpret_cast<const int32_t* const*>(cs_smem_base + F.zero + 8);
+      const int32_t* pv = PERM ? *reinterpret_cast<const int32_t* const*>(cs_smem_base + F.zero + 8) : nullptr;
       for (int i = tid; i < gio.ns; i += SW_NT) {
         const int j = supp[i];
-        vout[i] = apply_sign<T>(sign, j, zb[zt((int)mk_pos(pv ? pv[j] : j, N))]);
+        vout[i] = apply_sign<T>(sign, j, zb[zt((int)mk_pos((PERM && pv) ? pv[j] : j, N))]);
       }
       __syncthreads();
     }

@@ -70,6 +70,7 @@ struct OpMeta {
   int64_t stride;  // words per instance
   int64_t toff;    // word offset of the transposed mask within an instance
   const int32_t* perm;  // Eq.(7) randomizer R (R34): per instance [pi N][pi^-1 N], or null
+  int psi;              // dictionary: 0 = I, 1 = C_N (R35)
   CS_HD const uint32_t* sign(int64_t b) const { return base + b * stride; }
   CS_HD const uint32_t* rmask(int64_t b) const { return base + b * stride + nw; }
   CS_HD const int32_t* prefix(int64_t b) const {
@@ -117,8 +118,15 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   c.cidx = reinterpret_cast<int*>(smem + lay.cidx);
   c.ccnt = reinterpret_cast<int*>(smem + lay.ccnt);
   c.rbank = 0;
-  c.pm = meta.pm(b);
-  c.pinv = meta.pinv(b);
+  c.psi = meta.psi;
+  c.G = nullptr;
+  c.phi_sign = meta.sign(b);
+  c.phi_pinv = meta.pinv(b);
+  c.g_rmask = meta.rmask(b);
+  c.g_prefix = meta.prefix(b);
+  // Psi mode: the pursuit's index space is the s-domain (no sign, no permutation)
+  c.pm = meta.psi ? nullptr : meta.pm(b);
+  c.pinv = meta.psi ? nullptr : meta.pinv(b);
   if (threadIdx.x == 0) {
     *reinterpret_cast<int*>(smem + s_fixed<T>(meta.N).zero) = 0;
     *reinterpret_cast<const int32_t**>(smem + s_fixed<T>(meta.N).zero + 8) = c.pinv;  // sandwich_cta.cuh
@@ -136,7 +144,7 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   const uint32_t* gm = meta.rmask(b);
   const int32_t* gp = meta.prefix(b);
   for (int64_t w = c.gtid; w < nw; w += c.gnthr) {
-    c.sign[w] = gs[w];
+    c.sign[w] = meta.psi ? 0u : gs[w];
     c.rowmask[w] = gm[w];
     c.prefix[w] = gp[w];
   }
@@ -145,14 +153,33 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
 }
 
 // ---------------------------------------------------------------- kernels ---
+// A x = Phi (C_N x) (R35): dense x into Z, full DCT-II to G, then Phi.  Out of line so the
+// plain apply keeps its register allocation.
+template <typename T>
+CS_NOINL void s_apply_psi(CtaCtx<T>& c, const T* x, T* y, T* G) {
+  const int64_t N = c.N;
+  c.G = G;
+  T* zb = reinterpret_cast<T*>(c.Z);
+  for (int j = c.gtid; j < (int)N; j += c.gnthr) zb[CtaCtx<T>::zt((int)mk_pos(j, N))] = x[j];
+  __syncthreads();
+  c.psi_to_G(nullptr);
+  c.mask_real();
+  c.phi_in();
+  c.template sandwich<MID_FWD, false>(nullptr, nullptr, y);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout lay, const T* __restrict__ X,
-                                                 T* __restrict__ Y) {
+                                                 T* __restrict__ Y, T* __restrict__ Gws) {
   extern __shared__ __align__(16) char smem[];
   const int64_t b = blockIdx.x;
   CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, b);
   const int64_t N = c.N;
   const T* x = X + b * N;
+  if (c.psi) {
+    s_apply_psi<T>(c, x, Y + b * c.M, Gws + b * N);
+    return;
+  }
   if (c.pinv) {
     // Eq.(7) randomizer: x_j lands at the Makhoul position of pi^-1(j) (R34)
     T* zb = reinterpret_cast<T*>(c.Z);
@@ -197,11 +224,12 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout 
 
 template <typename T>
 __global__ void __launch_bounds__(TS_THREADS, 2) k_s_adjoint(OpMeta meta, SLayout lay, const T* __restrict__ Yin,
-                                                   T* __restrict__ X) {
+                                                   T* __restrict__ X, T* __restrict__ Gws) {
   extern __shared__ __align__(16) char smem[];
   const int64_t b = blockIdx.x;
   CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, b);
   c.y = Yin + b * c.M;
+  if (c.psi) c.G = Gws + b * c.N;
   c.RES(nullptr);  // A^T y (x = 0)
   const int64_t N = c.N;
   T* x = X + b * N;
@@ -217,7 +245,7 @@ template <typename T> struct SRecArgs {
   T* vals;
   int32_t* supp;
   cs_report* reps;
-  T* c0ws;  // [B][N]
+  T* c0ws;  // [B][2][N]: A^T y (Makhoul order), then the Psi-mode scratch G
 };
 
 template <typename T>
@@ -226,7 +254,8 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_recover(SRecArgs<T> a) {
   const int64_t b = blockIdx.x;
   CtaCtx<T> c = make_cta_ctx<T>(smem, a.lay, a.meta, b);
   c.y = a.Y + b * c.M;
-  c.c0 = a.c0ws + b * c.N;
+  c.c0 = a.c0ws + b * 2 * c.N;
+  c.G = c.c0 + c.N;
   // non-finite y check
   int bad = 0;
   for (int64_t m = c.gtid; m < c.M; m += c.gnthr) bad |= !isfinite((double)c.y[m]);
@@ -282,7 +311,7 @@ template <typename T>
 cs_status s_diag_topk_launch(const T* vals, int n, int K, int mode, uint32_t* out, cudaStream_t st,
                              std::atomic<uint64_t>& launches, std::string& err);
 template <typename T>
-cs_status s_apply_launch(const OpMeta& m, int64_t B, const T* in, T* out, bool adjoint, cudaStream_t st,
+cs_status s_apply_launch(const OpMeta& m, int64_t B, const T* in, T* out, bool adjoint, T* gws, cudaStream_t st,
                          std::atomic<uint64_t>& launches, std::string& err);
 template <typename T>
 cs_status s_recover_launch(const SRecArgs<T>& a, int64_t B, cudaStream_t st, std::atomic<uint64_t>& launches,
@@ -303,13 +332,13 @@ inline cs_status s_launched(std::atomic<uint64_t>& launches, std::string& err) {
   return CS_OK;
 }
 template <typename T>
-cs_status s_apply_launch(const OpMeta& m, int64_t B, const T* in, T* out, bool adjoint, cudaStream_t st,
+cs_status s_apply_launch(const OpMeta& m, int64_t B, const T* in, T* out, bool adjoint, T* gws, cudaStream_t st,
                          std::atomic<uint64_t>& launches, std::string& err) {
   SLayout lay = s_layout<T>(m.N, 0, 0, false);
   const void* fn = adjoint ? (const void*)k_s_adjoint<T> : (const void*)k_s_apply<T>;
   if (cs_status s = s_attr(fn, lay.bytes, err)) return s;
-  if (adjoint) k_s_adjoint<T><<<(unsigned)B, lay.nthreads, lay.bytes, st>>>(m, lay, in, out);
-  else k_s_apply<T><<<(unsigned)B, lay.nthreads, lay.bytes, st>>>(m, lay, in, out);
+  if (adjoint) k_s_adjoint<T><<<(unsigned)B, lay.nthreads, lay.bytes, st>>>(m, lay, in, out, gws);
+  else k_s_apply<T><<<(unsigned)B, lay.nthreads, lay.bytes, st>>>(m, lay, in, out, gws);
   return s_launched(launches, err);
 }
 template <typename T>

@@ -65,9 +65,18 @@ def test_host_validation_codes(lib):
     h = ctypes.c_void_p()
     assert lib.cs_operator_create(1024, 256, 1, None, None, None, 0, None, ctypes.byref(h)) == 1
     assert lib.cs_operator_create(1024, 2048, 1, None, None, None, 0, None, ctypes.byref(h)) == 1
-    # workspace sizes: Tier S = B*N*sizeof(T); Tier L larger than the dense scratch
+    # workspace sizes: Tier S = B*2N*sizeof(T) (A^T y + the Psi = DCT scratch); Tier L
+    # larger than the dense scratch
     assert lib.cs_workspace_bytes(1, 16384, 4096, 256, 4096, 0, None, ctypes.byref(n)) == 0
-    assert n.value == 4096 * 16384 * 4
+    assert n.value == 4096 * 2 * 16384 * 4
     assert lib.cs_workspace_bytes(1, 1 << 24, 1 << 22, 65536, 1, 0, None, ctypes.byref(n)) == 0
     assert n.value >= 4 * (1 << 24) * 4
     assert cs.REPORT_DTYPE.itemsize == 40
+
+
+def test_create_ex_rejects_bad_psi_and_large_n(lib):
+    """cs_operator_create_ex argument checks that run before any device work."""
+    h = ctypes.c_void_p()
+    assert lib.cs_operator_create_ex(1024, 256, 1, None, None, None, 7, None, 0, None, ctypes.byref(h)) == 1
+    assert lib.cs_operator_create_ex(1 << 15, 1 << 13, 1, None, None, None, 1, None, 0, None, ctypes.byref(h)) == 2
+    assert lib.cs_operator_create_ex(1024, 256, 1, None, None, None, 1, None, 0, None, ctypes.byref(h)) == 1
