@@ -49,6 +49,8 @@ def parse():
                     help="run the config's workload with another pursuit (not a BASELINE line)")
     ap.add_argument("--randomizer", choices=["sign", "perm"], default="sign",
                     help="perm: the paper's literal Eq.(7) D F R operator (R34; not a BASELINE line)")
+    ap.add_argument("--psi", choices=["I", "dct"], default="I",
+                    help="dct: A = Phi C_N, the paper's experimental dictionary (R35; not a BASELINE line)")
     ap.add_argument("--no-op-bench", action="store_true")
     return ap.parse_args()
 
@@ -59,14 +61,18 @@ def select_config(args):
         cfg = dataclasses.replace(cfg, alg=args.alg)
     if args.randomizer != cfg.randomizer:
         cfg = dataclasses.replace(cfg, randomizer=args.randomizer)
+    if args.psi != cfg.psi:
+        cfg = dataclasses.replace(cfg, psi=args.psi)
     return cfg
 
 
 def workload_desc(cfg):
     base = cs_inputs.CONFIGS[cfg.cid]
-    if cfg.alg != base.alg or cfg.randomizer != base.randomizer:
+    if cfg.alg != base.alg or cfg.randomizer != base.randomizer or cfg.psi != base.psi:
         names = {"omp": "OMP", "sp": "SP", "ompr": "OMPR(1)", "cosamp": "CoSaMP"}
         op = "D.F.R (Eq.(7) permutation randomizer)" if cfg.randomizer == "perm" else "P.DCT.diag(sigma)"
+        if cfg.psi == "dct":
+            op += " x Psi = DCT"
         return (f"c{cfg.cid}-shape with {names[cfg.alg]}+CG on {op} (override): "
                 f"N={cfg.N}, M={cfg.M}, K={cfg.K}")
     return {1: "c1: OMP+CG, N=4096, M=1024, K=64, noiseless",
@@ -174,7 +180,7 @@ def run_ours(args):
     perm = None
     if cfg.randomizer == "perm":
         perm = torch.from_numpy(np.stack([p.perm for p in probs]).astype(np.int32)).to(dev)
-    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=B, perm=perm)
+    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=B, perm=perm, psi=("dct" if cfg.psi == "dct" else None))
     Y = (cs.cs_operator_apply(A, S) + E).to(torch.float32).to(td)  # fp32-rounded y (R21)
     del S, E
     torch.cuda.synchronize()
@@ -307,8 +313,9 @@ def run_ours(args):
         meta_b = B * (3 * ((cfg.N + 31) // 32) * 4 + (cfg.M * 4 if cfg.N > 16384 else 0))
         if cfg.randomizer == "perm":
             meta_b += B * cfg.N * 4     # pi^-1 gathered once per apply / adjoint
-        bytes_fwd = B * (cfg.N + cfg.M) * es + meta_b
-        bytes_adj = B * (cfg.N + cfg.M) * es + meta_b
+        psi_b = B * 2 * cfg.N * es if cfg.psi == "dct" else 0   # scratch write + read
+        bytes_fwd = B * (cfg.N + cfg.M) * es + meta_b + psi_b
+        bytes_adj = B * (cfg.N + cfg.M) * es + meta_b + psi_b
         peaks = load_peaks()
         op_stats = {"applies_per_s_fwd": B / t_fwd, "applies_per_s_adj": B / t_adj,
                     "fwd_GBs": bytes_fwd / t_fwd / 1e9, "adj_GBs": bytes_adj / t_adj / 1e9,
@@ -326,7 +333,8 @@ def run_ours(args):
         # FP32-ALU bound: nominal DCT flops 2.5 N log2 N per transform, 2 per sandwich,
         # sandwiches counted on the device (cs_report.applies); peak = 148 SM x 128 FP32
         # lanes x 2 flop x sm_max_mhz (fp64: the fp64 pipe is half rate on B200)
-        nominal_flops_per_apply = 5.0 * cfg.N * np.log2(cfg.N)
+        # Psi = DCT: four transforms per sandwich (C_N, Phi's two, C_N^T)
+        nominal_flops_per_apply = (10.0 if cfg.psi == "dct" else 5.0) * cfg.N * np.log2(cfg.N)
         flops_step = applies * nominal_flops_per_apply
         achieved = flops_step / (kms / 1e3) / 1e12
         peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12 / (1 if es == 4 else 2)
@@ -350,7 +358,7 @@ def run_ours(args):
     if os.path.exists(tr):
         try:
             key = f"c{cfg.cid}_{args.precision}" + ("" if cfg.alg == cs_inputs.CONFIGS[cfg.cid].alg else f"_{cfg.alg}") \
-                + ("" if cfg.randomizer == "sign" else f"_{cfg.randomizer}")
+                + ("" if cfg.randomizer == "sign" else f"_{cfg.randomizer}") + ("" if cfg.psi == "I" else "_psi")
             roofline["traffic"] = json.load(open(tr)).get(key)
         except Exception:
             pass
