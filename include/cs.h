@@ -131,11 +131,11 @@ typedef enum { CS_PSI_IDENTITY = 0, CS_PSI_DCT = 1 } cs_psi;
 
 /* General constructor: Phi = P C_N R diag(sigma) (d_sign_bits and/or d_perm as in
  * cs_operator_create_perm; either may be NULL, not both) and the dictionary `psi`.
- * d_meta: cs_operator_meta_bytes_perm bytes with d_perm, else cs_operator_meta_bytes.
- * CS_PSI_DCT is built for N <= 16384 (the CTA tier): larger N returns CS_ERR_UNSUPPORTED
- * here, and a recovery whose pursuit state does not fit one CTA's shared memory returns
- * CS_ERR_UNSUPPORTED from cs_recover*.  With CS_PSI_DCT, apply/adjoint need a workspace of
- * cs_operator_ws_bytes (batch * N elements).  Supports and values are in the s-domain. */
+ * d_meta: cs_operator_meta_bytes_ex(N, M, batch, d_perm != NULL, psi) bytes (CS_PSI_DCT adds
+ * one all-rows metadata instance, about 4.4 N bytes, shared by the batch).  With CS_PSI_DCT,
+ * apply/adjoint need the workspace cs_operator_ws_bytes reports.  Supports and values are in
+ * the s-domain. */
+size_t cs_operator_meta_bytes_ex(int64_t N, int64_t M, int64_t batch, int has_perm, int psi);
 cs_status cs_operator_create_ex(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
                                 const int32_t* d_perm, const int32_t* d_rows, int psi, void* d_meta,
                                 size_t meta_bytes, cs_stream_t stream, cs_operator** out);

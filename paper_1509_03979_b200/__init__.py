@@ -57,6 +57,7 @@ EXPORTS = [
     "cs_recover_batched_host_f64", "cs_status_string", "cs_last_error",
     "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
     "cs_diag_topk", "cs_operator_meta_bytes_perm", "cs_operator_create_perm", "cs_operator_create_ex",
+    "cs_operator_meta_bytes_ex",
 ]
 
 
@@ -74,6 +75,7 @@ def load_library(path: str = LIB_PATH):
         "cs_operator_create": (I32, [I64, I64, I64, P, P, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_meta_bytes_perm": (SZ, [I64, I64, I64]),
         "cs_operator_create_perm": (I32, [I64, I64, I64, P, P, P, P, SZ, P, ctypes.POINTER(P)]),
+        "cs_operator_meta_bytes_ex": (SZ, [I64, I64, I64, ctypes.c_int, ctypes.c_int]),
         "cs_operator_create_ex": (I32, [I64, I64, I64, P, P, P, ctypes.c_int, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_destroy": (I32, [P]),
         "cs_operator_info": (I32, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
@@ -160,7 +162,7 @@ class Operator:
         if psi is not None:
             code = {"I": 0, "dct": 1}[psi]
             pm = None if perm is None else perm.to(device=dev, dtype=torch.int32).contiguous()
-            nb = (L.cs_operator_meta_bytes_perm if pm is not None else L.cs_operator_meta_bytes)(N, M, batch)
+            nb = L.cs_operator_meta_bytes_ex(N, M, batch, int(pm is not None), code)
             self.meta = torch.empty(nb, dtype=torch.uint8, device=dev)
             _check(L.cs_operator_create_ex(N, M, batch, _ptr(sb) if sb is not None else None,
                                            _ptr(pm) if pm is not None else None, _ptr(rw), code,

@@ -24,6 +24,7 @@ struct cs_operator {
   int* errflag;     // device int in the meta tail
   int32_t* perm;    // device: [B][pi N][pi^-1 N] after the meta tail (Eq.(7) randomizer), or null
   int psi;          // dictionary Psi: 0 = I, 1 = C_N (R35)
+  uint32_t* full;   // Psi mode: one all-rows instance (stride meta_stride(N, N)), or null
   int device;
 };
 
@@ -125,6 +126,11 @@ __global__ void k_perm_setup(int64_t N, int64_t B, const int32_t* pin, int32_t* 
   if (atomicExch(&perm[b * 2 * N + N + v], (int32_t)k) != -1) atomicOr(err, 2);
 }
 
+__global__ void k_iota(int64_t n, int32_t* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (int32_t)i;
+}
+
 // Tier L: tperm[rank of row m in the transposed order] = m
 __global__ void k_rows_tperm(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t stride, int64_t toff, TPos tp,
                              const int32_t* rows, uint32_t* meta) {
@@ -198,6 +204,7 @@ OpMeta meta_of(const cs_operator* op) {
   m.toff = meta_toff(op->N);
   m.perm = op->perm;
   m.psi = op->psi;
+  m.full = op->full;
   return m;
 }
 
@@ -219,8 +226,6 @@ cs_status apply_impl(const cs_operator* op, const T* x, T* y, void* ws, size_t w
   if (!op) return fail(CS_ERR_INVALID_ARG, "null operator");
   if (!x || !y) return fail(CS_ERR_INVALID_ARG, "null vector");
   if (cs_status s = check_device()) return s;
-  if (op->psi && op->N > TIER_S_MAX_N)
-    return fail(CS_ERR_UNSUPPORTED, "Psi = DCT operators are built for N <= 16384 (CTA tier) in this version");
   if (op->N <= TIER_S_MAX_N) {
     if (op->psi && (!ws || ws_bytes < (size_t)(op->B * op->N) * sizeof(T)))
       return fail(CS_ERR_WORKSPACE, "workspace too small (Psi = DCT needs batch * N elements)");
@@ -262,8 +267,6 @@ cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, in
   Params P = make_params(alg, K, tol, opts);
   const int64_t ucap = ucap_of(alg, K, l);
   const bool fits_s = tier_s_fits<T>(N, K, ucap, true);
-  if (op->psi && !fits_s)
-    return fail(CS_ERR_UNSUPPORTED, "Psi = DCT recovery runs on the CTA tier only (N <= 16384, pursuit in shared memory)");
   if (fits_s) {
     SRecArgs<T> a;
     a.meta = meta_of(op);
@@ -391,6 +394,15 @@ size_t cs_operator_meta_bytes(int64_t N, int64_t M, int64_t batch) {
   return (size_t)(align_up(batch * meta_stride(N, M) * 4, 256) + 256);
 }
 
+size_t cs_operator_meta_bytes_ex(int64_t N, int64_t M, int64_t batch, int has_perm, int psi) {
+  const size_t base = cs_operator_meta_bytes(N, M, batch);
+  if (!base) return 0;
+  size_t b = base;
+  if (has_perm) b += (size_t)align_up(batch * 2 * N * 4, 256);
+  if (psi) b += (size_t)align_up(meta_stride(N, N) * 4, 256) + (size_t)align_up(N * 4, 256);
+  return b;
+}
+
 static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
                              const int32_t* d_perm, const int32_t* d_rows, int psi, void* d_meta,
                              size_t meta_bytes, cs_stream_t stream, cs_operator** out) {
@@ -400,7 +412,7 @@ static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t
   if (M < 1 || M > N) return fail(CS_ERR_INVALID_ARG, "M must be in [1, N]");
   if (batch < 1 || batch > (1 << 30)) return fail(CS_ERR_INVALID_ARG, "bad batch");
   if ((!d_sign_bits && !d_perm) || !d_rows || !d_meta) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
-  const size_t need = d_perm ? cs_operator_meta_bytes_perm(N, M, batch) : cs_operator_meta_bytes(N, M, batch);
+  const size_t need = cs_operator_meta_bytes_ex(N, M, batch, d_perm != nullptr, psi);
   if (meta_bytes < need) return fail(CS_ERR_WORKSPACE, "meta buffer too small");
   if (cs_status s = check_device()) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -417,8 +429,31 @@ static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t
     k_perm_setup<<<(unsigned)((batch * N + 255) / 256), 256, 0, st>>>(N, batch, d_perm, perm, err);
     CS_LAUNCHED();
   }
-  int64_t nthr = std::max(batch * M, batch * nw);
   const int64_t toff = meta_toff(N), natural = N > TIER_S_MAX_N ? -1 : nw;
+  uint32_t* full = nullptr;
+  if (psi) {
+    // one all-rows instance (rows = 0..N-1, sigma = +1): the full DCT-II / DCT-III of the
+    // dictionary on the grid tier (R35); its rows array stays after it
+    char* fb = reinterpret_cast<char*>(d_meta) + base_bytes + (perm ? align_up(batch * 2 * N * 4, 256) : 0);
+    full = reinterpret_cast<uint32_t*>(fb);
+    const int64_t sf = meta_stride(N, N);
+    int32_t* frows = reinterpret_cast<int32_t*>(fb + align_up(sf * 4, 256));
+    CS_CUDA(cudaMemsetAsync(full, 0, (size_t)(sf * 4), st));
+    k_iota<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(N, frows);
+    CS_LAUNCHED();
+    k_rows_mask<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(N, N, 1, nw, sf, natural, toff, tp, frows,
+                                                             nullptr, full, err);
+    CS_LAUNCHED();
+    if (natural >= 0) {
+      k_rows_prefix<<<1, 1024, 0, st>>>(nw, sf, natural, full);
+      CS_LAUNCHED();
+    }
+    k_rows_prefix<<<1, 1024, 0, st>>>(nw, sf, toff, full);
+    CS_LAUNCHED();
+    k_rows_tperm<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(N, N, 1, nw, sf, toff, tp, frows, full);
+    CS_LAUNCHED();
+  }
+  int64_t nthr = std::max(batch * M, batch * nw);
   k_rows_mask<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(N, M, batch, nw, stride, natural, toff, tp, d_rows,
                                                            d_sign_bits, meta, err);
   CS_LAUNCHED();
@@ -444,6 +479,7 @@ static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t
   op->errflag = err;
   op->perm = perm;
   op->psi = psi;
+  op->full = full;
   CS_CUDA(cudaGetDevice(&op->device));
   *out = op;
   return CS_OK;
@@ -480,8 +516,6 @@ cs_status cs_operator_create_ex(int64_t N, int64_t M, int64_t batch, const uint3
                                 size_t meta_bytes, cs_stream_t stream, cs_operator** out) {
   if (out) *out = nullptr;
   if (psi != CS_PSI_IDENTITY && psi != CS_PSI_DCT) return fail(CS_ERR_INVALID_ARG, "psi must be CS_PSI_IDENTITY or CS_PSI_DCT");
-  if (psi == CS_PSI_DCT && N > TIER_S_MAX_N)
-    return fail(CS_ERR_UNSUPPORTED, "Psi = DCT operators are built for N <= 16384 (CTA tier) in this version");
   if (!d_sign_bits && !d_perm) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
   return create_impl(N, M, batch, d_sign_bits, d_perm, d_rows, psi, d_meta, meta_bytes, stream, out);
 }

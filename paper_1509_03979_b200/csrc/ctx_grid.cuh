@@ -141,6 +141,14 @@ template <typename T> struct GridCtx {
   const int32_t* tperm;  // [M] y index of the t-th selected row in the transposed order
   const int32_t* pm;     // Eq.(7) randomizer pi (R34), or null
   const int32_t* pinv;   // pi^-1, or null
+  // dictionary Psi = C_N (R35): the all-rows instance and the real one, Phi's sign and pi^-1
+  int psi;
+  T* G;                  // [N] natural-order scratch
+  T* yTf;                // [N] all-rows "y" (transposed order)
+  const uint32_t *ftmask, *r_tmask;
+  const int32_t *ftprefix, *ftperm, *r_tprefix, *r_tperm;
+  const uint32_t* phi_sign;
+  const int32_t* phi_pinv;
   T* yT;             // [M] workspace
   int s1, tsh;       // transposed mask position: t = (k mod 2^s1) << tsh | k >> s1
   T* c0;        // [N] Makhoul order
@@ -734,6 +742,7 @@ template <typename T> struct GridCtx {
     }
   }
   CS_NOINL void H(const T* d, T* q) {
+    if (psi) { H_psi(d, q); return; }
     mark(0);
     passA_sparse(d);
     sync();
@@ -750,6 +759,7 @@ template <typename T> struct GridCtx {
     cg_loop(*this, s, [this](const T* d, T* q) { H(d, q); });
   }
   CS_NOINL double RES(const T* x) {
+    if (psi) return RES_psi(x);
     mark(0);
     if (x) {
       passA_sparse(x);
@@ -762,6 +772,104 @@ template <typename T> struct GridCtx {
     passC();
     const double r = sum(rn2);  // the reduction's barrier also publishes Cb
     mark(6);
+    ++applies;
+    return r;
+  }
+
+  // ---- Psi = C_N (R35): C_N, Phi and C_N^T composed from the same passes.  A full DCT-II
+  // (all N outputs) is pass A + pass B (MID_FWD) on the all-rows instance (rank = the
+  // transposed position, mapped back to k by its tperm); C_N^T of a dense vector is pass B
+  // (MID_RES on a zero input) + pass C on the all-rows instance.  sigma and pi act between
+  // the two domains through G (natural order).
+  CS_DEV void use_full() { rowmask = ftmask; prefix = ftprefix; tperm = ftperm; }
+  CS_DEV void use_real() { rowmask = r_tmask; prefix = r_tprefix; tperm = r_tperm; }
+  // G <- C_N s: s = scatter_S(vals), or (vals == nullptr) the dense s already in U
+  CS_NOINL void psi_to_G(const T* vals) {
+    use_full();
+    if (vals) passA_sparse(vals); else passA();
+    sync();
+    passB<MID_FWD>(false, yTf);
+    sync();
+    const int32_t* tp = ftperm;
+    const T* yt = yTf;
+    T* g = G;
+    gstaged<TL_UNR, T>(N, gtid, gnthr, [&](int64_t t) { return yt[t]; }, [&](int64_t t, T v) { g[tp[t]] = v; });
+    sync();
+  }
+  // U <- Makhoul order of R diag(sigma) G
+  CS_NOINL void phi_in() {
+    const uint32_t* sg = phi_sign;
+    const int32_t* pv = phi_pinv;
+    const T* g = G;
+    T* u = U;
+    const int64_t n = N;
+    gstaged<TL_UNR, T>(N, gtid, gnthr, [&](int64_t j) { return apply_sign<T>(sg, j, g[j]); },
+                       [&](int64_t j, T v) { u[ppos(pv, j, n)] = v; });
+    sync();
+  }
+  // G <- diag(sigma) R^T v, v = Cb (Makhoul order)
+  CS_NOINL void phi_out() {
+    const uint32_t* sg = phi_sign;
+    const int32_t* pv = phi_pinv;
+    const T* cb = Cb;
+    T* g = G;
+    const int64_t n = N;
+    gstaged<TL_UNR, T>(N, gtid, gnthr, [&](int64_t j) { return apply_sign<T>(sg, j, cb[ppos(pv, j, n)]); },
+                       [&](int64_t j, T v) { g[j] = v; });
+    sync();
+  }
+  // pass B of C_N^T G on the all-rows instance (pass C follows in the caller)
+  CS_NOINL void psiT_passB() {
+    use_full();
+    const int32_t* tp = ftperm;
+    const T* g = G;
+    T* yt = yTf;
+    gstaged<TL_UNR, T>(N, gtid, gnthr, [&](int64_t t) { return g[tp[t]]; }, [&](int64_t t, T v) { yt[t] = v; });
+    sync();
+    const T* ys = y;
+    y = yTf;
+    passB<MID_RES>(true, nullptr);
+    sync();
+    y = ys;
+  }
+  CS_NOINL void H_psi(const T* d, T* q) {
+    psi_to_G(d);                     // C_N s
+    phi_in();                        // R diag(sigma)
+    use_real();
+    passA();
+    sync();
+    passB<MID_H>(false, nullptr);    // C^T P^T P C
+    sync();
+    passC();
+    sync();
+    phi_out();                       // diag(sigma) R^T
+    psiT_passB();                    // C_N^T ...
+    passC_sparse(q);                 // ... on the support only
+    sync();
+    use_real();
+    ++applies;
+  }
+  CS_NOINL double RES_psi(const T* x) {
+    double rn2;
+    if (x) {
+      psi_to_G(x);
+      phi_in();
+      use_real();
+      passA();
+      sync();
+      rn2 = passB<MID_RES>(false, nullptr);   // Phi^T (y - Phi u)
+    } else {
+      use_real();
+      rn2 = passB<MID_RES>(true, nullptr);    // Phi^T y
+    }
+    sync();
+    passC();
+    const double r = sum(rn2);                // also publishes Cb
+    phi_out();
+    psiT_passB();
+    passC();                                  // A^T r, s-domain, Makhoul order
+    sync();
+    use_real();
     ++applies;
     return r;
   }

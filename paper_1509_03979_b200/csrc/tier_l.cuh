@@ -43,7 +43,7 @@ CS_HD LGeom l_geom(int64_t N) {
 
 // Workspace layout (byte offsets) — identical on host and device.
 struct LLayout {
-  int64_t U, Wk, Cb, c0, yT, in_pos, tcnt, tfill, tlist;
+  int64_t U, Wk, Cb, c0, yT, G, yTf, in_pos, tcnt, tfill, tlist;
   int64_t S, S2, Ul, x, x2, xU, r, d, q, b, Sbits, Ubits, Pbits;
   int64_t ctl, bar, pd, pi, pk, ghist, ts, ctl_end;
   int64_t bytes;
@@ -61,6 +61,8 @@ CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int 
   s.yT = take(M * ts);  // y in the transposed row order (OpMeta)
   s.Wk = take(g.L * cs2);
   s.Cb = take(N * ts);
+  s.G = take(N * ts);    // Psi = DCT (R35): natural-order scratch
+  s.yTf = take(N * ts);  // Psi = DCT: all-rows "y" in the transposed order
   s.c0 = pursuit ? take(N * ts) : 0;
   if (pursuit) {
     s.in_pos = take((int64_t)ucap * 8);
@@ -150,6 +152,8 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.Wk = reinterpret_cast<C2<T>*>(ws + s.Wk);
   c.Cb = reinterpret_cast<T*>(ws + s.Cb);
   c.yT = reinterpret_cast<T*>(ws + s.yT);
+  c.G = reinterpret_cast<T*>(ws + s.G);
+  c.yTf = reinterpret_cast<T*>(ws + s.yTf);
   c.s1 = ilog2(g.L1);
   c.tsh = ilog2(2 * g.L2);
   c.c0 = reinterpret_cast<T*>(ws + s.c0);
@@ -211,6 +215,22 @@ template <typename T> CS_DEV void set_instance(GridCtx<T>& c, const OpMeta& m, i
   c.tperm = m.tperm(b);
   c.pm = m.pm(b);
   c.pinv = m.pinv(b);
+  c.psi = m.psi;
+  c.r_tmask = c.rowmask;
+  c.r_tprefix = c.prefix;
+  c.r_tperm = c.tperm;
+  if (m.psi) {
+    // the pursuit's index space is the s-domain: no sign (the all-rows instance's zero sign
+    // words), no permutation; Phi's own sign / pi^-1 act in phi_in / phi_out (R35)
+    c.phi_sign = c.sign;
+    c.phi_pinv = c.pinv;
+    c.sign = m.full_sign();
+    c.pm = nullptr;
+    c.pinv = nullptr;
+    c.ftmask = m.full_tmask();
+    c.ftprefix = m.full_tprefix();
+    c.ftperm = m.full_tperm();
+  }
 }
 
 // y (row order) -> yT (transposed row order of the stored mask); ends with a grid barrier
@@ -229,6 +249,20 @@ CS_NOINL void l_scatter_perm(int64_t t0, int64_t nt, int64_t N, const T* x, cons
                              const int32_t* pv, T* U) {
   gstaged<TL_UNR, T>(N, t0, nt, [&](int64_t j) { return apply_sign<T>(sg, j, x[j]); },
                      [&](int64_t j, T v) { U[mk_pos(pv[j], N)] = v; });
+}
+
+// A x = Phi (C_N x) (R35): dense x (s-domain) into U, full DCT-II to G, then Phi's input in
+// U.  Out of line so the plain apply keeps its register allocation.
+template <typename T>
+CS_NOINL void l_apply_psi_input(GridCtx<T>& c, const T* x) {
+  const int64_t N = c.N;
+  T* U = c.U;
+  gstaged<TL_UNR, T>(N, c.gtid, c.gnthr, [&](int64_t j) { return x[j]; },
+                     [&](int64_t j, T v) { U[mk_pos(j, N)] = v; });
+  c.sync();
+  c.psi_to_G(nullptr);
+  c.phi_in();
+  c.use_real();
 }
 
 template <typename T>
@@ -250,6 +284,8 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_apply(LArgs<T> a) {
       }
     };
     stamp(0);
+    if (c.psi) l_apply_psi_input<T>(c, x);
+    else
     // four consecutive j per unit: x[j..j+3] -> U[j/2], U[j/2+1] (even j) and
     // U[N-2-j/2], U[N-1-j/2] (odd j, descending) — Makhoul order, sign applied
     if (c.pinv) l_scatter_perm<T>(c.gtid, c.gnthr, N, x, sg, c.pinv, U);

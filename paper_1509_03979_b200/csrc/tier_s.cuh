@@ -71,6 +71,7 @@ struct OpMeta {
   int64_t toff;    // word offset of the transposed mask within an instance
   const int32_t* perm;  // Eq.(7) randomizer R (R34): per instance [pi N][pi^-1 N], or null
   int psi;              // dictionary: 0 = I, 1 = C_N (R35)
+  const uint32_t* full; // Psi mode: the all-rows instance (stride meta_stride(N, N)), or null
   CS_HD const uint32_t* sign(int64_t b) const { return base + b * stride; }
   CS_HD const uint32_t* rmask(int64_t b) const { return base + b * stride + nw; }
   CS_HD const int32_t* prefix(int64_t b) const {
@@ -83,6 +84,10 @@ struct OpMeta {
   CS_HD const int32_t* tperm(int64_t b) const {
     return reinterpret_cast<const int32_t*>(base + b * stride + toff + 2 * nw);
   }
+  CS_HD const uint32_t* full_sign() const { return full; }  // all zero (sigma = +1)
+  CS_HD const uint32_t* full_tmask() const { return full + toff; }
+  CS_HD const int32_t* full_tprefix() const { return reinterpret_cast<const int32_t*>(full + toff + nw); }
+  CS_HD const int32_t* full_tperm() const { return reinterpret_cast<const int32_t*>(full + toff + 2 * nw); }
   CS_HD const int32_t* pm(int64_t b) const { return perm ? perm + b * 2 * N : nullptr; }
   CS_HD const int32_t* pinv(int64_t b) const { return perm ? perm + b * 2 * N + N : nullptr; }
 };

@@ -74,9 +74,8 @@ def test_host_validation_codes(lib):
     assert cs.REPORT_DTYPE.itemsize == 40
 
 
-def test_create_ex_rejects_bad_psi_and_large_n(lib):
+def test_create_ex_rejects_bad_psi(lib):
     """cs_operator_create_ex argument checks that run before any device work."""
     h = ctypes.c_void_p()
     assert lib.cs_operator_create_ex(1024, 256, 1, None, None, None, 7, None, 0, None, ctypes.byref(h)) == 1
-    assert lib.cs_operator_create_ex(1 << 15, 1 << 13, 1, None, None, None, 1, None, 0, None, ctypes.byref(h)) == 2
     assert lib.cs_operator_create_ex(1024, 256, 1, None, None, None, 1, None, 0, None, ctypes.byref(h)) == 1

@@ -1,8 +1,8 @@
 """Dictionary Psi = DCT (A = Phi Psi, x = Psi s; "Psi is chosen to be a discrete
 cosine transform", R35) on the CUDA path, through the
 C ABI (cs_operator_create_ex): operator and adjoint against the fp64 oracle, with and
-without the Eq.(7) permutation, and recovery parity for all four pursuits (CTA tier; larger
-N is rejected with CS_ERR_UNSUPPORTED in this version)."""
+without the Eq.(7) permutation, on both tiers, and recovery parity for all four pursuits
+(CTA tier; grid tier for N > 2^14 and for pursuits that do not fit one CTA)."""
 import numpy as np
 import pytest
 
@@ -34,7 +34,8 @@ def _op(cs, probs, dev):
                        perm=perms_dev(probs, dev), psi="dct")
 
 
-@pytest.mark.parametrize("N,M,batch", [(8, 4, 2), (64, 16, 3), (1024, 256, 2), (16384, 4096, 2)])
+@pytest.mark.parametrize("N,M,batch", [(8, 4, 2), (64, 16, 3), (1024, 256, 2), (16384, 4096, 2),
+                                       (32768, 8192, 1), (1 << 18, 1 << 16, 1)])
 @pytest.mark.parametrize("randomizer", ["sign", "perm"])
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 def test_psi_apply_adjoint_match_oracle(cs, N, M, batch, randomizer, dtype):
@@ -52,13 +53,6 @@ def test_psi_apply_adjoint_match_oracle(cs, N, M, batch, randomizer, dtype):
         y_ref, x_ref = op.apply(X[b]), op.adjoint(W[b])
         assert np.linalg.norm(Yg[b] - y_ref) <= tol * np.linalg.norm(y_ref), b
         assert np.linalg.norm(Xg[b] - x_ref) <= tol * np.linalg.norm(x_ref), b
-
-
-def test_psi_large_n_unsupported(cs):
-    dev = torch.device("cuda:0")
-    _, probs = _probs(32768, 8192, 8, 1)
-    with pytest.raises(RuntimeError, match="Psi"):
-        _op(cs, probs, dev)
 
 
 def _recover(cs, cfg, probs, dtype="float32", ys=None, tol=None):
@@ -101,12 +95,25 @@ def test_psi_all_ties_zero_measurements(cs, alg):
         assert np.array_equal(np.sort(supp[b]), refs[b].support)
 
 
-def test_psi_recovery_beyond_cta_tier_unsupported(cs):
-    """fp64 with a large K does not fit one CTA's shared memory: the grid tier does not
-    implement Psi = DCT yet, so the call must fail loudly rather than fall back."""
-    cfg, probs = _probs(16384, 8192, 2048, 1)
-    dev = torch.device("cuda:0")
-    A = _op(cs, probs, dev)
-    ys = measured(probs)
-    with pytest.raises(RuntimeError, match="CTA tier"):
-        cs.cs_recover_batched(A, "sp", torch.from_numpy(ys).to(dev, torch.float64), cfg.K, 1e-12)
+def test_psi_recovery_small_n_on_grid_tier_fp64(cs):
+    """fp64 with a large K does not fit one CTA's shared memory: the grid tier runs it."""
+    cfg, probs = _probs(16384, 8192, 2048, 1, noise=1e-3)
+    ys, supp, vals, reps = _recover(cs, cfg, probs, "float64")
+    bad, _ = compare(probs, oracle_results(probs, ys), supp, vals, rtol=1e-8)
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("randomizer", ["sign", "perm"])
+def test_psi_recovery_grid_tier_fp64(cs, randomizer):
+    cfg, probs = _probs(65536, 16384, 1024, 1, randomizer=randomizer, noise=1e-3)
+    ys, supp, vals, reps = _recover(cs, cfg, probs, "float64")
+    bad, _ = compare(probs, oracle_results(probs, ys), supp, vals, rtol=1e-8)
+    assert not bad, bad
+
+
+def test_psi_recovery_grid_tier_ompr_fp32(cs):
+    cfg, probs = _probs(1 << 17, 1 << 15, 256, 1, alg="ompr", randomizer="perm")
+    ys, supp, vals, reps = _recover(cs, cfg, probs)
+    bad, _ = compare(probs, oracle_results(probs, ys), supp, vals)
+    assert not bad, bad
+    assert np.array_equal(np.sort(supp[0]), probs[0].support)
