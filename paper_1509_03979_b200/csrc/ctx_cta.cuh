@@ -188,7 +188,7 @@ template <typename T> struct CtaCtx {
   }
   // CG iterations with the sandwich of one compile-time length inlined: no call
   // (and no ABI register save/restore) inside the loop.
-  template <int LOG2L, class S> CS_NOINL void cg_iterate_t(S& s_io) {
+  template <int LOG2L, bool PERM, class S> CS_NOINL void cg_iterate_t(S& s_io) {
     // Algorithm 1 lines 14-22 for one compile-time transform length, the
     // sandwich inlined.  Only ~12 uniform scalars stay live across the sandwich (shared
     // offsets of the four vectors, rr, thr, ns, cap, j, status, bank): everything else
@@ -224,7 +224,7 @@ template <typename T> struct CtaCtx {
     while (true) {
       if (!(rr > thr)) break;                                              // line 15 (R6, R7)
       if (j >= cap) { status |= CS_DEV_CG_CAP; break; }
-      sw_body<T, LOG2L, MID_H, false, false>(nullptr, TwTable<T>{}, TwTable<T>{}, m0,
+      sw_body<T, LOG2L, MID_H, false, PERM>(nullptr, TwTable<T>{}, TwTable<T>{}, m0,
                                       SwIO<T>{sp, n, nullptr, dv, qv});    // q = H d_j
       double dq = 0;
       for (int i = threadIdx.x; i < n; i += NT) dq += (double)dv[i] * (double)qv[i];
@@ -251,27 +251,25 @@ template <typename T> struct CtaCtx {
     s_io.status = status;
     rbank = rb;
   }
-  template <int LO, int HI, class S> CS_DEV void cg_dispatch(S& s) {
+  template <int LO, int HI, bool PERM, class S> CS_DEV void cg_dispatch(S& s) {
     if constexpr (LO <= HI) {
-      if (log2L == LO) { cg_iterate_t<LO>(s); return; }
-      cg_dispatch<LO + 1, HI>(s);
+      if (log2L == LO) { cg_iterate_t<LO, PERM>(s); return; }
+      cg_dispatch<LO + 1, HI, PERM>(s);
     }
   }
   template <class S> CS_DEV void cg_iterate(S& s) {
-    if (psi | (pinv != nullptr)) { cg_iterate_generic(s); return; }
-    cg_dispatch<2, 13>(s);  // the hot loop: sandwich inlined, no permutation
+    if (psi | (pinv != nullptr)) { cg_iterate_variant(s); return; }
+    cg_dispatch<2, 13, false>(s);  // the hot loop: sandwich inlined, no permutation lookups
   }
-  // Psi = DCT or the Eq.(7) permutation: the generic CG loop around the out-of-line
-  // sandwiches (kept out of line so the plain path's caller stays small)
-  template <class S> CS_NOINL void cg_iterate_generic(S& s) {
+  // Psi = DCT: the generic CG loop around the composed sandwich; Eq.(7) permutation: the
+  // hot loop instantiated with the pi^-1 lookups (kept out of line so the plain path's
+  // caller stays small)
+  template <class S> CS_NOINL void cg_iterate_variant(S& s) {
     if (psi) {
       cg_loop(*this, s, [this](const T* d, T* q) { H_psi(d, q); });
       return;
     }
-    cg_loop(*this, s, [this](const T* d, T* q) {
-      sandwich<MID_H, false>(d, q, nullptr);
-      ++applies;
-    });
+    cg_dispatch<2, 13, true>(s);
   }
   // q = (A^T A scatter_S(d))[S] on the remembered support S (cg2)
   CS_DEV void H(const T* d, T* q) {
