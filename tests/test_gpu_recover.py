@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import cs_inputs
+import oracle
 from cs_inputs import CONFIGS
 from gpu_helpers import to_dev, perms_dev, measured, oracle_results, compare
 
@@ -234,3 +235,51 @@ def test_cosamp_tier_l_fp32_exact(cs):
     bad, worst = compare(probs, refs, supp, vals)
     assert not bad, bad
     assert np.array_equal(np.sort(supp[0]), probs[0].support)
+
+
+# ---------------------------------------------------------------- edge cases ------
+@pytest.mark.parametrize("N", [1024, 65536])
+@pytest.mark.parametrize("alg", ["omp", "sp"])
+def test_full_sampling_m_equals_n(cs, N, alg):
+    """M = N: every DCT row selected, A is orthogonal (A^T A = I) — one CG iteration
+    solves each LS exactly; the recovery equals the oracle's on both tiers."""
+    cfg = cs_inputs.Config(68, alg, N, N, 8, "gauss", 1e-2)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 1, "float64")
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals, rtol=1e-9)
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("alg", ["omp", "sp", "ompr", "cosamp"])
+def test_k_equals_one(cs, alg):
+    cfg = cs_inputs.Config(69, alg, 4096, 64, 1, "gauss", 0.0)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 3)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals)
+    assert not bad, bad
+
+
+def test_k_at_limit_n_over_2(cs):
+    """K = N/2 (the ABI's upper bound) with OMPR (K + 1 <= M = N): a degenerate but legal call."""
+    cfg = cs_inputs.Config(71, "ompr", 64, 64, 32, "gauss", 0.0)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 2, "float64")
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals, rtol=1e-8)
+    assert not bad, bad
+
+
+@pytest.mark.slow
+def test_max_size_n_2_pow_25(cs):
+    """N = 2^25 (the largest supported transform): noiseless SP recovers the planted support
+    and is LS-optimal against the oracle operator (two fp64 applies; a whole oracle recovery
+    at this size would take far too long)."""
+    cfg = cs_inputs.Config(72, "sp", 1 << 25, 1 << 23, 1024, "gauss", 0.0)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 1)
+    p = probs[0]
+    assert np.array_equal(np.sort(supp[0]), p.support)
+    op = oracle.SrmOperator(p.N, p.sign_bits, p.rows)
+    s = np.zeros(p.N)
+    s[supp[0]] = vals[0]
+    assert np.linalg.norm(s - p.s) <= 1e-4 * np.linalg.norm(p.s)
+    r = ys[0].astype(np.float64) - op.apply(s)
+    assert np.linalg.norm(op.adjoint(r)[supp[0]]) <= 1e-4 * np.linalg.norm(op.adjoint(ys[0].astype(np.float64))[supp[0]])
