@@ -546,21 +546,53 @@ template <typename T> struct GridCtx {
     const int* sp = in_supp;
     const int64_t* ip = in_pos;
     const uint32_t* sg = sign;
-    for (int64_t t = blockIdx.x; t < ntl; t += gridDim.x) {
-      if (tcnt[t + 1] == tcnt[t]) continue;  // no support entry in this tile: skip it
-      const int64_t c0i = t * ct;
-      for (int e = threadIdx.x; e < tile; e += blockDim.x)
-        cp_async_c<T>(&sb[swz<T>(e)], &wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);
-      cp_async_wait_all();
-      __syncthreads();
-      col_fft<true>();
-      for (int q = tcnt[t] + threadIdx.x; q < tcnt[t + 1]; q += blockDim.x) {
-        const int i = tlist[q];
-        const int64_t p = ip[i], c = p >> 1;
-        const int e = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
-        outv[i] = apply_sign<T>(sg, sp[i], sbt[2 * swz<T>(e) + (int)(p & 1)]);
+    // the tile's output entries are resolved (support list -> smem slot, sign, output index)
+    // while its cp.async loads and the column FFT run: staged in the pass-B metadata buffer
+    // (two words per entry); a tile with more entries than fit takes the direct path
+    int* stg = reinterpret_cast<int*>(shp(msm));
+    const int cap = (int)((2 * L2) >> 5) * 2;
+    int64_t t = blockIdx.x;
+    int q0 = t < ntl ? tcnt[t] : 0, q1 = t < ntl ? tcnt[t + 1] : 0;
+    for (; t < ntl; t += gridDim.x) {
+      const int64_t tn = t + gridDim.x;
+      const int q0n = tn < ntl ? tcnt[tn] : 0, q1n = tn < ntl ? tcnt[tn + 1] : 0;  // next tile's
+      if (q1 != q0) {  // a tile without support entries is skipped
+        const int64_t c0i = t * ct;
+        for (int e = threadIdx.x; e < tile; e += blockDim.x)
+          cp_async_c<T>(&sb[swz<T>(e)], &wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);
+        const int cnt = q1 - q0;
+        const bool staged = cnt <= cap;
+        if (staged) {
+          for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+            const int i = tlist[q0 + q];
+            const int64_t p = ip[i], c = p >> 1;
+            const int e = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
+            const int slot = 2 * swz<T>(e) + (int)(p & 1);
+            stg[2 * q] = slot | (bit_test(sg, sp[i]) ? (int)0x80000000 : 0);
+            stg[2 * q + 1] = i;
+          }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        col_fft<true>();
+        if (staged) {
+          for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+            const int w = stg[2 * q];
+            const T v = sbt[w & 0x7fffffff];
+            outv[stg[2 * q + 1]] = (w < 0) ? -v : v;
+          }
+        } else {
+          for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+            const int i = tlist[q];
+            const int64_t p = ip[i], c = p >> 1;
+            const int e = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
+            outv[i] = apply_sign<T>(sg, sp[i], sbt[2 * swz<T>(e) + (int)(p & 1)]);
+          }
+        }
+        __syncthreads();
       }
-      __syncthreads();
+      q0 = q0n;
+      q1 = q1n;
     }
   }
   template <int MODE> CS_NOINL double passB(bool zero_input, T* yout) {
