@@ -85,7 +85,9 @@ CS_DEV bool topk_cta_fast_v(Ctx& ctx, int nbits, int K, Visit&& visit, uint32_t*
   __syncthreads();
   visit([&](int i, Key k) {
     (void)i;
-    if (k) hist_add_warp(h, key_digit10(k));
+    // plain shared atomics: the 10-bit digits of a warp's keys rarely coincide, and the
+    // match_any aggregation cost more than the collisions it saves (c4: -2.3 %)
+    if (k) atomicAdd(&h[key_digit10(k)], 1u);
   });
   __syncthreads();
   if (warp == 0) {
