@@ -395,7 +395,7 @@ def run_ours(args):
 def _oracle_one(args):
     import oracle
     p, y = args
-    op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi)
+    op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi, p.transform)
     r = oracle.recover(p.alg, op, y.astype(np.float64), p.K, tol=1e-10)
     return r.outer_iters
 
@@ -442,7 +442,7 @@ def run_reference(args):
     probs = cs_inputs.make_batch(cfg, count=n)
     ys = []
     for p in probs:
-        op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi)
+        op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi, p.transform)
         ys.append((op.apply(p.s) + p.noise).astype(np.float32))
     for _ in range(args.warmup if cfg.batch > 1 else 0):
         pass

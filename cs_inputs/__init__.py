@@ -43,6 +43,7 @@ class Config:
     batch: int = 1
     randomizer: str = "sign"   # "sign": R = diag(+-1) (BASELINE); "perm": Eq.(7)'s permutation, sigma = +1
     psi: str = "I"             # dictionary: "I" (BASELINE) or "dct" (A = Phi C_N)
+    transform: str = "dct"     # F: "dct" (BASELINE) or "dft" (partial Fourier; M = 2 x freqs)
 
     def scaled(self, div: int, batch: Optional[int] = None) -> "Config":
         """Same recipe at N/div, M/div, K/div (ratios kept); used for parity tests."""
@@ -82,6 +83,11 @@ def draw_sign_bits(N: int, g: np.random.Generator) -> np.ndarray:
 
 def draw_rows(N: int, M: int, g: np.random.Generator) -> np.ndarray:
     return np.sort(g.choice(N, M, replace=False)).astype(np.int32)
+
+
+def draw_freqs(N: int, Mf: int, g: np.random.Generator) -> np.ndarray:
+    """Mf distinct frequencies in [1, N/2 - 1], sorted (partial Fourier rows, R36)."""
+    return np.sort(g.choice(np.arange(1, N // 2), Mf, replace=False)).astype(np.int32)
 
 
 def draw_perm(N: int, g: np.random.Generator) -> np.ndarray:
@@ -125,6 +131,7 @@ class Problem:
     noise: np.ndarray       # float64[M] eta
     perm: Optional[np.ndarray] = None   # int32[N] pi of the randomizer R (randomizer "perm")
     psi: Optional[str] = None           # None (Psi = I) or "dct"
+    transform: str = "dct"              # "dct" or "dft" (rows are then frequencies)
 
 
 def make_problem(cfg: Config, trial: int = 0, b: int = 0) -> Problem:
@@ -136,12 +143,17 @@ def make_problem(cfg: Config, trial: int = 0, b: int = 0) -> Problem:
     else:
         bits = draw_sign_bits(N, rng(c, trial, b, TAG_SIGMA))
         perm = None
-    rows = draw_rows(N, M, rng(c, trial, b, TAG_ROWS))
+    if cfg.transform == "dft":
+        rows = draw_freqs(N, M // 2, rng(c, trial, b, TAG_ROWS))
+        M = 2 * rows.size
+    else:
+        rows = draw_rows(N, M, rng(c, trial, b, TAG_ROWS))
     s, supp = draw_signal(cfg.signal, N, K, rng(c, trial, b, TAG_POS),
                           rng(c, trial, b, TAG_VAL), rng(c, trial, b, TAG_PERM))
     eta = rng(c, trial, b, TAG_NOISE).standard_normal(M) * cfg.noise if cfg.noise > 0 \
         else np.zeros(M)
-    return Problem(N, M, K, cfg.alg, bits, rows, s, supp, eta, perm, "dct" if cfg.psi == "dct" else None)
+    return Problem(N, M, K, cfg.alg, bits, rows, s, supp, eta, perm, "dct" if cfg.psi == "dct" else None,
+                   cfg.transform)
 
 
 def make_batch(cfg: Config, trial: int = 0, b0: int = 0, count: Optional[int] = None):

@@ -24,7 +24,7 @@ def measured(problems):
     """y via the ORACLE operator, rounded to fp32 (R21)."""
     ys = []
     for p in problems:
-        op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi)
+        op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi, p.transform)
         ys.append((op.apply(p.s) + p.noise).astype(np.float32))
     return np.stack(ys)
 
@@ -32,7 +32,7 @@ def measured(problems):
 def oracle_results(problems, ys, tol=1e-10, **kw):
     out = []
     for p, y in zip(problems, ys):
-        op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi)
+        op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi, p.transform)
         out.append(oracle.recover(p.alg, op, y.astype(np.float64), p.K, tol=tol, **kw))
     return out
 

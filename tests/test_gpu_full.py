@@ -45,7 +45,7 @@ def _recover(cs, cfg, probs, ys, dtype, tol):
 
 def _ls_optimality(p, y, supp, vals):
     """||A_S^T (y - A x)|| / ||A_S^T y|| with the oracle operator (fp64)."""
-    op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi)
+    op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi, p.transform)
     x = dense_from(p.N, supp, vals)
     r = y.astype(np.float64) - op.apply(x)
     g = op.adjoint(r)[supp]
@@ -131,7 +131,7 @@ def test_c3_full_exact_recovery(cs):
     supp, vals, reps = _recover(cs, cfg, probs, ys, "float32", 1e-6)
     p = probs[0]
     assert np.array_equal(supp[0], p.support)
-    op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi)
+    op = oracle.SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi, p.transform)
     c0 = op.adjoint(ys[0].astype(np.float64))
     ls = oracle.cg(op, p.support, c0, tol=1e-10)
     s_or = dense_from(p.N, p.support, ls.x)

@@ -189,3 +189,44 @@ def test_psi_dct_rows_orthonormal():
                      draw_perm(N, rng(96, 2, N, 2)), psi="dct")
     AAT = np.stack([op.apply(op.adjoint(e)) for e in np.eye(M)[:48]], axis=1)
     np.testing.assert_allclose(AAT, np.eye(M)[:, :48], atol=1e-13)
+
+
+# ---------------------------------------------------------------- F = partial Fourier (R36)
+from cs_inputs import draw_freqs  # noqa: E402
+from oracle.operator import dft_rows_matrix  # noqa: E402
+
+
+@pytest.mark.parametrize("N,Mf,use_perm", [(8, 2, False), (64, 12, True), (1024, 200, True)])
+def test_dft_operator_matches_dense_definition(N, Mf, use_perm):
+    """Explicit cos / sin rows (no FFT) against the FFT-based oracle operator."""
+    bits = draw_sign_bits(max(N, 32), rng(95, 0, N, 0))
+    freqs = draw_freqs(N, Mf, rng(95, 0, N, 1))
+    perm = draw_perm(N, rng(95, 0, N, 2)) if use_perm else None
+    op = SrmOperator(N, bits, freqs, perm, transform="dft")
+    A = dense_srm(N, bits, freqs, perm, transform="dft")
+    assert A.shape == (2 * Mf, N) and op.M == 2 * Mf
+    g = np.random.default_rng(N + 3)
+    for _ in range(3):
+        x, w = g.standard_normal(N), g.standard_normal(2 * Mf)
+        np.testing.assert_allclose(op.apply(x), A @ x, atol=1e-12 * np.linalg.norm(x))
+        np.testing.assert_allclose(op.adjoint(w), A.T @ w, atol=1e-12 * np.linalg.norm(w))
+
+
+def test_dft_worked_example_cosine_input():
+    """x_n = cos(2 pi f0 n / N) gives X_f0 = N/2 (real) and nothing at other frequencies:
+    y = sqrt(2/N) (N/2, 0) at f0 = sqrt(N/2) (1, 0)."""
+    N = 64
+    f0 = 5
+    x = np.cos(2 * np.pi * f0 * np.arange(N) / N)
+    op = SrmOperator(N, pack_sign_bits(np.zeros(N, bool)), np.array([3, f0, 17]), transform="dft")
+    np.testing.assert_allclose(op.apply(x), [0, 0, np.sqrt(N / 2), 0, 0, 0], atol=1e-12)
+
+
+def test_dft_rows_orthonormal():
+    N, Mf = 2048, 300
+    op = SrmOperator(N, draw_sign_bits(N, rng(95, 1, N, 0)), draw_freqs(N, Mf, rng(95, 1, N, 1)),
+                     draw_perm(N, rng(95, 1, N, 2)), transform="dft")
+    AAT = np.stack([op.apply(op.adjoint(e)) for e in np.eye(2 * Mf)[:64]], axis=1)
+    np.testing.assert_allclose(AAT, np.eye(2 * Mf)[:, :64], atol=1e-13)
+    C = dft_rows_matrix(16, [1, 7])
+    np.testing.assert_allclose(C @ C.T, np.eye(4), atol=1e-14)

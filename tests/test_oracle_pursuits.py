@@ -154,7 +154,7 @@ def test_perm_randomizer_is_a_column_relabelling(alg):
     s' = R s with D F (sigma = +1, no R) and mapping the support back through pi."""
     cfg = cs_inputs.Config(91, alg, 1024, 256, 16, "gauss", 0.0, randomizer="perm")
     p = cs_inputs.make_problem(cfg, 0)
-    op = SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi)
+    op = SrmOperator(p.N, p.sign_bits, p.rows, p.perm, p.psi, p.transform)
     y = op.apply(p.s)
     a = oracle.recover(alg, op, y, p.K, tol=1e-13)
     op1 = SrmOperator(p.N, p.sign_bits, p.rows)
@@ -177,6 +177,24 @@ def test_psi_dct_cg_backend_equals_dense_ls_and_recovers(alg):
         np.testing.assert_array_equal(a.support, b.support)
         assert np.linalg.norm(a.s_hat - b.s_hat) <= 1e-8 * np.linalg.norm(b.s_hat)
     cfg = cs_inputs.Config(92, alg, 4096, 1024, 64, "gauss", 0.0, psi="dct")
+    p = cs_inputs.make_problem(cfg, 0)
+    op, y32 = measure(p)
+    res = oracle_recover(p, y32)
+    _check_exact(p, res, 1e-6)
+
+
+@pytest.mark.parametrize("alg", ["omp", "sp", "ompr", "cosamp"])
+def test_partial_fourier_cg_backend_equals_dense_ls_and_recovers(alg):
+    """F = partial Fourier (R36): CG and dense-LS backends agree; noiseless exact recovery."""
+    for trial in range(3):
+        cfg = cs_inputs.Config(93, alg, 256, 96, 6, "gauss", 0.0, randomizer="perm", transform="dft")
+        p = cs_inputs.make_problem(cfg, trial)
+        op, y32 = measure(p)
+        a = oracle_recover(p, y32, tol=1e-13)
+        b = oracle_recover(p, y32, tol=1e-13, solver="lstsq")
+        np.testing.assert_array_equal(a.support, b.support)
+        assert np.linalg.norm(a.s_hat - b.s_hat) <= 1e-8 * np.linalg.norm(b.s_hat)
+    cfg = cs_inputs.Config(93, alg, 4096, 1024, 64, "gauss", 0.0, randomizer="perm", transform="dft")
     p = cs_inputs.make_problem(cfg, 0)
     op, y32 = measure(p)
     res = oracle_recover(p, y32)
