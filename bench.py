@@ -51,6 +51,8 @@ def parse():
                     help="perm: the paper's literal Eq.(7) D F R operator (R34; not a BASELINE line)")
     ap.add_argument("--psi", choices=["I", "dct"], default="I",
                     help="dct: A = Phi C_N, the paper's experimental dictionary (R35; not a BASELINE line)")
+    ap.add_argument("--transform", choices=["dct", "dft"], default="dct",
+                    help="dft: F = partial Fourier, the MRI case of D F R (R36; not a BASELINE line)")
     ap.add_argument("--no-op-bench", action="store_true")
     return ap.parse_args()
 
@@ -63,14 +65,19 @@ def select_config(args):
         cfg = dataclasses.replace(cfg, randomizer=args.randomizer)
     if args.psi != cfg.psi:
         cfg = dataclasses.replace(cfg, psi=args.psi)
+    if args.transform != cfg.transform:
+        cfg = dataclasses.replace(cfg, transform=args.transform)
     return cfg
 
 
 def workload_desc(cfg):
     base = cs_inputs.CONFIGS[cfg.cid]
-    if cfg.alg != base.alg or cfg.randomizer != base.randomizer or cfg.psi != base.psi:
+    if (cfg.alg != base.alg or cfg.randomizer != base.randomizer or cfg.psi != base.psi
+            or cfg.transform != base.transform):
         names = {"omp": "OMP", "sp": "SP", "ompr": "OMPR(1)", "cosamp": "CoSaMP"}
         op = "D.F.R (Eq.(7) permutation randomizer)" if cfg.randomizer == "perm" else "P.DCT.diag(sigma)"
+        if cfg.transform == "dft":
+            op = op.replace("DCT", "partial-DFT").replace("D.F.R", "D.F_dft.R")
         if cfg.psi == "dct":
             op += " x Psi = DCT"
         return (f"c{cfg.cid}-shape with {names[cfg.alg]}+CG on {op} (override): "
@@ -180,7 +187,8 @@ def run_ours(args):
     perm = None
     if cfg.randomizer == "perm":
         perm = torch.from_numpy(np.stack([p.perm for p in probs]).astype(np.int32)).to(dev)
-    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=B, perm=perm, psi=("dct" if cfg.psi == "dct" else None))
+    A = cs.Operator(cfg.N, probs[0].M, bits, rows, batch=B, perm=perm, psi=("dct" if cfg.psi == "dct" else None),
+                    transform=cfg.transform)
     Y = (cs.cs_operator_apply(A, S) + E).to(torch.float32).to(td)  # fp32-rounded y (R21)
     del S, E
     torch.cuda.synchronize()
@@ -358,7 +366,8 @@ def run_ours(args):
     if os.path.exists(tr):
         try:
             key = f"c{cfg.cid}_{args.precision}" + ("" if cfg.alg == cs_inputs.CONFIGS[cfg.cid].alg else f"_{cfg.alg}") \
-                + ("" if cfg.randomizer == "sign" else f"_{cfg.randomizer}") + ("" if cfg.psi == "I" else "_psi")
+                + ("" if cfg.randomizer == "sign" else f"_{cfg.randomizer}") + ("" if cfg.psi == "I" else "_psi") \
+                + ("" if cfg.transform == "dct" else "_dft")
             roofline["traffic"] = json.load(open(tr)).get(key)
         except Exception:
             pass

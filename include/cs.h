@@ -139,6 +139,17 @@ size_t cs_operator_meta_bytes_ex(int64_t N, int64_t M, int64_t batch, int has_pe
 cs_status cs_operator_create_ex(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
                                 const int32_t* d_perm, const int32_t* d_rows, int psi, void* d_meta,
                                 size_t meta_bytes, cs_stream_t stream, cs_operator** out);
+
+/* F = partial Fourier (the MRI case of D F R; R36): real x,
+ * n_freq frequencies f in [1, N/2 - 1] per instance (d_freqs [batch][n_freq], strictly
+ * increasing — checked here), M = 2 n_freq measurements y[2r] = sqrt(2/N) Re X_f,
+ * y[2r+1] = sqrt(2/N) Im X_f, X = unnormalised DFT of R diag(sigma) x.  d_sign_bits and
+ * d_perm may be NULL (sigma = +1, R = I).  d_meta: cs_operator_meta_bytes_dft bytes.
+ * The operator then works with every apply / adjoint / recover call, with M = 2 n_freq. */
+size_t cs_operator_meta_bytes_dft(int64_t N, int64_t n_freq, int64_t batch);
+cs_status cs_operator_create_dft(int64_t N, int64_t n_freq, int64_t batch, const uint32_t* d_sign_bits,
+                                 const int32_t* d_perm, const int32_t* d_freqs, void* d_meta,
+                                 size_t meta_bytes, cs_stream_t stream, cs_operator** out);
 cs_status cs_operator_destroy(cs_operator* op);
 cs_status cs_operator_info(const cs_operator* op, int64_t* N, int64_t* M, int64_t* batch);
 

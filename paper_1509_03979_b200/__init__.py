@@ -57,7 +57,7 @@ EXPORTS = [
     "cs_recover_batched_host_f64", "cs_status_string", "cs_last_error",
     "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
     "cs_diag_topk", "cs_operator_meta_bytes_perm", "cs_operator_create_perm", "cs_operator_create_ex",
-    "cs_operator_meta_bytes_ex",
+    "cs_operator_meta_bytes_ex", "cs_operator_meta_bytes_dft", "cs_operator_create_dft",
 ]
 
 
@@ -76,6 +76,8 @@ def load_library(path: str = LIB_PATH):
         "cs_operator_meta_bytes_perm": (SZ, [I64, I64, I64]),
         "cs_operator_create_perm": (I32, [I64, I64, I64, P, P, P, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_meta_bytes_ex": (SZ, [I64, I64, I64, ctypes.c_int, ctypes.c_int]),
+        "cs_operator_meta_bytes_dft": (SZ, [I64, I64, I64]),
+        "cs_operator_create_dft": (I32, [I64, I64, I64, P, P, P, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_create_ex": (I32, [I64, I64, I64, P, P, P, ctypes.c_int, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_destroy": (I32, [P]),
         "cs_operator_info": (I32, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
@@ -150,7 +152,8 @@ class Operator:
     `perm` ([batch][N] int32 pi), the Eq.(7) operator P . DCT-II . R . diag(sigma)
     (cs_operator_create_perm; sign_bits may then be None for sigma = +1)."""
 
-    def __init__(self, N: int, M: int, sign_bits, rows, batch: int = 1, stream=None, perm=None, psi=None):
+    def __init__(self, N: int, M: int, sign_bits, rows, batch: int = 1, stream=None, perm=None, psi=None,
+                 transform="dct"):
         torch = _torch()
         L = load_library()
         self.N, self.M, self.batch = int(N), int(M), int(batch)
@@ -159,7 +162,18 @@ class Operator:
         rw = rows.to(device=dev, dtype=torch.int32).contiguous()
         sb = None if sign_bits is None else sign_bits.to(device=dev).contiguous()
         h = ctypes.c_void_p()
-        if psi is not None:
+        if transform == "dft":
+            # partial Fourier (R36): `rows` are frequencies, M = 2 x their count
+            nf = int(rw.shape[-1])
+            if M != 2 * nf:
+                raise ValueError("partial Fourier: M must be twice the number of frequencies")
+            pm = None if perm is None else perm.to(device=dev, dtype=torch.int32).contiguous()
+            nb = L.cs_operator_meta_bytes_dft(N, nf, batch)
+            self.meta = torch.empty(nb, dtype=torch.uint8, device=dev)
+            _check(L.cs_operator_create_dft(N, nf, batch, _ptr(sb) if sb is not None else None,
+                                            _ptr(pm) if pm is not None else None, _ptr(rw), _ptr(self.meta),
+                                            nb, _stream(stream), ctypes.byref(h)), "cs_operator_create_dft")
+        elif psi is not None:
             code = {"I": 0, "dct": 1}[psi]
             pm = None if perm is None else perm.to(device=dev, dtype=torch.int32).contiguous()
             nb = L.cs_operator_meta_bytes_ex(N, M, batch, int(pm is not None), code)

@@ -24,6 +24,8 @@ struct cs_operator {
   int* errflag;     // device int in the meta tail
   int32_t* perm;    // device: [B][pi N][pi^-1 N] after the meta tail (Eq.(7) randomizer), or null
   int psi;          // dictionary Psi: 0 = I, 1 = C_N (R35)
+  int fkind;        // F: 0 = DCT-II, 1 = partial Fourier (R36)
+  int64_t Mr;       // metadata rows (= M for the DCT; frequencies = M / 2 for the DFT)
   uint32_t* full;   // Psi mode: one all-rows instance (stride meta_stride(N, N)), or null
   int device;
 };
@@ -131,6 +133,27 @@ __global__ void k_iota(int64_t n, int32_t* out) {
   if (i < n) out[i] = (int32_t)i;
 }
 
+// partial Fourier: rows are frequencies in [1, N/2 - 1] (err bit 4)
+__global__ void k_freq_check(int64_t N, int64_t n, const int32_t* f, int* err) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && (f[i] < 1 || f[i] > N / 2 - 1)) atomicOr(err, 4);
+}
+
+// Partial Fourier (R36): the plain packing z_m = u_{2m} + i u_{2m+1} as an effective
+// permutation of the Makhoul machinery: position of x_j = pi^-1(j) = mk_pos(pinv_eff[j]), so
+// pinv_eff[j] = mk_nat(pi^-1(j)) and pm_eff[mk_nat(i)] = pi(i) (pi = identity without a
+// randomizer).  err |= 2 unless pi is a permutation.
+__global__ void k_perm_dft(int64_t N, int64_t B, const int32_t* pin, int32_t* perm, int* err) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= B * N) return;
+  const int64_t b = g / N, i = g % N;
+  const int32_t j = pin ? pin[g] : (int32_t)i;
+  if (j < 0 || j >= N) { atomicOr(err, 2); return; }
+  const int32_t mi = (int32_t)((2 * i < N) ? 2 * i : 2 * (N - 1 - i) + 1);  // mk_nat(i)
+  perm[b * 2 * N + mi] = j;
+  if (atomicExch(&perm[b * 2 * N + N + j], mi) != -1) atomicOr(err, 2);
+}
+
 // Tier L: tperm[rank of row m in the transposed order] = m
 __global__ void k_rows_tperm(int64_t N, int64_t M, int64_t B, int64_t nw, int64_t stride, int64_t toff, TPos tp,
                              const int32_t* rows, uint32_t* meta) {
@@ -199,8 +222,10 @@ OpMeta meta_of(const cs_operator* op) {
   m.base = op->meta;
   m.N = op->N;
   m.M = op->M;
+  m.Mr = op->Mr;
+  m.fkind = op->fkind;
   m.nw = op->nw;
-  m.stride = meta_stride(op->N, op->M);
+  m.stride = meta_stride(op->N, op->Mr);
   m.toff = meta_toff(op->N);
   m.perm = op->perm;
   m.psi = op->psi;
@@ -360,7 +385,7 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
     cudaStream_t sc = (c & 1) ? hp.s_comp : st;
     CS_CUDA(cudaStreamWaitEvent(sc, hp.ev[0][c], 0));
     cs_operator sub = *op;
-    sub.meta = op->meta + b0 * meta_stride(op->N, op->M);
+    sub.meta = op->meta + b0 * meta_stride(op->N, op->Mr);
     if (op->perm) sub.perm = op->perm + b0 * 2 * N;
     sub.B = cnt;
     char* rws = tier_s ? w + (size_t)(b0 * 2 * N) * sizeof(T) : w;
@@ -403,16 +428,19 @@ size_t cs_operator_meta_bytes_ex(int64_t N, int64_t M, int64_t batch, int has_pe
   return b;
 }
 
+// M = metadata rows: DCT rows, or (fkind 1) partial-Fourier frequencies (2 measurements each)
 static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,
                              const int32_t* d_perm, const int32_t* d_rows, int psi, void* d_meta,
-                             size_t meta_bytes, cs_stream_t stream, cs_operator** out) {
+                             size_t meta_bytes, cs_stream_t stream, cs_operator** out, int fkind = 0) {
   if (!out) return fail(CS_ERR_INVALID_ARG, "out is null");
   *out = nullptr;
   if (cs_status s = check_N(N)) return s;
-  if (M < 1 || M > N) return fail(CS_ERR_INVALID_ARG, "M must be in [1, N]");
+  if (fkind == 0 && (M < 1 || M > N)) return fail(CS_ERR_INVALID_ARG, "M must be in [1, N]");
+  if (fkind == 1 && (M < 1 || M > N / 2 - 1)) return fail(CS_ERR_INVALID_ARG, "frequency count must be in [1, N/2 - 1]");
   if (batch < 1 || batch > (1 << 30)) return fail(CS_ERR_INVALID_ARG, "bad batch");
-  if ((!d_sign_bits && !d_perm) || !d_rows || !d_meta) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
-  const size_t need = cs_operator_meta_bytes_ex(N, M, batch, d_perm != nullptr, psi);
+  if ((fkind == 0 && !d_sign_bits && !d_perm) || !d_rows || !d_meta) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
+  const bool has_perm = d_perm != nullptr || fkind == 1;
+  const size_t need = cs_operator_meta_bytes_ex(N, M, batch, has_perm, psi);
   if (meta_bytes < need) return fail(CS_ERR_WORKSPACE, "meta buffer too small");
   if (cs_status s = check_device()) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -423,10 +451,15 @@ static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t
   int* err = reinterpret_cast<int*>(reinterpret_cast<char*>(d_meta) + align_up(batch * stride * 4, 256));
   const size_t base_bytes = cs_operator_meta_bytes(N, M, batch);
   CS_CUDA(cudaMemsetAsync(d_meta, 0, base_bytes, st));
-  int32_t* perm = d_perm ? reinterpret_cast<int32_t*>(reinterpret_cast<char*>(d_meta) + base_bytes) : nullptr;
+  int32_t* perm = has_perm ? reinterpret_cast<int32_t*>(reinterpret_cast<char*>(d_meta) + base_bytes) : nullptr;
   if (perm) {
     CS_CUDA(cudaMemsetAsync(perm, 0xFF, (size_t)(batch * 2 * N) * 4, st));
-    k_perm_setup<<<(unsigned)((batch * N + 255) / 256), 256, 0, st>>>(N, batch, d_perm, perm, err);
+    if (fkind == 1) k_perm_dft<<<(unsigned)((batch * N + 255) / 256), 256, 0, st>>>(N, batch, d_perm, perm, err);
+    else k_perm_setup<<<(unsigned)((batch * N + 255) / 256), 256, 0, st>>>(N, batch, d_perm, perm, err);
+    CS_LAUNCHED();
+  }
+  if (fkind == 1) {
+    k_freq_check<<<(unsigned)((batch * M + 255) / 256), 256, 0, st>>>(N, batch * M, d_rows, err);
     CS_LAUNCHED();
   }
   const int64_t toff = meta_toff(N), natural = N > TIER_S_MAX_N ? -1 : nw;
@@ -470,9 +503,12 @@ static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t
   CS_CUDA(cudaStreamSynchronize(st));
   if (herr & 1) return fail(CS_ERR_INVALID_ARG, "rows must be strictly increasing and in [0, N)");
   if (herr & 2) return fail(CS_ERR_INVALID_ARG, "perm must be a permutation of [0, N)");
+  if (herr & 4) return fail(CS_ERR_INVALID_ARG, "frequencies must be in [1, N/2 - 1]");
   cs_operator* op = new cs_operator;
   op->N = N;
-  op->M = M;
+  op->M = fkind == 1 ? 2 * M : M;
+  op->Mr = M;
+  op->fkind = fkind;
   op->B = batch;
   op->nw = nw;
   op->meta = meta;
@@ -509,6 +545,16 @@ cs_status cs_operator_create_perm(int64_t N, int64_t M, int64_t batch, const uin
     return fail(CS_ERR_INVALID_ARG, "null pointer argument");
   }
   return create_impl(N, M, batch, d_sign_bits, d_perm, d_rows, 0, d_meta, meta_bytes, stream, out);
+}
+
+size_t cs_operator_meta_bytes_dft(int64_t N, int64_t n_freq, int64_t batch) {
+  return cs_operator_meta_bytes_ex(N, n_freq, batch, 1, 0);
+}
+
+cs_status cs_operator_create_dft(int64_t N, int64_t n_freq, int64_t batch, const uint32_t* d_sign_bits,
+                                 const int32_t* d_perm, const int32_t* d_freqs, void* d_meta,
+                                 size_t meta_bytes, cs_stream_t stream, cs_operator** out) {
+  return create_impl(N, n_freq, batch, d_sign_bits, d_perm, d_freqs, 0, d_meta, meta_bytes, stream, out, 1);
 }
 
 cs_status cs_operator_create_ex(int64_t N, int64_t M, int64_t batch, const uint32_t* d_sign_bits,

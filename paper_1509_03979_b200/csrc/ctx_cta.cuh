@@ -59,6 +59,7 @@ template <typename T> struct CtaCtx {
   // dictionary Psi = C_N (R35): A = Phi Psi.  The pursuit's index space is the s-domain
   // (no sign, no permutation: `sign` holds zeros, pm/pinv are null); Phi's sign bits,
   // pi^-1 and row mask are read from the instance metadata by the Psi-mode helpers.
+  int fkind;                 // F: 0 = DCT-II, 1 = partial Fourier (R36)
   int psi;                   // 0: Psi = I, 1: Psi = C_N
   T* G;                      // global [N] scratch of this problem (Psi mode)
   const uint32_t* phi_sign;  // global
@@ -184,11 +185,12 @@ template <typename T> struct CtaCtx {
   template <int MODE, bool ZERO> CS_DEV double sandwich(const T* vin, T* vout, T* yout) {
     const MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, yout);
     const SwIO<T> io{in_supp, in_ns, sign, vin, vout};
-    return sw_dispatch<T, 2, 13, MODE, ZERO>(Z, log2L, twL, tw4, m, io);
+    if (fkind) return sw_dispatch<T, 2, 13, MODE, ZERO, 1>(Z, log2L, twL, tw4, m, io);
+    return sw_dispatch<T, 2, 13, MODE, ZERO, 0>(Z, log2L, twL, tw4, m, io);
   }
   // CG iterations with the sandwich of one compile-time length inlined: no call
   // (and no ABI register save/restore) inside the loop.
-  template <int LOG2L, bool PERM, class S> CS_NOINL void cg_iterate_t(S& s_io) {
+  template <int LOG2L, bool PERM, int KIND, class S> CS_NOINL void cg_iterate_t(S& s_io) {
     // Algorithm 1 lines 14-22 for one compile-time transform length, the
     // sandwich inlined.  Only ~12 uniform scalars stay live across the sandwich (shared
     // offsets of the four vectors, rr, thr, ns, cap, j, status, bank): everything else
@@ -224,7 +226,7 @@ template <typename T> struct CtaCtx {
     while (true) {
       if (!(rr > thr)) break;                                              // line 15 (R6, R7)
       if (j >= cap) { status |= CS_DEV_CG_CAP; break; }
-      sw_body<T, LOG2L, MID_H, false, PERM>(nullptr, TwTable<T>{}, TwTable<T>{}, m0,
+      sw_body<T, LOG2L, MID_H, false, PERM, KIND>(nullptr, TwTable<T>{}, TwTable<T>{}, m0,
                                       SwIO<T>{sp, n, nullptr, dv, qv});    // q = H d_j
       double dq = 0;
       for (int i = threadIdx.x; i < n; i += NT) dq += (double)dv[i] * (double)qv[i];
@@ -251,15 +253,15 @@ template <typename T> struct CtaCtx {
     s_io.status = status;
     rbank = rb;
   }
-  template <int LO, int HI, bool PERM, class S> CS_DEV void cg_dispatch(S& s) {
+  template <int LO, int HI, bool PERM, int KIND, class S> CS_DEV void cg_dispatch(S& s) {
     if constexpr (LO <= HI) {
-      if (log2L == LO) { cg_iterate_t<LO, PERM>(s); return; }
-      cg_dispatch<LO + 1, HI, PERM>(s);
+      if (log2L == LO) { cg_iterate_t<LO, PERM, KIND>(s); return; }
+      cg_dispatch<LO + 1, HI, PERM, KIND>(s);
     }
   }
   template <class S> CS_DEV void cg_iterate(S& s) {
     if (psi | (pinv != nullptr)) { cg_iterate_variant(s); return; }
-    cg_dispatch<2, 13, false>(s);  // the hot loop: sandwich inlined, no permutation lookups
+    cg_dispatch<2, 13, false, 0>(s);  // the hot loop: sandwich inlined, no permutation lookups
   }
   // Psi = DCT: the generic CG loop around the composed sandwich; Eq.(7) permutation: the
   // hot loop instantiated with the pi^-1 lookups (kept out of line so the plain path's
@@ -269,7 +271,8 @@ template <typename T> struct CtaCtx {
       cg_loop(*this, s, [this](const T* d, T* q) { H_psi(d, q); });
       return;
     }
-    cg_dispatch<2, 13, true>(s);
+    if (fkind) cg_dispatch<2, 13, true, 1>(s);  // partial Fourier: always position-mapped
+    else cg_dispatch<2, 13, true, 0>(s);
   }
   // q = (A^T A scatter_S(d))[S] on the remembered support S (cg2)
   CS_DEV void H(const T* d, T* q) {

@@ -141,6 +141,8 @@ template <typename T> struct GridCtx {
   const int32_t* tperm;  // [M] y index of the t-th selected row in the transposed order
   const int32_t* pm;     // Eq.(7) randomizer pi (R34), or null
   const int32_t* pinv;   // pi^-1, or null
+  int fkind;             // F: 0 = DCT-II, 1 = partial Fourier (R36: y holds (Re, Im) pairs)
+  int64_t Mr;            // metadata rows (frequencies for the DFT)
   // dictionary Psi = C_N (R35): the all-rows instance and the real one, Phi's sign and pi^-1
   int psi;
   T* G;                  // [N] natural-order scratch
@@ -644,7 +646,25 @@ template <typename T> struct GridCtx {
         m.staged = W > 0;
         m.ra = (int)ka;
       }
-      if (it == 0) {
+      if (fkind == 1) {
+        // partial Fourier (R36): the same pairs (n, L - n), the real-DFT split
+        if (it == 0) {
+          for (int k2 = threadIdx.x; k2 <= n2 / 2; k2 += blockDim.x) {
+            if (k2 == 0) dft_zero<T, MODE>(zb[swz<T>(0)], m, rn2);
+            else dft_pair<T, MODE>(zb[swz<T>(k2)], zb[swz<T>(n2 - k2)], L1 * k2, tw4(L1 * k2), m, rn2);
+          }
+        } else if (it == L1 / 2) {
+          for (int k2 = threadIdx.x; k2 < n2 / 2; k2 += blockDim.x) {
+            const int64_t k = L1 / 2 + L1 * k2;
+            dft_pair<T, MODE>(zb[swz<T>(k2)], zb[swz<T>(n2 - 1 - k2)], k, tw4(k), m, rn2);
+          }
+        } else {
+          for (int k2 = threadIdx.x; k2 < n2; k2 += blockDim.x) {
+            const int64_t k = ka + L1 * k2;
+            dft_pair<T, MODE>(zb[swz<T>(2 * k2)], zb[swz<T>(2 * (n2 - 1 - k2) + 1)], k, tw4(k), m, rn2);
+          }
+        }
+      } else if (it == 0) {
         for (int k2 = threadIdx.x; k2 <= n2 / 2; k2 += blockDim.x) {
           if (k2 == 0) mid_zero<T, MODE>(zb[swz<T>(0)], m, rn2);
           else {

@@ -127,6 +127,78 @@ CS_DEV void mid_pair(C2<T>& Zk, C2<T>& Zkk, int64_t k, C2<T> a, const MidCtx<T>&
   }
 }
 
+// ---- F = partial Fourier (R36): the real DFT from the same half-length FFT ----
+// z_m = u_{2m} + i u_{2m+1} (plain packing: the operator's position map, built as an
+// effective permutation at create time), Z = FFT_L(z).  For the pair (n, L - n):
+//   E = (Z_n + conj Z_{L-n})/2,  O = -i (Z_n - conj Z_{L-n})/2,  w = W_N^n,
+//   X_n = E + w O,  X_{L-n} = conj(E - w O)          (unnormalised DFT of u)
+// A selected frequency f (row rank r) is measured as y[2r] = s Re X_f, y[2r+1] = s Im X_f,
+// s = sqrt(2/N).  The adjoint, with the unnormalised inverse FFT (z'_m = sum Z'_k
+// e^{+2 pi i k m / L} = u'_{2m} + i u'_{2m+1}), takes V~_f = (s/2) V_f (V = s X for H,
+// y - s X for RES) and
+//   E' = V~_n + conj V~_{L-n},  O' = V~_n - conj V~_{L-n},
+//   Z'_n = E' + i conj(w) O',  Z'_{L-n} = conj(E' - i conj(w) O').
+// DC and Nyquist (n = 0) are never measured.
+template <typename T, int MODE>
+CS_DEV C2<T> dft_op(const MidCtx<T>& m, int64_t f, C2<T> X, double& rn2) {
+  const int64_t t = m.tpos(f);
+  const bool sel = m.sel(t);
+  const T s = m.sk;  // sqrt(2/N)
+  if constexpr (MODE == MID_H) {
+    const T h = (T)0.5 * s * s;  // (s/2) s = 1/N
+    return sel ? mk<T>(X.x * h, X.y * h) : mk<T>(0, 0);
+  } else if constexpr (MODE == MID_RES) {
+    if (!sel) return mk<T>(0, 0);
+    const int64_t r = m.rank(t);
+    const T dx = m.y[2 * r] - s * X.x, dy = m.y[2 * r + 1] - s * X.y;
+    rn2 += (double)dx * (double)dx + (double)dy * (double)dy;
+    const T h = (T)0.5 * s;
+    return mk<T>(dx * h, dy * h);
+  } else {
+    if (sel) {
+      const int64_t r = m.rank(t);
+      m.yout[2 * r] = s * X.x;
+      m.yout[2 * r + 1] = s * X.y;
+    }
+    return mk<T>(0, 0);
+  }
+}
+// n = 0 element: DC and Nyquist, never measured
+template <typename T, int MODE>
+CS_DEV void dft_zero(C2<T>& Z0, const MidCtx<T>& m, double& rn2) {
+  (void)m;
+  (void)rn2;
+  if constexpr (MODE != MID_FWD) Z0 = mk<T>(0, 0);
+}
+// pair (n, L - n), 1 <= n <= L/2 (n = L/2: the self pair, Zk and Zkk the same element);
+// w = W_N^n.  Zk, Zkk updated in place.
+template <typename T, int MODE>
+CS_DEV void dft_pair_w(C2<T>& Zk, C2<T>& Zkk, int64_t n, C2<T> w, const MidCtx<T>& m, double& rn2) {
+  const int64_t L = m.N >> 1, nn = L - n;
+  const bool self = (n == nn);
+  const C2<T> P2 = mk<T>(Zk.x + Zkk.x, Zk.y - Zkk.y);   // 2E
+  const C2<T> O2 = mk<T>(Zk.y + Zkk.y, Zkk.x - Zk.x);   // 2O = -i (Zk - conj Zkk)
+  const C2<T> Q2 = cmul<T>(w, O2);
+  const C2<T> Xa = mk<T>((P2.x + Q2.x) * (T)0.5, (P2.y + Q2.y) * (T)0.5);     // X_n
+  const C2<T> Xb = mk<T>((P2.x - Q2.x) * (T)0.5, -(P2.y - Q2.y) * (T)0.5);    // X_{L-n}
+  const C2<T> Va = dft_op<T, MODE>(m, n, Xa, rn2);
+  const C2<T> Vb = self ? Va : dft_op<T, MODE>(m, nn, Xb, rn2);
+  if constexpr (MODE != MID_FWD) {
+    const C2<T> E = mk<T>(Va.x + Vb.x, Va.y - Vb.y);     // V~_n + conj V~_{L-n}
+    const C2<T> O = mk<T>(Va.x - Vb.x, Va.y + Vb.y);     // V~_n - conj V~_{L-n}
+    const C2<T> c = cmulc<T>(O, w);                      // conj(w) O
+    const C2<T> t = mk<T>(-c.y, c.x);                    // i conj(w) O
+    Zk = mk<T>(E.x + t.x, E.y + t.y);
+    if (!self) Zkk = mk<T>(E.x - t.x, -(E.y - t.y));
+  }
+}
+// the same with a = W_4N^n (the DCT tables' twiddle; w = a^4)
+template <typename T, int MODE>
+CS_DEV void dft_pair(C2<T>& Zk, C2<T>& Zkk, int64_t n, C2<T> a, const MidCtx<T>& m, double& rn2) {
+  const C2<T> a2 = cmul<T>(a, a);
+  dft_pair_w<T, MODE>(Zk, Zkk, n, cmul<T>(a2, a2), m, rn2);
+}
+
 // ---- the same pair operation with the constant factors folded (Tier S) ----
 // Forward split without the two 1/2 factors: raw_k = 2 X_k, raw_{N-k} = 2 X_{N-k},
 // and for the kk pair the e^{-i pi/4} rotation split into (1 - i) and a factor

@@ -107,7 +107,8 @@ template <typename T> CS_DEV C2<T> w16c() {
 //   A0 = Z_k, A1 = Z_{k+L/2}, B0 = Z_{L/2-k}, B1 = Z_{L-k};
 // mirror pairs: (A0, B1) at n = k and (A1, B0) at n = k + L/2.
 // Unit 0 (items 0 and L/4): Z_0 (alone), Z_{L/2} (self pair), (Z_{L/4}, Z_{3L/4}).
-template <typename T, int LOG2L, int MODE, bool ZERO>
+// KIND 0: F = DCT-II (the middle above); KIND 1: F = partial Fourier (dct_mid.cuh dft_*, R36)
+template <typename T, int LOG2L, int MODE, bool ZERO, int KIND = 0>
 CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, const MidCtx<T>& m) {
   using SP = SwPlan<LOG2L>;
   constexpr int L = 1 << LOG2L, H = L / 2, U = SP::U, UPT = SP::UPT;
@@ -134,6 +135,19 @@ CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, 
         B0[it] = cadd<T>(b0, b1);
         B1[it] = csub<T>(b0, b1);
       }
+      if constexpr (KIND == 1) {
+        if (k != 0) {
+          const C2<T> a = tw4(k);
+          const C2<T> a2 = cmul<T>(a, a);
+          const C2<T> w = cmul<T>(a2, a2);                     // W_N^k
+          dft_pair_w<T, MODE>(A0[it], B1[it], k, w, m, rn2);
+          dft_pair_w<T, MODE>(A1[it], B0[it], k + H, mk<T>(w.y, -w.x), m, rn2);
+        } else {
+          dft_zero<T, MODE>(A0[it], m, rn2);
+          dft_pair<T, MODE>(A1[it], A1[it], H, tw4(H), m, rn2);  // self pair n = L/2
+          dft_pair<T, MODE>(B0[it], B1[it], L / 4, tw4(L / 4), m, rn2);
+        }
+      } else {
       if (k != 0) {
         const C2<T> a = tw4(k);
         const C2<T> a2 = cmul<T>(a, a);
@@ -146,6 +160,7 @@ CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, 
         mid_zero<T, MODE>(A0[it], m, rn2);
         mid_pair<T, MODE>(A1[it], A1[it], H, tw4(H), m, rn2);  // self pair n = L/2
         mid_pair<T, MODE>(B0[it], B1[it], L / 4, tw4(L / 4), m, rn2);
+      }
       }
     }
   }
@@ -193,7 +208,7 @@ template <typename T> struct SwIO {
 
 // PERM = false: the caller guarantees no Eq.(7) permutation (the CG loop of a plain
 // operator), so the scatter / gather carry no pi^-1 lookup.
-template <typename T, int LOG2L, int MODE, bool ZERO, bool PERM = true>
+template <typename T, int LOG2L, int MODE, bool ZERO, bool PERM = true, int KIND = 0>
 CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4, const MidCtx<T>& gm,
                       const SwIO<T>& gio) {
   using SP = SwPlan<LOG2L>;
@@ -233,7 +248,7 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
 #pragma unroll 1
     for (int q = 0; q < SP::Q; ++q) sw_pass<T, LOG2L, 4, false>(buf, tw, SP::NS_R16_FWD0 + 4 * q);
   }
-  const double rn2 = sw_fused<T, LOG2L, MODE, ZERO>(buf, tw, tw4, m);
+  const double rn2 = sw_fused<T, LOG2L, MODE, ZERO, KIND>(buf, tw, tw4, m);
   if constexpr (MODE != MID_FWD) {
 #pragma unroll 1
     for (int q = 0; q < SP::Q; ++q) sw_pass<T, LOG2L, 4, true>(buf, tw, 1 + 4 * q);
@@ -253,19 +268,19 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
   return rn2;
 }
 
-template <typename T, int LOG2L, int MODE, bool ZERO>
+template <typename T, int LOG2L, int MODE, bool ZERO, int KIND = 0>
 CS_NOINL double sw_sandwich_t(C2<T>* gbuf, const TwTable<T> gtw, const TwTable<T> gtw4, const MidCtx<T> gm,
                               const SwIO<T> gio) {
-  return sw_body<T, LOG2L, MODE, ZERO>(gbuf, gtw, gtw4, gm, gio);
+  return sw_body<T, LOG2L, MODE, ZERO, true, KIND>(gbuf, gtw, gtw4, gm, gio);
 }
 
 // runtime dispatch over log2 L in [LO, HI]
-template <typename T, int LO, int HI, int MODE, bool ZERO>
+template <typename T, int LO, int HI, int MODE, bool ZERO, int KIND = 0>
 CS_DEV double sw_dispatch(C2<T>* buf, int log2l, const TwTable<T>& tw, const TwTable<T>& tw4, const MidCtx<T>& m,
                           const SwIO<T>& io) {
   if constexpr (LO <= HI) {
-    if (log2l == LO) return sw_sandwich_t<T, LO, MODE, ZERO>(buf, tw, tw4, m, io);
-    return sw_dispatch<T, LO + 1, HI, MODE, ZERO>(buf, log2l, tw, tw4, m, io);
+    if (log2l == LO) return sw_sandwich_t<T, LO, MODE, ZERO, KIND>(buf, tw, tw4, m, io);
+    return sw_dispatch<T, LO + 1, HI, MODE, ZERO, KIND>(buf, log2l, tw, tw4, m, io);
   }
   return 0.0;
 }

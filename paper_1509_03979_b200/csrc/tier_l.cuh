@@ -216,6 +216,8 @@ template <typename T> CS_DEV void set_instance(GridCtx<T>& c, const OpMeta& m, i
   c.pm = m.pm(b);
   c.pinv = m.pinv(b);
   c.psi = m.psi;
+  c.fkind = m.fkind;
+  c.Mr = m.Mr;
   c.r_tmask = c.rowmask;
   c.r_tprefix = c.prefix;
   c.r_tperm = c.tperm;
@@ -237,6 +239,10 @@ template <typename T> CS_DEV void set_instance(GridCtx<T>& c, const OpMeta& m, i
 template <typename T> CS_DEV void load_yT(GridCtx<T>& c, const T* y) {
   const int32_t* tp = c.tperm;
   T* yT = c.yT;
+  if (c.fkind == 1)   // partial Fourier: (Re, Im) pairs follow their frequency
+    gstaged<TL_UNR, T>(2 * c.Mr, c.gtid, c.gnthr, [&](int64_t t) { return y[2 * tp[t >> 1] + (t & 1)]; },
+                       [&](int64_t t, T v) { yT[t] = v; });
+  else
   gstaged<TL_UNR, T>(c.M, c.gtid, c.gnthr, [&](int64_t t) { return y[tp[t]]; }, [&](int64_t t, T v) { yT[t] = v; });
   c.sync();
   c.y = c.yT;
@@ -322,6 +328,10 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_apply(LArgs<T> a) {
     T* y = a.out + b * c.M;
     const int32_t* tp = c.tperm;
     const T* yT = c.yT;
+    if (c.fkind == 1)
+      gstaged<TL_UNR, T>(2 * c.Mr, c.gtid, c.gnthr, [&](int64_t t) { return yT[t]; },
+                         [&](int64_t t, T v) { y[2 * tp[t >> 1] + (t & 1)] = v; });
+    else
     gstaged<TL_UNR, T>(c.M, c.gtid, c.gnthr, [&](int64_t t) { return yT[t]; },
                        [&](int64_t t, T v) { y[tp[t]] = v; });
     c.sync();

@@ -65,12 +65,14 @@ CS_HD SLayout s_layout(int64_t N, int K, int ucap, bool pursuit) {
 // and tperm[t_rank] = y index of the t_rank-th selected row in that order.
 struct OpMeta {
   const uint32_t* base;
-  int64_t N, M;
+  int64_t N, M;          // M: measurements (= rows for the DCT, 2 x frequencies for the DFT)
+  int64_t Mr;            // metadata rows (tperm length)
   int64_t nw;
   int64_t stride;  // words per instance
   int64_t toff;    // word offset of the transposed mask within an instance
   const int32_t* perm;  // Eq.(7) randomizer R (R34): per instance [pi N][pi^-1 N], or null
   int psi;              // dictionary: 0 = I, 1 = C_N (R35)
+  int fkind;            // F: 0 = DCT-II, 1 = partial Fourier (R36; perm then holds the position map)
   const uint32_t* full; // Psi mode: the all-rows instance (stride meta_stride(N, N)), or null
   CS_HD const uint32_t* sign(int64_t b) const { return base + b * stride; }
   CS_HD const uint32_t* rmask(int64_t b) const { return base + b * stride + nw; }
@@ -124,6 +126,7 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   c.ccnt = reinterpret_cast<int*>(smem + lay.ccnt);
   c.rbank = 0;
   c.psi = meta.psi;
+  c.fkind = meta.fkind;
   c.G = nullptr;
   c.phi_sign = meta.sign(b);
   c.phi_pinv = meta.pinv(b);
