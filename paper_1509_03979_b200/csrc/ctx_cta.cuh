@@ -312,16 +312,55 @@ template <typename T> struct CtaCtx {
     __syncthreads();
   }
   // Z <- Makhoul order of u = R diag(sigma) G: u_{pi^-1(j)} = sigma_j G_j
+  // (8 elements per thread in flight: the global loads of G, pi^-1 and the sign words are
+  // issued before any dependent shared access)
   CS_NOINL void phi_in() {
     T* zb = reinterpret_cast<T*>(Z);
-    for (int64_t j = gtid; j < N; j += gnthr)
-      zb[zt(ppos(phi_pinv, j, N))] = apply_sign<T>(phi_sign, j, G[j]);
+    const int n = (int)N, t0 = threadIdx.x, nt = blockDim.x;
+    const int32_t* pv = phi_pinv;
+    const uint32_t* sg = phi_sign;
+    const T* g = G;
+    for (int j0 = t0; j0 < n; j0 += 8 * nt) {
+      T v[8];
+      int p[8];
+      uint32_t w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * nt;
+        if (j < n) { v[u] = g[j]; p[u] = pv ? pv[j] : j; w[u] = sg[j >> 5]; }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * nt;
+        if (j < n) zb[zt((int)mk_pos(p[u], n))] = ((w[u] >> (j & 31)) & 1u) ? -v[u] : v[u];
+      }
+    }
     __syncthreads();
   }
   // G <- diag(sigma) R^T v, v in Makhoul order in Z: G_j = sigma_j v_{pi^-1(j)}
   CS_NOINL void phi_out() {
     const T* zb = zbuf();
-    for (int64_t j = gtid; j < N; j += gnthr) G[j] = apply_sign<T>(phi_sign, j, zb[zt(ppos(phi_pinv, j, N))]);
+    const int n = (int)N, t0 = threadIdx.x, nt = blockDim.x;
+    const int32_t* pv = phi_pinv;
+    const uint32_t* sg = phi_sign;
+    T* g = G;
+    for (int j0 = t0; j0 < n; j0 += 8 * nt) {
+      int p[8];
+      uint32_t w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * nt;
+        if (j < n) { p[u] = pv ? pv[j] : j; w[u] = sg[j >> 5]; }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * nt;
+        if (j < n) {
+          const T v = zb[zt((int)mk_pos(p[u], n))];
+          g[j] = ((w[u] >> (j & 31)) & 1u) ? -v : v;
+        }
+      }
+    }
     __syncthreads();
   }
   // G <- C_N s, s = scatter_S(vin) (vin == nullptr: s already in Z, Makhoul order)

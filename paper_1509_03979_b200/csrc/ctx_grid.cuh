@@ -855,8 +855,21 @@ template <typename T> struct GridCtx {
     const T* g = G;
     T* u = U;
     const int64_t n = N;
-    gstaged<TL_UNR, T>(N, gtid, gnthr, [&](int64_t j) { return apply_sign<T>(sg, j, g[j]); },
-                       [&](int64_t j, T v) { u[ppos(pv, j, n)] = v; });
+    // value and position loaded together (no dependent load in the store phase)
+    for (int64_t j0 = gtid; j0 < n; j0 += TL_UNR * gnthr) {
+      T v[TL_UNR];
+      int64_t p[TL_UNR];
+#pragma unroll
+      for (int q = 0; q < TL_UNR; ++q) {
+        const int64_t j = j0 + q * gnthr;
+        if (j < n) { v[q] = apply_sign<T>(sg, j, g[j]); p[q] = pv ? pv[j] : j; }
+      }
+#pragma unroll
+      for (int q = 0; q < TL_UNR; ++q) {
+        const int64_t j = j0 + q * gnthr;
+        if (j < n) u[mk_pos(p[q], n)] = v[q];
+      }
+    }
     sync();
   }
   // G <- diag(sigma) R^T v, v = Cb (Makhoul order)
