@@ -115,3 +115,12 @@ def test_dft_all_ties_zero_measurements(cs, N, M, K):
     refs = oracle_results(probs, ys)
     for b in range(2):
         assert np.array_equal(np.sort(supp[b]), refs[b].support)
+
+
+@pytest.mark.parametrize("N,M,K,alg", [(16, 6, 1, "omp"), (32, 12, 2, "sp"), (64, 24, 3, "ompr"),
+                                       (64, 30, 4, "cosamp"), (128, 48, 5, "sp")])
+def test_dft_tiny_sizes_fp64(cs, N, M, K, alg):
+    cfg, probs = _probs(N, M, K, 3, alg=alg)
+    ys, supp, vals, reps = _recover(cs, cfg, probs, "float64")
+    bad, _ = compare(probs, oracle_results(probs, ys), supp, vals, rtol=1e-9)
+    assert not bad, bad

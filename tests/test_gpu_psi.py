@@ -117,3 +117,12 @@ def test_psi_recovery_grid_tier_ompr_fp32(cs):
     bad, _ = compare(probs, oracle_results(probs, ys), supp, vals)
     assert not bad, bad
     assert np.array_equal(np.sort(supp[0]), probs[0].support)
+
+
+@pytest.mark.parametrize("N,M,K,alg", [(16, 8, 2, "sp"), (32, 16, 3, "ompr"), (64, 32, 4, "omp"),
+                                       (64, 32, 4, "cosamp")])
+def test_psi_tiny_sizes_fp64(cs, N, M, K, alg):
+    cfg, probs = _probs(N, M, K, 3, alg=alg, randomizer="perm")
+    ys, supp, vals, reps = _recover(cs, cfg, probs, "float64")
+    bad, _ = compare(probs, oracle_results(probs, ys), supp, vals, rtol=1e-9)
+    assert not bad, bad
