@@ -268,7 +268,10 @@ template <typename T> struct CtaCtx {
   // caller stays small)
   template <class S> CS_NOINL void cg_iterate_variant(S& s) {
     if (psi) {
-      cg_loop(*this, s, [this](const T* d, T* q) { H_psi(d, q); });
+      cg_loop(*this, s, [this](const T* d, T* q) {
+        H_psi(d, q);
+        return dot_n(*this, d, q, in_ns);
+      });
       return;
     }
     if (fkind) cg_dispatch<2, 13, true, 1>(s);  // partial Fourier: always position-mapped

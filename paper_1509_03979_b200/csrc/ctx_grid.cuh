@@ -538,7 +538,10 @@ template <typename T> struct GridCtx {
   // pass C with a sparse output (H d restricted to the support): after the inverse column
   // FFT each tile writes only its support entries, q_i = sigma_j . buf[p_i] — Cb is never
   // written and no separate gather runs
-  CS_NOINL void passC_sparse(T* outv) {
+  // dvec != nullptr: also returns this thread's share of sum_i dvec_i outv_i (H's dot
+  // product, reduced by the caller with the pass's closing barrier)
+  CS_NOINL double passC_sparse(T* outv, const T* dvec = nullptr) {
+    double dot = 0;
     const int ct = CT, lct = (ct == 4) ? 2 : 1;
     const int64_t l2 = L2, ntl = L2 / ct;
     const int tile = (int)(L1 * ct);
@@ -581,14 +584,19 @@ template <typename T> struct GridCtx {
           for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
             const int w = stg[2 * q];
             const T v = sbt[w & 0x7fffffff];
-            outv[stg[2 * q + 1]] = (w < 0) ? -v : v;
+            const int oi = stg[2 * q + 1];
+            const T o = (w < 0) ? -v : v;
+            outv[oi] = o;
+            if (dvec) dot += (double)dvec[oi] * (double)o;
           }
         } else {
           for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
             const int i = tlist[q];
             const int64_t p = ip[i], c = p >> 1;
             const int e = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
-            outv[i] = apply_sign<T>(sg, sp[i], sbt[2 * swz<T>(e) + (int)(p & 1)]);
+            const T o = apply_sign<T>(sg, sp[i], sbt[2 * swz<T>(e) + (int)(p & 1)]);
+            outv[i] = o;
+            if (dvec) dot += (double)dvec[i] * (double)o;
           }
         }
         __syncthreads();
@@ -596,6 +604,7 @@ template <typename T> struct GridCtx {
       q0 = q0n;
       q1 = q1n;
     }
+    return dot;
   }
   template <int MODE> CS_NOINL double passB(bool zero_input, T* yout) {
     MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, yout);
@@ -807,8 +816,40 @@ template <typename T> struct GridCtx {
     mark(3);
     ++applies;
   }
+  // q = H d and d.q: the dot product rides on pass C (each block sums the entries it
+  // writes) and on the barrier that closes H — one grid barrier per CG iteration less
+  CS_NOINL double H_dot(const T* d, T* q) {
+    if (psi) {
+      H_psi(d, q);
+      return dot_n(*this, d, q, in_ns);
+    }
+    mark(0);
+    passA_sparse(d);
+    sync();
+    mark(1);
+    passB<MID_H>(false, nullptr);
+    sync();
+    mark(2);
+    const double t = block_sum(passC_sparse(q, d));
+    double* P = g.pd + bank * g.maxgrid;
+    if (threadIdx.x == 0) P[blockIdx.x] = t;
+    sync();                                    // publishes q and the per-block partials
+    if (threadIdx.x < 32) {
+      double a = 0;
+      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) a += P[c];
+      a = warp_sum_g(a);
+      if (threadIdx.x == 0) sd[32] = a;
+    }
+    __syncthreads();
+    const double tot = sd[32];
+    __syncthreads();
+    bank ^= 1;
+    mark(3);
+    ++applies;
+    return tot;
+  }
   template <class S> CS_NOINL void cg_iterate(S& s) {
-    cg_loop(*this, s, [this](const T* d, T* q) { H(d, q); });
+    cg_loop(*this, s, [this](const T* d, T* q) { return H_dot(d, q); });
   }
   CS_NOINL double RES(const T* x) {
     if (psi) return RES_psi(x);

@@ -49,8 +49,17 @@ template <typename T> struct CgState {
   unsigned status;
 };
 
+// sum_i a_i b_i over i < n, deterministic (the context's fixed-order sum)
+template <class Ctx, typename T>
+CS_DEV double dot_n(Ctx& c, const T* a, const T* b, int n) {
+  double v = 0;
+  for (int i = c.gtid; i < n; i += c.gnthr) v += (double)a[i] * (double)b[i];
+  return c.sum(v);
+}
+
 // The CG iteration loop, generic over the context; Hf(d, q) applies
-// q = H d on the context's remembered support.  Each context runs it from its
+// q = H d on the context's remembered support and returns d.q (the grid context fuses
+// the dot product into H's last pass and barrier).  Each context runs it from its
 // cg_iterate(): the grid context directly, the CTA context from an out-of-line
 // instance per transform length with the sandwich inlined.
 template <class Ctx, typename T, class HFn>
@@ -62,10 +71,7 @@ CS_DEV void cg_loop(Ctx& c, CgState<T>& s_io, HFn&& Hf) {
   while (true) {
     if (!(s.rr > s.thr)) break;                                            // line 15 (R6, R7)
     if (s.j >= s.cap) { s.status |= CS_DEV_CG_CAP; break; }
-    Hf(dv, qv);                                                            // H d_j
-    double dq = 0;
-    for (int i = a0; i < n; i += s0) dq += (double)dv[i] * (double)qv[i];
-    dq = c.sum(dq);
+    const double dq = Hf(dv, qv);                                          // H d_j, d_j.H d_j
     if (!(dq > 0.0)) { s.status |= CS_DEV_CG_BREAKDOWN; break; }
     const T alpha = (T)(s.rr / dq);                                        // line 16
     double rr2 = 0;
