@@ -28,7 +28,16 @@ CS_DEV double warp_sum(double v) {
 template <typename T> struct CtaCtx {
   using Key = typename KeyT<T>::type;
   // ids
-  int gtid, gnthr, lane, gwarp, gnwarps;
+  // ids: derived from the special registers / compile-time block size on every use, never
+  // stored (the context object lives in local memory; a stored id is a local load per use)
+  struct TidV { CS_DEV operator int() const { return (int)threadIdx.x; } };
+  struct LaneV { CS_DEV operator int() const { return (int)(threadIdx.x & 31); } };
+  struct WarpV { CS_DEV operator int() const { return (int)(threadIdx.x >> 5); } };
+  TidV gtid;
+  LaneV lane;
+  WarpV gwarp;
+  static constexpr int gnthr = SW_NT;
+  static constexpr int gnwarps = SW_NT / 32;
   int64_t N, M, L;
   int log2L;
   // shared-memory state

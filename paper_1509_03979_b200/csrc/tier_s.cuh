@@ -97,11 +97,6 @@ struct OpMeta {
 template <typename T>
 CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta, int64_t b) {
   CtaCtx<T> c;
-  c.gtid = threadIdx.x;
-  c.gnthr = blockDim.x;
-  c.lane = threadIdx.x & 31;
-  c.gwarp = threadIdx.x >> 5;
-  c.gnwarps = blockDim.x >> 5;
   c.N = meta.N;
   c.M = meta.M;
   c.L = meta.N / 2;
@@ -294,11 +289,6 @@ __global__ void __launch_bounds__(TS_THREADS, 1) k_s_diag_topk(SLayout lay, cons
                                                               uint32_t* out_bits) {
   extern __shared__ __align__(16) char smem[];
   CtaCtx<T> c;
-  c.gtid = threadIdx.x;
-  c.gnthr = blockDim.x;
-  c.lane = threadIdx.x & 31;
-  c.gwarp = threadIdx.x >> 5;
-  c.gnwarps = blockDim.x >> 5;
   c.redd = reinterpret_cast<double*>(smem + lay.redd);
   c.redi = reinterpret_cast<int64_t*>(smem + lay.redi);
   c.redk = reinterpret_cast<typename CtaCtx<T>::Key*>(smem + lay.redk);
