@@ -130,7 +130,17 @@ template <typename T> CS_DEV void stp(C2<T>* p, const CP<T>& v) {
 
 template <typename T> struct GridCtx {
   using Key = typename KeyT<T>::type;
-  int gtid, gnthr, lane, gwarp, gnwarps;
+  // ids derived from the special registers on use (the context lives in local memory)
+  struct TidV { CS_DEV operator int() const { return (int)(blockIdx.x * blockDim.x + threadIdx.x); } };
+  struct NthrV { CS_DEV operator int() const { return (int)(gridDim.x * blockDim.x); } };
+  struct LaneV { CS_DEV operator int() const { return (int)(threadIdx.x & 31); } };
+  struct WarpV { CS_DEV operator int() const { return (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); } };
+  struct NwarpV { CS_DEV operator int() const { return (int)((gridDim.x * blockDim.x) >> 5); } };
+  TidV gtid;
+  NthrV gnthr;
+  LaneV lane;
+  WarpV gwarp;
+  NwarpV gnwarps;
   int64_t N, M, L, L1, L2;
   int CT, log2L1, log2L2;
   // global per-problem state

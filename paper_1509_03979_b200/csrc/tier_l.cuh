@@ -134,11 +134,6 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   GridCtx<T> c;
   LGeom g = l_geom(a.meta.N);
   const LLayout& s = a.lay;
-  c.gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  c.gnthr = gridDim.x * blockDim.x;
-  c.lane = threadIdx.x & 31;
-  c.gwarp = c.gtid >> 5;
-  c.gnwarps = c.gnthr >> 5;
   c.N = a.meta.N;
   c.M = a.meta.M;
   c.L = g.L;
@@ -272,7 +267,7 @@ CS_NOINL void l_apply_psi_input(GridCtx<T>& c, const T* x) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(TL_THREADS) k_l_apply(LArgs<T> a) {
+__global__ void __launch_bounds__(TL_THREADS, 2) k_l_apply(LArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
   GridCtx<T> c = make_grid_ctx<T>(smem, a);
   const int64_t N = c.N;
@@ -340,7 +335,7 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_apply(LArgs<T> a) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(TL_THREADS) k_l_adjoint(LArgs<T> a) {
+__global__ void __launch_bounds__(TL_THREADS, 2) k_l_adjoint(LArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
   GridCtx<T> c = make_grid_ctx<T>(smem, a);
   const int64_t N = c.N;
@@ -360,7 +355,7 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_adjoint(LArgs<T> a) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(TL_THREADS) k_l_recover(LArgs<T> a) {
+__global__ void __launch_bounds__(TL_THREADS, 2) k_l_recover(LArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
   GridCtx<T> c = make_grid_ctx<T>(smem, a);
   const LLayout& s = a.lay;
