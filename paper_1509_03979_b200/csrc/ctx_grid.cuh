@@ -222,7 +222,7 @@ template <typename T> struct GridCtx {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     return v;
   }
-  CS_NOINL double sum(double v) {
+  CS_DEV double sum(double v) {
     double t = block_sum(v);
     double* P = g.pd + bank * g.maxgrid;
     if (threadIdx.x == 0) P[blockIdx.x] = t;
@@ -239,7 +239,7 @@ template <typename T> struct GridCtx {
     bank ^= 1;
     return tot;
   }
-  CS_NOINL int64_t argmax(Key k, int64_t idx) {
+  CS_DEV int64_t argmax(Key k, int64_t idx) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       Key k2 = __shfl_down_sync(0xffffffffu, k, o);
@@ -281,7 +281,7 @@ template <typename T> struct GridCtx {
     bank ^= 1;
     return r;
   }
-  CS_NOINL int64_t excl_scan(int64_t v, int64_t* total) {
+  CS_DEV int64_t excl_scan(int64_t v, int64_t* total) {
     int64_t inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
