@@ -316,6 +316,7 @@ struct HostPipe {
   cudaEvent_t ev[2][64] = {};
   cudaEvent_t fin = nullptr;
   bool ok = false;
+  std::mutex enq;  // one host thread enqueues a pipeline at a time (the events are reused)
 };
 HostPipe& host_pipe(int dev) {
   static std::mutex mu;
@@ -367,6 +368,9 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
   CS_CUDA(cudaGetDevice(&dev));
   HostPipe& hp = host_pipe(dev);
   if (!hp.ok) return fail(CS_ERR_CUDA, "could not create the host-pipeline streams");
+  // the streams and events are per device: concurrent callers enqueue one after the other
+  // (cudaStreamWaitEvent binds each wait to the event's record at enqueue time)
+  std::lock_guard<std::mutex> enqueue_lock(hp.enq);
   const int l = (opts && opts->ompr_l > 0) ? opts->ompr_l : 1;
   const bool tier_s = tier_s_fits<T>(N, K, ucap_of(alg, K, l), true);
   int nsm = 148;
