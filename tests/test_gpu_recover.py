@@ -283,3 +283,31 @@ def test_max_size_n_2_pow_25(cs):
     assert np.linalg.norm(s - p.s) <= 1e-4 * np.linalg.norm(p.s)
     r = ys[0].astype(np.float64) - op.apply(s)
     assert np.linalg.norm(op.adjoint(r)[supp[0]]) <= 1e-4 * np.linalg.norm(op.adjoint(ys[0].astype(np.float64))[supp[0]])
+
+
+@pytest.mark.parametrize("variant", ["perm", "psi", "dft"])
+def test_host_buffer_entry_point_operator_variants(cs, variant):
+    """The chunked host pipeline slices per-instance operator data (pi / pi^-1, the DFT
+    position map; the shared all-rows instance of Psi) correctly: host results equal the
+    device entry point's over several chunks and a ragged tail."""
+    kw = {"perm": dict(randomizer="perm"), "psi": dict(randomizer="perm", psi="dct"),
+          "dft": dict(randomizer="perm", transform="dft")}[variant]
+    cfg = cs_inputs.Config(73, "sp", 2048, 512, 16, "gauss", 0.0, **kw)
+    B = 1300
+    probs = cs_inputs.make_batch(cfg, count=B)
+    ys = measured(probs)
+    dev = torch.device("cuda:0")
+    bits, rows = to_dev(probs, dev)
+    A = cs.Operator(cfg.N, probs[0].M, None, rows, batch=B, perm=perms_dev(probs, dev),
+                    psi=("dct" if variant == "psi" else None), transform=probs[0].transform)
+    Yd = torch.from_numpy(ys).to(dev)
+    ref = cs.cs_recover_batched(A, cfg.alg, Yd, cfg.K, 1e-6)
+    host = cs.cs_recover_batched_host(A, cfg.alg, torch.from_numpy(ys).pin_memory(), cfg.K, 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(host.support, ref.support.cpu())
+    assert torch.equal(host.values, ref.values.cpu())
+    pick = [0, 517, 1299]
+    sub = [probs[i] for i in pick]
+    bad, _ = compare(sub, oracle_results(sub, ys[pick]), ref.support.cpu().numpy()[pick],
+                     ref.values.cpu().numpy()[pick].astype(np.float64))
+    assert not bad, bad
