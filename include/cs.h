@@ -209,6 +209,29 @@ cs_status cs_recover_batched_f64(const cs_operator* op, int alg, const double* d
                                  cs_report* d_reports, void* d_ws, size_t ws_bytes,
                                  cs_stream_t stream);
 
+/* Dense output: d_dense [B][N] = 0 except d_dense[b][d_support[b][k]] = d_vals[b][k]
+ * (support entries < 0, as written for a short support, are skipped).  Async on `stream`. */
+cs_status cs_support_to_dense(int64_t B, int64_t N, int32_t K, const int32_t* d_support, const float* d_vals,
+                              float* d_dense, cs_stream_t stream);
+cs_status cs_support_to_dense_f64(int64_t B, int64_t N, int32_t K, const int32_t* d_support,
+                                  const double* d_vals, double* d_dense, cs_stream_t stream);
+
+/* ---------------------------------------------------------------- multi-GPU ---
+ * Results gather for independent problems sharded over the GPUs of one process (SV §8e:
+ * the only cross-GPU traffic of the batched path; no data-path collective).  NCCL is
+ * loaded at run time (libnccl.so.2); without it cs_comm_init returns CS_ERR_UNSUPPORTED.
+ *   cs_comm_init(ndev, devices, &comm): one communicator per device (ncclCommInitAll).
+ *   cs_gather_batched: device i (in `devices` order) holds B_per_dev records in
+ *     d_vals[i] [B][K] fp32, d_support[i] [B][K], d_reports[i] [B]; they land at block i of
+ *     the root's d_vals_all / d_support_all / d_reports_all ([ndev][B]...).  Blocking: returns
+ *     after the transfers (NCCL send/recv over NVLink; the root copies its own block).
+ * (Multi-process jobs use torch.distributed, paper_1509_03979_b200/dist.py.) */
+cs_status cs_comm_init(int ndev, const int* devices, void** comm);
+cs_status cs_gather_batched(void* comm, int root, int64_t B_per_dev, int32_t K, const float* const* d_vals,
+                            const int32_t* const* d_support, const cs_report* const* d_reports,
+                            float* d_vals_all, int32_t* d_support_all, cs_report* d_reports_all);
+cs_status cs_comm_destroy(void* comm);
+
 /* Host-buffer variants (the end-to-end entry points): h_Y [B][M] and the outputs
  * h_vals [B][K], h_support [B][K], h_reports [B] are HOST memory (pinned for overlap).
  * The batch is copied in, recovered and copied out in chunks of two recovery waves, on

@@ -58,6 +58,7 @@ EXPORTS = [
     "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
     "cs_diag_topk", "cs_operator_meta_bytes_perm", "cs_operator_create_perm", "cs_operator_create_ex",
     "cs_operator_meta_bytes_ex", "cs_operator_meta_bytes_dft", "cs_operator_create_dft",
+    "cs_support_to_dense", "cs_support_to_dense_f64", "cs_comm_init", "cs_gather_batched", "cs_comm_destroy",
 ]
 
 
@@ -77,6 +78,12 @@ def load_library(path: str = LIB_PATH):
         "cs_operator_create_perm": (I32, [I64, I64, I64, P, P, P, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_meta_bytes_ex": (SZ, [I64, I64, I64, ctypes.c_int, ctypes.c_int]),
         "cs_operator_meta_bytes_dft": (SZ, [I64, I64, I64]),
+        "cs_support_to_dense": (I32, [I64, I64, I32, P, P, P, P]),
+        "cs_support_to_dense_f64": (I32, [I64, I64, I32, P, P, P, P]),
+        "cs_comm_init": (I32, [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(P)]),
+        "cs_gather_batched": (I32, [P, ctypes.c_int, I64, I32, ctypes.POINTER(P), ctypes.POINTER(P),
+                                    ctypes.POINTER(P), P, P, P]),
+        "cs_comm_destroy": (I32, [P]),
         "cs_operator_create_dft": (I32, [I64, I64, I64, P, P, P, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_create_ex": (I32, [I64, I64, I64, P, P, P, ctypes.c_int, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_destroy": (I32, [P]),
@@ -351,3 +358,51 @@ def cs_recover(op: Operator, alg, y, M: int, N: int, K: int, tol: float,
              _ptr(out.values), _ptr(out.support), _ptr(out.report_dev), _ptr(ws), ws.numel(),
              _stream(stream)), "cs_recover")
     return out
+
+
+def cs_support_to_dense(support, values, N: int, stream=None):
+    """Dense [B][N] signals from (support, values) of a recovery (cs_support_to_dense)."""
+    torch = _torch()
+    B, K = support.shape
+    out = torch.empty((B, N), dtype=values.dtype, device=values.device)
+    f = _lib.cs_support_to_dense_f64 if values.dtype == torch.float64 else _lib.cs_support_to_dense
+    _check(f(B, N, K, _ptr(support.contiguous()), _ptr(values.contiguous()), _ptr(out), _stream(stream)),
+           "cs_support_to_dense")
+    return out
+
+
+class Comm:
+    """Single-process multi-GPU results gather (cs_comm_init / cs_gather_batched)."""
+
+    def __init__(self, devices):
+        load_library()
+        self.devices = [int(d) for d in devices]
+        arr = (ctypes.c_int * len(self.devices))(*self.devices)
+        h = ctypes.c_void_p()
+        _check(_lib.cs_comm_init(len(self.devices), arr, ctypes.byref(h)), "cs_comm_init")
+        self.handle = h
+
+    def gather(self, results, root: int = 0):
+        """results: one Recovery per device (same B, K; fp32), in `devices` order.  Returns the
+        root's concatenated (support, values, raw reports) tensors."""
+        torch = _torch()
+        nd = len(self.devices)
+        B, K = results[0].support.shape
+        dev = results[root].support.device
+        vals = torch.empty((nd * B, K), dtype=torch.float32, device=dev)
+        supp = torch.empty((nd * B, K), dtype=torch.int32, device=dev)
+        reps = torch.empty((nd * B, 40), dtype=torch.uint8, device=dev)
+        P = ctypes.c_void_p
+        pv = (P * nd)(*[r.values.data_ptr() for r in results])
+        ps = (P * nd)(*[r.support.data_ptr() for r in results])
+        pr = (P * nd)(*[r.report_dev.data_ptr() for r in results])
+        _check(_lib.cs_gather_batched(self.handle, root, B, K, pv, ps, pr, _ptr(vals), _ptr(supp), _ptr(reps)),
+               "cs_gather_batched")
+        return supp, vals, reps
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and _lib is not None:
+                _lib.cs_comm_destroy(self.handle)
+        except Exception:
+            pass

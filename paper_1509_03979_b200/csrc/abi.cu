@@ -6,7 +6,11 @@
 //     one thread block per problem (tier_s.cuh);
 //   Tier L (larger N): one cooperative persistent grid per problem with a
 //     four-step FFT over L2-resident scratch (tier_l.cuh).
+#include <dlfcn.h>
+#include <nccl.h>  // types and prototypes only: libnccl is loaded at run time (cs_comm_init)
+
 #include <algorithm>
+#include <vector>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -413,6 +417,63 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
 
 }  // namespace
 
+namespace {
+// dense output: d_dense[b] = scatter(d_support[b], d_vals[b]) (support entries < 0 skipped)
+template <typename T>
+__global__ void k_dense(int64_t B, int64_t N, int32_t K, const int32_t* supp, const T* vals, T* dense) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= B * (int64_t)K) return;
+  const int64_t b = i / K;
+  const int32_t j = supp[i];
+  if (j >= 0 && j < N) dense[b * N + j] = vals[i];
+}
+template <typename T>
+cs_status dense_impl(int64_t B, int64_t N, int32_t K, const int32_t* supp, const T* vals, T* dense,
+                     cudaStream_t st) {
+  if (!supp || !vals || !dense) return fail(CS_ERR_INVALID_ARG, "null pointer argument");
+  if (B < 1 || N < 1 || K < 1) return fail(CS_ERR_INVALID_ARG, "bad sizes");
+  CS_CUDA(cudaMemsetAsync(dense, 0, (size_t)(B * N) * sizeof(T), st));
+  k_dense<T><<<(unsigned)((B * K + 255) / 256), 256, 0, st>>>(B, N, K, supp, vals, dense);
+  CS_LAUNCHED();
+  return CS_OK;
+}
+
+// NCCL, resolved at run time (the torch process has usually loaded it already)
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclCommInitAll) init_all = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) err = nullptr;
+};
+const NcclApi& nccl_api() {
+  static NcclApi a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    a.init_all = reinterpret_cast<decltype(&ncclCommInitAll)>(dlsym(h, "ncclCommInitAll"));
+    a.destroy = reinterpret_cast<decltype(&ncclCommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.send = reinterpret_cast<decltype(&ncclSend)>(dlsym(h, "ncclSend"));
+    a.recv = reinterpret_cast<decltype(&ncclRecv)>(dlsym(h, "ncclRecv"));
+    a.group_start = reinterpret_cast<decltype(&ncclGroupStart)>(dlsym(h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<decltype(&ncclGroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    a.err = reinterpret_cast<decltype(&ncclGetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.init_all && a.destroy && a.send && a.recv && a.group_start && a.group_end && a.err;
+  });
+  return a;
+}
+struct CsComm {
+  std::vector<int> dev;
+  std::vector<ncclComm_t> comms;
+  std::vector<cudaStream_t> streams;
+};
+}  // namespace
+
 extern "C" {
 
 size_t cs_operator_meta_bytes(int64_t N, int64_t M, int64_t batch) {
@@ -727,6 +788,111 @@ int64_t cs_diag_phase_offset(int alg, int64_t N, int64_t M, int32_t K, int32_t o
   const LLayout s = precision ? l_layout<double>(N, M, K, (int)ucap, true, l_grid_upper<double>())
                               : l_layout<float>(N, M, K, (int)ucap, true, l_grid_upper<float>());
   return s.ts + 8 * 8;
+}
+
+// ---------------------------------------------------------------- dense output ----
+cs_status cs_support_to_dense(int64_t B, int64_t N, int32_t K, const int32_t* d_support, const float* d_vals,
+                              float* d_dense, cs_stream_t stream) {
+  return dense_impl<float>(B, N, K, d_support, d_vals, d_dense, reinterpret_cast<cudaStream_t>(stream));
+}
+cs_status cs_support_to_dense_f64(int64_t B, int64_t N, int32_t K, const int32_t* d_support,
+                                  const double* d_vals, double* d_dense, cs_stream_t stream) {
+  return dense_impl<double>(B, N, K, d_support, d_vals, d_dense, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- multi-GPU gather ----
+cs_status cs_comm_init(int ndev, const int* devices, void** comm) {
+  if (!comm || !devices || ndev < 1 || ndev > 64) return fail(CS_ERR_INVALID_ARG, "bad arguments");
+  *comm = nullptr;
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(CS_ERR_UNSUPPORTED, "libnccl.so.2 could not be loaded");
+  CsComm* c = new CsComm;
+  c->dev.assign(devices, devices + ndev);
+  c->comms.assign(ndev, nullptr);
+  c->streams.assign(ndev, nullptr);
+  ncclResult_t r = api.init_all(c->comms.data(), ndev, devices);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(CS_ERR_CUDA, std::string("ncclCommInitAll: ") + api.err(r));
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int i = 0; i < ndev; ++i) {
+    cudaSetDevice(devices[i]);
+    cudaStreamCreateWithFlags(&c->streams[i], cudaStreamNonBlocking);
+  }
+  cudaSetDevice(cur);
+  *comm = c;
+  return CS_OK;
+}
+
+cs_status cs_gather_batched(void* comm, int root, int64_t B_per_dev, int32_t K, const float* const* d_vals,
+                            const int32_t* const* d_support, const cs_report* const* d_reports, float* d_vals_all,
+                            int32_t* d_support_all, cs_report* d_reports_all) {
+  CsComm* c = reinterpret_cast<CsComm*>(comm);
+  if (!c || !d_vals || !d_support || !d_reports || !d_vals_all || !d_support_all || !d_reports_all)
+    return fail(CS_ERR_INVALID_ARG, "null pointer argument");
+  const int nd = (int)c->dev.size();
+  if (root < 0 || root >= nd || B_per_dev < 1 || K < 1) return fail(CS_ERR_INVALID_ARG, "bad arguments");
+  const NcclApi& api = nccl_api();
+  const size_t bv = (size_t)(B_per_dev * K) * 4, br = (size_t)B_per_dev * sizeof(cs_report);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  // device i's records land at block i of the root's arrays; the root copies its own block
+  CS_CUDA(cudaSetDevice(c->dev[root]));
+  for (int kind = 0; kind < 3; ++kind) {
+    const size_t bytes = kind == 2 ? br : bv;
+    char* dst = kind == 0 ? reinterpret_cast<char*>(d_vals_all)
+              : kind == 1 ? reinterpret_cast<char*>(d_support_all) : reinterpret_cast<char*>(d_reports_all);
+    const void* src = kind == 0 ? (const void*)d_vals[root] : kind == 1 ? (const void*)d_support[root]
+                                                                        : (const void*)d_reports[root];
+    CS_CUDA(cudaMemcpyAsync(dst + (size_t)root * bytes, src, bytes, cudaMemcpyDeviceToDevice, c->streams[root]));
+  }
+  if (nd > 1) {
+    api.group_start();
+    for (int i = 0; i < nd; ++i) {
+      if (i == root) continue;
+      for (int kind = 0; kind < 3; ++kind) {
+        const size_t bytes = kind == 2 ? br : bv;
+        char* dst = kind == 0 ? reinterpret_cast<char*>(d_vals_all)
+                  : kind == 1 ? reinterpret_cast<char*>(d_support_all) : reinterpret_cast<char*>(d_reports_all);
+        const void* src = kind == 0 ? (const void*)d_vals[i] : kind == 1 ? (const void*)d_support[i]
+                                                                         : (const void*)d_reports[i];
+        api.send(src, bytes, ncclUint8, root, c->comms[i], c->streams[i]);
+        api.recv(dst + (size_t)i * bytes, bytes, ncclUint8, i, c->comms[root], c->streams[root]);
+      }
+    }
+    const ncclResult_t r = api.group_end();
+    if (r != ncclSuccess) {
+      cudaSetDevice(cur);
+      return fail(CS_ERR_CUDA, std::string("nccl gather: ") + api.err(r));
+    }
+  }
+  for (int i = 0; i < nd; ++i) {
+    cudaSetDevice(c->dev[i]);
+    if (cudaStreamSynchronize(c->streams[i]) != cudaSuccess) {
+      cudaSetDevice(cur);
+      return fail(CS_ERR_CUDA, "gather stream synchronisation failed");
+    }
+  }
+  cudaSetDevice(cur);
+  return CS_OK;
+}
+
+cs_status cs_comm_destroy(void* comm) {
+  CsComm* c = reinterpret_cast<CsComm*>(comm);
+  if (!c) return CS_OK;
+  const NcclApi& api = nccl_api();
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (size_t i = 0; i < c->dev.size(); ++i) {
+    cudaSetDevice(c->dev[i]);
+    if (c->streams[i]) cudaStreamDestroy(c->streams[i]);
+    if (c->comms[i] && api.ok) api.destroy(c->comms[i]);
+  }
+  cudaSetDevice(cur);
+  delete c;
+  return CS_OK;
 }
 
 }  // extern "C"
