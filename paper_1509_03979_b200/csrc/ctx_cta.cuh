@@ -194,10 +194,8 @@ template <typename T> struct CtaCtx {
   }
   // fused sandwich (sandwich_cta.cuh): scatter, forward FFT, DCT middle, inverse FFT, gather
   template <int MODE, bool ZERO> CS_DEV double sandwich(const T* vin, T* vout, T* yout) {
-    const MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, yout);
-    const SwIO<T> io{in_supp, in_ns, sign, vin, vout};
-    if (fkind) return sw_dispatch<T, 2, 13, MODE, ZERO, 1>(Z, log2L, twL, tw4, m, io);
-    return sw_dispatch<T, 2, 13, MODE, ZERO, 0>(Z, log2L, twL, tw4, m, io);
+    if (fkind) return sw_dispatch<T, 2, 13, MODE, ZERO, 1>(log2L, y, yout, in_supp, in_ns, vin, vout);
+    return sw_dispatch<T, 2, 13, MODE, ZERO, 0>(log2L, y, yout, in_supp, in_ns, vin, vout);
   }
   // CG iterations with the sandwich of one compile-time length inlined: no call
   // (and no ABI register save/restore) inside the loop.

@@ -268,19 +268,23 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
   return rn2;
 }
 
+// Out of line: only scalars cross the call (no structs passed by value — at 1024
+// threads per SM every by-value byte is a local-memory store and load).
 template <typename T, int LOG2L, int MODE, bool ZERO, int KIND = 0>
-CS_NOINL double sw_sandwich_t(C2<T>* gbuf, const TwTable<T> gtw, const TwTable<T> gtw4, const MidCtx<T> gm,
-                              const SwIO<T> gio) {
-  return sw_body<T, LOG2L, MODE, ZERO, true, KIND>(gbuf, gtw, gtw4, gm, gio);
+CS_NOINL double sw_sandwich_t(const T* y, T* yout, const int* supp, int ns, const T* vin, T* vout) {
+  MidCtx<T> gm;
+  gm.y = y;
+  gm.yout = yout;
+  const SwIO<T> gio{supp, ns, nullptr, vin, vout};
+  return sw_body<T, LOG2L, MODE, ZERO, true, KIND>(nullptr, TwTable<T>{}, TwTable<T>{}, gm, gio);
 }
 
 // runtime dispatch over log2 L in [LO, HI]
 template <typename T, int LO, int HI, int MODE, bool ZERO, int KIND = 0>
-CS_DEV double sw_dispatch(C2<T>* buf, int log2l, const TwTable<T>& tw, const TwTable<T>& tw4, const MidCtx<T>& m,
-                          const SwIO<T>& io) {
+CS_DEV double sw_dispatch(int log2l, const T* y, T* yout, const int* supp, int ns, const T* vin, T* vout) {
   if constexpr (LO <= HI) {
-    if (log2l == LO) return sw_sandwich_t<T, LO, MODE, ZERO, KIND>(buf, tw, tw4, m, io);
-    return sw_dispatch<T, LO + 1, HI, MODE, ZERO, KIND>(buf, log2l, tw, tw4, m, io);
+    if (log2l == LO) return sw_sandwich_t<T, LO, MODE, ZERO, KIND>(y, yout, supp, ns, vin, vout);
+    return sw_dispatch<T, LO + 1, HI, MODE, ZERO, KIND>(log2l, y, yout, supp, ns, vin, vout);
   }
   return 0.0;
 }
