@@ -104,14 +104,21 @@ CS_DEV bool topk_cta_fast_v(Ctx& ctx, int nbits, int K, Visit&& visit, uint32_t*
     const unsigned ball = __ballot_sync(0xffffffffu, inc >= K);
     const int fl = ball ? __ffs(ball) - 1 : -1;
     if (lane == 0 && fl < 0) { pk[0] = -1; pk[1] = 0; pk[2] = 0; }
-    if (lane == fl) {
-      int cu = inc - s;
-      for (int i = 0; i < 32; ++i) {
-        const int b = TOPK_BINS - 1 - 32 * lane - i;
-        const int c = (int)h[b];
-        if (cu + c >= K) { pk[0] = b; pk[1] = cu; pk[2] = c; break; }
-        cu += c;
+    if (fl >= 0) {
+      // the boundary bin inside lane fl's 32 bins, found by the whole warp (one bin per
+      // lane, a warp scan and a ballot) instead of a serial 32-step search
+      const int base = __shfl_sync(0xffffffffu, inc - s, fl);   // keys above lane fl's bins
+      const int b = TOPK_BINS - 1 - 32 * fl - lane;
+      const int c = (int)h[b];
+      int ic = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, ic, o);
+        if (lane >= o) ic += t;
       }
+      const unsigned bb = __ballot_sync(0xffffffffu, base + ic >= K);
+      const int fb = __ffs(bb) - 1;   // exists: lane fl's bins reach K
+      if (lane == fb) { pk[0] = b; pk[1] = base + ic - c; pk[2] = c; }
     }
   }
   const int nwords = (nbits + 31) >> 5;
