@@ -179,9 +179,22 @@ CS_DEV void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* out
           const C2<T> z = zs[swz<T>(q)];
           int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;        // mk_nat(2q)
           int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;  // mk_nat(2q+1)
-          if constexpr (HP) { j0 = pm[j0]; j1 = pm[j1]; }
-          f(j0, (excl && bit_test(excl, j0)) ? Key(0) : full_key(z.x));
-          f(j1, (excl && bit_test(excl, j1)) ? Key(0) : full_key(z.y));
+          Key k0 = full_key(z.x), k1 = full_key(z.y);
+          if constexpr (HP) {
+            j0 = pm[j0];
+            j1 = pm[j1];
+            if (excl) {
+              if (bit_test(excl, j0)) k0 = Key(0);
+              if (bit_test(excl, j1)) k1 = Key(0);
+            }
+          } else if (excl) {
+            // j0, j1 = 4q, 4q+2 or 2n-1-4q, 2n-3-4q: always one exclusion word (n >= 16)
+            const uint32_t w = excl[j0 >> 5];
+            k0 = ((w >> (j0 & 31)) & 1u) ? Key(0) : k0;
+            k1 = ((w >> (j1 & 31)) & 1u) ? Key(0) : k1;
+          }
+          f(j0, k0);
+          f(j1, k1);
         }
       };
       return topk_cta_fast_v<Ctx, Key>(ctx, n, (int)K, visit, out);
@@ -228,9 +241,16 @@ CS_DEV int64_t detect_argmax(Ctx& ctx, const uint32_t* excl) {
         const C2<T> z = zs[swz<T>(q)];
         int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;
         int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;
-        if constexpr (HP) { j0 = pm[j0]; j1 = pm[j1]; }
-        take(j0, bit_test(excl, j0) ? Key(0) : full_key(z.x));
-        take(j1, bit_test(excl, j1) ? Key(0) : full_key(z.y));
+        if constexpr (HP) {
+          j0 = pm[j0];
+          j1 = pm[j1];
+          take(j0, bit_test(excl, j0) ? Key(0) : full_key(z.x));
+          take(j1, bit_test(excl, j1) ? Key(0) : full_key(z.y));
+        } else {
+          const uint32_t w = excl[j0 >> 5];   // one word for both (see detect_topk)
+          take(j0, ((w >> (j0 & 31)) & 1u) ? Key(0) : full_key(z.x));
+          take(j1, ((w >> (j1 & 31)) & 1u) ? Key(0) : full_key(z.y));
+        }
       }
     };
     if (pm) scan(std::true_type{}); else scan(std::false_type{});
