@@ -655,7 +655,13 @@ template <typename T> struct GridCtx {
         }, [&](int e, uint32_t v) { ms[e] = v; });
       }
       __syncthreads();
+#ifdef CS_DIAG_PASSB
+      if (MODE == MID_H) mark(10);  // load + metadata staging
+#endif
       if (!zero_input) row_fft<false>(B);
+#ifdef CS_DIAG_PASSB
+      if (MODE == MID_H) mark(11);  // forward row FFTs
+#endif
       C2<T>* zb = shp(buf);
       {
         // a transposed row shorter than a word (small-N fallback): read the mask in place
@@ -756,8 +762,14 @@ template <typename T> struct GridCtx {
         }
       }
       __syncthreads();
+#ifdef CS_DIAG_PASSB
+      if (MODE == MID_H) mark(12);  // middle
+#endif
       if constexpr (MODE != MID_FWD) {
         row_fft<true>(B);
+#ifdef CS_DIAG_PASSB
+        if (MODE == MID_H) mark(13);  // inverse row FFTs
+#endif
         C2<T>* sb = shp(buf);
         C2<T>* wk = Wk;
         const GTw<T> tf = twF;
@@ -786,6 +798,9 @@ template <typename T> struct GridCtx {
         }
       }
       __syncthreads();
+#ifdef CS_DIAG_PASSB
+      if (MODE == MID_H) mark(14);  // twiddle + store
+#endif
     }
     return rn2;
   }
