@@ -66,15 +66,13 @@ template <typename T> struct CtaCtx {
   int in_ns;
   int applies;
   // dictionary Psi = C_N (R35): A = Phi Psi.  The pursuit's index space is the s-domain
-  // (no sign, no permutation: `sign` holds zeros, pm/pinv are null); Phi's sign bits,
-  // pi^-1 and row mask are read from the instance metadata by the Psi-mode helpers.
+  // (no sign, no permutation: `sign` holds zeros, pm/pinv are null); Phi's sign bits and
+  // pi^-1 are applied by the MID_FWDZ / MID_INVZ sandwiches (sandwich_cta.cuh).
   int fkind;                 // F: 0 = DCT-II, 1 = partial Fourier (R36)
   int psi;                   // 0: Psi = I, 1: Psi = C_N
-  T* G;                      // global [N] scratch of this problem (Psi mode)
+  T* G;                      // unused on the CTA tier
   const uint32_t* phi_sign;  // global
   const int32_t* phi_pinv;   // global, or null
-  const uint32_t* g_rmask;   // global natural-order row mask / prefix of the instance
-  const int32_t* g_prefix;
 
   CS_DEV void sync() { __syncthreads(); }
   CS_DEV void mark(int) {}  // phase accounting is a grid-context diagnostic
@@ -301,121 +299,29 @@ template <typename T> struct CtaCtx {
     return sum(rn2);
   }
 
-  // ---- Psi = C_N (R35): every A / A^T is C_N, Phi, and C_N^T composed from the same
-  // sandwich kernels.  A full DCT-II (all N outputs) is the forward sandwich with every
-  // row selected (rank(k) = k), and C_N^T of a dense vector is the adjoint sandwich with
-  // every row selected; the Eq.(7) permutation and the signs sit between them, moved
-  // through the problem's global scratch G (natural order).
-  CS_NOINL void mask_full() {
-    const int64_t nw = (N + 31) >> 5;
-    const uint32_t last = (N & 31) ? ((1u << (N & 31)) - 1u) : ~0u;
-    for (int64_t w = gtid; w < nw; w += gnthr) {
-      rowmask[w] = (w == nw - 1) ? last : ~0u;
-      prefix[w] = (int32_t)(32 * w);
-    }
-    __syncthreads();
-  }
-  CS_NOINL void mask_real() {
-    const int64_t nw = (N + 31) >> 5;
-    for (int64_t w = gtid; w < nw; w += gnthr) {
-      rowmask[w] = g_rmask[w];
-      prefix[w] = g_prefix[w];
-    }
-    __syncthreads();
-  }
-  // Z <- Makhoul order of u = R diag(sigma) G: u_{pi^-1(j)} = sigma_j G_j
-  // (8 elements per thread in flight: the global loads of G, pi^-1 and the sign words are
-  // issued before any dependent shared access)
-  CS_NOINL void phi_in() {
-    T* zb = reinterpret_cast<T*>(Z);
-    const int n = (int)N, t0 = threadIdx.x, nt = blockDim.x;
-    const int32_t* pv = phi_pinv;
-    const uint32_t* sg = phi_sign;
-    const T* g = G;
-    for (int j0 = t0; j0 < n; j0 += 8 * nt) {
-      T v[8];
-      int p[8];
-      uint32_t w[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u * nt;
-        if (j < n) { v[u] = g[j]; p[u] = pv ? pv[j] : j; w[u] = sg[j >> 5]; }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u * nt;
-        if (j < n) zb[zt((int)mk_pos(p[u], n))] = ((w[u] >> (j & 31)) & 1u) ? -v[u] : v[u];
-      }
-    }
-    __syncthreads();
-  }
-  // G <- diag(sigma) R^T v, v in Makhoul order in Z: G_j = sigma_j v_{pi^-1(j)}
-  CS_NOINL void phi_out() {
-    const T* zb = zbuf();
-    const int n = (int)N, t0 = threadIdx.x, nt = blockDim.x;
-    const int32_t* pv = phi_pinv;
-    const uint32_t* sg = phi_sign;
-    T* g = G;
-    for (int j0 = t0; j0 < n; j0 += 8 * nt) {
-      int p[8];
-      uint32_t w[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u * nt;
-        if (j < n) { p[u] = pv ? pv[j] : j; w[u] = sg[j >> 5]; }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u * nt;
-        if (j < n) {
-          const T v = zb[zt((int)mk_pos(p[u], n))];
-          g[j] = ((w[u] >> (j & 31)) & 1u) ? -v : v;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  // G <- C_N s, s = scatter_S(vin) (vin == nullptr: s already in Z, Makhoul order)
-  CS_NOINL void psi_to_G(const T* vin) {
-    mask_full();
-    sandwich<MID_FWD, false>(vin, nullptr, G);
-    __syncthreads();
-  }
-  // Z <- C_N^T G (Makhoul order)
-  CS_NOINL void psiT_from_G() {
-    mask_full();
-    const T* ys = y;
-    y = G;
-    sandwich<MID_RES, true>(nullptr, nullptr, nullptr);
-    y = ys;
-    __syncthreads();
+  // Psi = DCT fused (R35): C_N and C_N^T are the extra transforms of MID_FWDZ / MID_INVZ
+  // sandwiches that write / read the buffer in place (sigma and pi of Phi applied there), so
+  // H is three back-to-back sandwiches with four transforms in shared memory — no global
+  // scratch, no row-mask swaps (the shared mask stays the instance's)
+  template <int MODE, bool ZERO> CS_DEV double sandwich_psi(const T* vin, T* vout) {
+    return sw_dispatch<T, 2, 13, MODE, ZERO, 0>(log2L, y, nullptr, in_supp, in_ns, vin, vout, phi_sign, phi_pinv);
   }
   CS_NOINL void H_psi(const T* d, T* q) {
-    psi_to_G(d);                                        // C_N s
-    mask_real();
-    phi_in();                                           // R diag(sigma)
+    sandwich_psi<MID_FWDZ, false>(d, nullptr);          // Makhoul(R sigma C_N scatter_S(d))
     sandwich<MID_H, false>(nullptr, nullptr, nullptr);  // C^T P^T P C
-    phi_out();                                          // diag(sigma) R^T
-    psiT_from_G();                                      // C_N^T
-    const T* zb = zbuf();
-    for (int i = gtid; i < in_ns; i += gnthr) q[i] = zb[zt((int)mk_pos(in_supp[i], N))];
-    __syncthreads();
+    sandwich_psi<MID_INVZ, true>(nullptr, q);           // C_N^T (sigma R^T .), gather on S
     ++applies;
   }
   CS_NOINL double RES_psi(const T* x) {
     double rn2;
     if (x) {
-      psi_to_G(x);
-      mask_real();
-      phi_in();
+      sandwich_psi<MID_FWDZ, false>(x, nullptr);
       rn2 = sandwich<MID_RES, false>(nullptr, nullptr, nullptr);   // Phi^T (y - Phi u)
     } else {
-      mask_real();
       rn2 = sandwich<MID_RES, true>(nullptr, nullptr, nullptr);    // Phi^T y
     }
     rn2 = sum(rn2);
-    phi_out();
-    psiT_from_G();                                                 // A^T r, s-domain
+    sandwich_psi<MID_INVZ, true>(nullptr, nullptr);                // A^T r, s-domain
     ++applies;
     return rn2;
   }

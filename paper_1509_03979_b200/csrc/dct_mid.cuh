@@ -25,7 +25,10 @@
 
 namespace cs {
 
-enum MidMode { MID_H = 0, MID_RES = 1, MID_FWD = 2 };
+enum MidMode { MID_H = 0, MID_RES = 1, MID_FWD = 2,
+               // Psi = DCT, CTA tier (R35): the full DCT-II written back into the transform buffer
+               // (for the next transform) / C_N^T read from it — no rows, no y
+               MID_FWDZ = 3, MID_INVZ = 4 };
 
 template <typename T> struct MidCtx {
   const uint32_t* rowmask;  // [N/32] row-selection bitmask (P)
@@ -125,6 +128,58 @@ CS_DEV void mid_pair(C2<T>& Zk, C2<T>& Zkk, int64_t k, C2<T> a, const MidCtx<T>&
     Zk = cadd<T>(E, iO);
     if (!self) Zkk = cconj<T>(csub<T>(E, iO));
   }
+}
+
+// ---- full orthonormal DCT-II outputs / C_N^T inputs of a pair (Psi = DCT, R35) ----
+// o = s X at (k, N-k, kk, N-kk), kk = L - k (the self pair k = L/2 repeats o[0], o[1])
+template <typename T>
+CS_DEV void dct_out_pair(const C2<T>& Zk, const C2<T>& Zkk, C2<T> a, const MidCtx<T>& m, T* o) {
+  constexpr T r2 = (T)0.70710678118654752440;
+  const C2<T> e4 = mk<T>(r2, -r2);
+  const C2<T> a2 = cmul<T>(a, a);
+  const C2<T> w = cmul<T>(a2, a2);
+  const C2<T> P = cscale<T>(cadd<T>(Zk, cconj<T>(Zkk)), (T)0.5);
+  const C2<T> D = csub<T>(Zk, cconj<T>(Zkk));
+  const C2<T> O = mk<T>(D.y * (T)0.5, -D.x * (T)0.5);
+  const C2<T> Q = cmul<T>(w, O);
+  const C2<T> ck = cmul<T>(a, cadd<T>(P, Q));
+  const C2<T> ckk = cmul<T>(e4, cconj<T>(cmul<T>(a, csub<T>(P, Q))));
+  o[0] = m.sk * ck.x;
+  o[1] = -m.sk * ck.y;
+  o[2] = m.sk * ckk.x;
+  o[3] = -m.sk * ckk.y;
+}
+// k = 0: o = (s_0 X_0, s X_L)
+template <typename T> CS_DEV void dct_out_zero(const C2<T>& Z0, const MidCtx<T>& m, T* o) {
+  constexpr T r2 = (T)0.70710678118654752440;
+  o[0] = m.s0 * (Z0.x + Z0.y);
+  o[1] = m.sk * (Z0.x - Z0.y) * r2;
+}
+// inverse split of C_N^T applied to v with v = wv at (k, N-k, kk, N-kk): the spectrum slots
+// Zk, Zkk of the unnormalised inverse FFT (mid_pair's inverse half, X' = v / (s L))
+template <typename T>
+CS_DEV void dct_in_pair(C2<T>& Zk, C2<T>& Zkk, int64_t k, C2<T> a, const MidCtx<T>& m, const T* wv) {
+  constexpr T r2 = (T)0.70710678118654752440;
+  const C2<T> e4 = mk<T>(r2, -r2);
+  const int64_t kk = (m.N >> 1) - k;
+  const bool self = (k == kk);
+  const T f = m.inv_sk * m.invL;
+  const C2<T> a2 = cmul<T>(a, a);
+  const C2<T> w = cmul<T>(a2, a2);
+  const C2<T> cpk = mk<T>(wv[0] * f, -wv[1] * f);
+  const C2<T> cpkk = self ? cpk : mk<T>(wv[2] * f, -wv[3] * f);
+  const C2<T> Vk = cmulc<T>(cpk, a);
+  const C2<T> Vkk = cmul<T>(cconj<T>(e4), cmul<T>(a, cpkk));
+  const C2<T> cVkk = cconj<T>(Vkk);
+  const C2<T> E = cscale<T>(cadd<T>(Vk, cVkk), (T)0.5);
+  const C2<T> Od = cscale<T>(cmulc<T>(csub<T>(Vk, cVkk), w), (T)0.5);
+  const C2<T> iO = mk<T>(-Od.y, Od.x);
+  Zk = cadd<T>(E, iO);
+  if (!self) Zkk = cconj<T>(csub<T>(E, iO));
+}
+template <typename T> CS_DEV void dct_in_zero(C2<T>& Z0, const MidCtx<T>& m, const T* wv) {
+  const T V0 = wv[0] * m.inv_s0 * m.invL, VL = wv[1] * m.inv_sk * m.invL * (T)1.41421356237309504880;
+  Z0 = mk<T>((V0 + VL) * (T)0.5, (V0 - VL) * (T)0.5);
 }
 
 // ---- F = partial Fourier (R36): the real DFT from the same half-length FFT ----

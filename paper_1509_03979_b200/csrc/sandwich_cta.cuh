@@ -186,6 +186,118 @@ CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, 
   }
 }
 
+// ---- Psi = DCT (R35): the fused last-forward / first-inverse pass of the two extra
+// transforms.  MID_FWDZ: after the forward FFT of s, the orthonormal DCT-II X = C_N s is
+// written straight back into the buffer as the next transform's input, u_{pi^-1(k)} =
+// sigma_k X_k at Makhoul position mk_pos(pi^-1(k)) (sigma, pi^-1 of Phi).  MID_INVZ: reads
+// w_k = sigma_k v_{pi^-1(k)} from the buffer (v = Phi's sandwich output, Makhoul order) and
+// writes the inverse-split spectrum of C_N^T w for the inverse FFT.  Every unit reads all
+// of its values before the barrier and writes after it (in place).
+// Unit k's indices: slot 0..3 pair n = k (k, N-k, L-k, N-L+k); slot 4..7 pair n = k + L/2;
+// unit 0: (0, L), (L/2, N-L/2), (L/4, N-L/4, 3L/4, N-3L/4).
+template <int LOG2L> CS_DEV int psi_idx(int k, int q) {
+  constexpr int L = 1 << LOG2L, H = L / 2, N = 2 * L;
+  if (k != 0) {
+    const int n = (q < 4) ? k : k + H;
+    const int kk = L - n;
+    const int r = q & 3;
+    return r == 0 ? n : r == 1 ? N - n : r == 2 ? kk : N - kk;
+  }
+  constexpr int t[8] = {0, L, H, N - H, L / 4, N - L / 4, 3 * L / 4, N - 3 * L / 4};
+  return t[q];
+}
+template <typename T, int LOG2L, int MODE>
+CS_DEV void sw_fused_psi(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, const MidCtx<T>& m,
+                         const uint32_t* psig, const int32_t* ppinv) {
+  using SP = SwPlan<LOG2L>;
+  constexpr int L = 1 << LOG2L, H = L / 2, U = SP::U, UPT = SP::UPT, N = 2 * L;
+  static_assert(L >= 4, "N >= 8");
+  const int tid = threadIdx.x;
+  T* zb = reinterpret_cast<T*>(buf);
+  auto pos = [&](int idx) {
+    const int p = (int)mk_pos(ppinv ? ppinv[idx] : idx, N);
+    return 2 * swz<T>(p >> 1) + (p & 1);
+  };
+  auto sgn = [&](int idx, T v) { return ((psig[idx >> 5] >> (idx & 31)) & 1u) ? -v : v; };
+  T o[UPT][8];
+  if constexpr (MODE == MID_FWDZ) {
+#pragma unroll
+    for (int it = 0; it < UPT; ++it) {
+      const int k = tid + it * SW_NT;
+      if ((U % SW_NT == 0) || k < U) {
+        const int kb = (k == 0) ? L / 4 : H - k;
+        C2<T> a0 = buf[swz<T>(k)], a1 = buf[swz<T>(k + H)];
+        C2<T> b0 = buf[swz<T>(kb)], b1 = buf[swz<T>(kb + H)];
+        a1 = cmul<T>(a1, tw(k));
+        b1 = cmul<T>(b1, tw(kb));
+        const C2<T> A0 = cadd<T>(a0, a1), A1 = csub<T>(a0, a1), B0 = cadd<T>(b0, b1), B1 = csub<T>(b0, b1);
+        if (k != 0) {
+          const C2<T> a = tw4(k);
+          dct_out_pair<T>(A0, B1, a, m, &o[it][0]);
+          dct_out_pair<T>(A1, B0, cmul<T>(a, w16c<T>()), m, &o[it][4]);
+        } else {
+          dct_out_zero<T>(A0, m, &o[it][0]);
+          T t4[4];
+          dct_out_pair<T>(A1, A1, tw4(H), m, t4);   // self pair n = L/2: (H, N-H)
+          o[it][2] = t4[0];
+          o[it][3] = t4[1];
+          dct_out_pair<T>(B0, B1, tw4(L / 4), m, &o[it][4]);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < UPT; ++it) {
+      const int k = tid + it * SW_NT;
+      if ((U % SW_NT == 0) || k < U) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int idx = psi_idx<LOG2L>(k, q);
+          zb[pos(idx)] = sgn(idx, o[it][q]);
+        }
+      }
+    }
+    __syncthreads();
+  } else {  // MID_INVZ
+#pragma unroll
+    for (int it = 0; it < UPT; ++it) {
+      const int k = tid + it * SW_NT;
+      if ((U % SW_NT == 0) || k < U) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int idx = psi_idx<LOG2L>(k, q);
+          o[it][q] = sgn(idx, zb[pos(idx)]);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < UPT; ++it) {
+      const int k = tid + it * SW_NT;
+      if ((U % SW_NT == 0) || k < U) {
+        const int kb = (k == 0) ? L / 4 : H - k;
+        C2<T> A0, A1, B0, B1;
+        if (k != 0) {
+          const C2<T> a = tw4(k);
+          dct_in_pair<T>(A0, B1, k, a, m, &o[it][0]);
+          dct_in_pair<T>(A1, B0, k + H, cmul<T>(a, w16c<T>()), m, &o[it][4]);
+        } else {
+          dct_in_zero<T>(A0, m, &o[it][0]);
+          dct_in_pair<T>(A1, A1, H, tw4(H), m, &o[it][2]);   // self pair (reads o[2], o[3])
+          dct_in_pair<T>(B0, B1, L / 4, tw4(L / 4), m, &o[it][4]);
+        }
+        // inverse radix-2 pass, Ns = 1 (as in sw_fused)
+        const int sa = swz<T>(2 * k), sb = swz<T>(2 * kb);
+        buf[sa] = cadd<T>(A0, A1);
+        buf[sa ^ 1] = csub<T>(A0, A1);
+        buf[sb] = cadd<T>(B0, B1);
+        buf[sb ^ 1] = csub<T>(B0, B1);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <typename T, int LOG2L, bool INV>
 CS_DEV void sw_remainder(C2<T>* buf, const TwTable<T>& tw, int nsb) {
   constexpr int M = SwPlan<LOG2L>::M;
@@ -201,9 +313,10 @@ CS_DEV void sw_remainder(C2<T>* buf, const TwTable<T>& tw, int nsb) {
 template <typename T> struct SwIO {
   const int* supp;
   int ns;
-  const uint32_t* sign;
+  const uint32_t* sign;       // MID_FWDZ / MID_INVZ: Phi's sign bits (global); otherwise unused
   const T* vin;
   T* vout;
+  const int32_t* pinv_phi;    // MID_FWDZ / MID_INVZ: Phi's pi^-1 (global) or null
 };
 
 // PERM = false: the caller guarantees no Eq.(7) permutation (the CG loop of a plain
@@ -229,6 +342,7 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
   const int tid = threadIdx.x;
   T* zb = reinterpret_cast<T*>(buf);
   auto zt = [](int p) { return 2 * swz<T>(p >> 1) + (p & 1); };
+  static_assert(MODE != MID_INVZ || ZERO, "MID_INVZ reads the buffer as it is (no forward FFT)");
   if constexpr (!ZERO) {
     if (gio.vin) {
       const int* supp = shp(gio.supp);
@@ -248,8 +362,13 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
 #pragma unroll 1
     for (int q = 0; q < SP::Q; ++q) sw_pass<T, LOG2L, 4, false>(buf, tw, SP::NS_R16_FWD0 + 4 * q);
   }
-  const double rn2 = sw_fused<T, LOG2L, MODE, ZERO, KIND>(buf, tw, tw4, m);
-  if constexpr (MODE != MID_FWD) {
+  double rn2 = 0;
+  if constexpr (MODE == MID_FWDZ || MODE == MID_INVZ) {
+    sw_fused_psi<T, LOG2L, MODE>(buf, tw, tw4, m, gio.sign, gio.pinv_phi);
+  } else {
+    rn2 = sw_fused<T, LOG2L, MODE, ZERO, KIND>(buf, tw, tw4, m);
+  }
+  if constexpr (MODE != MID_FWD && MODE != MID_FWDZ) {
 #pragma unroll 1
     for (int q = 0; q < SP::Q; ++q) sw_pass<T, LOG2L, 4, true>(buf, tw, 1 + 4 * q);
     sw_remainder<T, LOG2L, true>(buf, tw, 1 + 4 * SP::Q);
@@ -271,20 +390,22 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
 // Out of line: only scalars cross the call (no structs passed by value — at 1024
 // threads per SM every by-value byte is a local-memory store and load).
 template <typename T, int LOG2L, int MODE, bool ZERO, int KIND = 0>
-CS_NOINL double sw_sandwich_t(const T* y, T* yout, const int* supp, int ns, const T* vin, T* vout) {
+CS_NOINL double sw_sandwich_t(const T* y, T* yout, const int* supp, int ns, const T* vin, T* vout,
+                              const uint32_t* psig, const int32_t* ppinv) {
   MidCtx<T> gm;
   gm.y = y;
   gm.yout = yout;
-  const SwIO<T> gio{supp, ns, nullptr, vin, vout};
+  const SwIO<T> gio{supp, ns, psig, vin, vout, ppinv};
   return sw_body<T, LOG2L, MODE, ZERO, true, KIND>(nullptr, TwTable<T>{}, TwTable<T>{}, gm, gio);
 }
 
 // runtime dispatch over log2 L in [LO, HI]
 template <typename T, int LO, int HI, int MODE, bool ZERO, int KIND = 0>
-CS_DEV double sw_dispatch(int log2l, const T* y, T* yout, const int* supp, int ns, const T* vin, T* vout) {
+CS_DEV double sw_dispatch(int log2l, const T* y, T* yout, const int* supp, int ns, const T* vin, T* vout,
+                          const uint32_t* psig = nullptr, const int32_t* ppinv = nullptr) {
   if constexpr (LO <= HI) {
-    if (log2l == LO) return sw_sandwich_t<T, LO, MODE, ZERO, KIND>(y, yout, supp, ns, vin, vout);
-    return sw_dispatch<T, LO + 1, HI, MODE, ZERO, KIND>(log2l, y, yout, supp, ns, vin, vout);
+    if (log2l == LO) return sw_sandwich_t<T, LO, MODE, ZERO, KIND>(y, yout, supp, ns, vin, vout, psig, ppinv);
+    return sw_dispatch<T, LO + 1, HI, MODE, ZERO, KIND>(log2l, y, yout, supp, ns, vin, vout, psig, ppinv);
   }
   return 0.0;
 }

@@ -125,8 +125,6 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   c.G = nullptr;
   c.phi_sign = meta.sign(b);
   c.phi_pinv = meta.pinv(b);
-  c.g_rmask = meta.rmask(b);
-  c.g_prefix = meta.prefix(b);
   // Psi mode: the pursuit's index space is the s-domain (no sign, no permutation)
   c.pm = meta.psi ? nullptr : meta.pm(b);
   c.pinv = meta.psi ? nullptr : meta.pinv(b);
@@ -160,14 +158,12 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
 // plain apply keeps its register allocation.
 template <typename T>
 CS_NOINL void s_apply_psi(CtaCtx<T>& c, const T* x, T* y, T* G) {
+  (void)G;
   const int64_t N = c.N;
-  c.G = G;
   T* zb = reinterpret_cast<T*>(c.Z);
   for (int j = c.gtid; j < (int)N; j += c.gnthr) zb[CtaCtx<T>::zt((int)mk_pos(j, N))] = x[j];
   __syncthreads();
-  c.psi_to_G(nullptr);
-  c.mask_real();
-  c.phi_in();
+  c.template sandwich_psi<MID_FWDZ, false>(nullptr, nullptr);       // Phi's input in place
   c.template sandwich<MID_FWD, false>(nullptr, nullptr, y);
 }
 
