@@ -174,11 +174,10 @@ CS_DEV void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* out
     // the permuted and the plain visitor are separate instances (no per-element branch)
     auto run = [&](auto has_pm) -> bool {
       constexpr bool HP = decltype(has_pm)::value;
-      auto visit = [&](auto&& f) {
-        for (int q = threadIdx.x; q < L; q += blockDim.x) {
+      // slot q holds Makhoul positions 2q, 2q+1: indices (4q, 4q+2) for q < n/4 and
+      // (2n-1-4q, 2n-3-4q) above — two loops, no per-slot selection of the formula
+      auto slot = [&](auto&& f, int q, int j0, int j1) {
           const C2<T> z = zs[swz<T>(q)];
-          int j0 = (4 * q < n) ? 4 * q : 2 * (n - 1 - 2 * q) + 1;        // mk_nat(2q)
-          int j1 = (4 * q + 2 < n) ? 4 * q + 2 : 2 * (n - 2 - 2 * q) + 1;  // mk_nat(2q+1)
           Key k0 = full_key(z.x), k1 = full_key(z.y);
           if constexpr (HP) {
             j0 = pm[j0];
@@ -195,7 +194,11 @@ CS_DEV void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* out
           }
           f(j0, k0);
           f(j1, k1);
-        }
+      };
+      auto visit = [&](auto&& f) {
+        const int h = n >> 2;
+        for (int q = threadIdx.x; q < h; q += blockDim.x) slot(f, q, 4 * q, 4 * q + 2);
+        for (int q = h + threadIdx.x; q < L; q += blockDim.x) slot(f, q, 2 * n - 1 - 4 * q, 2 * n - 3 - 4 * q);
       };
       return topk_cta_fast_v<Ctx, Key>(ctx, n, (int)K, visit, out);
     };
