@@ -81,7 +81,13 @@ CS_DEV void cg_loop(Ctx& c, CgState<T>& s_io, HFn&& Hf) {
       rv[i] = ri;
       rr2 += (double)ri * (double)ri;
     }
+#ifdef CS_DIAG_CG
+    c.mark(15);  // x, r update
+#endif
     rr2 = c.sum(rr2);
+#ifdef CS_DIAG_CG
+    c.mark(16);  // ||r||^2 reduction
+#endif
     const T beta = (T)(rr2 / s.rr);                                        // line 19
     for (int i = a0; i < n; i += s0) dv[i] = rv[i] + beta * dv[i];        // line 20
     s.rr = rr2;

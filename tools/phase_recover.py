@@ -28,7 +28,8 @@ names = ["between sandwiches", "H pass A", "H pass B", "H pass C", "RES pass A",
 rep = r.reports()[0]
 print("total ms", tot, "outer", rep["outer_iters"], "cg", rep["cg_iters_total"], "applies", rep["applies"])
 off = cs.load_library().cs_diag_phase_offset(cs.ALGS[cfg.alg], cfg.N, cfg.M, cfg.K, 0, 0)
-acc = raw[off:off + 8 * 16].view(np.uint64)
+acc = raw[off:off + 8 * 24].view(np.uint64)
 # slots 10-14: pass-B item phases of H, only with CS_NVCC_EXTRA=-DCS_DIAG_PASSB
-names += ["passB load+stage", "passB fwd FFT", "passB middle", "passB inv FFT", "passB twiddle+store"]
+names += ["passB load+stage", "passB fwd FFT", "passB middle", "passB inv FFT", "passB twiddle+store",
+          "CG x/r update", "CG rr reduction"]  # 15-16: -DCS_DIAG_CG
 print({n: round(float(v) / 1e6, 3) for n, v in zip(names, acc) if v}, "ms (block 0)")
