@@ -95,6 +95,9 @@ struct OpMeta {
 };
 
 template <typename T>
+CS_DEV void cta_set_instance(CtaCtx<T>& c, char* smem, const OpMeta& meta, int64_t b);
+
+template <typename T>
 CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta, int64_t b) {
   CtaCtx<T> c;
   c.N = meta.N;
@@ -123,24 +126,32 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   c.psi = meta.psi;
   c.fkind = meta.fkind;
   c.G = nullptr;
+  c.in_supp = nullptr;
+  c.in_ns = 0;
+  c.applies = 0;
+  if (threadIdx.x == 0) *reinterpret_cast<int*>(smem + s_fixed<T>(meta.N).zero) = 0;
+  // twiddles into shared memory (once per CTA), then the instance
+  const int64_t L = c.L;
+  tw_init<T>(const_cast<C2<T>*>(c.twL.lo), const_cast<C2<T>*>(c.twL.hi), L,
+             (int)(L >= 64 ? L / 64 : 1), c.gtid, c.gnthr);
+  tw_init<T>(const_cast<C2<T>*>(c.tw4.lo), const_cast<C2<T>*>(c.tw4.hi), 8 * L,
+             (int)(L / 128 + 1), c.gtid, c.gnthr);
+  cta_set_instance<T>(c, smem, meta, b);
+  return c;
+}
+
+// point the context at instance b: its sign / row mask / prefix into shared memory, its
+// permutation pointers (the caller orders this after every use of the previous instance)
+template <typename T>
+CS_DEV void cta_set_instance(CtaCtx<T>& c, char* smem, const OpMeta& meta, int64_t b) {
   c.phi_sign = meta.sign(b);
   c.phi_pinv = meta.pinv(b);
   // Psi mode: the pursuit's index space is the s-domain (no sign, no permutation)
   c.pm = meta.psi ? nullptr : meta.pm(b);
   c.pinv = meta.psi ? nullptr : meta.pinv(b);
-  if (threadIdx.x == 0) {
-    *reinterpret_cast<int*>(smem + s_fixed<T>(meta.N).zero) = 0;
+  if (threadIdx.x == 0)
     *reinterpret_cast<const int32_t**>(smem + s_fixed<T>(meta.N).zero + 8) = c.pinv;  // sandwich_cta.cuh
-  }
-  c.in_supp = nullptr;
-  c.in_ns = 0;
-  c.applies = 0;
-  // twiddles and this instance's metadata into shared memory
-  const int64_t L = c.L, nw = meta.nw;
-  tw_init<T>(const_cast<C2<T>*>(c.twL.lo), const_cast<C2<T>*>(c.twL.hi), L,
-             (int)(L >= 64 ? L / 64 : 1), c.gtid, c.gnthr);
-  tw_init<T>(const_cast<C2<T>*>(c.tw4.lo), const_cast<C2<T>*>(c.tw4.hi), 8 * L,
-             (int)(L / 128 + 1), c.gtid, c.gnthr);
+  const int64_t nw = meta.nw;
   const uint32_t* gs = meta.sign(b);
   const uint32_t* gm = meta.rmask(b);
   const int32_t* gp = meta.prefix(b);
@@ -150,7 +161,6 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
     c.prefix[w] = gp[w];
   }
   __syncthreads();
-  return c;
 }
 
 // ---------------------------------------------------------------- kernels ---
@@ -169,15 +179,20 @@ CS_NOINL void s_apply_psi(CtaCtx<T>& c, const T* x, T* y, T* G) {
 
 template <typename T>
 __global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout lay, const T* __restrict__ X,
-                                                 T* __restrict__ Y, T* __restrict__ Gws) {
+                                                 T* __restrict__ Y, T* __restrict__ Gws, int64_t B) {
   extern __shared__ __align__(16) char smem[];
-  const int64_t b = blockIdx.x;
-  CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, b);
+  // persistent: the CTA sets up its twiddle tables once and loops over instances
+  CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, blockIdx.x);
   const int64_t N = c.N;
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+  if (b != blockIdx.x) {
+    __syncthreads();  // the previous instance's sandwich is done with the buffer and metadata
+    cta_set_instance<T>(c, smem, meta, b);
+  }
   const T* x = X + b * N;
   if (c.psi) {
     s_apply_psi<T>(c, x, Y + b * c.M, Gws + b * N);
-    return;
+    continue;
   }
   if (c.pinv) {
     // Eq.(7) randomizer: x_j lands at the Makhoul position of pi^-1(j) (R34)
@@ -219,20 +234,26 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout 
   }
   __syncthreads();
   c.template sandwich<MID_FWD, false>(nullptr, nullptr, Y + b * c.M);
+  }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(TS_THREADS, 2) k_s_adjoint(OpMeta meta, SLayout lay, const T* __restrict__ Yin,
-                                                   T* __restrict__ X, T* __restrict__ Gws) {
+                                                   T* __restrict__ X, T* __restrict__ Gws, int64_t B) {
   extern __shared__ __align__(16) char smem[];
-  const int64_t b = blockIdx.x;
-  CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, b);
-  c.y = Yin + b * c.M;
-  if (c.psi) c.G = Gws + b * c.N;
-  c.RES(nullptr);  // A^T y (x = 0)
+  CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, blockIdx.x);   // persistent, as k_s_apply
   const int64_t N = c.N;
-  T* x = X + b * N;
-  for (int64_t j = c.gtid; j < N; j += c.gnthr) x[j] = c.c_at(j);
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    if (b != blockIdx.x) {
+      __syncthreads();
+      cta_set_instance<T>(c, smem, meta, b);
+    }
+    c.y = Yin + b * c.M;
+    if (c.psi) c.G = Gws + b * c.N;
+    c.RES(nullptr);  // A^T y (x = 0)
+    T* x = X + b * N;
+    for (int64_t j = c.gtid; j < N; j += c.gnthr) x[j] = c.c_at(j);
+  }
 }
 
 template <typename T> struct SRecArgs {
@@ -331,8 +352,13 @@ cs_status s_apply_launch(const OpMeta& m, int64_t B, const T* in, T* out, bool a
   SLayout lay = s_layout<T>(m.N, 0, 0, false);
   const void* fn = adjoint ? (const void*)k_s_adjoint<T> : (const void*)k_s_apply<T>;
   if (cs_status s = s_attr(fn, lay.bytes, err)) return s;
-  if (adjoint) k_s_adjoint<T><<<(unsigned)B, lay.nthreads, lay.bytes, st>>>(m, lay, in, out, gws);
-  else k_s_apply<T><<<(unsigned)B, lay.nthreads, lay.bytes, st>>>(m, lay, in, out, gws);
+  // persistent grid: two CTAs per SM (the occupancy of the 512-thread, ~110 KB CTA)
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<int64_t>(B, 2 * (int64_t)nsm);
+  if (adjoint) k_s_adjoint<T><<<grid, lay.nthreads, lay.bytes, st>>>(m, lay, in, out, gws, B);
+  else k_s_apply<T><<<grid, lay.nthreads, lay.bytes, st>>>(m, lay, in, out, gws, B);
   return s_launched(launches, err);
 }
 template <typename T>
