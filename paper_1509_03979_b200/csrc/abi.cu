@@ -647,7 +647,7 @@ cs_status cs_operator_info(const cs_operator* op, int64_t* N, int64_t* M, int64_
 size_t cs_operator_ws_bytes(const cs_operator* op, int precision) {
   if (op && op->psi && op->N <= TIER_S_MAX_N) return (size_t)(op->B * op->N) * (precision ? 8 : 4);
   if (!op || op->N <= TIER_S_MAX_N) return 0;
-  return precision ? tier_l_apply_ws_bytes<double>(op->N, op->M) : tier_l_apply_ws_bytes<float>(op->N, op->M);
+  return precision ? tier_l_apply_ws_bytes<double>(op->N, op->M, op->B) : tier_l_apply_ws_bytes<float>(op->N, op->M, op->B);
 }
 
 cs_status cs_operator_apply(const cs_operator* op, const float* d_x, float* d_y, void* d_ws,
@@ -679,8 +679,8 @@ cs_status cs_workspace_bytes(int alg, int64_t N, int64_t M, int32_t K, int64_t b
   if (s) {
     *bytes = (size_t)(batch * 2 * N * (dbl ? 8 : 4));   // A^T y and the Psi-mode scratch per problem
   } else {
-    *bytes = dbl ? tier_l_recover_ws_bytes<double>(N, M, K, (int)ucap)
-                 : tier_l_recover_ws_bytes<float>(N, M, K, (int)ucap);
+    *bytes = dbl ? tier_l_recover_ws_bytes<double>(N, M, K, (int)ucap, batch)
+                 : tier_l_recover_ws_bytes<float>(N, M, K, (int)ucap, batch);
   }
   return CS_OK;
 }

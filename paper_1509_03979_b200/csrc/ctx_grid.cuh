@@ -42,12 +42,13 @@ CS_DEV unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
 // Grid-wide barrier: block-level barrier, then thread 0 arrives with an acq_rel atomic and
 // spins on the generation word with acquire loads (release/acquire make every block's
 // writes before the barrier visible after it); bounded spin with a watchdog trap (~15 s).
-static CS_NOINL void grid_barrier(GridBar* gb) {
+// nblk = the blocks that meet at this barrier (a group of the grid, or all of it).
+static CS_NOINL void grid_barrier(GridBar* gb, unsigned nblk) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned g = ld_acquire_gpu(&gb->gen);
     const unsigned arrived = atom_add_acq_rel_gpu(&gb->count, 1u) + 1u;
-    if (arrived == gridDim.x) {
+    if (arrived == nblk) {
       gb->count = 0u;                 // ordered before the release below
       st_release_gpu(&gb->gen, g + 1u);
     } else {
@@ -128,14 +129,27 @@ template <typename T> CS_DEV void stp(C2<T>* p, const CP<T>& v) {
   }
 }
 
+// this block's index within its group and the group size (GridCtx ids): the first two
+// words of the dynamic shared memory (a header-level static __shared__ would be a different
+// variable in every translation unit)
+CS_DEV int tl_group(int i) { return reinterpret_cast<const int*>(cs_smem_base)[i]; }
+
 template <typename T> struct GridCtx {
   using Key = typename KeyT<T>::type;
-  // ids derived from the special registers on use (the context lives in local memory)
-  struct TidV { CS_DEV operator int() const { return (int)(blockIdx.x * blockDim.x + threadIdx.x); } };
-  struct NthrV { CS_DEV operator int() const { return (int)(gridDim.x * blockDim.x); } };
+  // the grid may be split into groups of nblk blocks, each running its own instances with
+  // its own workspace and barrier; blk = this block's index in its group.  Ids are
+  // group-relative and derived on use from two shared words (tl_group, set once per block):
+  // the context lives in local memory, and a stored id is a local load in every loop.
+  struct BlkV { CS_DEV operator int() const { return tl_group(0); } };
+  struct NblkV { CS_DEV operator int() const { return tl_group(1); } };
+  struct TidV { CS_DEV operator int() const { return tl_group(0) * (int)blockDim.x + (int)threadIdx.x; } };
+  struct NthrV { CS_DEV operator int() const { return tl_group(1) * (int)blockDim.x; } };
   struct LaneV { CS_DEV operator int() const { return (int)(threadIdx.x & 31); } };
-  struct WarpV { CS_DEV operator int() const { return (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); } };
-  struct NwarpV { CS_DEV operator int() const { return (int)((gridDim.x * blockDim.x) >> 5); } };
+  struct WarpV { CS_DEV operator int() const { return (tl_group(0) * (int)blockDim.x + (int)threadIdx.x) >> 5; } };
+  struct NwarpV { CS_DEV operator int() const { return (tl_group(1) * (int)blockDim.x) >> 5; } };
+  BlkV blk;
+  NblkV nblk;
+  int grp, ngrp;
   TidV gtid;
   NthrV gnthr;
   LaneV lane;
@@ -191,7 +205,7 @@ template <typename T> struct GridCtx {
   uint64_t* ptime;
   uint64_t tprev;
   CS_DEV void mark(int phase) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blk == 0 && threadIdx.x == 0) {
       uint64_t t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (tprev) ptime[phase] += t - tprev;
@@ -202,7 +216,7 @@ template <typename T> struct GridCtx {
   int in_ns;
   int applies;
 
-  CS_DEV void sync() { grid_barrier(g.bar); }
+  CS_DEV void sync() { grid_barrier(g.bar, (unsigned)nblk); }
   static constexpr bool kTopkFast = false;
   template <typename P> CS_DEV P* loc(P* p) const { return p; }  // global (Tier L)
 
@@ -225,11 +239,11 @@ template <typename T> struct GridCtx {
   CS_DEV double sum(double v) {
     double t = block_sum(v);
     double* P = g.pd + bank * g.maxgrid;
-    if (threadIdx.x == 0) P[blockIdx.x] = t;
+    if (threadIdx.x == 0) P[blk] = t;
     sync();
     if (threadIdx.x < 32) {
       double a = 0;
-      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) a += P[c];
+      for (int c = threadIdx.x; c < (int)nblk; c += 32) a += P[c];
       a = warp_sum_g(a);
       if (threadIdx.x == 0) sd[32] = a;
     }
@@ -255,14 +269,14 @@ template <typename T> struct GridCtx {
       int64_t bi = -1;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
         if (sk[w] > bk || (sk[w] == bk && bk != 0 && si[w] < bi)) { bk = sk[w]; bi = si[w]; }
-      PK[blockIdx.x] = (uint64_t)bk;
-      PI[blockIdx.x] = bi;
+      PK[blk] = (uint64_t)bk;
+      PI[blk] = bi;
     }
     sync();
     if (threadIdx.x < 32) {  // warp 0 merges the per-block partials (lanes stride, then shuffle)
       Key bk = 0;
       int64_t bi = -1;
-      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) {
+      for (int c = threadIdx.x; c < (int)nblk; c += 32) {
         const Key kc = (Key)PK[c];
         const int64_t ic = PI[c];
         if (kc > bk || (kc == bk && kc != 0 && ic < bi)) { bk = kc; bi = ic; }
@@ -297,13 +311,13 @@ template <typename T> struct GridCtx {
       ctot += si[k];
     }
     int64_t* P = g.pi + bank * g.maxgrid;
-    if (threadIdx.x == 0) P[blockIdx.x] = ctot;
+    if (threadIdx.x == 0) P[blk] = ctot;
     sync();
     if (threadIdx.x < 32) {  // warp 0: lanes stride over the per-block partials, then shuffle
       int64_t before = 0, all = 0;
-      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) {
+      for (int c = threadIdx.x; c < (int)nblk; c += 32) {
         const int64_t v = P[c];
-        if (c < (int)blockIdx.x) before += v;
+        if (c < (int)blk) before += v;
         all += v;
       }
 #pragma unroll
@@ -326,7 +340,7 @@ template <typename T> struct GridCtx {
   // histogram: shared per-CTA counts, merged into a rotating global bank
   CS_DEV void hist_clear() {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) shist[i] = 0;
-    if (blockIdx.x == 0) {
+    if (blk == 0) {
       unsigned* nb = g.ghist + ((hpass + 1) % 3) * 256;
       for (int i = threadIdx.x; i < 256; i += blockDim.x) nb[i] = 0;
     }
@@ -394,7 +408,7 @@ template <typename T> struct GridCtx {
       atomicAdd(&tcnt[tile_of(p)], 1);
     }
     sync();
-    if (blockIdx.x == 0) {  // exclusive scan of the tile counts (one block; nt <= 4096)
+    if (blk == 0) {  // exclusive scan of the tile counts (one block; nt <= 4096)
       __shared__ int carry;
       if (threadIdx.x == 0) carry = 0;
       __syncthreads();
@@ -463,7 +477,7 @@ template <typename T> struct GridCtx {
     C2<T>* sb = shp(buf);
     C2<T>* wk = Wk;
     const GTw<T> tf = twF;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int64_t t = blk; t < ntiles; t += nblk) {
       const int64_t c0i = t * ct;
       // element e = (m1, cc): the whole tile in flight as cp.async
       for (int e = threadIdx.x; e < tile; e += blockDim.x)
@@ -510,7 +524,7 @@ template <typename T> struct GridCtx {
     const int* sp = in_supp;
     const int64_t* ip = in_pos;
     const uint32_t* sg = sign;
-    for (int64_t t = blockIdx.x; t < ntl; t += gridDim.x) {
+    for (int64_t t = blk; t < ntl; t += nblk) {
       const int64_t c0i = t * ct;
       for (int e = threadIdx.x; e < tile; e += blockDim.x) sb[e] = mk<T>(0, 0);
       __syncthreads();
@@ -566,10 +580,10 @@ template <typename T> struct GridCtx {
     // (two words per entry); a tile with more entries than fit takes the direct path
     int* stg = reinterpret_cast<int*>(shp(msm));
     const int cap = (int)((2 * L2) >> 5) * 2;
-    int64_t t = blockIdx.x;
+    int64_t t = blk;
     int q0 = t < ntl ? tcnt[t] : 0, q1 = t < ntl ? tcnt[t + 1] : 0;
-    for (; t < ntl; t += gridDim.x) {
-      const int64_t tn = t + gridDim.x;
+    for (; t < ntl; t += nblk) {
+      const int64_t tn = t + nblk;
       const int q0n = tn < ntl ? tcnt[tn] : 0, q1n = tn < ntl ? tcnt[tn + 1] : 0;  // next tile's
       if (q1 != q0) {  // a tile without support entries is skipped
         const int64_t c0i = t * ct;
@@ -622,7 +636,7 @@ template <typename T> struct GridCtx {
     m.tsh = tsh;
     double rn2 = 0;
     const int64_t nitems = L1 / 2 + 1;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    for (int64_t it = blk; it < nitems; it += nblk) {
       const int64_t ka = it, kb = L1 - it;
       const bool self = (it == 0 || it == L1 / 2);
       const int B = self ? 1 : 2;
@@ -811,7 +825,7 @@ template <typename T> struct GridCtx {
     const int tile = (int)(L1 * ct);
     C2<T>* sb = shp(buf);
     const C2<T>* wk = Wk;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int64_t t = blk; t < ntiles; t += nblk) {
       const int64_t c0i = t * ct;
       for (int e = threadIdx.x; e < tile; e += blockDim.x)
         cp_async_c<T>(&sb[swz<T>(e)], &wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);
@@ -857,11 +871,11 @@ template <typename T> struct GridCtx {
     mark(2);
     const double t = block_sum(passC_sparse(q, d));
     double* P = g.pd + bank * g.maxgrid;
-    if (threadIdx.x == 0) P[blockIdx.x] = t;
+    if (threadIdx.x == 0) P[blk] = t;
     sync();                                    // publishes q and the per-block partials
     if (threadIdx.x < 32) {
       double a = 0;
-      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) a += P[c];
+      for (int c = threadIdx.x; c < (int)nblk; c += 32) a += P[c];
       a = warp_sum_g(a);
       if (threadIdx.x == 0) sd[32] = a;
     }

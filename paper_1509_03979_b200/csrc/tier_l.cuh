@@ -106,6 +106,7 @@ template <typename T> CS_HD int64_t l_smem_bytes(int64_t N) {
   const int64_t cs2 = 2 * sizeof(T);
   int64_t o = 0;
   auto take = [&](int64_t b) { o = align_up(o + b, 16); };
+  take(16);                                               // group words (tl_group)
   take(TL_TILE * cs2);                                    // buf
   take(64 * cs2); take((g.L1 >= 64 ? g.L1 / 64 : 1) * cs2);   // tw1
   take(64 * cs2); take((g.L2 >= 64 ? g.L2 / 64 : 1) * cs2);   // tw2
@@ -127,11 +128,22 @@ template <typename T> struct LArgs {
   int32_t* supp;
   cs_report* reps;
   char* ws;
+  size_t ws_bytes;
+  int gblocks;      // blocks per group (the passes' work-item cap)
+  int ngroups;      // groups: instances b = grp, grp + ngroups, ... run concurrently
+  int64_t gstride;  // workspace bytes per group (one LLayout)
 };
 
 template <typename T>
 CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   GridCtx<T> c;
+  c.grp = (int)(blockIdx.x / (unsigned)a.gblocks);
+  c.ngrp = a.ngroups;
+  if (threadIdx.x == 0) {   // the group words: dynamic shared offset 0 (ctx_grid.cuh tl_group)
+    reinterpret_cast<int*>(smem)[0] = (int)(blockIdx.x - (unsigned)c.grp * (unsigned)a.gblocks);
+    reinterpret_cast<int*>(smem)[1] = a.gblocks;
+  }
+  __syncthreads();
   LGeom g = l_geom(a.meta.N);
   const LLayout& s = a.lay;
   c.N = a.meta.N;
@@ -142,7 +154,7 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.CT = g.CT;
   c.log2L1 = ilog2(g.L1);
   c.log2L2 = ilog2(g.L2);
-  char* ws = a.ws;
+  char* ws = a.ws + (int64_t)c.grp * a.gstride;  // this group's workspace
   c.U = reinterpret_cast<T*>(ws + s.U);
   c.Wk = reinterpret_cast<C2<T>*>(ws + s.Wk);
   c.Cb = reinterpret_cast<T*>(ws + s.Cb);
@@ -166,6 +178,7 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   const int64_t cs2 = 2 * sizeof(T);
   int64_t o = 0;
   auto take = [&](int64_t b) { int64_t r = o; o = align_up(o + b, 16); return smem + r; };
+  take(16);                                               // group words (tl_group)
   c.buf = reinterpret_cast<C2<T>*>(take(TL_TILE * cs2));
   C2<T>* t1lo = reinterpret_cast<C2<T>*>(take(64 * cs2));
   const int n1 = (int)(g.L1 >= 64 ? g.L1 / 64 : 1);
@@ -271,14 +284,14 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_apply(LArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
   GridCtx<T> c = make_grid_ctx<T>(smem, a);
   const int64_t N = c.N;
-  for (int64_t b = 0; b < a.B; ++b) {
+  for (int64_t b = c.grp; b < a.B; b += c.ngrp) {
     set_instance(c, a.meta, b);
     const T* x = a.Y + b * N;
     const uint32_t* sg = c.sign;
     T* U = c.U;
     uint64_t* ts = reinterpret_cast<uint64_t*>(a.ws + a.lay.ts);
     auto stamp = [&](int i) {
-      if (blockIdx.x == 0 && threadIdx.x == 0 && b == 0) {
+      if (blockIdx.x == 0 && threadIdx.x == 0 && b == 0) {   // group 0, block 0
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         ts[i] = t;
@@ -339,7 +352,7 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_adjoint(LArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
   GridCtx<T> c = make_grid_ctx<T>(smem, a);
   const int64_t N = c.N;
-  for (int64_t b = 0; b < a.B; ++b) {
+  for (int64_t b = c.grp; b < a.B; b += c.ngrp) {
     set_instance(c, a.meta, b);
     load_yT(c, a.Y + b * c.M);
     c.RES(nullptr);
@@ -359,8 +372,8 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_recover(LArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
   GridCtx<T> c = make_grid_ctx<T>(smem, a);
   const LLayout& s = a.lay;
-  char* ws = a.ws;
-  for (int64_t b = 0; b < a.B; ++b) {
+  char* ws = a.ws + (int64_t)c.grp * a.gstride;
+  for (int64_t b = c.grp; b < a.B; b += c.ngrp) {
     set_instance(c, a.meta, b);
     const T* yb = a.Y + b * c.M;
     c.applies = 0;
@@ -409,7 +422,7 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_barrier_bench(GridBar* gb, dou
         pd[(i & 1) * gridDim.x + blockIdx.x] = t;
       }
     }
-    grid_barrier(gb);
+    grid_barrier(gb, gridDim.x);
     if (with_sum && threadIdx.x < 32) {
       double a = 0;
       for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) a += pd[(i & 1) * gridDim.x + c];
@@ -442,12 +455,18 @@ template <typename T> inline int l_grid_upper() {
   return nsm * 4;  // generous upper bound for workspace sizing
 }
 
-template <typename T> inline size_t tier_l_apply_ws_bytes(int64_t N, int64_t M) {
-  return (size_t)l_layout<T>(N, M, 0, 0, false, l_grid_upper<T>()).bytes;
+// groups a batch of B instances can run as (an upper bound; the launch may use fewer)
+template <typename T> inline int64_t l_groups_upper(int64_t N, int64_t B) {
+  const LGeom g = l_geom(N);
+  const int64_t work = std::max<int64_t>(g.L2 / g.CT, g.L1 / 2 + 1);
+  return std::max<int64_t>(1, std::min<int64_t>(B, l_grid_upper<T>() / std::max<int64_t>(work, 1)));
 }
-template <typename T> inline size_t tier_l_recover_ws_bytes(int64_t N, int64_t M, int K, int ucap) {
-  (void)M;
-  return (size_t)l_layout<T>(N, M, K, ucap, true, l_grid_upper<T>()).bytes;
+template <typename T> inline size_t tier_l_apply_ws_bytes(int64_t N, int64_t M, int64_t B = 1) {
+  return (size_t)(align_up(l_layout<T>(N, M, 0, 0, false, l_grid_upper<T>()).bytes, 256) * l_groups_upper<T>(N, B));
+}
+template <typename T> inline size_t tier_l_recover_ws_bytes(int64_t N, int64_t M, int K, int ucap, int64_t B = 1) {
+  return (size_t)(align_up(l_layout<T>(N, M, K, ucap, true, l_grid_upper<T>()).bytes, 256) *
+                  l_groups_upper<T>(N, B));
 }
 
 // Declared everywhere; defined (and explicitly instantiated) in k_l_f32.cu / k_l_f64.cu.
@@ -470,9 +489,20 @@ inline cs_status l_launch(const void* fn, LArgs<T>& a, int64_t N, cudaStream_t s
   // 65 row pairs) extra blocks only make every grid barrier and reduction slower
   const LGeom g = l_geom(N);
   const int64_t work = std::max<int64_t>(g.L2 / g.CT, g.L1 / 2 + 1);
+  const int occ_grid = grid;
   if (work < grid) grid = (int)work;
-  cudaError_t e = cudaMemsetAsync(a.ws + a.lay.ctl, 0, (size_t)(a.lay.ctl_end - a.lay.ctl), st);
+  // a batch of instances whose passes need fewer blocks than the GPU holds runs as several
+  // groups side by side, each with its own workspace slice and barrier
+  a.gblocks = grid;
+  a.gstride = align_up(a.lay.bytes, 256);
+  int64_t ng = std::min<int64_t>(a.B, occ_grid / grid);
+  ng = std::min<int64_t>(ng, (int64_t)(a.ws_bytes / (size_t)a.gstride));
+  a.ngroups = (int)std::max<int64_t>(1, ng);
+  cudaError_t e = cudaSuccess;
+  for (int q = 0; q < a.ngroups && e == cudaSuccess; ++q)
+    e = cudaMemsetAsync(a.ws + q * a.gstride + a.lay.ctl, 0, (size_t)(a.lay.ctl_end - a.lay.ctl), st);
   if (e != cudaSuccess) { err = std::string("memset: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  grid = a.gblocks * a.ngroups;
   void* args[] = {&a};
   e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(TL_THREADS), args, (size_t)smem, st);
   launches.fetch_add(1);
@@ -492,6 +522,7 @@ cs_status tier_l_apply(OpMeta meta, int64_t B, const T* in, T* out, void* ws, si
   a.Y = in;
   a.out = out;
   a.ws = reinterpret_cast<char*>(ws);
+  a.ws_bytes = ws_bytes;
   a.vals = nullptr; a.supp = nullptr; a.reps = nullptr;
   const void* fn = adjoint ? (const void*)k_l_adjoint<T> : (const void*)k_l_apply<T>;
   return l_launch<T>(fn, a, meta.N, st, launches, err);
@@ -513,6 +544,7 @@ cs_status tier_l_recover(OpMeta meta, Params P, int ucap, const T* Y, int64_t B,
   a.supp = supp;
   a.reps = reps;
   a.ws = reinterpret_cast<char*>(ws);
+  a.ws_bytes = ws_bytes;
   return l_launch<T>((const void*)k_l_recover<T>, a, meta.N, st, launches, err);
 }
 

@@ -311,3 +311,14 @@ def test_host_buffer_entry_point_operator_variants(cs, variant):
     bad, _ = compare(sub, oracle_results(sub, ys[pick]), ref.support.cpu().numpy()[pick],
                      ref.values.cpu().numpy()[pick].astype(np.float64))
     assert not bad, bad
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_batched_grid_tier_groups(cs, dtype):
+    """A batch on the grid tier (N = 2^15) runs as several groups of blocks side by side, each
+    with its own workspace slice and barrier: every instance equals the oracle."""
+    cfg = cs_inputs.Config(75, "sp", 32768, 8192, 64, "gauss", 1e-3)
+    probs, ys, supp, vals, reps = _run(cs, cfg, 7, dtype)
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals, rtol=1e-4 if dtype == "float32" else 1e-8)
+    assert not bad, bad
