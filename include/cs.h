@@ -154,7 +154,7 @@ cs_status cs_operator_destroy(cs_operator* op);
 cs_status cs_operator_info(const cs_operator* op, int64_t* N, int64_t* M, int64_t* batch);
 
 /* Workspace bytes for apply/adjoint (0 for N <= 16384 — batch * N elements with
- * CS_PSI_DCT — else the four-step scratch). */
+ * CS_PSI_DCT — else the four-step scratch per group of a batch run side by side). */
 size_t cs_operator_ws_bytes(const cs_operator* op, int precision /*0 fp32, 1 fp64*/);
 
 /* y[b] = A_b x[b] for every instance b.  x [batch][N], y [batch][M]. */
@@ -182,6 +182,11 @@ cs_status cs_operator_adjoint_f64(const cs_operator* op, const double* d_y, doub
  * Outputs: d_support [K] int32 ascending, d_vals [K] the LS coefficients on it,
  * d_report one cs_report (DEVICE memory).  Requirements: 1 <= K; OMP: K <= M;
  * SP: 2K <= M; OMPR: K + l <= M; CoSaMP: 3K <= M; K <= N/2; 0 <= tol.
+ *
+ * cs_workspace_bytes: DEVICE workspace for cs_recover*: 2 * batch * N elements when the
+ * pursuit fits one CTA (N <= 16384, small K: A^T y per problem plus the Psi scratch), else
+ * the grid tier's per-group layout times the groups a batch can run side by side.  The
+ * workspace may be reused across calls on one stream; it needs no initialisation.
  */
 cs_status cs_workspace_bytes(int alg, int64_t N, int64_t M, int32_t K, int64_t batch,
                              int precision /*0 fp32, 1 fp64*/, const cs_options* opts,
