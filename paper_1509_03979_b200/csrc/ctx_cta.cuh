@@ -57,6 +57,8 @@ template <typename T> struct CtaCtx {
   int* cidx;         // [TOPK_CAP]
   int* ccnt;         // [1]
   static constexpr bool kTopkFast = true;
+  static constexpr bool kDeferD = false;  // d update and scatter use the same thread mapping
+  CS_DEV void defer_d(T*, const T*, T) {}
   int64_t* pick;     // [4]
   // global state of this problem
   const T* y;        // [M]

@@ -215,9 +215,19 @@ template <typename T> struct GridCtx {
   const int* in_supp;
   int in_ns;
   int applies;
+  // CG direction update d = r + beta d (Algorithm 1 line 20) deferred into the next H's
+  // pass A (cg_loop, kDeferD): pass A reads d[i] for the support entries of its tile, i.e.
+  // from other blocks than the one that would update it, with no grid barrier between the
+  // update and the read — so the entry's single reader applies the update (r is published
+  // by the ||r||^2 reduction's barrier) and writes d back for the CG vector update.
+  T* dfr_d = nullptr;
+  const T* dfr_r = nullptr;
+  T dfr_beta = T(0);
+  CS_DEV void defer_d(T* d, const T* r, T beta) { dfr_d = d; dfr_r = r; dfr_beta = beta; }
 
   CS_DEV void sync() { grid_barrier(g.bar, (unsigned)nblk); }
   static constexpr bool kTopkFast = false;
+  static constexpr bool kDeferD = true;
   template <typename P> CS_DEV P* loc(P* p) const { return p; }  // global (Tier L)
 
   // block-level deterministic sum; result valid in thread 0
@@ -524,6 +534,10 @@ template <typename T> struct GridCtx {
     const int* sp = in_supp;
     const int64_t* ip = in_pos;
     const uint32_t* sg = sign;
+    T* const upd = (dfr_d == vals) ? dfr_d : nullptr;   // deferred d = r + beta d (cg_loop)
+    const T* const ur = dfr_r;
+    const T ub = dfr_beta;
+    dfr_d = nullptr;
     for (int64_t t = blk; t < ntl; t += nblk) {
       const int64_t c0i = t * ct;
       for (int e = threadIdx.x; e < tile; e += blockDim.x) sb[e] = mk<T>(0, 0);
@@ -532,7 +546,12 @@ template <typename T> struct GridCtx {
         const int i = tlist[q];
         const int64_t p = ip[i], c = p >> 1;
         const int e = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
-        sbt[2 * swz<T>(e) + (int)(p & 1)] = apply_sign<T>(sg, sp[i], vals[i]);
+        T v = vals[i];
+        if (upd) {
+          v = ur[i] + ub * v;
+          upd[i] = v;
+        }
+        sbt[2 * swz<T>(e) + (int)(p & 1)] = apply_sign<T>(sg, sp[i], v);
       }
       __syncthreads();
       col_fft<false>();

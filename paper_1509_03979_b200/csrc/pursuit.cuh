@@ -89,11 +89,15 @@ CS_DEV void cg_loop(Ctx& c, CgState<T>& s_io, HFn&& Hf) {
     c.mark(16);  // ||r||^2 reduction
 #endif
     const T beta = (T)(rr2 / s.rr);                                        // line 19
-    for (int i = a0; i < n; i += s0) dv[i] = rv[i] + beta * dv[i];        // line 20
+    if constexpr (Ctx::kDeferD)
+      c.defer_d(dv, rv, beta);   // line 20, applied by the next H's scatter (ctx_grid.cuh)
+    else
+      for (int i = a0; i < n; i += s0) dv[i] = rv[i] + beta * dv[i];      // line 20
     s.rr = rr2;
     s.j += 1;                                                              // line 21
     if (!(rr2 == rr2)) { s.status |= CS_DEV_CG_BREAKDOWN; break; }
   }
+  if constexpr (Ctx::kDeferD) c.defer_d(nullptr, nullptr, T(0));   // d is dead after the loop
   s_io = s;
 }
 
