@@ -18,8 +18,8 @@
 
 namespace cs {
 
-struct GridBar {
-  unsigned count;
+struct alignas(8) GridBar {
+  unsigned count;   // count and gen form one 64-bit arrival counter (grid_barrier)
   unsigned gen;
 };
 
@@ -40,23 +40,28 @@ CS_DEV unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
 }
 
 // Grid-wide barrier: block-level barrier, then thread 0 arrives with an acq_rel atomic and
-// spins on the generation word with acquire loads (release/acquire make every block's
+// spins on the arrival counter with acquire loads (release/acquire make every block's
 // writes before the barrier visible after it); bounded spin with a watchdog trap (~15 s).
 // nblk = the blocks that meet at this barrier (a group of the grid, or all of it).
 static CS_NOINL void grid_barrier(GridBar* gb, unsigned nblk) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g = ld_acquire_gpu(&gb->gen);
-    const unsigned arrived = atom_add_acq_rel_gpu(&gb->count, 1u) + 1u;
-    if (arrived == nblk) {
-      gb->count = 0u;                 // ordered before the release below
-      st_release_gpu(&gb->gen, g + 1u);
-    } else {
-      long long t0 = clock64();
-      unsigned spins = 0;
-      while (ld_acquire_gpu(&gb->gen) == g) {
-        if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 35)) __trap();  // never hang the GPU
-      }
+    // One monotonic 64-bit arrival counter (zeroed per launch): the block that arrives at
+    // barrier e sees old in [e nblk, (e+1) nblk) and waits for the count to reach (e+1) nblk.
+    // No generation word: the waiters watch the arrivals themselves, so the barrier costs
+    // one atomic round trip plus the poll that sees the last arrival (no pre-load of a
+    // generation, no release store by the last arriver).
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(gb);
+    unsigned long long old;
+    asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(cnt) : "memory");
+    const unsigned long long target = old - old % nblk + nblk;
+    long long t0 = clock64();
+    unsigned spins = 0;
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+      if (v >= target) break;
+      if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 35)) __trap();  // never hang the GPU
     }
   }
   __syncthreads();
