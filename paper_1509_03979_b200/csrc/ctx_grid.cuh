@@ -220,15 +220,18 @@ template <typename T> struct GridCtx {
   const int* in_supp;
   int in_ns;
   int applies;
-  // CG direction update d = r + beta d (Algorithm 1 line 20) deferred into the next H's
-  // pass A (cg_loop, kDeferD): pass A reads d[i] for the support entries of its tile, i.e.
-  // from other blocks than the one that would update it, with no grid barrier between the
-  // update and the read — so the entry's single reader applies the update (r is published
-  // by the ||r||^2 reduction's barrier) and writes d back for the CG vector update.
+  // CG vector updates deferred into the next H's pass A (cg_iterate / cg_loop, kDeferD):
+  // pass A reads d[i] for the support entries of its tile, i.e. from other blocks than the
+  // one that would update it, with no grid barrier between the update and the read — so the
+  // entry's single reader applies  x += alpha d, r -= alpha q (lines 17-18; dfr_x set) and
+  // d = r + beta d (line 20), and writes them back.
   T* dfr_d = nullptr;
-  const T* dfr_r = nullptr;
-  T dfr_beta = T(0);
-  CS_DEV void defer_d(T* d, const T* r, T beta) { dfr_d = d; dfr_r = r; dfr_beta = beta; }
+  T* dfr_r = nullptr;
+  T* dfr_x = nullptr;
+  const T* dfr_q = nullptr;
+  T dfr_alpha = T(0), dfr_beta = T(0);
+  CS_DEV void defer_d(T* d, T* r, T beta) { dfr_d = d; dfr_r = r; dfr_x = nullptr; dfr_beta = beta; }
+  double p_rq, p_qq, p_rr;   // pass C partials r.q, q.q, r.r of H_dot4 (this block)
 
   CS_DEV void sync() { grid_barrier(g.bar, (unsigned)nblk); }
   static constexpr bool kTopkFast = false;
@@ -539,9 +542,11 @@ template <typename T> struct GridCtx {
     const int* sp = in_supp;
     const int64_t* ip = in_pos;
     const uint32_t* sg = sign;
-    T* const upd = (dfr_d == vals) ? dfr_d : nullptr;   // deferred d = r + beta d (cg_loop)
-    const T* const ur = dfr_r;
-    const T ub = dfr_beta;
+    T* const upd = (dfr_d == vals) ? dfr_d : nullptr;   // deferred CG updates (above)
+    T* const ur = dfr_r;
+    T* const ux = dfr_x;
+    const T* const uq = dfr_q;
+    const T ua = dfr_alpha, ub = dfr_beta;
     dfr_d = nullptr;
     for (int64_t t = blk; t < ntl; t += nblk) {
       const int64_t c0i = t * ct;
@@ -553,7 +558,13 @@ template <typename T> struct GridCtx {
         const int e = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
         T v = vals[i];
         if (upd) {
-          v = ur[i] + ub * v;
+          T ri = ur[i];
+          if (ux) {
+            ux[i] += ua * v;                 // line 17
+            ri -= ua * uq[i];                // line 18
+            ur[i] = ri;
+          }
+          v = ri + ub * v;                   // line 20
           upd[i] = v;
         }
         sbt[2 * swz<T>(e) + (int)(p & 1)] = apply_sign<T>(sg, sp[i], v);
@@ -588,8 +599,8 @@ template <typename T> struct GridCtx {
   // written and no separate gather runs
   // dvec != nullptr: also returns this thread's share of sum_i dvec_i outv_i (H's dot
   // product, reduced by the caller with the pass's closing barrier)
-  CS_NOINL double passC_sparse(T* outv, const T* dvec = nullptr) {
-    double dot = 0;
+  CS_NOINL double passC_sparse(T* outv, const T* dvec = nullptr, const T* rvec = nullptr) {
+    double dot = 0, rq = 0, qq = 0, rr = 0;
     const int ct = CT, lct = (ct == 4) ? 2 : 1;
     const int64_t l2 = L2, ntl = L2 / ct;
     const int tile = (int)(L1 * ct);
@@ -636,6 +647,12 @@ template <typename T> struct GridCtx {
             const T o = (w < 0) ? -v : v;
             outv[oi] = o;
             if (dvec) dot += (double)dvec[oi] * (double)o;
+            if (rvec) {
+              const double rv = (double)rvec[oi];
+              rq += rv * (double)o;
+              qq += (double)o * (double)o;
+              rr += rv * rv;
+            }
           }
         } else {
           for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
@@ -645,6 +662,12 @@ template <typename T> struct GridCtx {
             const T o = apply_sign<T>(sg, sp[i], sbt[2 * swz<T>(e) + (int)(p & 1)]);
             outv[i] = o;
             if (dvec) dot += (double)dvec[i] * (double)o;
+            if (rvec) {
+              const double rv = (double)rvec[i];
+              rq += rv * (double)o;
+              qq += (double)o * (double)o;
+              rr += rv * rv;
+            }
           }
         }
         __syncthreads();
@@ -652,6 +675,9 @@ template <typename T> struct GridCtx {
       q0 = q0n;
       q1 = q1n;
     }
+    p_rq = rq;
+    p_qq = qq;
+    p_rr = rr;
     return dot;
   }
   template <int MODE> CS_NOINL double passB(bool zero_input, T* yout) {
@@ -911,8 +937,94 @@ template <typename T> struct GridCtx {
     ++applies;
     return tot;
   }
-  template <class S> CS_NOINL void cg_iterate(S& s) {
-    cg_loop(*this, s, [this](const T* d, T* q) { return H_dot(d, q); });
+  // q = H d with pass C summing d.q, r.q, q.q and r.r in one grid reduction (H's closing
+  // barrier); r = the current residual (updated by pass A).  sums = {d.q, r.q, q.q, r.r}.
+  CS_NOINL void H_dot4(const T* d, T* q, const T* r, double* sums) {
+    mark(0);
+    passA_sparse(d);
+    sync();
+    mark(1);
+    passB<MID_H>(false, nullptr);
+    sync();
+    mark(2);
+    double t[4];
+    t[0] = passC_sparse(q, d, r);
+    t[1] = p_rq;
+    t[2] = p_qq;
+    t[3] = p_rr;
+    constexpr int NW = (1 << TL_LOG2NT) / 32;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      t[k] = warp_sum_g(t[k]);
+      if (lane == 0) sd[k * NW + (threadIdx.x >> 5)] = t[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {   // [4][2][maxgrid] per-block partials (pd)
+      double a = 0;
+      for (int w = 0; w < NW; ++w) a += sd[threadIdx.x * NW + w];
+      g.pd[((int)threadIdx.x * 2 + bank) * g.maxgrid + blk] = a;
+    }
+    sync();                                    // publishes q, r and the per-block partials
+    if (threadIdx.x < 128) {
+      const int k = (int)threadIdx.x >> 5;
+      const double* P = g.pd + (k * 2 + bank) * g.maxgrid;
+      double a = 0;
+      for (int c = lane; c < (int)nblk; c += 32) a += P[c];
+      a = warp_sum_g(a);
+      if (lane == 0) sd[k] = a;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sums[k] = sd[k];
+    __syncthreads();
+    bank ^= 1;
+    mark(3);
+    ++applies;
+  }
+  // Algorithm 1 lines 14-22 with one grid reduction per iteration (R37): pass C
+  // of H sums d.q, r.q, q.q and the residual's true r.r, so every block then has
+  //   alpha = r.r / d.q  and  |r - alpha q|^2 = r.r - 2 alpha r.q + alpha^2 q.q
+  // (beta and the stopping test) without a second reduction.  r.r is re-anchored on the
+  // vector every iteration — a running recurrence drifts by ~eps |r_0|^2 and diverges once
+  // |r| falls below that.  The updates of x, r (lines 17-18) and d (line 20) are applied by
+  // the next H's pass A to the entries it scatters, and by a flush after the loop.
+  template <class S> CS_NOINL void cg_iterate(S& s_io) {
+    if (psi) {
+      cg_loop(*this, s_io, [this](const T* d, T* q) { return H_dot(d, q); });
+      return;
+    }
+    S s = s_io;
+    T *xx = s.x, *rv = s.r, *dv = s.d, *qv = s.q;
+    bool pend = false;
+    T alpha = T(0);
+    while (true) {
+      if (!(s.rr > s.thr)) break;                                          // line 15 (R6, R7)
+      if (s.j >= s.cap) { s.status |= CS_DEV_CG_CAP; break; }
+      double sums[4];
+      H_dot4(dv, qv, rv, sums);                                            // applies the pending updates
+      const double dq = sums[0], rq = sums[1], qq = sums[2], rrt = sums[3];
+      pend = false;
+      if (!(dq > 0.0)) { s.status |= CS_DEV_CG_BREAKDOWN; break; }
+      alpha = (T)(rrt / dq);                                               // line 16
+      const double a = (double)alpha;
+      double rr2 = rrt - 2.0 * a * rq + a * a * qq;                        // |r_{j+1}|^2
+      if (rr2 < 0.0) rr2 = 0.0;
+      const T beta = (T)(rr2 / rrt);                                       // line 19
+      dfr_d = dv; dfr_r = rv; dfr_x = xx; dfr_q = qv; dfr_alpha = alpha; dfr_beta = beta;
+      pend = true;
+      s.rr = rr2;
+      s.j += 1;                                                            // line 21
+      if (!(rr2 == rr2)) { s.status |= CS_DEV_CG_BREAKDOWN; break; }
+    }
+    dfr_d = nullptr;
+    if (pend) {                                                            // lines 17-18 of the last iteration
+      for (int i = gtid; i < s.ns; i += gnthr) {
+        xx[i] += alpha * dv[i];
+        rv[i] -= alpha * qv[i];
+      }
+    }
+    sync();
+    s_io = s;
   }
   CS_NOINL double RES(const T* x) {
     if (psi) return RES_psi(x);

@@ -90,7 +90,7 @@ CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int 
   // control block (zeroed before every launch)
   s.ctl = o;
   s.bar = take(256);
-  s.pd = take(2 * (int64_t)maxgrid * 8);
+  s.pd = take(8 * (int64_t)maxgrid * 8);   // [4][2][maxgrid]: sum() uses [0], the CG reduction all four
   s.pi = take(2 * (int64_t)maxgrid * 8);
   s.pk = take(2 * (int64_t)maxgrid * 8);
   s.ghist = take(3 * 256 * 4);
