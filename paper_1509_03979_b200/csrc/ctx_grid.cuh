@@ -189,8 +189,9 @@ template <typename T> struct GridCtx {
   int64_t* in_pos;  // [cap] positions of the remembered input support
   // the support bucketed by pass-A / pass-C column tile (CSR): tile t owns the entries
   // tlist[tstart[t] .. tstart[t+1]) (indices into the support list)
-  int* tcnt;        // [ntiles + 1] counts, then exclusive starts
-  int* tfill;       // [ntiles]
+  int* tcnt;        // [ntiles + 1] exclusive starts of the tiles' entries in tlist
+  int* tfill;       // [2][2][ntiles] counts and fill cursors of set_input_support (two parities)
+  int sis_par = 0;  // parity of the next set_input_support
   int* tlist;       // [cap]
   GTw<T> twF;   // W_L
   GTw<T> tw4;   // W_4N
@@ -270,6 +271,35 @@ template <typename T> struct GridCtx {
     __syncthreads();
     bank ^= 1;
     return tot;
+  }
+  // two sums in one grid reduction (partials in pd slots 0 and 1); results in a, b
+  CS_DEV void sum2(double& a, double& b) {
+    constexpr int NW = (1 << TL_LOG2NT) / 32;
+    double t0 = warp_sum_g(a), t1 = warp_sum_g(b);
+    if (lane == 0) {
+      sd[threadIdx.x >> 5] = t0;
+      sd[NW + (threadIdx.x >> 5)] = t1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      double v = 0;
+      for (int w = 0; w < NW; ++w) v += sd[threadIdx.x * NW + w];
+      g.pd[((int)threadIdx.x * 2 + bank) * g.maxgrid + blk] = v;
+    }
+    sync();
+    if (threadIdx.x < 64) {
+      const int k = (int)threadIdx.x >> 5;
+      const double* P = g.pd + (k * 2 + bank) * g.maxgrid;
+      double v = 0;
+      for (int c = lane; c < (int)nblk; c += 32) v += P[c];
+      v = warp_sum_g(v);
+      if (lane == 0) sd[k] = v;
+    }
+    __syncthreads();
+    a = sd[0];
+    b = sd[1];
+    __syncthreads();
+    bank ^= 1;
   }
   CS_DEV int64_t argmax(Key k, int64_t idx) {
 #pragma unroll
@@ -416,48 +446,52 @@ template <typename T> struct GridCtx {
   CS_DEV int ntiles() const { return (int)(L2 / CT); }
   // column tile of Makhoul position p: complex index p/2 = m1 L2 + m2, tile m2 / CT
   CS_DEV int tile_of(int64_t p) const { return (int)(((p >> 1) & (L2 - 1)) / CT); }
+  // Bucket the input support by pass-A/C column tile (CSR: tcnt starts, tlist entries) with
+  // two grid barriers: counts by atomics into this call's zeroed arrays; every block scans the
+  // counts itself into shared memory (block 0 also publishes them as tcnt) and fills tlist
+  // with its own copy; the other parity's arrays are zeroed for the next call.
   CS_DEV void set_input_support(const int* supp, int ns) {
     const int nt = ntiles();
-    for (int t = gtid; t <= nt; t += gnthr) { tcnt[t] = 0; if (t < nt) tfill[t] = 0; }
-    sync();
+    int* cnt = tfill + sis_par * 2 * nt;
+    int* fil = cnt + nt;
+    int* ncnt = tfill + (sis_par ^ 1) * 2 * nt;
     for (int i = gtid; i < ns; i += gnthr) {
       const int64_t p = ppos(pinv, supp[i], N);
       in_pos[i] = p;
-      atomicAdd(&tcnt[tile_of(p)], 1);
+      atomicAdd(&cnt[tile_of(p)], 1);
     }
     sync();
-    if (blk == 0) {  // exclusive scan of the tile counts (one block; nt <= 4096)
-      __shared__ int carry;
-      if (threadIdx.x == 0) carry = 0;
-      __syncthreads();
-      for (int base = 0; base <= nt; base += blockDim.x) {
-        const int t = base + threadIdx.x;
-        const int v = (t < nt) ? tcnt[t] : 0;
-        int inc = v;
+    int* offs = reinterpret_cast<int*>(shp(buf));   // [nt + 1], the tile buffer is free here
+    {
+      const int per = (nt + (int)blockDim.x - 1) / (int)blockDim.x;
+      const int a = (int)threadIdx.x * per, e = min(nt, a + per);
+      int loc = 0;
+      for (int t = a; t < e; ++t) loc += __ldcg(&cnt[t]);
+      int inc = loc;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int u = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += u;
-        }
-        if (lane == 31) si[threadIdx.x >> 5] = inc;
-        __syncthreads();
-        int off = carry, tot = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-          if (w < (int)(threadIdx.x >> 5)) off += (int)si[w];
-          tot += (int)si[w];
-        }
-        __syncthreads();
-        if (t <= nt) tcnt[t] = off + inc - v;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += tot;
-        __syncthreads();
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
       }
+      if (lane == 31) si[threadIdx.x >> 5] = inc;
+      __syncthreads();
+      int base = inc - loc;
+      for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) base += (int)si[w];
+      for (int t = a; t < e; ++t) {
+        offs[t] = base;
+        base += __ldcg(&cnt[t]);
+      }
+      if (threadIdx.x == blockDim.x - 1) offs[nt] = base;
+      __syncthreads();
     }
-    sync();
+    if (blk == 0)
+      for (int t = threadIdx.x; t <= nt; t += blockDim.x) tcnt[t] = offs[t];
     for (int i = gtid; i < ns; i += gnthr) {
       const int t = tile_of(in_pos[i]);
-      tlist[tcnt[t] + atomicAdd(&tfill[t], 1)] = i;
+      tlist[offs[t] + atomicAdd(&fil[t], 1)] = i;
     }
+    for (int t = gtid; t < 2 * nt; t += gnthr) ncnt[t] = 0;
+    sis_par ^= 1;
     in_supp = supp;
     in_ns = ns;
     sync();

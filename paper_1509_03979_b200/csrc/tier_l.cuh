@@ -67,7 +67,6 @@ CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int 
   if (pursuit) {
     s.in_pos = take((int64_t)ucap * 8);
     s.tcnt = take((g.L2 / g.CT + 1) * 4);
-    s.tfill = take((g.L2 / g.CT) * 4);
     s.tlist = take((int64_t)ucap * 4);
     s.S = take((int64_t)K * 4);
     s.S2 = take((int64_t)K * 4);
@@ -95,6 +94,7 @@ CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int 
   s.pk = take(2 * (int64_t)maxgrid * 8);
   s.ghist = take(3 * 256 * 4);
   s.ts = take(64 * 8);  // diagnostics: %globaltimer at phase boundaries (block 0)
+  s.tfill = pursuit ? take(4 * (g.L2 / g.CT) * 4) : 0;   // [2 parities][count, fill][ntiles], zero at launch
   s.ctl_end = o;
   s.bytes = o;
   s.maxgrid = maxgrid;
