@@ -1057,8 +1057,7 @@ template <typename T> struct GridCtx {
         rv[i] -= alpha * qv[i];
       }
     }
-    sync();
-    s_io = s;
+    s_io = s;   // cg_solve's barrier right after this call publishes the flush
   }
   CS_NOINL double RES(const T* x) {
     if (psi) return RES_psi(x);

@@ -123,7 +123,7 @@ CS_DEV void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q, 
     const auto c0v = ctx.c0view();
     for (int i = t0; i < ns; i += sd) b[i] = c0v.at(supp[i]);             // line 12
   }
-  ctx.sync();
+  // no barrier: b[i] is read below only by the thread that wrote it (same i mapping)
   if (!r_given) {
     ctx.H(x, q);
     for (int i = t0; i < ns; i += sd) r[i] = b[i] - q[i];
