@@ -426,7 +426,8 @@ CS_NOINL int run_ompr(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& 
           xU[i] = xv + eta * cv.at(u);                                // z on S u J
         }
       }
-      ctx.sync();
+      // no barrier: the argmin below reads xU[i] in the thread that wrote it; U and xU are
+      // read across threads only after its reduction barrier
       using Key = decltype(full_key(T(0)));
       const Key kmax = Key(1) << (sizeof(Key) * 8 - 1);              // above every key
       Key bk = 0;
