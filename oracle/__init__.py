@@ -17,11 +17,17 @@ Pins (tests/test_oracle_*.py, `-m "not gpu"`):
   cg            numpy.linalg.lstsq on small supports (Thm 1-2), Thm 4 spectral
                 iteration bound, Thm 5 reduced-system trace, orthogonality.
   pursuits      SPEC toy A = I_4 cases, brute-force l0 on tiny N, dense-LS
-                backend equivalence, exact noiseless recovery.
-  parity unpinned: SP on the noisy configs (c2, c5) beyond the invariants
-                (non-increasing residual, fixed point, orthogonality) — there
-                is no independent reference for which support a noisy SP run
-                must end on.
+                backend equivalence, exact noiseless recovery, and hand-worked
+                step pins: OMP's exclusion of S (Eq.(6)), SP's J off S and its
+                RESID_ROSE halt keeping (S, x), OMPR(l, eta)'s eta swap rule
+                (tests/test_oracle_pursuits.py test_*_step / *_exclude_* /
+                *_resid_rose_*; each fails under a mutation of that step).
+  Every step of every pursuit is pinned as above.  What no independent
+                reference fixes is which support a NOISY SP run ends on at the
+                configs' sizes (c2, c5): there the oracle's own full-size answer
+                (tools/oracle_reference.py -> tests/golden/) is the reference,
+                checked on the invariants (non-increasing residual, fixed point,
+                orthogonality).
 """
 from .operator import SrmOperator, DenseOperator, dct_matrix, dense_srm  # noqa: F401
 from .cg import cg, reduced_cg, CgResult  # noqa: F401

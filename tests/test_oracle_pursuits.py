@@ -199,3 +199,84 @@ def test_partial_fourier_cg_backend_equals_dense_ls_and_recovers(alg):
     op, y32 = measure(p)
     res = oracle_recover(p, y32)
     _check_exact(p, res, 1e-6)
+
+
+# ---- step-level pins (VERDICT r1 "What's weak #1"): each one fails if the named step of
+# oracle/pursuits.py is mutated.  Every expected value is worked out by hand in the docstring.
+
+def test_omp_excludes_current_support_on_zero_ties():
+    """Eq.(6) with reading R12: the argmax runs over j not in S.  A = I_4,
+    y = (5, 0, -3, 0), K = 3: t1 = 0 (x = 5), t2 = 2 (x = -3), after which r = 0 and every
+    |c_j| = 0; the argmax over j not in S picks the lowest such index, 1.  Without the
+    exclusion it would re-pick index 0."""
+    res = omp(DenseOperator(np.eye(4)), np.array([5.0, 0.0, -3.0, 0.0]), 3, tol=1e-13)
+    np.testing.assert_array_equal(res.support, [0, 1, 2])
+    np.testing.assert_allclose(res.x, [5.0, 0.0, -3.0], atol=1e-14)
+
+
+def test_sp_resid_rose_keeps_previous_support():
+    """SP halting (reading R15): when the pruned support's residual does not fall,
+    stop and KEEP (S, x).  K = 1, A = [[3,1,0],[-1,0,-1]], y = (3, 2):
+      A^T y = (7, 3, -2)                 -> S = {0}, x = 7/10 = 0.7
+      r = (0.9, 2.7), ||r||^2 = 8.1;  c = A^T r = (0, 0.9, -2.7) -> J = {2}
+      LS on T = {0, 2}: x_T = (1, -3)    -> S' = {2}, x' = a_2.y/|a_2|^2 = -2
+      r' = (3, 0), ||r'|| = 3 >= sqrt(8.1) = 2.846 -> RESID_ROSE, return S = {0}, x = 0.7.
+    Without the halting rule SP would move to {2} and stop there (S' = S next time)."""
+    A = np.array([[3.0, 1.0, 0.0], [-1.0, 0.0, -1.0]])
+    res = sp(DenseOperator(A), np.array([3.0, 2.0]), 1, tol=1e-13)
+    assert res.termination == oracle.pursuits.T_RESID_ROSE
+    np.testing.assert_array_equal(res.support, [0])
+    np.testing.assert_allclose(res.x, [0.7], rtol=1e-12)
+    np.testing.assert_allclose(res.resid_norm, np.sqrt(8.1), rtol=1e-12)
+    assert res.outer_iters == 1
+
+
+def test_sp_candidates_exclude_current_support():
+    """SP's J = top-K of |c| over j NOT in S.  K = 2,
+    A = [[0,0,2,-1,1],[1,0,0,2,0],[2,2,-1,0,0],[0,0,0,0,2]], y = (0,-2,-3,1):
+      A^T y = (-8, -6, 3, -4, 2)                  -> S = {0, 1}, x = (-2, 0.5)
+      r = (0, 0, 0, 1), c = A^T r = (0, 0, 0, 0, 2): off S only c_4 != 0, so J = {4, 2}
+      (the zero tie goes to the lowest index NOT in S);  T = {0,1,2,4} is square:
+      x_T = (-2, 0.375, -0.25, 0.5)              -> S' = {0, 4}
+      a_0 and a_4 are orthogonal: x' = (a_0.y/5, a_4.y/5) = (-1.6, 0.4),
+      r' = (-0.4, -0.4, 0.2, 0.2), ||r'||^2 = 0.4 < 1 -> accept
+      c = A^T r' = (0, 0.4, -1, -0.4, 0) -> J = {2, 1} (or {2, 3}: both give S' = {0, 4})
+      -> S' = S: SUPPORT_FIXED after 2 outer iterations with S = {0, 4}, x = (-1.6, 0.4).
+    Taking J over ALL indices gives J = {4, 0}, T = {0, 1, 4}, x_T = (-2, 0.5, 0.4) and a
+    premature fixed point at {0, 1}.  The exact dense-LS backend keeps the zero ties exact
+    (integer data, r = (0, 0, 0, 1) exactly); CG would leave ~1e-16 correlations that
+    break them arbitrarily."""
+    A = np.array([[0, 0, 2, -1, 1], [1, 0, 0, 2, 0], [2, 2, -1, 0, 0], [0, 0, 0, 0, 2]], float)
+    res = sp(DenseOperator(A), np.array([0.0, -2.0, -3.0, 1.0]), 2, tol=1e-13, solver="lstsq")
+    np.testing.assert_array_equal(res.support, [0, 4])
+    np.testing.assert_allclose(res.x, [-1.6, 0.4], rtol=1e-10)
+    assert res.termination == oracle.pursuits.T_SUPPORT_FIXED and res.outer_iters == 2
+    np.testing.assert_allclose(res.resid_history, [1.0, np.sqrt(0.4)], rtol=1e-10)
+
+
+@pytest.mark.parametrize("eta,support,x,term", [
+    (1.0, [0, 2], [5.0, 4.0], 3),     # z_J = (3, 2.5) < min|x_S| = 4: S' = S
+    (1.5, [0, 3], [5.0, 3.0], 1),     # z = (5, 4, 4.5, 3.75): keep 0 and 3
+    (2.5, [3, 5], [3.0, 2.5], 1),     # z = (5, 4, 7.5, 6.25): keep 3 and 5
+])
+def test_ompr_eta_step(eta, support, x, term):
+    """One OMPR(l, eta) step (reading R16): z = x~ + eta A^T r,
+    J = top-l of |z| off S, S' = top-K of |z| over S u J.  A = I_8, K = 2, l = 2,
+    y = (5, 0, 4, 3, 0, 2.5, 0, 0): S = {0, 2}, x = (5, 4), r = c = y off S, so on
+    U = {0, 2, 3, 5}: z = (5, 4, 3 eta, 2.5 eta).  One outer iteration (max_outer = 1);
+    the new x is y on S' (LS with A = I).  eta decides every swap."""
+    y = np.array([5.0, 0.0, 4.0, 3.0, 0.0, 2.5, 0.0, 0.0])
+    res = ompr(DenseOperator(np.eye(8)), y, 2, tol=1e-13, l=2, eta=eta, max_outer=1)
+    np.testing.assert_array_equal(res.support, support)
+    np.testing.assert_allclose(res.x, x, atol=1e-12)
+    assert res.termination == term and res.outer_iters == 1
+
+
+@pytest.mark.parametrize("eta,support,term,outer", [(1.0, [0], 3, 1), (2.0, [1], 1, 1)])
+def test_ompr1_eta_decides_the_swap(eta, support, term, outer):
+    """OMPR(1): A = I_4, y = (4, 3, 0, 0), K = 1: S = {0}, x = 4, c = (0, 3, 0, 0), so the
+    single candidate j = 1 has z_1 = 3 eta.  eta = 1: 3 < 4, S' = S (SUPPORT_FIXED);
+    eta = 2: 6 > 4, swap to {1} with x = 3 (one step, max_outer = 1)."""
+    res = ompr(DenseOperator(np.eye(4)), np.array([4.0, 3.0, 0.0, 0.0]), 1, tol=1e-13, eta=eta, max_outer=1)
+    np.testing.assert_array_equal(res.support, support)
+    assert res.termination == term and res.outer_iters == outer
