@@ -8,7 +8,7 @@
 namespace cs {
 
 struct SFix {
-  int64_t Z, twLlo, twLhi, tw4lo, tw4hi, sign, rmask, prefix, redd, redi, redk, hist, pick, h1, ckey, cidx, ccnt, zero, end;
+  int64_t Z, twLlo, twLhi, tw4lo, tw4hi, sign, rmask, prefix, usel, redd, redi, redk, hist, pick, h1, ckey, cidx, ccnt, zero, end;
 };
 
 __host__ __device__ constexpr int64_t al16(int64_t x) { return (x + 15) / 16 * 16; }
@@ -25,6 +25,9 @@ template <typename T> __host__ __device__ constexpr SFix s_fixed(int64_t N) {
   s.sign = o;   o = al16(o + nw * 4);
   s.rmask = o;  o = al16(o + nw * 4);
   s.prefix = o; o = al16(o + nw * 4);
+  // row selection in the fused pass's unit order (sandwich_cta.cuh sw_fused): one word per
+  // thread, bit 8 it + q = [DCT index q of the thread's unit it is a row]
+  s.usel = o;   o = al16(o + 512 * 4);
   s.redd = o;   o = al16(o + 2 * 32 * 8);  // two banks: one barrier per reduction
   s.redi = o;   o = al16(o + 33 * 8);
   s.redk = o;   o = al16(o + 32 * 8);

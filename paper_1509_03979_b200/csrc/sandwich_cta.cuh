@@ -87,6 +87,56 @@ CS_DEV void sw_pass(C2<T>* buf, const TwTable<T>& tw, int nsb) {
   __syncthreads();
 }
 
+// ---- the transposed pass (conjugated): the inverse FFT is conj(F)^T = conj(P_1)^T ...
+// conj(P_last)^T (the DFT matrix is symmetric), i.e. the forward passes transposed and
+// applied in reverse order.  Pass (radix 2^RB, stride Ns = 2^nsb), item j < L/R, k = j mod Ns:
+//    V_r = x'[(j-k) R + k + r Ns],  u = DFT_R^{-1}(V),  x[j + s L/R] = u_s W_{Ns R}^{-s k}
+// (the forward pass's write pattern read, its read pattern written, the twiddle after the
+// DFT).  Compared with a second forward-ordered (DIT) inverse, the strides of the inverse
+// are the forward's: Ns = 1 needs no twiddle, and the fused radix-2 pass stays in place.
+template <typename T, int LOG2L, int RB>
+CS_DEV void sw_pass_t(C2<T>* buf, const TwTable<T>& tw, int nsb) {
+  constexpr int R = 1 << RB, Lr = (1 << LOG2L) >> RB;
+  static_assert(Lr <= SW_NT, "one item per thread");
+  const int j = opaque_tid<T, LOG2L>();
+  C2<T> v[R];
+  const bool act = (Lr == SW_NT) || j < Lr;
+  const int Ns = 1 << nsb, k = j & (Ns - 1);
+  if (act) {
+    const int sb = swz<T>((j - k) * R + k);  // bit-disjoint from r Ns
+    int e[RB];                                 // swz(Ns << b)
+#pragma unroll
+    for (int b = 0; b < RB; ++b) e[b] = swz<T>(Ns << b);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      int o = sb;
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+        if (r & (1 << b)) o ^= e[b];
+      v[r] = buf[o];
+    }
+    dft_reg<T, R, true>(v);  // u_s at v[bitrev(s)]
+    if (Ns > 1) {
+      C2<T> u[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) u[q] = v[bitrev<R>(q)];
+      tw_stream<T, R>(u, cconj<T>(tw(k << (LOG2L - nsb - RB))));
+#pragma unroll
+      for (int q = 0; q < R; ++q) v[bitrev<R>(q)] = u[q];
+    }
+  }
+  __syncthreads();
+  if (act) {
+    const int sj = swz<T>(j);  // j < Lr: bit-disjoint from s Lr
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if constexpr (Lr % 512 == 0) buf[sj + q * Lr] = v[bitrev<R>(q)];
+      else buf[sj ^ swz_c<T>(q * Lr)] = v[bitrev<R>(q)];
+    }
+  }
+  __syncthreads();
+}
+
 template <int LOG2L> struct SwPlan {
   // forward radices: [remainder 2^M if M > 0] [16] x Q [2 (fused)]; inverse reversed
   static constexpr int M = (LOG2L - 1) % 4;
@@ -103,87 +153,127 @@ template <typename T> CS_DEV C2<T> w16c() {
 }
 
 // ---- the fused unit: last forward pass (radix 2), DCT middle, first inverse pass ----
-// Unit k (1 <= k < L/4) owns items k and L/2 - k of the radix-2 pass, i.e.
+// Unit k (1 <= k < L/4) owns items k and kb = L/2 - k of the radix-2 pass (Ns = L/2), i.e.
+// the slots k, k + L/2, kb, kb + L/2 holding, after the pass,
 //   A0 = Z_k, A1 = Z_{k+L/2}, B0 = Z_{L/2-k}, B1 = Z_{L-k};
 // mirror pairs: (A0, B1) at n = k and (A1, B0) at n = k + L/2.
 // Unit 0 (items 0 and L/4): Z_0 (alone), Z_{L/2} (self pair), (Z_{L/4}, Z_{3L/4}).
+// The pass twiddles are W_L^k and W_L^{kb} = W_L^{L/2} W_L^{-k} = -conj(W_L^k) (one lookup).
+// The first inverse pass is this pass transposed (sw_pass_t): inverse radix-2 butterfly,
+// then the conjugate twiddle, written back to the SAME four slots — every thread writes
+// only what it read, so the pass needs no barrier between its loads and stores.
+// Row selection: for KIND 0 the 8 DCT indices of each of the thread's units are one byte of
+// its `usel` word (built per instance by sw_build_usel): 8 it + q, q = 0..3 the pair n = k
+// (k, N-k, L-k, N-L+k), q = 4..7 the pair n = k + L/2 (k+L/2, N-k-L/2, L/2-k, N-L/2+k).
 // KIND 0: F = DCT-II (the middle above); KIND 1: F = partial Fourier (dct_mid.cuh dft_*, R36)
+template <int LOG2L> CS_DEV int usel_idx(int k, int q) {
+  constexpr int L = 1 << LOG2L, H = L / 2, N = 2 * L;
+  const int n = (q < 4) ? k : k + H;
+  const int kk = L - n;
+  const int r = q & 3;
+  return r == 0 ? n : r == 1 ? N - n : r == 2 ? kk : N - kk;
+}
+
+// usel[t]: bit 8 it + q set <=> DCT index usel_idx(t + SW_NT it, q) is a row (k >= 1 only)
+template <typename T, int LOG2L>
+CS_DEV void sw_build_usel_t(uint32_t* usel, const uint32_t* rowmask) {
+  using SP = SwPlan<LOG2L>;
+  for (int t = threadIdx.x; t < SW_NT; t += blockDim.x) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int it = 0; it < SP::UPT; ++it) {
+      const int k = t + it * SW_NT;
+      if (k >= 1 && k < SP::U) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w |= (uint32_t)bit_test32(rowmask, usel_idx<LOG2L>(k, q)) << (8 * it + q);
+      }
+    }
+    usel[t] = w;
+  }
+}
+
+template <typename T, int MODE, int TY>
+CS_DEV T mid_sel_op(const MidCtx<T>& m, const MidK<T>& c, bool sel, int idx, T raw, double& rn2) {
+  return mid_op2g<T, MODE, TY>(m, c, sel, [&] { return row_rank32(m.rowmask, m.prefix, idx); }, raw, rn2);
+}
+
 template <typename T, int LOG2L, int MODE, bool ZERO, int KIND = 0>
 CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, const MidCtx<T>& m) {
   using SP = SwPlan<LOG2L>;
-  constexpr int L = 1 << LOG2L, H = L / 2, U = SP::U, UPT = SP::UPT;
+  constexpr int L = 1 << LOG2L, H = L / 2, U = SP::U, UPT = SP::UPT, N = 2 * L;
   static_assert(L >= 4, "N >= 8");
+  constexpr SFix F = s_fixed<T>(N);
   const int tid = opaque_tid<T, LOG2L>();
   const MidK<T> cst = make_midk_c<T, LOG2L + 1>();
+  const uint32_t selw = (KIND == 0 && MODE == MID_H) ? reinterpret_cast<const uint32_t*>(cs_smem_base + F.usel)[tid] : 0u;
   double rn2 = 0;
-  C2<T> A0[UPT], A1[UPT], B0[UPT], B1[UPT];
 #pragma unroll
   for (int it = 0; it < UPT; ++it) {
     const int k = tid + it * SW_NT;
     if ((U % SW_NT == 0) || k < U) {
       const int kb = (k == 0) ? L / 4 : H - k;
+      const C2<T> wk = (k == 0) ? mk<T>(1, 0) : tw(k);                    // W_L^k
+      const C2<T> wb = (k == 0) ? mk<T>(0, -1) : mk<T>(-wk.x, wk.y);       // W_L^{kb}
+      const int sa = swz<T>(k), sa2 = swz<T>(k + H), sb = swz<T>(kb), sb2 = swz<T>(kb + H);
+      C2<T> A0, A1, B0, B1;
       if constexpr (ZERO) {
-        A0[it] = A1[it] = B0[it] = B1[it] = mk<T>(0, 0);
+        A0 = A1 = B0 = B1 = mk<T>(0, 0);
       } else {
         // radix-2 pass, Ns = L/2: item j reads x[j], x[j + L/2]; twiddle W_L^j
-        C2<T> a0 = buf[swz<T>(k)], a1 = buf[swz<T>(k + H)];
-        C2<T> b0 = buf[swz<T>(kb)], b1 = buf[swz<T>(kb + H)];
-        a1 = cmul<T>(a1, tw(k));
-        b1 = cmul<T>(b1, tw(kb));
-        A0[it] = cadd<T>(a0, a1);
-        A1[it] = csub<T>(a0, a1);
-        B0[it] = cadd<T>(b0, b1);
-        B1[it] = csub<T>(b0, b1);
+        const C2<T> a0 = buf[sa], b0 = buf[sb];
+        const C2<T> a1 = cmul<T>(buf[sa2], wk), b1 = cmul<T>(buf[sb2], wb);
+        A0 = cadd<T>(a0, a1);
+        A1 = csub<T>(a0, a1);
+        B0 = cadd<T>(b0, b1);
+        B1 = csub<T>(b0, b1);
       }
       if constexpr (KIND == 1) {
         if (k != 0) {
           const C2<T> a = tw4(k);
           const C2<T> a2 = cmul<T>(a, a);
           const C2<T> w = cmul<T>(a2, a2);                     // W_N^k
-          dft_pair_w<T, MODE>(A0[it], B1[it], k, w, m, rn2);
-          dft_pair_w<T, MODE>(A1[it], B0[it], k + H, mk<T>(w.y, -w.x), m, rn2);
+          dft_pair_w<T, MODE>(A0, B1, k, w, m, rn2);
+          dft_pair_w<T, MODE>(A1, B0, k + H, mk<T>(w.y, -w.x), m, rn2);
         } else {
-          dft_zero<T, MODE>(A0[it], m, rn2);
-          dft_pair<T, MODE>(A1[it], A1[it], H, tw4(H), m, rn2);  // self pair n = L/2
-          dft_pair<T, MODE>(B0[it], B1[it], L / 4, tw4(L / 4), m, rn2);
+          dft_zero<T, MODE>(A0, m, rn2);
+          dft_pair<T, MODE>(A1, A1, H, tw4(H), m, rn2);  // self pair n = L/2
+          dft_pair<T, MODE>(B0, B1, L / 4, tw4(L / 4), m, rn2);
         }
       } else {
-      if (k != 0) {
-        const C2<T> a = tw4(k);
-        const C2<T> a2 = cmul<T>(a, a);
-        const C2<T> w = cmul<T>(a2, a2);                       // W_N^k
-        mid_pair2<T, MODE>(A0[it], B1[it], k, a, w, m, cst, rn2);
-        const C2<T> ah = cmul<T>(a, w16c<T>());                // W_4N^{k + L/2}
-        const C2<T> wh = mk<T>(w.y, -w.x);                     // W_N^{k + L/2} = -i W_N^k
-        mid_pair2<T, MODE>(A1[it], B0[it], k + H, ah, wh, m, cst, rn2);
-      } else {
-        mid_zero<T, MODE>(A0[it], m, rn2);
-        mid_pair<T, MODE>(A1[it], A1[it], H, tw4(H), m, rn2);  // self pair n = L/2
-        mid_pair<T, MODE>(B0[it], B1[it], L / 4, tw4(L / 4), m, rn2);
+        if (k != 0) {
+          const C2<T> a = tw4(k);
+          const C2<T> a2 = cmul<T>(a, a);
+          const C2<T> w = cmul<T>(a2, a2);                     // W_N^k
+          // MID_H: selection from the thread's usel byte; RES / FWD: from the row mask (their
+          // rank lookups read it anyway; the apply / adjoint kernels do not build usel)
+          const uint32_t sl = selw >> (8 * it);
+          auto sel = [&](int q) {
+            if constexpr (MODE == MID_H) return ((sl >> q) & 1u) != 0;
+            else return bit_test32(m.rowmask, usel_idx<LOG2L>(k, q));
+          };
+          mid_pair2g<T, MODE>(A0, B1, a, w, m, cst, rn2, [&](int q) { return sel(q); },
+                              [&](int q) { return row_rank32(m.rowmask, m.prefix, usel_idx<LOG2L>(k, q)); });
+          const C2<T> ah = cmul<T>(a, w16c<T>());              // W_4N^{k + L/2}
+          const C2<T> wh = mk<T>(w.y, -w.x);                   // W_N^{k + L/2} = -i W_N^k
+          mid_pair2g<T, MODE>(A1, B0, ah, wh, m, cst, rn2, [&](int q) { return sel(q + 4); },
+                              [&](int q) { return row_rank32(m.rowmask, m.prefix, usel_idx<LOG2L>(k, q + 4)); });
+        } else {
+          mid_zero<T, MODE>(A0, m, rn2);
+          mid_pair<T, MODE>(A1, A1, H, tw4(H), m, rn2);  // self pair n = L/2
+          mid_pair<T, MODE>(B0, B1, L / 4, tw4(L / 4), m, rn2);
+        }
       }
+      if constexpr (MODE != MID_FWD) {
+        // first inverse pass = the radix-2 pass transposed: butterfly, conj twiddle, in place
+        buf[sa] = cadd<T>(A0, A1);
+        buf[sa2] = cmulc<T>(csub<T>(A0, A1), wk);
+        buf[sb] = cadd<T>(B0, B1);
+        buf[sb2] = cmulc<T>(csub<T>(B0, B1), wb);
       }
     }
   }
-  if constexpr (MODE == MID_FWD) {
-    return rn2;
-  } else {
-    __syncthreads();  // every load of the pass precedes every store (in place)
-#pragma unroll
-    for (int it = 0; it < UPT; ++it) {
-      const int k = tid + it * SW_NT;
-      if ((U % SW_NT == 0) || k < U) {
-        const int kb = (k == 0) ? L / 4 : H - k;
-        // inverse radix-2 pass, Ns = 1: item j reads x[j], x[j + L/2], writes x'[2j], x'[2j+1]
-        const int sa = swz<T>(2 * k), sb = swz<T>(2 * kb);
-        buf[sa] = cadd<T>(A0[it], A1[it]);
-        buf[sa ^ 1] = csub<T>(A0[it], A1[it]);
-        buf[sb] = cadd<T>(B0[it], B1[it]);
-        buf[sb ^ 1] = csub<T>(B0[it], B1[it]);
-      }
-    }
-    __syncthreads();
-    return rn2;
-  }
+  if constexpr (MODE != MID_FWD) __syncthreads();
+  return rn2;
 }
 
 // ---- Psi = DCT (R35): the fused last-forward / first-inverse pass of the two extra
@@ -286,12 +376,13 @@ CS_DEV void sw_fused_psi(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4
           dct_in_pair<T>(A1, A1, H, tw4(H), m, &o[it][2]);   // self pair (reads o[2], o[3])
           dct_in_pair<T>(B0, B1, L / 4, tw4(L / 4), m, &o[it][4]);
         }
-        // inverse radix-2 pass, Ns = 1 (as in sw_fused)
-        const int sa = swz<T>(2 * k), sb = swz<T>(2 * kb);
-        buf[sa] = cadd<T>(A0, A1);
-        buf[sa ^ 1] = csub<T>(A0, A1);
-        buf[sb] = cadd<T>(B0, B1);
-        buf[sb ^ 1] = csub<T>(B0, B1);
+        // first inverse pass: the radix-2 pass transposed, in place (as in sw_fused)
+        const C2<T> wk = (k == 0) ? mk<T>(1, 0) : tw(k);
+        const C2<T> wb = (k == 0) ? mk<T>(0, -1) : mk<T>(-wk.x, wk.y);
+        buf[swz<T>(k)] = cadd<T>(A0, A1);
+        buf[swz<T>(k + H)] = cmulc<T>(csub<T>(A0, A1), wk);
+        buf[swz<T>(kb)] = cadd<T>(B0, B1);
+        buf[swz<T>(kb + H)] = cmulc<T>(csub<T>(B0, B1), wb);
       }
     }
     __syncthreads();
@@ -302,6 +393,15 @@ template <typename T, int LOG2L, bool INV>
 CS_DEV void sw_remainder(C2<T>* buf, const TwTable<T>& tw, int nsb) {
   constexpr int M = SwPlan<LOG2L>::M;
   if constexpr (M > 0) sw_pass<T, LOG2L, M, INV>(buf, tw, nsb);
+}
+
+// the usel table for a runtime transform length (log2 L in [2, 13])
+template <typename T, int LO = 2, int HI = 13>
+CS_DEV void sw_build_usel(int log2l, uint32_t* usel, const uint32_t* rowmask) {
+  if constexpr (LO <= HI) {
+    if (log2l == LO) { sw_build_usel_t<T, LO>(usel, rowmask); return; }
+    sw_build_usel<T, LO + 1, HI>(log2l, usel, rowmask);
+  }
 }
 
 // The whole sandwich as ONE out-of-line unit (one ABI register save/restore per
@@ -370,8 +470,8 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
   }
   if constexpr (MODE != MID_FWD && MODE != MID_FWDZ) {
 #pragma unroll 1
-    for (int q = 0; q < SP::Q; ++q) sw_pass<T, LOG2L, 4, true>(buf, tw, 1 + 4 * q);
-    sw_remainder<T, LOG2L, true>(buf, tw, 1 + 4 * SP::Q);
+    for (int q = SP::Q - 1; q >= 0; --q) sw_pass_t<T, LOG2L, 4>(buf, tw, SP::NS_R16_FWD0 + 4 * q);
+    if constexpr (SP::M > 0) sw_pass_t<T, LOG2L, SP::M>(buf, tw, 0);
     if (gio.vout) {
       const int* supp = shp(gio.supp);
       const uint32_t* sign = signs;

@@ -273,6 +273,9 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_recover(SRecArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
   const int64_t b = blockIdx.x;
   CtaCtx<T> c = make_cta_ctx<T>(smem, a.lay, a.meta, b);
+  // row selection in the fused pass's unit order for the CG loop's H (sandwich_cta.cuh sw_fused)
+  sw_build_usel<T>(c.log2L, reinterpret_cast<uint32_t*>(smem + s_fixed<T>(a.meta.N).usel), c.rowmask);
+  __syncthreads();
   c.y = a.Y + b * c.M;
   c.c0 = a.c0ws + b * 2 * c.N;
   c.G = c.c0 + c.N;
