@@ -87,7 +87,7 @@ template <typename T> struct CtaCtx {
   // sum's readers by the next sum's barrier — so one barrier per reduction.
   CS_DEV double sum(double v) {
     v = warp_sum(v);
-    double* rb = shp(redd) + 32 * rbank;
+    double* rb = shp(redd) + 64 * rbank;  // banks of 64 (cg_iterate_t bsum4 uses [4][16])
     rbank ^= 1;
     if (lane == 0) rb[gwarp] = v;
     __syncthreads();
@@ -223,7 +223,7 @@ template <typename T> struct CtaCtx {
     constexpr int64_t REDD = F.redd;
     auto bsum = [&rb](double v) {
       v = warp_sum(v);
-      double* slots = reinterpret_cast<double*>(cs_smem_base + REDD) + 32 * rb;
+      double* slots = reinterpret_cast<double*>(cs_smem_base + REDD) + 64 * rb;
       rb ^= 1;
       if ((threadIdx.x & 31) == 0) slots[threadIdx.x >> 5] = v;
       __syncthreads();
@@ -232,26 +232,67 @@ template <typename T> struct CtaCtx {
       for (int w = 0; w < NWARP; ++w) t += slots[w];
       return t;
     };
+    // One block reduction per iteration (as the grid tier's R37): after q = H d the four
+    // sums d.q, r.q, q.q and the current r.r go through ONE barrier; alpha uses the measured
+    // r.r, and ||r_{j+1}||^2 = r.r - 2 alpha r.q + alpha^2 q.q (line 18 expanded, exact in
+    // real arithmetic with the alpha actually applied) gives beta and the stopping test.
+    // Each thread owns the same elements in the gather, the updates and the next scatter,
+    // so the x, r, d updates need no barrier of their own.
+    constexpr int64_t REDD4 = F.redd;
+    auto bsum4 = [&rb](double& a, double& b, double& c, double& d) {
+      const unsigned full = 0xffffffffu;
+      const int lane = threadIdx.x & 31;
+      // transpose-reduce: 4 values over 32 lanes -> lane 0: a, 8: b, 16: c, 24: d
+      const bool h16 = lane & 16, h8 = lane & 8;
+      double k0 = h16 ? c : a, k1 = h16 ? d : b;
+      k0 += __shfl_xor_sync(full, h16 ? a : c, 16);
+      k1 += __shfl_xor_sync(full, h16 ? b : d, 16);
+      double k = h8 ? k1 : k0;
+      k += __shfl_xor_sync(full, h8 ? k0 : k1, 8);
+      k += __shfl_xor_sync(full, k, 4);
+      k += __shfl_xor_sync(full, k, 2);
+      k += __shfl_xor_sync(full, k, 1);
+      double* slots = reinterpret_cast<double*>(cs_smem_base + REDD4) + 64 * rb;   // [4][16]
+      rb ^= 1;
+      if ((lane & 7) == 0) slots[(lane >> 3) * 16 + (threadIdx.x >> 5)] = k;
+      __syncthreads();
+      // lane l sums warps 2 (l & 7), 2 (l & 7) + 1 of value l >> 3, then 8 lanes per value
+      const double* sv = slots + (lane >> 3) * 16 + 2 * (lane & 7);
+      double t = sv[0] + sv[1];
+      t += __shfl_xor_sync(full, t, 4);
+      t += __shfl_xor_sync(full, t, 2);
+      t += __shfl_xor_sync(full, t, 1);
+      a = __shfl_sync(full, t, 0);
+      b = __shfl_sync(full, t, 8);
+      c = __shfl_sync(full, t, 16);
+      d = __shfl_sync(full, t, 24);
+    };
+    (void)bsum;
     while (true) {
       if (!(rr > thr)) break;                                              // line 15 (R6, R7)
       if (j >= cap) { status |= CS_DEV_CG_CAP; break; }
       sw_body<T, LOG2L, MID_H, false, PERM, KIND>(nullptr, TwTable<T>{}, TwTable<T>{}, m0,
                                       SwIO<T>{sp, n, nullptr, dv, qv});    // q = H d_j
-      double dq = 0;
-      for (int i = threadIdx.x; i < n; i += NT) dq += (double)dv[i] * (double)qv[i];
-      dq = bsum(dq);
+      double dq = 0, rq = 0, qq = 0, rrm = 0;
+      for (int i = threadIdx.x; i < n; i += NT) {
+        const double di = dv[i], qi = qv[i], ri = rv[i];
+        dq += di * qi;
+        rq += ri * qi;
+        qq += qi * qi;
+        rrm += ri * ri;
+      }
+      bsum4(dq, rq, qq, rrm);
       if (!(dq > 0.0)) { status |= CS_DEV_CG_BREAKDOWN; break; }
-      const T alpha = (T)(rr / dq);                                        // line 16
-      double rr2 = 0;
+      const T alpha = (T)(rrm / dq);                                       // line 16
+      const double al = (double)alpha;
+      const double rr2 = rrm - 2.0 * al * rq + al * al * qq;               // ||r_{j+1}||^2
+      const T beta = (T)(rr2 / rrm);                                       // line 19
       for (int i = threadIdx.x; i < n; i += NT) {
         xv[i] += alpha * dv[i];                                            // line 17
         const T ri = rv[i] - alpha * qv[i];                                // line 18
         rv[i] = ri;
-        rr2 += (double)ri * (double)ri;
+        dv[i] = ri + beta * dv[i];                                         // line 20
       }
-      rr2 = bsum(rr2);
-      const T beta = (T)(rr2 / rr);                                        // line 19
-      for (int i = threadIdx.x; i < n; i += NT) dv[i] = rv[i] + beta * dv[i];  // line 20
       rr = rr2;
       ++j;                                                                 // line 21
       if (!(rr2 == rr2)) { status |= CS_DEV_CG_BREAKDOWN; break; }

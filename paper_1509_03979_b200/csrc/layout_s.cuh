@@ -8,7 +8,7 @@
 namespace cs {
 
 struct SFix {
-  int64_t Z, twLlo, twLhi, tw4lo, tw4hi, sign, rmask, prefix, usel, redd, redi, redk, hist, pick, h1, ckey, cidx, ccnt, zero, end;
+  int64_t Z, twLlo, twLhi, tw4lo, tw4hi, sign, rmask, prefix, usel, tw16, redd, redi, redk, hist, pick, h1, ckey, cidx, ccnt, zero, end;
 };
 
 __host__ __device__ constexpr int64_t al16(int64_t x) { return (x + 15) / 16 * 16; }
@@ -28,7 +28,9 @@ template <typename T> __host__ __device__ constexpr SFix s_fixed(int64_t N) {
   // row selection in the fused pass's unit order (sandwich_cta.cuh sw_fused): one word per
   // thread, bit 8 it + q = [DCT index q of the thread's unit it is a row]
   s.usel = o;   o = al16(o + 512 * 4);
-  s.redd = o;   o = al16(o + 2 * 32 * 8);  // two banks: one barrier per reduction
+  // twiddles of the first twiddled radix-16 pass (stride Ns1 <= 16): [r][k] = W_{16 Ns1}^{r k}
+  s.tw16 = o;   o = al16(o + 256 * cs2);
+  s.redd = o;   o = al16(o + 2 * 64 * 8);  // two banks of [4][16] (CG) or [32] (sum): one barrier per reduction
   s.redi = o;   o = al16(o + 33 * 8);
   s.redk = o;   o = al16(o + 32 * 8);
   s.hist = o;   o = al16(o + 256 * 4);

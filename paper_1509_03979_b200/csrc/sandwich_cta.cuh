@@ -43,6 +43,19 @@ template <typename T, int LOG2L> CS_DEV int opaque_tid() {
   return (int)threadIdx.x + *reinterpret_cast<volatile int*>(cs_smem_base + F.zero);
 }
 
+template <int LOG2L> struct SwPlan {
+  // forward radices: [remainder 2^M if M > 0] [16] x Q [2 (fused)]; inverse reversed
+  static constexpr int M = (LOG2L - 1) % 4;
+  static constexpr int Q = (LOG2L - 1) / 4;
+  static constexpr int NS_R16_FWD0 = M;                                  // log2 Ns, first fwd radix-16 pass
+  // log2 Ns of the first radix-16 pass that has twiddles (Ns1 <= 16: its 16 Ns1 twiddles
+  // W_{16 Ns1}^{r k} come from the tw16 table, one LDS each, instead of a product chain)
+  static constexpr int NS1B = (M == 0) ? 4 : M;
+  static constexpr int U = (1 << LOG2L) / 4 > 0 ? (1 << LOG2L) / 4 : 1;  // fused units
+  static constexpr int UPT = (U + SW_NT - 1) / SW_NT;                     // units per thread
+  static_assert(UPT <= 4, "L <= 8192");
+};
+
 // ---- one Stockham pass of radix 2^RB at runtime stride Ns = 2^nsb; L = 2^LOG2L ----
 template <typename T, int LOG2L, int RB, bool INV>
 CS_DEV void sw_pass(C2<T>* buf, const TwTable<T>& tw, int nsb) {
@@ -63,9 +76,16 @@ CS_DEV void sw_pass(C2<T>* buf, const TwTable<T>& tw, int nsb) {
       for (int r = 0; r < R; ++r) v[r] = buf[sj ^ swz_c<T>(r * Lr)];
     }
     if (Ns > 1) {
-      C2<T> w1 = tw(k << (LOG2L - nsb - RB));
-      if (INV) w1 = cconj<T>(w1);
-      tw_stream<T, R>(v, w1);
+      if (RB == 4 && nsb == SwPlan<LOG2L>::NS1B) {
+        constexpr SFix F = s_fixed<T>(int64_t(2) << LOG2L);
+        const C2<T>* t16 = reinterpret_cast<const C2<T>*>(cs_smem_base + F.tw16) + k;  // [r][k]: conflict-free
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = INV ? cmulc<T>(v[r], t16[16 * r]) : cmul<T>(v[r], t16[16 * r]);
+      } else {
+        C2<T> w1 = tw(k << (LOG2L - nsb - RB));
+        if (INV) w1 = cconj<T>(w1);
+        tw_stream<T, R>(v, w1);
+      }
     }
     dft_reg<T, R, INV>(v);
   }
@@ -117,12 +137,19 @@ CS_DEV void sw_pass_t(C2<T>* buf, const TwTable<T>& tw, int nsb) {
     }
     dft_reg<T, R, true>(v);  // u_s at v[bitrev(s)]
     if (Ns > 1) {
-      C2<T> u[R];
+      if (RB == 4 && nsb == SwPlan<LOG2L>::NS1B) {
+        constexpr SFix F = s_fixed<T>(int64_t(2) << LOG2L);
+        const C2<T>* t16 = reinterpret_cast<const C2<T>*>(cs_smem_base + F.tw16) + k;  // [r][k]: conflict-free
 #pragma unroll
-      for (int q = 0; q < R; ++q) u[q] = v[bitrev<R>(q)];
-      tw_stream<T, R>(u, cconj<T>(tw(k << (LOG2L - nsb - RB))));
+        for (int q = 1; q < R; ++q) v[bitrev<R>(q)] = cmulc<T>(v[bitrev<R>(q)], t16[16 * q]);
+      } else {
+        C2<T> u[R];
 #pragma unroll
-      for (int q = 0; q < R; ++q) v[bitrev<R>(q)] = u[q];
+        for (int q = 0; q < R; ++q) u[q] = v[bitrev<R>(q)];
+        tw_stream<T, R>(u, cconj<T>(tw(k << (LOG2L - nsb - RB))));
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[bitrev<R>(q)] = u[q];
+      }
     }
   }
   __syncthreads();
@@ -137,15 +164,6 @@ CS_DEV void sw_pass_t(C2<T>* buf, const TwTable<T>& tw, int nsb) {
   __syncthreads();
 }
 
-template <int LOG2L> struct SwPlan {
-  // forward radices: [remainder 2^M if M > 0] [16] x Q [2 (fused)]; inverse reversed
-  static constexpr int M = (LOG2L - 1) % 4;
-  static constexpr int Q = (LOG2L - 1) / 4;
-  static constexpr int NS_R16_FWD0 = M;                                  // log2 Ns, first fwd radix-16 pass
-  static constexpr int U = (1 << LOG2L) / 4 > 0 ? (1 << LOG2L) / 4 : 1;  // fused units
-  static constexpr int UPT = (U + SW_NT - 1) / SW_NT;                     // units per thread
-  static_assert(UPT <= 4, "L <= 8192");
-};
 
 // W_16^1 (a_{k + L/2} = a_k W_16)
 template <typename T> CS_DEV C2<T> w16c() {

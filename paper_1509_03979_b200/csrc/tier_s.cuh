@@ -136,6 +136,17 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
              (int)(L >= 64 ? L / 64 : 1), c.gtid, c.gnthr);
   tw_init<T>(const_cast<C2<T>*>(c.tw4.lo), const_cast<C2<T>*>(c.tw4.hi), 8 * L,
              (int)(L / 128 + 1), c.gtid, c.gnthr);
+  {
+    // [r][k] = W_{16 Ns1}^{r k}, Ns1 = 2^NS1B of sandwich_cta.cuh SwPlan (fp64 sincospi)
+    const int m = (c.log2L - 1) % 4, ns1 = 1 << (m == 0 ? 4 : m);
+    C2<T>* t16 = reinterpret_cast<C2<T>*>(smem + s_fixed<T>(meta.N).tw16);
+    for (int i = c.gtid; i < 256; i += c.gnthr) {
+      const int r = i >> 4, k = i & 15;
+      double sn, cn;
+      sincospi(-2.0 * (double)((r * k) % (16 * ns1)) / (double)(16 * ns1), &sn, &cn);
+      t16[i] = mk<T>((T)cn, (T)sn);
+    }
+  }
   cta_set_instance<T>(c, smem, meta, b);
   return c;
 }
