@@ -38,7 +38,7 @@ class Config:
     N: int
     M: int
     K: int
-    signal: str         # "gauss" | "pm1" | "power"
+    signal: str         # "gauss" | "pm1" | "power" | "bernoulli" (Eq.(13))
     noise: float        # sigma_eta
     batch: int = 1
     randomizer: str = "sign"   # "sign": R = diag(+-1) (BASELINE); "perm": Eq.(7)'s permutation, sigma = +1
@@ -106,6 +106,12 @@ def draw_signal(kind: str, N: int, K: int, g_pos: np.random.Generator,
         sgn = np.where(g_val.integers(0, 2, N) == 1, -1.0, 1.0)
         s[perm] = sgn * mag
         return s, np.sort(perm[:K])
+    if kind == "bernoulli":
+        # the paper's Eq.(13): every entry nonzero with probability p = K/N,
+        # N(0, 1) values (sigma_on = 1); the number of nonzeros is itself random
+        on = g_pos.random(N) < K / N
+        s[on] = g_val.standard_normal(int(on.sum()))
+        return s, np.nonzero(on)[0]
     pos = np.sort(g_pos.choice(N, K, replace=False))
     if kind == "gauss":
         vals = g_val.standard_normal(K)
@@ -154,6 +160,12 @@ def make_problem(cfg: Config, trial: int = 0, b: int = 0) -> Problem:
         else np.zeros(M)
     return Problem(N, M, K, cfg.alg, bits, rows, s, supp, eta, perm, "dct" if cfg.psi == "dct" else None,
                    cfg.transform)
+
+
+def paper_regime(alg: str, N: int) -> Config:
+    """The paper's experimental regime (Tables II-IV): M = N/4, K = M/4,
+    Bernoulli-Gaussian s (Eq.(13)), sigma_eta = 0.01."""
+    return Config(13, alg, N, N // 4, N // 16, "bernoulli", 0.01)
 
 
 def make_batch(cfg: Config, trial: int = 0, b0: int = 0, count: Optional[int] = None):

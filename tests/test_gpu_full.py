@@ -9,9 +9,14 @@ answer at any size:
     is orthogonal to the selected columns, ||A_S^T (y - A_S x)|| <= eps ||A_S^T y||,
     evaluated with the ORACLE operator in fp64;
   * coefficients equal the oracle's CG-solved LS on that support (c3).
-The oracle's full-recovery parity for c3 and c5 is pinned at reduced scale in
-test_gpu_recover.py.
+c3 and c5 are ALSO held to the oracle's own full-size answer: tools/oracle_reference.py
+(oracle/ only) ran the fp64 oracle once on the same seeded inputs and stored support,
+coefficients and iteration counts in tests/golden/oracle_c{3,5}.npz; the fp32 / fp64 GPU
+results are compared with those (the y fed to the GPU is checked to be the y the oracle saw).
 """
+import hashlib
+import os
+
 import numpy as np
 import pytest
 
@@ -75,6 +80,7 @@ def test_c4_full_batch_sampled(cs):
     # only under compare_fp32_floor's rule.
     planted = np.stack([p.support for p in probs])
     miss = np.nonzero(~(supp == planted).all(axis=1))[0]
+    print(f"c4 fp32: {miss.size} of {cfg.batch} problems off the planted support: {miss.tolist()}")
     assert miss.size <= cfg.batch // 100, miss.size
     if miss.size:
         sub = [probs[i] for i in miss]
@@ -108,17 +114,18 @@ def test_c2_full_fp64_matches_oracle(cs):
     assert not bad, bad
 
 
-def test_c2_full_fp32_valid_and_close(cs):
-    """fp32 on the noisy c2 is precision-fragile (~15% of seeds flip a
-    boundary index).  Bar: LS-optimal on its own support at the fp32 CG floor, and
-    the support overlaps the oracle's by >= 99%."""
+def test_c2_full_fp32_matches_oracle(cs):
+    """fp32 on the noisy c2 (SURVEY App. A flags ~15% of seeds as precision-fragile at a
+    boundary index): on the BASELINE seed the fp32 GPU run ends on exactly the oracle's
+    support, with coefficients within the BASELINE bar, and is LS-optimal at its CG floor."""
     cfg = CONFIGS[2]
     probs = cs_inputs.make_batch(cfg, count=1)
     ys = measured(probs)
     supp, vals, reps = _recover(cs, cfg, probs, ys, "float32", 1e-6)
-    ref = oracle_results(probs, ys)[0]
-    overlap = np.intersect1d(supp[0], ref.support).size / cfg.K
-    assert overlap >= 0.99, overlap
+    refs = oracle_results(probs, ys)
+    bad, worst = compare(probs, refs, supp, vals, rtol=1e-4)
+    print(f"c2 fp32 vs oracle: symdiff {np.setxor1d(supp[0], refs[0].support).size}, rel {worst:.3e}")
+    assert not bad, bad
     assert _ls_optimality(probs[0], ys[0], supp[0], vals[0]) < 5e-5
 
 
@@ -155,3 +162,88 @@ def test_c5_full_fp64_ls_optimal(cs):
     overlap = np.intersect1d(s32[0], supp[0]).size / cfg.K
     assert overlap >= 0.9, overlap   # fp32 diverges on the noise-dominated tail
     assert _ls_optimality(probs[0], ys[0], s32[0], v32[0]) < 1e-4
+
+
+# ---- c3 / c5 against the oracle's full-size answer (tests/golden, tools/oracle_reference.py)
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(cid):
+    g = np.load(os.path.join(GOLDEN, f"oracle_c{cid}.npz"))
+    return {k: g[k] for k in g.files}
+
+
+def _same_input(cfg, ys, g):
+    y_sha = hashlib.sha256(np.ascontiguousarray(ys[0], dtype=np.float32).tobytes()).hexdigest()
+    assert y_sha == str(g["y_sha"]), "the GPU must see the y the oracle reference was computed on"
+
+
+def _vs_golden(cfg, supp, vals, g):
+    sg = np.sort(supp[0])
+    symdiff = int(np.setxor1d(sg, g["support"]).size)
+    s_or = dense_from(cfg.N, g["support"], g["x"])
+    s_gpu = dense_from(cfg.N, supp[0], vals[0])
+    rel = float(np.linalg.norm(s_gpu - s_or) / np.linalg.norm(s_or))
+    return symdiff, rel
+
+
+@pytest.mark.parametrize("dtype,tol,rtol", [("float32", 1e-6, 1e-4), ("float64", 1e-10, 1e-8)])
+def test_c3_full_matches_oracle_reference(cs, dtype, tol, rtol):
+    """OMPR(1) at N = 2^20 (the paper's P:89 size): the oracle's 698-swap trajectory ends on
+    the planted support; the GPU (fp32 at the BASELINE bar, fp64 at the oracle's tol to
+    1e-8) returns the same support and coefficients after the same number of swaps."""
+    cfg = CONFIGS[3]
+    g = _golden(3)
+    probs = cs_inputs.make_batch(cfg, count=1)
+    ys = measured(probs)
+    _same_input(cfg, ys, g)
+    supp, vals, reps = _recover(cs, cfg, probs, ys, dtype, tol)
+    symdiff, rel = _vs_golden(cfg, supp, vals, g)
+    print(f"c3 {dtype} vs oracle: symdiff {symdiff}, rel {rel:.3e}, outer {reps[0]['outer_iters']} "
+          f"(oracle {int(g['outer_iters'])}), cg {reps[0]['cg_iters_total']} (oracle {int(g['cg_iters'])})")
+    assert symdiff == 0 and rel <= rtol, (symdiff, rel)
+    assert reps[0]["outer_iters"] == int(g["outer_iters"])
+    assert reps[0]["termination"] == int(g["termination"])
+
+
+@pytest.mark.slow
+def test_c5_full_fp64_matches_oracle_reference(cs):
+    """SP at N = 2^24, K = 65536, compressible + noise (Table IV's largest N): the
+    fp64 GPU path at the oracle's tolerance ends on the oracle's support (all 65536 indices,
+    most of them noise-dominated) with coefficients within 1e-8, the same outer iterations
+    and the same halting reason."""
+    cfg = CONFIGS[5]
+    g = _golden(5)
+    probs = cs_inputs.make_batch(cfg, count=1)
+    ys = measured(probs)
+    _same_input(cfg, ys, g)
+    supp, vals, reps = _recover(cs, cfg, probs, ys, "float64", 1e-10)
+    symdiff, rel = _vs_golden(cfg, supp, vals, g)
+    print(f"c5 fp64 vs oracle: symdiff {symdiff}, rel {rel:.3e}, outer {reps[0]['outer_iters']} "
+          f"(oracle {int(g['outer_iters'])}), term {reps[0]['termination']} (oracle {int(g['termination'])})")
+    assert symdiff == 0 and rel <= 1e-8, (symdiff, rel)
+    assert reps[0]["outer_iters"] == int(g["outer_iters"])
+    assert reps[0]["termination"] == int(g["termination"])
+
+
+@pytest.mark.slow
+def test_c5_full_fp32_reported_against_oracle_reference(cs):
+    """fp32 at c5 cannot match the oracle index for index (the tail of the
+    power-law signal sits under the noise, below the fp32 LS floor).  Measured and printed:
+    the support symmetric difference and coefficient rel-diff against the oracle's answer;
+    held to: a finished pursuit, LS optimality on its own support, and the large coefficients
+    (every index with |s_or| above the noise floor sigma sqrt(N/M)) all selected."""
+    cfg = CONFIGS[5]
+    g = _golden(5)
+    probs = cs_inputs.make_batch(cfg, count=1)
+    ys = measured(probs)
+    supp, vals, reps = _recover(cs, cfg, probs, ys, "float32", 1e-6)
+    symdiff, rel = _vs_golden(cfg, supp, vals, g)
+    print(f"c5 fp32 vs oracle: symdiff {symdiff} of {2 * cfg.K}, rel {rel:.3e}, "
+          f"outer {reps[0]['outer_iters']} (oracle {int(g['outer_iters'])})")
+    assert reps[0]["termination"] in (3, 4)
+    assert _ls_optimality(probs[0], ys[0], supp[0], vals[0]) < 1e-4
+    floor = cfg.noise * np.sqrt(cfg.N / cfg.M)
+    big = g["support"][np.abs(g["x"]) > 10 * floor]
+    assert np.isin(big, supp[0]).all()
+    assert rel < 0.1     # measured 5.0e-2 (symdiff 8892 of 131072, DESIGN.md §10)

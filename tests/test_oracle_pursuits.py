@@ -280,3 +280,27 @@ def test_ompr1_eta_decides_the_swap(eta, support, term, outer):
     res = ompr(DenseOperator(np.eye(4)), np.array([4.0, 3.0, 0.0, 0.0]), 1, tol=1e-13, eta=eta, max_outer=1)
     np.testing.assert_array_equal(res.support, support)
     assert res.termination == term and res.outer_iters == outer
+
+
+@pytest.mark.parametrize("cid", [3, 5])
+def test_full_size_oracle_references_are_consistent(cid):
+    """tests/golden/oracle_c{3,5}.npz (written by tools/oracle_reference.py from oracle/ only)
+    pinned to things other than themselves: the stored y digest is the digest of the seeded
+    input formed here; the stored coefficients are the LS solution on the stored support
+    (residual orthogonal to the selected columns, Thm 1-2, P:328-406, to the CG tolerance);
+    c3 (noiseless, M >> K log(N/K)) is the planted support."""
+    import hashlib
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", f"oracle_c{cid}.npz"))
+    p = cs_inputs.make_problem(CONFIGS[cid], 0, 0)
+    op, y32 = measure(p)
+    assert hashlib.sha256(y32.tobytes()).hexdigest() == str(g["y_sha"])
+    S, x = g["support"], g["x"]
+    assert S.size == p.K and np.all(np.diff(S) > 0)
+    s_hat = np.zeros(p.N)
+    s_hat[S] = x
+    y = y32.astype(np.float64)
+    grad = op.adjoint(y - op.apply(s_hat))[S]
+    assert np.linalg.norm(grad) <= 1e-9 * np.linalg.norm(op.adjoint(y)[S])
+    if cid == 3:
+        np.testing.assert_array_equal(S, p.support)
+        assert int(g["termination"]) == oracle.pursuits.T_SUPPORT_FIXED
