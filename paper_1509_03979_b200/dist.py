@@ -44,13 +44,23 @@ def unpack_records(rec, K: int, value_dtype):
     return supp, vals, rep
 
 
-def gather_records(rec, world: int, out=None, group=None):
-    """All-gather every rank's [B_r, rec] block (equal B_r on all ranks) into
-    [world * B_r, rec] in rank order (= problem order for `shard` with total % world == 0)."""
+def gather_records(rec, world: int, total: int = 0, out=None, group=None):
+    """All-gather every rank's [B_r, rec] block into [total, rec] in rank order (= problem
+    order for `shard`).  Blocks may differ by one problem (total % world != 0): each rank's
+    block is padded to ceil(total / world) records for the collective and the padding is
+    dropped afterwards.  total = 0 means world * B_r (equal blocks)."""
     import torch
     import torch.distributed as dist
+    B_r, R = rec.shape
+    if total <= 0:
+        total = world * B_r
+    per = -(-total // world)
+    if B_r != per:
+        pad = torch.zeros((per, R), dtype=rec.dtype, device=rec.device)
+        pad[:B_r] = rec
+        rec = pad
     flat = rec.contiguous().reshape(-1)
-    if out is None:
+    if out is None or out.numel() != world * flat.numel():
         out = torch.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, flat, group=group)
@@ -58,4 +68,8 @@ def gather_records(rec, world: int, out=None, group=None):
         parts = list(out.chunk(world))
         dist.all_gather(parts, flat, group=group)
         out = torch.cat(parts)
-    return out.reshape(world * rec.shape[0], rec.shape[1])
+    full = out.reshape(world, per, R)
+    if per * world == total:
+        return full.reshape(total, R)
+    keep = [shard(total, r, world)[1] for r in range(world)]
+    return torch.cat([full[r, :keep[r]] for r in range(world)])

@@ -43,7 +43,7 @@ def _worker(rank, world, port, total, q):
         supp, vals, rep = _fake_results(b0, cnt, torch.float32)
         rec = csd.pack_records(supp, vals, rep)
         assert rec.shape == (cnt, csd.record_bytes(K, 4))
-        allrec = csd.gather_records(rec, world)
+        allrec = csd.gather_records(rec, world, total=total)
         if rank == 0:
             s, v, r = csd.unpack_records(allrec, K, torch.float32)
             q.put((s.numpy(), v.numpy(), r.numpy()))
@@ -65,8 +65,11 @@ def test_pack_unpack_roundtrip():
     assert torch.equal(s, supp) and torch.equal(v, vals) and torch.equal(r, rep)
 
 
-def test_gloo_world2_gather_in_problem_order():
-    world, total = 2, 64
+@pytest.mark.parametrize("total", [64, 65])
+def test_gloo_world2_gather_in_problem_order(total):
+    """Equal blocks (the 4096 / G split of bench.py) and uneven ones (total % world != 0:
+    the first rank holds one extra problem; gather_records pads and trims)."""
+    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
