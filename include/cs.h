@@ -229,12 +229,21 @@ cs_status cs_support_to_dense_f64(int64_t B, int64_t N, int32_t K, const int32_t
  *   cs_gather_batched: device i (in `devices` order) holds B_per_dev records in
  *     d_vals[i] [B][K] fp32, d_support[i] [B][K], d_reports[i] [B]; they land at block i of
  *     the root's d_vals_all / d_support_all / d_reports_all ([ndev][B]...).  Blocking: returns
- *     after the transfers (NCCL send/recv over NVLink; the root copies its own block).
+ *     after the transfers (NCCL send/recv over NVLink; the root copies its own block).  It runs
+ *     on the library's own per-device streams and is NOT ordered after the caller's work: the
+ *     caller synchronises the producing streams first, or uses cs_gather_batched_after.
+ *   cs_gather_batched_after: the same, ordered after everything enqueued so far on
+ *     after[i] (device i's producer stream; NULL entries / a NULL array: no ordering), so the
+ *     recovery kernels that write the records need no host synchronisation in between.
  * (Multi-process jobs use torch.distributed, paper_1509_03979_b200/dist.py.) */
 cs_status cs_comm_init(int ndev, const int* devices, void** comm);
 cs_status cs_gather_batched(void* comm, int root, int64_t B_per_dev, int32_t K, const float* const* d_vals,
                             const int32_t* const* d_support, const cs_report* const* d_reports,
                             float* d_vals_all, int32_t* d_support_all, cs_report* d_reports_all);
+cs_status cs_gather_batched_after(void* comm, int root, int64_t B_per_dev, int32_t K, const float* const* d_vals,
+                                  const int32_t* const* d_support, const cs_report* const* d_reports,
+                                  float* d_vals_all, int32_t* d_support_all, cs_report* d_reports_all,
+                                  const cs_stream_t* after);
 cs_status cs_comm_destroy(void* comm);
 
 /* Host-buffer variants (the end-to-end entry points): h_Y [B][M] and the outputs

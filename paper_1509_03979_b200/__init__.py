@@ -58,7 +58,7 @@ EXPORTS = [
     "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
     "cs_diag_topk", "cs_operator_meta_bytes_perm", "cs_operator_create_perm", "cs_operator_create_ex",
     "cs_operator_meta_bytes_ex", "cs_operator_meta_bytes_dft", "cs_operator_create_dft",
-    "cs_support_to_dense", "cs_support_to_dense_f64", "cs_comm_init", "cs_gather_batched", "cs_comm_destroy",
+    "cs_support_to_dense", "cs_support_to_dense_f64", "cs_comm_init", "cs_gather_batched", "cs_gather_batched_after", "cs_comm_destroy",
 ]
 
 
@@ -83,6 +83,8 @@ def load_library(path: str = LIB_PATH):
         "cs_comm_init": (I32, [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(P)]),
         "cs_gather_batched": (I32, [P, ctypes.c_int, I64, I32, ctypes.POINTER(P), ctypes.POINTER(P),
                                     ctypes.POINTER(P), P, P, P]),
+        "cs_gather_batched_after": (I32, [P, ctypes.c_int, I64, I32, ctypes.POINTER(P), ctypes.POINTER(P),
+                                          ctypes.POINTER(P), P, P, P, ctypes.POINTER(P)]),
         "cs_comm_destroy": (I32, [P]),
         "cs_operator_create_dft": (I32, [I64, I64, I64, P, P, P, P, SZ, P, ctypes.POINTER(P)]),
         "cs_operator_create_ex": (I32, [I64, I64, I64, P, P, P, ctypes.c_int, P, SZ, P, ctypes.POINTER(P)]),
@@ -396,8 +398,11 @@ class Comm:
         pv = (P * nd)(*[r.values.data_ptr() for r in results])
         ps = (P * nd)(*[r.support.data_ptr() for r in results])
         pr = (P * nd)(*[r.report_dev.data_ptr() for r in results])
-        _check(_lib.cs_gather_batched(self.handle, root, B, K, pv, ps, pr, _ptr(vals), _ptr(supp), _ptr(reps)),
-               "cs_gather_batched")
+        # ordered after each device's current torch stream (the producers of the records and
+        # of the freshly allocated outputs): no host synchronisation needed before the call
+        after = (P * nd)(*[torch.cuda.current_stream(d).cuda_stream for d in self.devices])
+        _check(_lib.cs_gather_batched_after(self.handle, root, B, K, pv, ps, pr, _ptr(vals), _ptr(supp),
+                                            _ptr(reps), after), "cs_gather_batched_after")
         return supp, vals, reps
 
     def __del__(self):

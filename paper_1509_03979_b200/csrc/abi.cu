@@ -14,6 +14,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -324,9 +325,9 @@ struct HostPipe {
 };
 HostPipe& host_pipe(int dev) {
   static std::mutex mu;
-  static HostPipe pipes[16];
+  static std::map<int, HostPipe> pipes;   // keyed by device ordinal; references stay valid
   std::lock_guard<std::mutex> lock(mu);
-  HostPipe& p = pipes[dev & 15];
+  HostPipe& p = pipes[dev];
   if (!p.ok) {
     bool good = cudaStreamCreateWithFlags(&p.s_in, cudaStreamNonBlocking) == cudaSuccess &&
                 cudaStreamCreateWithFlags(&p.s_out, cudaStreamNonBlocking) == cudaSuccess &&
@@ -379,12 +380,27 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
   const bool tier_s = tier_s_fits<T>(N, K, ucap_of(alg, K, l), true);
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // chunk = two waves of the Tier S recovery (two blocks per SM); Tier L: one chunk
-  const int64_t CH = tier_s ? std::max<int64_t>(1, (int64_t)4 * nsm) : B;
+  // chunk = two waves of the Tier S recovery (two blocks per SM), enlarged so that a batch
+  // never needs more than the 64 event pairs of the pipeline; Tier L: one chunk
+  int64_t CH = tier_s ? std::max<int64_t>(1, (int64_t)4 * nsm) : B;
+  CH = std::max<int64_t>(CH, (B + 63) / 64);
   const int64_t nch = (B + CH - 1) / CH;
-  if (nch > 64) return fail(CS_ERR_INVALID_ARG, "batch too large for the host pipeline (64 chunks)");
   CS_CUDA(cudaEventRecord(hp.fin, st));             // order behind earlier work on the caller's stream
   CS_CUDA(cudaStreamWaitEvent(hp.s_in, hp.fin, 0));
+  // on a failure after copies were queued, the caller's stream still waits for everything
+  // already on the pipeline streams (so the caller can free its pinned buffers safely)
+  auto drain = [&](cs_status s) {
+    cudaStream_t ss[3] = {hp.s_in, hp.s_comp, hp.s_out};
+    for (cudaStream_t x : ss)
+      if (cudaEventRecord(hp.fin, x) == cudaSuccess) cudaStreamWaitEvent(st, hp.fin, 0);
+    return s;
+  };
+#undef CS_CUDA
+#define CS_CUDA(call)                                                   \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) return drain(cuda_fail(e_, #call));          \
+  } while (0)
   for (int64_t c = 0; c < nch; ++c) {
     const int64_t b0 = c * CH, cnt = std::min(CH, B - b0);
     CS_CUDA(cudaMemcpyAsync(dY + b0 * M, hY + b0 * M, (size_t)(cnt * M) * sizeof(T), cudaMemcpyHostToDevice,
@@ -400,7 +416,7 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
     const size_t rws_bytes = tier_s ? (size_t)(cnt * 2 * N) * sizeof(T) : need_rec;
     if (cs_status s = recover_impl<T>(&sub, alg, dY + b0 * M, cnt, M, N, K, tol, opts, dvals + b0 * K,
                                       dsupp + b0 * K, dreps + b0, rws, rws_bytes, sc))
-      return s;
+      return drain(s);
     CS_CUDA(cudaEventRecord(hp.ev[1][c], sc));
     CS_CUDA(cudaStreamWaitEvent(hp.s_out, hp.ev[1][c], 0));
     CS_CUDA(cudaMemcpyAsync(hsupp + b0 * K, dsupp + b0 * K, (size_t)(cnt * K) * 4, cudaMemcpyDeviceToHost,
@@ -413,6 +429,12 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
   CS_CUDA(cudaEventRecord(hp.fin, hp.s_out));
   CS_CUDA(cudaStreamWaitEvent(st, hp.fin, 0));      // the caller's stream completes after everything
   return CS_OK;
+#undef CS_CUDA
+#define CS_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
 }
 
 }  // namespace
@@ -471,6 +493,7 @@ struct CsComm {
   std::vector<int> dev;
   std::vector<ncclComm_t> comms;
   std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> ready;   // per device: the producers' point the gather waits for
 };
 }  // namespace
 
@@ -810,6 +833,7 @@ cs_status cs_comm_init(int ndev, const int* devices, void** comm) {
   c->dev.assign(devices, devices + ndev);
   c->comms.assign(ndev, nullptr);
   c->streams.assign(ndev, nullptr);
+  c->ready.assign(ndev, nullptr);
   ncclResult_t r = api.init_all(c->comms.data(), ndev, devices);
   if (r != ncclSuccess) {
     delete c;
@@ -817,18 +841,32 @@ cs_status cs_comm_init(int ndev, const int* devices, void** comm) {
   }
   int cur = 0;
   cudaGetDevice(&cur);
-  for (int i = 0; i < ndev; ++i) {
-    cudaSetDevice(devices[i]);
-    cudaStreamCreateWithFlags(&c->streams[i], cudaStreamNonBlocking);
+  bool good = true;
+  for (int i = 0; i < ndev && good; ++i) {
+    good = cudaSetDevice(devices[i]) == cudaSuccess &&
+           cudaStreamCreateWithFlags(&c->streams[i], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&c->ready[i], cudaEventDisableTiming) == cudaSuccess;
   }
   cudaSetDevice(cur);
+  if (!good) {
+    cs_comm_destroy(c);
+    return fail(CS_ERR_CUDA, "could not create the gather streams");
+  }
   *comm = c;
   return CS_OK;
 }
 
-cs_status cs_gather_batched(void* comm, int root, int64_t B_per_dev, int32_t K, const float* const* d_vals,
-                            const int32_t* const* d_support, const cs_report* const* d_reports, float* d_vals_all,
-                            int32_t* d_support_all, cs_report* d_reports_all) {
+// restores the caller's current device on every exit path
+struct DeviceGuard {
+  int cur = 0;
+  DeviceGuard() { cudaGetDevice(&cur); }
+  ~DeviceGuard() { cudaSetDevice(cur); }
+};
+
+cs_status cs_gather_batched_after(void* comm, int root, int64_t B_per_dev, int32_t K, const float* const* d_vals,
+                                  const int32_t* const* d_support, const cs_report* const* d_reports,
+                                  float* d_vals_all, int32_t* d_support_all, cs_report* d_reports_all,
+                                  const cs_stream_t* after) {
   CsComm* c = reinterpret_cast<CsComm*>(comm);
   if (!c || !d_vals || !d_support || !d_reports || !d_vals_all || !d_support_all || !d_reports_all)
     return fail(CS_ERR_INVALID_ARG, "null pointer argument");
@@ -836,8 +874,17 @@ cs_status cs_gather_batched(void* comm, int root, int64_t B_per_dev, int32_t K, 
   if (root < 0 || root >= nd || B_per_dev < 1 || K < 1) return fail(CS_ERR_INVALID_ARG, "bad arguments");
   const NcclApi& api = nccl_api();
   const size_t bv = (size_t)(B_per_dev * K) * 4, br = (size_t)B_per_dev * sizeof(cs_report);
-  int cur = 0;
-  cudaGetDevice(&cur);
+  DeviceGuard guard;
+  // order the gather after the producers: device i's internal stream waits for everything
+  // enqueued so far on after[i] (the streams that wrote the records and the outputs)
+  if (after) {
+    for (int i = 0; i < nd; ++i) {
+      if (!after[i]) continue;
+      CS_CUDA(cudaSetDevice(c->dev[i]));
+      CS_CUDA(cudaEventRecord(c->ready[i], after[i]));
+      CS_CUDA(cudaStreamWaitEvent(c->streams[i], c->ready[i], 0));
+    }
+  }
   // device i's records land at block i of the root's arrays; the root copies its own block
   CS_CUDA(cudaSetDevice(c->dev[root]));
   for (int kind = 0; kind < 3; ++kind) {
@@ -849,34 +896,36 @@ cs_status cs_gather_batched(void* comm, int root, int64_t B_per_dev, int32_t K, 
     CS_CUDA(cudaMemcpyAsync(dst + (size_t)root * bytes, src, bytes, cudaMemcpyDeviceToDevice, c->streams[root]));
   }
   if (nd > 1) {
-    api.group_start();
-    for (int i = 0; i < nd; ++i) {
+    if (!api.ok) return fail(CS_ERR_UNSUPPORTED, "NCCL not available");
+    ncclResult_t r = api.group_start();
+    for (int i = 0; i < nd && r == ncclSuccess; ++i) {
       if (i == root) continue;
-      for (int kind = 0; kind < 3; ++kind) {
+      for (int kind = 0; kind < 3 && r == ncclSuccess; ++kind) {
         const size_t bytes = kind == 2 ? br : bv;
         char* dst = kind == 0 ? reinterpret_cast<char*>(d_vals_all)
                   : kind == 1 ? reinterpret_cast<char*>(d_support_all) : reinterpret_cast<char*>(d_reports_all);
         const void* src = kind == 0 ? (const void*)d_vals[i] : kind == 1 ? (const void*)d_support[i]
                                                                          : (const void*)d_reports[i];
-        api.send(src, bytes, ncclUint8, root, c->comms[i], c->streams[i]);
-        api.recv(dst + (size_t)i * bytes, bytes, ncclUint8, i, c->comms[root], c->streams[root]);
+        r = api.send(src, bytes, ncclUint8, root, c->comms[i], c->streams[i]);
+        if (r == ncclSuccess) r = api.recv(dst + (size_t)i * bytes, bytes, ncclUint8, i, c->comms[root], c->streams[root]);
       }
     }
-    const ncclResult_t r = api.group_end();
-    if (r != ncclSuccess) {
-      cudaSetDevice(cur);
-      return fail(CS_ERR_CUDA, std::string("nccl gather: ") + api.err(r));
-    }
+    const ncclResult_t re = api.group_end();
+    if (r == ncclSuccess) r = re;
+    if (r != ncclSuccess) return fail(CS_ERR_CUDA, std::string("nccl gather: ") + api.err(r));
   }
   for (int i = 0; i < nd; ++i) {
-    cudaSetDevice(c->dev[i]);
-    if (cudaStreamSynchronize(c->streams[i]) != cudaSuccess) {
-      cudaSetDevice(cur);
-      return fail(CS_ERR_CUDA, "gather stream synchronisation failed");
-    }
+    CS_CUDA(cudaSetDevice(c->dev[i]));
+    if (cudaStreamSynchronize(c->streams[i]) != cudaSuccess) return fail(CS_ERR_CUDA, "gather stream synchronisation failed");
   }
-  cudaSetDevice(cur);
   return CS_OK;
+}
+
+cs_status cs_gather_batched(void* comm, int root, int64_t B_per_dev, int32_t K, const float* const* d_vals,
+                            const int32_t* const* d_support, const cs_report* const* d_reports, float* d_vals_all,
+                            int32_t* d_support_all, cs_report* d_reports_all) {
+  return cs_gather_batched_after(comm, root, B_per_dev, K, d_vals, d_support, d_reports, d_vals_all, d_support_all,
+                                 d_reports_all, nullptr);
 }
 
 cs_status cs_comm_destroy(void* comm) {
@@ -888,6 +937,7 @@ cs_status cs_comm_destroy(void* comm) {
   for (size_t i = 0; i < c->dev.size(); ++i) {
     cudaSetDevice(c->dev[i]);
     if (c->streams[i]) cudaStreamDestroy(c->streams[i]);
+    if (c->ready[i]) cudaEventDestroy(c->ready[i]);
     if (c->comms[i] && api.ok) api.destroy(c->comms[i]);
   }
   cudaSetDevice(cur);

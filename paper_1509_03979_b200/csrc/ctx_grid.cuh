@@ -193,6 +193,7 @@ template <typename T> struct GridCtx {
   int* tfill;       // [2][2][ntiles] counts and fill cursors of set_input_support (two parities)
   int sis_par = 0;  // parity of the next set_input_support
   int* tlist;       // [cap]
+  int* tscr;        // [cap] the atomically filled (unordered) buckets before ranking
   GTw<T> twF;   // W_L
   GTw<T> tw4;   // W_4N
   // shared memory
@@ -447,7 +448,7 @@ template <typename T> struct GridCtx {
   // column tile of Makhoul position p: complex index p/2 = m1 L2 + m2, tile m2 / CT
   CS_DEV int tile_of(int64_t p) const { return (int)(((p >> 1) & (L2 - 1)) / CT); }
   // Bucket the input support by pass-A/C column tile (CSR: tcnt starts, tlist entries) with
-  // two grid barriers: counts by atomics into this call's zeroed arrays; every block scans the
+  // three grid barriers: counts by atomics into this call's zeroed arrays; every block scans the
   // counts itself into shared memory (block 0 also publishes them as tcnt) and fills tlist
   // with its own copy; the other parity's arrays are zeroed for the next call.
   CS_DEV void set_input_support(const int* supp, int ns) {
@@ -488,9 +489,26 @@ template <typename T> struct GridCtx {
       for (int t = threadIdx.x; t <= nt; t += blockDim.x) tcnt[t] = offs[t];
     for (int i = gtid; i < ns; i += gnthr) {
       const int t = tile_of(in_pos[i]);
-      tlist[offs[t] + atomicAdd(&fil[t], 1)] = i;
+      tscr[offs[t] + atomicAdd(&fil[t], 1)] = i;
     }
     for (int t = gtid; t < 2 * nt; t += gnthr) ncnt[t] = 0;
+    sync();
+    // deterministic order inside every bucket (ascending support index): the atomic fill
+    // order varies run to run, and pass C's per-thread dot-product partials follow the list
+    // order, so ranking the entries makes the fp64 sums (alpha, beta, the stop test) and
+    // hence every result bitwise reproducible
+    // (one warp per entry: the lanes read the bucket in parallel and a ballot counts the
+    // entries below i — one L2 round trip per 32 bucket entries)
+    for (int i = gwarp; i < ns; i += gnwarps) {
+      const int t = tile_of(in_pos[i]);
+      const int a = offs[t], e = offs[t + 1];
+      int rank = 0;
+      for (int q0 = a; q0 < e; q0 += 32) {
+        const int q = q0 + (int)lane;
+        rank += __popc(__ballot_sync(0xffffffffu, q < e && __ldcg(&tscr[q]) < i));
+      }
+      if (lane == 0) tlist[a + rank] = i;
+    }
     sis_par ^= 1;
     in_supp = supp;
     in_ns = ns;

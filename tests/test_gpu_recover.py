@@ -187,13 +187,18 @@ def test_nonfinite_measurements_flagged(cs, N, M, K):
     assert not bad, bad
 
 
-def test_deterministic_rerun_grid_tier(cs):
-    """Fixed-order grid reductions: two runs of the grid tier agree bit for bit."""
-    cfg = CONFIGS[2].scaled(2)            # N = 32768
-    a = _run(cs, cfg, 1)
-    b = _run(cs, cfg, 1)
-    assert np.array_equal(a[2], b[2])
-    assert np.array_equal(a[3], b[3])
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("cid,div", [(2, 2), (5, 64), (3, 16)])
+def test_deterministic_rerun_grid_tier(cs, dtype, cid, div):
+    """Fixed-order grid reductions and a deterministic order inside every support bucket
+    (set_input_support ranks the atomically filled lists): repeated runs of the grid tier
+    agree bit for bit — values, supports and every report field — in fp32 and fp64."""
+    cfg = CONFIGS[cid].scaled(div)
+    runs = [_run(cs, cfg, 1, dtype=dtype) for _ in range(3)]
+    for r in runs[1:]:
+        assert np.array_equal(runs[0][2], r[2])
+        assert runs[0][3].tobytes() == r[3].tobytes()
+        assert runs[0][4].tobytes() == r[4].tobytes()
 
 
 # ---------------------------------------------------------------- CoSaMP (R33) ----
