@@ -286,6 +286,12 @@ int64_t cs_diag_phase_offset(int alg, int64_t N, int64_t M, int32_t K, int32_t o
  * mode 1: the radix path.  One CTA; asynchronous on `stream`.  1 <= K <= n <= 2^24. */
 cs_status cs_diag_topk(const void* d_vals, int64_t n, int64_t K, int precision, int mode,
                        uint32_t* d_out_bits, cs_stream_t stream);
+/* Test hook: the GRID tier's top-K (the radix select of detection at N >= 2^15) on d_vals [n]
+ * over a full cooperative grid; same output and tie rule as cs_diag_topk.  d_ws: DEVICE
+ * workspace of cs_diag_topk_grid_ws_bytes() bytes (caller-owned).  1 <= K <= n <= 2^26. */
+size_t cs_diag_topk_grid_ws_bytes(void);
+cs_status cs_diag_topk_grid(const void* d_vals, int64_t n, int64_t K, int precision, uint32_t* d_out_bits,
+                            void* d_ws, size_t ws_bytes, cs_stream_t stream);
 /* Diagnostics: microseconds per grid-wide barrier (with_sum: plus a grid reduction) in a
  * cooperative launch shaped like the Tier L recovery; synchronous; -1 on error. */
 double cs_diag_grid_barrier_us(int iters, int with_sum);

@@ -56,7 +56,7 @@ EXPORTS = [
     "cs_recover_batched", "cs_recover_batched_f64", "cs_workspace_bytes_host", "cs_recover_batched_host",
     "cs_recover_batched_host_f64", "cs_status_string", "cs_last_error",
     "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
-    "cs_diag_topk", "cs_operator_meta_bytes_perm", "cs_operator_create_perm", "cs_operator_create_ex",
+    "cs_diag_topk", "cs_diag_topk_grid", "cs_diag_topk_grid_ws_bytes", "cs_operator_meta_bytes_perm", "cs_operator_create_perm", "cs_operator_create_ex",
     "cs_operator_meta_bytes_ex", "cs_operator_meta_bytes_dft", "cs_operator_create_dft",
     "cs_support_to_dense", "cs_support_to_dense_f64", "cs_comm_init", "cs_gather_batched", "cs_gather_batched_after", "cs_comm_destroy",
 ]
@@ -118,6 +118,8 @@ def load_library(path: str = LIB_PATH):
         "cs_diag_phase_offset": (I64, [ctypes.c_int, I64, I64, I32, I32, ctypes.c_int]),
         "cs_diag_grid_barrier_us": (ctypes.c_double, [ctypes.c_int, ctypes.c_int]),
         "cs_diag_topk": (I32, [P, I64, I64, ctypes.c_int, ctypes.c_int, P, P]),
+        "cs_diag_topk_grid": (I32, [P, I64, I64, ctypes.c_int, P, P, SZ, P]),
+        "cs_diag_topk_grid_ws_bytes": (SZ, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

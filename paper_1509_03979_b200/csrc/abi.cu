@@ -787,6 +787,22 @@ cs_status cs_diag_topk(const void* d_vals, int64_t n, int64_t K, int precision, 
                                               d_out_bits, st, g_launches, g_last_error);
 }
 
+size_t cs_diag_topk_grid_ws_bytes(void) {
+  return std::max(tier_l_diag_topk_ws_bytes<float>(), tier_l_diag_topk_ws_bytes<double>());
+}
+
+cs_status cs_diag_topk_grid(const void* d_vals, int64_t n, int64_t K, int precision, uint32_t* d_out_bits,
+                            void* d_ws, size_t ws_bytes, cs_stream_t stream) {
+  if (!d_vals || !d_out_bits) return fail(CS_ERR_INVALID_ARG, "null pointer");
+  if (n < 1 || n > ((int64_t)1 << 26) || K < 1 || K > n) return fail(CS_ERR_INVALID_ARG, "need 1 <= K <= n <= 2^26");
+  if (cs_status s = check_device()) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return precision ? tier_l_diag_topk<double>(reinterpret_cast<const double*>(d_vals), n, K, d_out_bits, d_ws,
+                                              ws_bytes, st, g_launches, g_last_error)
+                   : tier_l_diag_topk<float>(reinterpret_cast<const float*>(d_vals), n, K, d_out_bits, d_ws,
+                                             ws_bytes, st, g_launches, g_last_error);
+}
+
 double cs_diag_grid_barrier_us(int iters, int with_sum) {
   const int64_t smem = l_smem_bytes<float>(1 << 20);
   const void* fn = (const void*)k_l_recover<float>;

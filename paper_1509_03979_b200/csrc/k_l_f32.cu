@@ -7,4 +7,6 @@ template cs_status tier_l_apply<float>(OpMeta, int64_t, const float*, float*, vo
                                      std::atomic<uint64_t>&, std::string&);
 template cs_status tier_l_recover<float>(OpMeta, Params, int, const float*, int64_t, float*, int32_t*, cs_report*,
                                        void*, size_t, cudaStream_t, std::atomic<uint64_t>&, std::string&);
+template cs_status tier_l_diag_topk<float>(const float*, int64_t, int64_t, uint32_t*, void*, size_t, cudaStream_t,
+                                        std::atomic<uint64_t>&, std::string&);
 }  // namespace cs

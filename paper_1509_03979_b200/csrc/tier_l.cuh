@@ -403,6 +403,18 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_recover(LArgs<T> a) {
   }
 }
 
+// Diagnostics / test hook: the grid tier's top-K (select.cuh topk_bits, the radix path used
+// by detection at c2, c3, c5) on a caller's value array, over a full cooperative grid.
+// The context is built for the smallest Tier L geometry (only its collectives are used).
+constexpr int64_t TL_DIAG_N = 32768;
+template <typename T>
+__global__ void __launch_bounds__(TL_THREADS, 2) k_l_diag_topk(LArgs<T> a, const T* vals, int64_t n, int64_t K,
+                                                              uint32_t* out_bits) {
+  extern __shared__ __align__(16) char smem[];
+  GridCtx<T> c = make_grid_ctx<T>(smem, a);
+  topk_bits(c, n, K, [vals](int64_t i) { return full_key(vals[i]); }, out_bits, false);
+}
+
 // Diagnostics: `iters` grid barriers (and grid sums) in a cooperative launch of the
 // recovery's shape; block 0 / thread 0 records the elapsed %globaltimer.
 template <typename T>
@@ -480,6 +492,13 @@ cs_status tier_l_recover(OpMeta meta, Params P, int ucap, const T* Y, int64_t B,
                          int32_t* supp, cs_report* reps, void* ws, size_t ws_bytes,
                          cudaStream_t st, std::atomic<uint64_t>& launches, std::string& err);
 
+template <typename T> inline size_t tier_l_diag_topk_ws_bytes() {
+  return (size_t)align_up(l_layout<T>(TL_DIAG_N, TL_DIAG_N / 4, 0, 0, false, l_grid_upper<T>()).bytes, 256);
+}
+template <typename T>
+cs_status tier_l_diag_topk(const T* vals, int64_t n, int64_t K, uint32_t* out, void* ws, size_t ws_bytes,
+                           cudaStream_t st, std::atomic<uint64_t>& launches, std::string& err);
+
 #ifdef CS_TIER_L_IMPL
 template <typename T>
 inline cs_status l_launch(const void* fn, LArgs<T>& a, int64_t N, cudaStream_t st,
@@ -548,6 +567,34 @@ cs_status tier_l_recover(OpMeta meta, Params P, int ucap, const T* Y, int64_t B,
   a.ws = reinterpret_cast<char*>(ws);
   a.ws_bytes = ws_bytes;
   return l_launch<T>((const void*)k_l_recover<T>, a, meta.N, st, launches, err);
+}
+
+template <typename T>
+cs_status tier_l_diag_topk(const T* vals, int64_t n, int64_t K, uint32_t* out, void* ws, size_t ws_bytes,
+                           cudaStream_t st, std::atomic<uint64_t>& launches, std::string& err) {
+  LArgs<T> a;
+  a.meta = OpMeta{};
+  a.meta.N = TL_DIAG_N;
+  a.meta.M = TL_DIAG_N / 4;
+  a.lay = l_layout<T>(TL_DIAG_N, TL_DIAG_N / 4, 0, 0, false, l_grid_upper<T>());
+  if (!ws || ws_bytes < (size_t)a.lay.bytes) { err = "workspace too small"; return CS_ERR_WORKSPACE; }
+  a.B = 1;
+  a.ws = reinterpret_cast<char*>(ws);
+  a.ws_bytes = ws_bytes;
+  const void* fn = (const void*)k_l_diag_topk<T>;
+  const int64_t smem = l_smem_bytes<T>(TL_DIAG_N);
+  int grid = l_maxgrid<T>(fn, smem);   // the whole GPU: every multi-block merge path runs
+  if (grid > a.lay.maxgrid) grid = a.lay.maxgrid;
+  a.gblocks = grid;
+  a.ngroups = 1;
+  a.gstride = align_up(a.lay.bytes, 256);
+  cudaError_t e = cudaMemsetAsync(a.ws + a.lay.ctl, 0, (size_t)(a.lay.ctl_end - a.lay.ctl), st);
+  if (e != cudaSuccess) { err = std::string("memset: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  void* args[] = {&a, &vals, &n, &K, &out};
+  e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(TL_THREADS), args, (size_t)smem, st);
+  launches.fetch_add(1);
+  if (e != cudaSuccess) { err = std::string("cooperative launch: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  return CS_OK;
 }
 
 #endif  // CS_TIER_L_IMPL

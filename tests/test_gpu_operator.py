@@ -27,7 +27,9 @@ def _setup(N, M, batch, seed=0):
 
 # Tier S: N <= 16384 (one CTA per vector); Tier L: four-step cooperative grid.
 SIZES = [(8, 4, 3), (16, 8, 2), (32, 8, 2), (64, 16, 3), (256, 64, 2), (1024, 256, 2), (4096, 1024, 2),
-         (16384, 4096, 3), (32768, 8192, 1), (65536, 16384, 2), (1 << 18, 1 << 16, 1), (1 << 20, 1 << 18, 1)]
+         (16384, 4096, 3), (32768, 8192, 1), (65536, 16384, 2), (1 << 18, 1 << 16, 1), (1 << 20, 1 << 18, 1),
+         # the full-size grid-tier shapes: c5's N = 2^24 (pass tiles of 4096 points) and beyond
+         (1 << 22, 1 << 20, 1), (1 << 24, 1 << 22, 1), (1 << 25, 1 << 23, 1)]
 
 
 @pytest.mark.parametrize("N,M,batch", SIZES)

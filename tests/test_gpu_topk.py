@@ -69,3 +69,50 @@ def test_topk_matches_oracle_definition(cs, mode):
         got = gpu_topk(cs, v, K, mode)
         want = oracle.topk(np.abs(v.astype(np.float64)) if v.dtype == np.float64 else np.abs(v), K)
         assert np.array_equal(got, want), (name, v.dtype, mode, np.setxor1d(got, want)[:10])
+
+
+# ---- the grid tier's radix top-K (detection at N >= 2^15: c2, c3, c5), full cooperative grid
+def gpu_topk_grid(cs, v, K):
+    lib = cs.load_library()
+    dev = torch.device("cuda:0")
+    t = torch.from_numpy(v).to(dev)
+    out = torch.zeros((v.size + 31) // 32, dtype=torch.int32, device=dev)
+    ws = torch.empty(int(lib.cs_diag_topk_grid_ws_bytes()), dtype=torch.uint8, device=dev)
+    prec = 1 if v.dtype == np.float64 else 0
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    rc = lib.cs_diag_topk_grid(ctypes.c_void_p(t.data_ptr()), v.size, K, prec, ctypes.c_void_p(out.data_ptr()),
+                               ctypes.c_void_p(ws.data_ptr()), ws.numel(), st)
+    assert rc == 0, lib.cs_last_error()
+    torch.cuda.synchronize()
+    bits = np.unpackbits(out.cpu().numpy().view(np.uint8), bitorder="little")[: v.size]
+    return np.nonzero(bits)[0]
+
+
+def grid_cases():
+    rng = np.random.default_rng(11)
+    out = []
+    for dt in (np.float32, np.float64):
+        for n, K in [(1 << 16, 2048), (1 << 20, 8192), (1 << 24, 65536)]:
+            out.append((f"gauss-{n}", rng.standard_normal(n).astype(dt), K))
+        n = 1 << 20
+        out.append(("integer-ties", np.round(rng.standard_normal(n) * 4).astype(dt), 9000))
+        v = np.zeros(n, dt)
+        v[rng.choice(n, 3000, replace=False)] = 1.0                   # fewer nonzeros than K
+        out.append(("zeros-fill", v, 8192))
+        v = np.full(n, dt(1.2345), dtype=dt) + (rng.integers(0, 8, n) * np.finfo(dt).eps).astype(dt)
+        out.append(("last-ulp", v, 65536))
+        v = (rng.standard_normal(1 << 16) * 1e-39).astype(dt)
+        out.append(("denormal", v, 1000))
+        out.append(("all-equal", np.full(1 << 18, dt(-2.5), dtype=dt), 12345))
+        out.append(("K=n", rng.standard_normal(70000).astype(dt), 70000))
+        v = np.abs(rng.standard_normal(1 << 24)).astype(dt)
+        v[::3] = v[5]                                                 # one value tied across 2^24 / 3 slots
+        out.append(("tied-2^24", v, 65536))
+    return out
+
+
+def test_grid_topk_matches_oracle_definition(cs):
+    for name, v, K in grid_cases():
+        got = gpu_topk_grid(cs, v, K)
+        want = oracle.topk(np.abs(v.astype(np.float64)) if v.dtype == np.float64 else np.abs(v), K)
+        assert np.array_equal(got, want), (name, v.dtype, np.setxor1d(got, want)[:10])
