@@ -146,6 +146,23 @@ CS_DEV bool topk_cta_fast_v(Ctx& ctx, int nbits, int K, Visit&& visit, uint32_t*
     __syncthreads();
     return true;
   }
+  if (C <= 128) {
+    // few candidates: every candidate counts the candidates ranked above it (key descending,
+    // index ascending — R12, R32; a broadcast read of the list) and is taken iff fewer than
+    // `need` are — one barrier instead of the byte radix passes below (four barriers each)
+    for (int c = tid; c < C; c += nt) {
+      const Key kc = ck[c];
+      const int ic = ci[c];
+      int above_c = 0;
+      for (int j = 0; j < C; ++j) {
+        const Key kj = ck[j];
+        above_c += (kj > kc) || (kj == kc && ci[j] < ic);
+      }
+      if (above_c < need) atomicOr(&out_bits[ic >> 5], 1u << (ic & 31));
+    }
+    __syncthreads();
+    return true;
+  }
   // MSB-first byte radix select of the `need` largest candidate keys
   unsigned* hist = shp(ctx.hist);
   constexpr int NB = (int)sizeof(Key) * 8;
