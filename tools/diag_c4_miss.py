@@ -32,3 +32,14 @@ for i in miss32[:12]:
           "| gpu32 outer", r32["outer_iters"], "term", r32["termination"], "res", r32["resid_norm"],
           "| gpu64==oracle", np.array_equal(np.sort(s64[i]), ref.support), "outer", r64["outer_iters"], "term", r64["termination"],
           "| symdiff32-or", np.setxor1d(s32[i], ref.support))
+# margins: min |x_S| / ||x|| of the fp32 result, misses vs the whole batch
+v32 = out["float32"][1]
+rel = np.min(np.abs(v32), axis=1) / np.linalg.norm(v32, axis=1)
+t32 = out["float32"][2]["termination"]
+o32 = out["float32"][2]["outer_iters"]
+print("miss min|x|/||x||:", np.round(rel[miss32], 9).tolist())
+print("miss term:", t32[miss32].tolist(), "outer:", o32[miss32].tolist())
+for thr in [1e-4, 3e-5, 1e-5, 3e-6, 1e-6]:
+    fl = rel < thr
+    print(f"flag min|x|/||x|| < {thr:g}: {int(fl.sum())} problems, misses caught {int(fl[miss32].sum())}/{miss32.size}")
+print("term counts all:", np.bincount(t32).tolist(), "misses:", np.bincount(t32[miss32], minlength=5).tolist())
