@@ -117,6 +117,13 @@ CS_DEV void gstaged(int64_t n, int64_t gtid, int64_t gnthr, LD&& ld, ST&& st) {
   }
 }
 
+// Bulk prefetch of [p, p + bytes) into L2 (one thread issues it; 16-byte aligned, bytes a
+// multiple of 16): the next instance of a persistent loop streams into L2 while this one is
+// computed, so its loads hit L2 instead of HBM.
+CS_DEV void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Two-pass top-K of the CTA context (select.cuh): first-digit bins, candidate cap.
 constexpr int TOPK_BINS = 1024;
 constexpr int TOPK_CAP = 1024;

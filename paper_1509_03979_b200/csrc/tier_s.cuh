@@ -201,6 +201,8 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout 
     cta_set_instance<T>(c, smem, meta, b);
   }
   const T* x = X + b * N;
+  if (threadIdx.x == 0 && b + gridDim.x < B)
+    prefetch_l2(X + (b + gridDim.x) * N, (uint32_t)(N * sizeof(T)));   // the next instance's x
   if (c.psi) {
     s_apply_psi<T>(c, x, Y + b * c.M, Gws + b * N);
     continue;
@@ -260,6 +262,8 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_adjoint(OpMeta meta, SLayou
       cta_set_instance<T>(c, smem, meta, b);
     }
     c.y = Yin + b * c.M;
+    if (threadIdx.x == 0 && b + gridDim.x < B && ((c.M * sizeof(T)) & 15) == 0)
+      prefetch_l2(Yin + (b + gridDim.x) * c.M, (uint32_t)(c.M * sizeof(T)));   // the next instance's y
     if (c.psi) c.G = Gws + b * c.N;
     c.RES(nullptr);  // A^T y (x = 0)
     T* x = X + b * N;
