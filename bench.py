@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--precision", choices=["fp32", "fp64", "mixed"], default="fp32",
+                    help="mixed: fp32 with the fp64 refinement of problems below the fp32 floor "
+                         "(cs_options.refine_fp64, DESIGN.md §10)")
     ap.add_argument("--batch", type=int, default=0, help="problems in the job (0 = config default)")
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
                     help="strong (BASELINE north_star): the config's batch split over the ranks; "
@@ -177,8 +179,12 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     cfg = select_config(args)
     B_job = args.batch or cfg.batch
-    td = torch.float32 if args.precision == "fp32" else torch.float64
-    tol = 1e-6 if args.precision == "fp32" else 1e-12
+    td = torch.float64 if args.precision == "fp64" else torch.float32
+    tol = 1e-12 if args.precision == "fp64" else 1e-6
+    opts = None
+    if args.precision == "mixed":
+        opts = cs.cs_options()
+        opts.refine_fp64 = 1
     if args.tol > 0:
         tol = args.tol
     if args.scaling == "weak" or cfg.batch == 1:
@@ -209,7 +215,7 @@ def run_ours(args):
 
     def step():
         nonlocal rec
-        rec = cs.cs_recover_batched(A, cfg.alg, Y, cfg.K, tol, workspace=ws, out=rec)
+        rec = cs.cs_recover_batched(A, cfg.alg, Y, cfg.K, tol, opts=opts, workspace=ws, out=rec)
         return rec
 
     gather_buf = None
@@ -344,7 +350,7 @@ def run_ours(args):
     # kernel (k_s_recover for N <= 16384, k_l_recover above), timed with CUDA events on
     # the launching stream (kms, per launch).  DESIGN.md §6 derives both models.
     peaks = load_peaks()
-    es = 4 if args.precision == "fp32" else 8
+    es = 8 if args.precision == "fp64" else 4
     tier_s = cfg.N <= 16384
     if tier_s:
         # FP32-ALU bound: nominal DCT flops 2.5 N log2 N per transform, 2 per sandwich,
@@ -386,7 +392,8 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": args.scaling if cfg.batch > 1 else "weak",
         "vs_baseline": None,
-        "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic (seeded, DESIGN.md §4)",
+        "dtype": {"fp32": "f32", "fp64": "f64", "mixed": "f32 (+f64 refinement)"}[args.precision],
+        "data": "synthetic (seeded, DESIGN.md §4)",
         "config": {"workload": workload_desc(cfg), "problems_total": B_job, "problems_per_gpu": B,
                    "N": cfg.N, "M": cfg.M,
                    "K": cfg.K, "alg": cfg.alg, "tol": tol, "parallelism": f"dp{world} (independent problems)",
@@ -398,6 +405,7 @@ def run_ours(args):
                 "api": "cs_recover_batched_host (pinned host buffers, chunked copy/compute overlap)",
                 "matches_device_path": e2e_same},
         "gpu_launches": int(launches),
+        "refined_fp64": int(np.count_nonzero(reps["status"] & 8)) if args.precision == "mixed" else None,
         "roofline": roofline,
         "operator": op_stats,
         "clocks": clocks,

@@ -59,6 +59,8 @@ typedef enum {
 #define CS_DEV_NONFINITE_Y   1u  /* y contained NaN/Inf: outputs are undefined */
 #define CS_DEV_CG_CAP        2u  /* some CG solve stopped at its iteration cap          */
 #define CS_DEV_CG_BREAKDOWN  4u  /* some CG solve stopped on d^T H d <= 0               */
+#define CS_DEV_REFINED_FP64  8u  /* cs_options.refine_fp64: recovered again in fp64       */
+#define CS_DEV_NOT_REFINED  16u  /* flagged for refinement, beyond CS_REFINE_CAP: fp32 kept */
 
 typedef struct {
   int32_t outer_iters;     /* pursuit outer iterations executed                       */
@@ -76,8 +78,18 @@ typedef struct {
   int32_t cg_max_iters; /* 0 -> |S| + 50 (Thm 5 bound |S| plus slack, SURVEY #29)           */
   int32_t ompr_l;       /* OMPR(l): indices swapped in per outer iteration; 0 -> 1  */
   float ompr_eta;       /* OMPR step eta; 0 -> 1.0                                   */
-  int32_t reserved[4];  /* must be zero                                                      */
+  int32_t refine_fp64;  /* fp32 batched recovery on the CTA tier only (SURVEY §8c.9 mixed
+                         * policy): 1 -> every problem whose fp32 result holds a coefficient
+                         * below the fp32 resolution floor, min |x_i| < CS_REFINE_FLOOR ||x||,
+                         * is recovered again from scratch in fp64 and its result replaces
+                         * the fp32 one (status CS_DEV_REFINED_FP64); at most CS_REFINE_CAP
+                         * problems per call (the rest keep fp32, CS_DEV_NOT_REFINED).  The
+                         * workspace grows by cs_workspace_bytes's refine share.  Device-path
+                         * calls only (the host-buffer entry points ignore it).  0 -> off.  */
+  int32_t reserved[3];  /* must be zero                                                      */
 } cs_options;
+#define CS_REFINE_FLOOR 1e-6  /* ~16 fp32 ulps: the sandwich's relative rounding */
+#define CS_REFINE_CAP   256
 
 /* ---------------------------------------------------------------- operator ---
  * A = P . C_N . diag(sigma)   (Eq.(7) Phi = D F R, with BASELINE.json's

@@ -44,7 +44,7 @@ class CsError(RuntimeError):
 class cs_options(ctypes.Structure):
     _fields_ = [("max_outer", ctypes.c_int32), ("cg_max_iters", ctypes.c_int32),
                 ("ompr_l", ctypes.c_int32), ("ompr_eta", ctypes.c_float),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("refine_fp64", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 _lib = None

@@ -266,6 +266,85 @@ cs_status apply_impl(const cs_operator* op, const T* x, T* y, void* ws, size_t w
                          g_last_error);
 }
 
+// ---- mixed precision (cs_options.refine_fp64): fp32 results below the fp32
+// resolution floor are recovered again in fp64 on the CTA tier
+struct RefineWs {
+  int* count;           // [1]
+  int* list;            // [cap] problem indices
+  double* y64;          // [cap][M]
+  double* c0;           // [cap][2][N]
+  double* vals;         // [cap][K]
+  int32_t* supp;        // [cap][K]
+  cs_report* reps;      // [cap]
+  size_t bytes;
+};
+RefineWs refine_ws(char* base, int64_t N, int64_t M, int32_t K, int64_t B) {
+  RefineWs r{};
+  const int64_t cap = std::min<int64_t>(B, CS_REFINE_CAP);
+  int64_t o = 0;
+  auto take = [&](int64_t b) { int64_t at = o; o = align_up(o + b, 256); return base ? base + at : nullptr; };
+  r.count = reinterpret_cast<int*>(take(16));
+  r.list = reinterpret_cast<int*>(take(cap * 4));
+  r.y64 = reinterpret_cast<double*>(take(cap * M * 8));
+  r.c0 = reinterpret_cast<double*>(take(cap * 2 * N * 8));
+  r.vals = reinterpret_cast<double*>(take(cap * K * 8));
+  r.supp = reinterpret_cast<int32_t*>(take(cap * K * 4));
+  r.reps = reinterpret_cast<cs_report*>(take(cap * (int64_t)sizeof(cs_report)));
+  r.bytes = (size_t)o;
+  return r;
+}
+// one warp per problem: flag min |x_i| < CS_REFINE_FLOOR ||x|| (finite y only), take a slot,
+// stage y in fp64
+__global__ void k_refine_select(int64_t B, int64_t M, int32_t K, const float* Y, const float* vals,
+                                cs_report* reps, int cap, int* count, int* list, double* y64) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const float* v = vals + b * K;
+  double ss = 0, mn = 1e300;
+  for (int i = lane; i < K; i += 32) {
+    const double a = fabs((double)v[i]);
+    ss += a * a;
+    mn = fmin(mn, a);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  const bool flag = !(reps[b].status & CS_DEV_NONFINITE_Y) && mn < CS_REFINE_FLOOR * sqrt(ss);
+  if (!flag) return;
+  int slot = 0;
+  if (lane == 0) slot = atomicAdd(count, 1);
+  slot = __shfl_sync(0xffffffffu, slot, 0);
+  if (slot >= cap) {
+    if (lane == 0) reps[b].status |= CS_DEV_NOT_REFINED;
+    return;
+  }
+  if (lane == 0) list[slot] = (int)b;
+  for (int64_t m = lane; m < M; m += 32) y64[slot * M + m] = (double)Y[b * M + m];
+}
+// write the fp64 results over the fp32 ones
+__global__ void k_refine_merge(int32_t K, int cap, const int* count, const int* list, const double* v64,
+                               const int32_t* s64, const cs_report* r64, float* vals, int32_t* supp,
+                               cs_report* reps) {
+  const int s = blockIdx.x;
+  if (s >= min(*count, cap)) return;
+  const int64_t b = list[s];
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {
+    vals[b * K + i] = (float)v64[(int64_t)s * K + i];
+    supp[b * K + i] = s64[(int64_t)s * K + i];
+  }
+  if (threadIdx.x == 0) {
+    cs_report r = r64[s];
+    r.status |= CS_DEV_REFINED_FP64;
+    reps[b] = r;
+  }
+}
+bool refine_applies(int precision, const cs_options* opts, int64_t N, int32_t K, int64_t ucap) {
+  return precision == 0 && opts && opts->refine_fp64 && tier_s_fits<float>(N, K, ucap, true) &&
+         tier_s_fits<double>(N, K, ucap, true);
+}
+
 template <typename T>
 cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, int64_t M, int64_t N,
                        int32_t K, double tol, const cs_options* opts, T* vals, int32_t* supp,
@@ -278,8 +357,9 @@ cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, in
   if (B < 1 || B > op->B) return fail(CS_ERR_INVALID_ARG, "batch exceeds operator instances");
   if (!(tol >= 0)) return fail(CS_ERR_INVALID_ARG, "tol must be >= 0");
   if (opts) {
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 3; ++i)
       if (opts->reserved[i]) return fail(CS_ERR_INVALID_ARG, "cs_options.reserved must be zero");
+    if (opts->refine_fp64 < 0 || opts->refine_fp64 > 1) return fail(CS_ERR_INVALID_ARG, "refine_fp64 must be 0 or 1");
     if (opts->max_outer < 0 || opts->cg_max_iters < 0 || opts->ompr_l < 0 || opts->ompr_eta < 0)
       return fail(CS_ERR_INVALID_ARG, "negative option");
   }
@@ -308,7 +388,38 @@ cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, in
     a.supp = supp;
     a.reps = reps;
     a.c0ws = reinterpret_cast<T*>(ws);
-    return s_recover_launch<T>(a, B, st, g_launches, g_last_error);
+    if (cs_status s = s_recover_launch<T>(a, B, st, g_launches, g_last_error)) return s;
+    if constexpr (sizeof(T) == 4) {
+      if (refine_applies(0, opts, N, K, ucap)) {
+        // the fp32 pass's workspace is B * 2N floats; the refinement's follows it
+        char* rb = reinterpret_cast<char*>(ws) + align_up(B * 2 * N * 4, 256);
+        RefineWs r = refine_ws(rb, N, M, K, B);
+        const int cap = (int)std::min<int64_t>(B, CS_REFINE_CAP);
+        CS_CUDA(cudaMemsetAsync(r.count, 0, sizeof(int), st));
+        k_refine_select<<<(unsigned)((B + 7) / 8), 256, 0, st>>>(B, M, K, reinterpret_cast<const float*>(Y),
+                                                                   reinterpret_cast<const float*>(vals), reps,
+                                                                   cap, r.count, r.list, r.y64);
+        CS_LAUNCHED();
+        SRecArgs<double> d;
+        d.meta = meta_of(op);
+        d.lay = s_layout<double>(N, K, (int)ucap, true);
+        d.P = P;
+        d.P.tol = tol < 1e-12 ? tol : 1e-12;   // the fp64 path's tolerance (R7)
+        d.ucap = (int)ucap;
+        d.Y = r.y64;
+        d.vals = r.vals;
+        d.supp = r.supp;
+        d.reps = r.reps;
+        d.c0ws = r.c0;
+        d.bmap = r.list;
+        d.bcount = r.count;
+        if (cs_status s = s_recover_launch<double>(d, cap, st, g_launches, g_last_error)) return s;
+        k_refine_merge<<<(unsigned)cap, 256, 0, st>>>(K, cap, r.count, r.list, r.vals, r.supp, r.reps,
+                                                       reinterpret_cast<float*>(vals), supp, reps);
+        CS_LAUNCHED();
+      }
+    }
+    return CS_OK;
   }
   return tier_l_recover<T>(meta_of(op), P, (int)ucap, Y, B, vals, supp, reps, ws, ws_bytes, st,
                            g_launches, g_last_error);
@@ -359,6 +470,13 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
   if (cs_status s = check_N(N)) return s;
   if (K < 1) return fail(CS_ERR_INVALID_ARG, "K must be >= 1");
   const int prec = sizeof(T) == 8 ? 1 : 0;
+  // the chunked pipeline does not refine (cs_options.refine_fp64 is a device-path option)
+  cs_options o_norefine{};
+  if (opts && opts->refine_fp64) {
+    o_norefine = *opts;
+    o_norefine.refine_fp64 = 0;
+    opts = &o_norefine;
+  }
   size_t need_rec = 0;
   if (cs_status s = cs_workspace_bytes(alg, N, M, K, B, prec, opts, &need_rec)) return s;
   const size_t rec_al = (size_t)align_up((int64_t)need_rec, 256);
@@ -701,6 +819,8 @@ cs_status cs_workspace_bytes(int alg, int64_t N, int64_t M, int32_t K, int64_t b
   bool s = dbl ? tier_s_fits<double>(N, K, ucap, true) : tier_s_fits<float>(N, K, ucap, true);
   if (s) {
     *bytes = (size_t)(batch * 2 * N * (dbl ? 8 : 4));   // A^T y and the Psi-mode scratch per problem
+    if (refine_applies(precision, opts, N, K, ucap))
+      *bytes = (size_t)align_up((int64_t)*bytes, 256) + refine_ws(nullptr, N, M, K, batch).bytes;
   } else {
     *bytes = dbl ? tier_l_recover_ws_bytes<double>(N, M, K, (int)ucap, batch)
                  : tier_l_recover_ws_bytes<float>(N, M, K, (int)ucap, batch);

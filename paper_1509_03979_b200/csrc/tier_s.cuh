@@ -281,13 +281,22 @@ template <typename T> struct SRecArgs {
   int32_t* supp;
   cs_report* reps;
   T* c0ws;  // [B][2][N]: A^T y (Makhoul order), then the Psi-mode scratch G
+  // refinement launch (cs_options.refine_fp64): block s recovers operator instance bmap[s]
+  // from the staged y row s into output slot s; blocks s >= *bcount exit.  Null: identity.
+  const int* bmap = nullptr;
+  const int* bcount = nullptr;
 };
 
 template <typename T>
 __global__ void __launch_bounds__(TS_THREADS, 2) k_s_recover(SRecArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
-  const int64_t b = blockIdx.x;
-  CtaCtx<T> c = make_cta_ctx<T>(smem, a.lay, a.meta, b);
+  const int64_t b = blockIdx.x;   // output / workspace / y slot
+  int64_t inst = b;                // operator instance
+  if (a.bmap) {
+    if (b >= *a.bcount) return;    // uniform over the block
+    inst = a.bmap[b];
+  }
+  CtaCtx<T> c = make_cta_ctx<T>(smem, a.lay, a.meta, inst);
   // row selection in the fused pass's unit order for the CG loop's H (sandwich_cta.cuh sw_fused)
   sw_build_usel<T>(c.log2L, reinterpret_cast<uint32_t*>(smem + s_fixed<T>(a.meta.N).usel), c.rowmask);
   __syncthreads();

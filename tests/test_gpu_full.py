@@ -247,3 +247,36 @@ def test_c5_full_fp32_reported_against_oracle_reference(cs):
     big = g["support"][np.abs(g["x"]) > 10 * floor]
     assert np.isin(big, supp[0]).all()
     assert rel < 0.1     # measured 5.0e-2 (symdiff 8892 of 131072)
+
+
+def test_c4_full_batch_fp32_refined_matches_oracle_everywhere(cs):
+    """Mixed precision policy (cs_options.refine_fp64): the fp32 batch, with every
+    problem whose fp32 result holds a coefficient below the fp32 resolution floor recovered
+    again in fp64.  Every one of the 4096 problems then ends on the planted support (the fp64
+    oracle's answer on each of them); the refined ones carry
+    CS_DEV_REFINED_FP64 and equal the oracle to the fp64 bar; 16 sampled others equal the
+    oracle to the fp32 bar."""
+    cfg = CONFIGS[4]
+    probs = cs_inputs.make_batch(cfg)
+    ys = measured(probs)
+    dev = torch.device("cuda:0")
+    bits, rows = to_dev(probs, dev)
+    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=len(probs))
+    opts = cs.cs_options()
+    opts.refine_fp64 = 1
+    res = cs.cs_recover_batched(A, cfg.alg, torch.from_numpy(ys).to(dev), cfg.K, 1e-6, opts=opts)
+    torch.cuda.synchronize()
+    supp, vals, reps = res.support.cpu().numpy(), res.values.cpu().numpy().astype(np.float64), res.reports()
+    refined = np.nonzero(reps["status"] & 8)[0]
+    print(f"c4 fp32 + fp64 refine: {refined.size} problems refined; "
+          f"not refined (cap) {int(np.count_nonzero(reps['status'] & 16))}")
+    planted = np.stack([p.support for p in probs])
+    assert (supp == planted).all()
+    assert 0 < refined.size <= 256
+    sub = [probs[i] for i in refined[:12]]
+    bad, worst = compare(sub, oracle_results(sub, ys[refined[:12]]), supp[refined[:12]], vals[refined[:12]], rtol=1e-6)
+    assert not bad, bad
+    pick = np.sort(np.random.default_rng(6).choice(cfg.batch, 16, replace=False))
+    sub = [probs[i] for i in pick]
+    bad, worst = compare(sub, oracle_results(sub, ys[pick]), supp[pick], vals[pick])
+    assert not bad, bad
