@@ -44,10 +44,16 @@ template <typename T, int LOG2L> CS_DEV int opaque_tid() {
 }
 
 template <int LOG2L> struct SwPlan {
-  // forward radices: [remainder 2^M if M > 0] [16] x Q [2 (fused)]; inverse reversed
-  static constexpr int M = (LOG2L - 1) % 4;
-  static constexpr int Q = (LOG2L - 1) / 4;
-  static constexpr int NS_R16_FWD0 = M;                                  // log2 Ns, first fwd radix-16 pass
+  // forward radices: [remainder 2^M if M > 0] [2^RBM] x Q [2 (fused)]; inverse reversed.
+  // The main radix is the largest of 16, 8, 4 whose passes still give every one of the 512
+  // threads an item (L / 2^RBM >= 512): radix 16 at N = 2^14 (c4), radix 4 at N = 2^12
+  // (c1) — a radix-16 pass there would leave three quarters of the block idle on a
+  // latency-bound critical path.
+  static constexpr int L_ = 1 << LOG2L;
+  static constexpr int RBM = ((L_ >> 4) >= SW_NT) ? 4 : (((L_ >> 3) >= SW_NT) ? 3 : 2);
+  static constexpr int M = (LOG2L - 1) % RBM;
+  static constexpr int Q = (LOG2L - 1) / RBM;
+  static constexpr int NS_R16_FWD0 = M;                                  // log2 Ns, first main pass
   // log2 Ns of the first radix-16 pass that has twiddles (Ns1 <= 16: its 16 Ns1 twiddles
   // W_{16 Ns1}^{r k} come from the tw16 table, one LDS each, instead of a product chain)
   static constexpr int NS1B = (M == 0) ? 4 : M;
@@ -57,51 +63,61 @@ template <int LOG2L> struct SwPlan {
 };
 
 // ---- one Stockham pass of radix 2^RB at runtime stride Ns = 2^nsb; L = 2^LOG2L ----
+// Items j < L/R; thread t owns j = t + 512 it (it < IPT: several items when L/R > 512).
 template <typename T, int LOG2L, int RB, bool INV>
 CS_DEV void sw_pass(C2<T>* buf, const TwTable<T>& tw, int nsb) {
   constexpr int R = 1 << RB, Lr = (1 << LOG2L) >> RB;
-  static_assert(Lr <= SW_NT, "one item per thread");
-  const int j = opaque_tid<T, LOG2L>();
-  C2<T> v[R];
-  const bool act = (Lr == SW_NT) || j < Lr;
-  const int Ns = 1 << nsb, k = j & (Ns - 1);
-  if (act) {
-    const int sj = swz<T>(j);  // j < Lr: bit-disjoint from r Lr
-    if constexpr (Lr % 512 == 0) {
-      // swz(r Lr) = r Lr and sj < Lr: plain offsets (immediate-addressed LDS, no registers)
+  constexpr int IPT = Lr > SW_NT ? Lr / SW_NT : 1;
+  const int t0 = opaque_tid<T, LOG2L>();
+  C2<T> v[IPT][R];
+  const int Ns = 1 << nsb;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = buf[sj + r * Lr];
-    } else {
+  for (int it = 0; it < IPT; ++it) {
+    const int j = t0 + it * SW_NT;
+    const int k = j & (Ns - 1);
+    if ((Lr >= SW_NT) || j < Lr) {
+      const int sj = swz<T>(j);  // j < Lr: bit-disjoint from r Lr
+      if constexpr (Lr % 512 == 0) {
+        // swz(r Lr) = r Lr and sj < Lr: plain offsets (immediate-addressed LDS, no registers)
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = buf[sj ^ swz_c<T>(r * Lr)];
-    }
-    if (Ns > 1) {
-      if (RB == 4 && nsb == SwPlan<LOG2L>::NS1B) {
-        constexpr SFix F = s_fixed<T>(int64_t(2) << LOG2L);
-        const C2<T>* t16 = reinterpret_cast<const C2<T>*>(cs_smem_base + F.tw16) + k;  // [r][k]: conflict-free
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = INV ? cmulc<T>(v[r], t16[16 * r]) : cmul<T>(v[r], t16[16 * r]);
+        for (int r = 0; r < R; ++r) v[it][r] = buf[sj + r * Lr];
       } else {
-        C2<T> w1 = tw(k << (LOG2L - nsb - RB));
-        if (INV) w1 = cconj<T>(w1);
-        tw_stream<T, R>(v, w1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[it][r] = buf[sj ^ swz_c<T>(r * Lr)];
       }
+      if (Ns > 1) {
+        if (RB == 4 && SwPlan<LOG2L>::RBM == 4 && nsb == SwPlan<LOG2L>::NS1B) {
+          constexpr SFix F = s_fixed<T>(int64_t(2) << LOG2L);
+          const C2<T>* t16 = reinterpret_cast<const C2<T>*>(cs_smem_base + F.tw16) + k;  // [r][k]: conflict-free
+#pragma unroll
+          for (int r = 1; r < R; ++r) v[it][r] = INV ? cmulc<T>(v[it][r], t16[16 * r]) : cmul<T>(v[it][r], t16[16 * r]);
+        } else {
+          C2<T> w1 = tw(k << (LOG2L - nsb - RB));
+          if (INV) w1 = cconj<T>(w1);
+          tw_stream<T, R>(v[it], w1);
+        }
+      }
+      dft_reg<T, R, INV>(v[it]);
     }
-    dft_reg<T, R, INV>(v);
   }
   __syncthreads();
-  if (act) {
-    const int sb = swz<T>((j - k) * R + k);  // bit-disjoint from r Ns
-    int e[RB];                                 // swz(Ns << b)
+  int e[RB];                                 // swz(Ns << b)
 #pragma unroll
-    for (int b = 0; b < RB; ++b) e[b] = swz<T>(Ns << b);
+  for (int b = 0; b < RB; ++b) e[b] = swz<T>(Ns << b);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      int o = sb;
+  for (int it = 0; it < IPT; ++it) {
+    const int j = t0 + it * SW_NT;
+    const int k = j & (Ns - 1);
+    if ((Lr >= SW_NT) || j < Lr) {
+      const int sb = swz<T>((j - k) * R + k);  // bit-disjoint from r Ns
 #pragma unroll
-      for (int b = 0; b < RB; ++b)
-        if (r & (1 << b)) o ^= e[b];
-      buf[o] = v[bitrev<R>(r)];
+      for (int r = 0; r < R; ++r) {
+        int o = sb;
+#pragma unroll
+        for (int b = 0; b < RB; ++b)
+          if (r & (1 << b)) o ^= e[b];
+        buf[o] = v[it][bitrev<R>(r)];
+      }
     }
   }
   __syncthreads();
@@ -117,48 +133,56 @@ CS_DEV void sw_pass(C2<T>* buf, const TwTable<T>& tw, int nsb) {
 template <typename T, int LOG2L, int RB>
 CS_DEV void sw_pass_t(C2<T>* buf, const TwTable<T>& tw, int nsb) {
   constexpr int R = 1 << RB, Lr = (1 << LOG2L) >> RB;
-  static_assert(Lr <= SW_NT, "one item per thread");
-  const int j = opaque_tid<T, LOG2L>();
-  C2<T> v[R];
-  const bool act = (Lr == SW_NT) || j < Lr;
-  const int Ns = 1 << nsb, k = j & (Ns - 1);
-  if (act) {
-    const int sb = swz<T>((j - k) * R + k);  // bit-disjoint from r Ns
-    int e[RB];                                 // swz(Ns << b)
+  constexpr int IPT = Lr > SW_NT ? Lr / SW_NT : 1;
+  const int t0 = opaque_tid<T, LOG2L>();
+  C2<T> v[IPT][R];
+  const int Ns = 1 << nsb;
+  int e[RB];                                 // swz(Ns << b)
 #pragma unroll
-    for (int b = 0; b < RB; ++b) e[b] = swz<T>(Ns << b);
+  for (int b = 0; b < RB; ++b) e[b] = swz<T>(Ns << b);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      int o = sb;
+  for (int it = 0; it < IPT; ++it) {
+    const int j = t0 + it * SW_NT;
+    const int k = j & (Ns - 1);
+    if ((Lr >= SW_NT) || j < Lr) {
+      const int sb = swz<T>((j - k) * R + k);  // bit-disjoint from r Ns
 #pragma unroll
-      for (int b = 0; b < RB; ++b)
-        if (r & (1 << b)) o ^= e[b];
-      v[r] = buf[o];
-    }
-    dft_reg<T, R, true>(v);  // u_s at v[bitrev(s)]
-    if (Ns > 1) {
-      if (RB == 4 && nsb == SwPlan<LOG2L>::NS1B) {
-        constexpr SFix F = s_fixed<T>(int64_t(2) << LOG2L);
-        const C2<T>* t16 = reinterpret_cast<const C2<T>*>(cs_smem_base + F.tw16) + k;  // [r][k]: conflict-free
+      for (int r = 0; r < R; ++r) {
+        int o = sb;
 #pragma unroll
-        for (int q = 1; q < R; ++q) v[bitrev<R>(q)] = cmulc<T>(v[bitrev<R>(q)], t16[16 * q]);
-      } else {
-        C2<T> u[R];
+        for (int b = 0; b < RB; ++b)
+          if (r & (1 << b)) o ^= e[b];
+        v[it][r] = buf[o];
+      }
+      dft_reg<T, R, true>(v[it]);  // u_s at v[bitrev(s)]
+      if (Ns > 1) {
+        if (RB == 4 && SwPlan<LOG2L>::RBM == 4 && nsb == SwPlan<LOG2L>::NS1B) {
+          constexpr SFix F = s_fixed<T>(int64_t(2) << LOG2L);
+          const C2<T>* t16 = reinterpret_cast<const C2<T>*>(cs_smem_base + F.tw16) + k;  // [r][k]: conflict-free
 #pragma unroll
-        for (int q = 0; q < R; ++q) u[q] = v[bitrev<R>(q)];
-        tw_stream<T, R>(u, cconj<T>(tw(k << (LOG2L - nsb - RB))));
+          for (int q = 1; q < R; ++q) v[it][bitrev<R>(q)] = cmulc<T>(v[it][bitrev<R>(q)], t16[16 * q]);
+        } else {
+          C2<T> u[R];
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[bitrev<R>(q)] = u[q];
+          for (int q = 0; q < R; ++q) u[q] = v[it][bitrev<R>(q)];
+          tw_stream<T, R>(u, cconj<T>(tw(k << (LOG2L - nsb - RB))));
+#pragma unroll
+          for (int q = 0; q < R; ++q) v[it][bitrev<R>(q)] = u[q];
+        }
       }
     }
   }
   __syncthreads();
-  if (act) {
-    const int sj = swz<T>(j);  // j < Lr: bit-disjoint from s Lr
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-      if constexpr (Lr % 512 == 0) buf[sj + q * Lr] = v[bitrev<R>(q)];
-      else buf[sj ^ swz_c<T>(q * Lr)] = v[bitrev<R>(q)];
+  for (int it = 0; it < IPT; ++it) {
+    const int j = t0 + it * SW_NT;
+    if ((Lr >= SW_NT) || j < Lr) {
+      const int sj = swz<T>(j);  // j < Lr: bit-disjoint from s Lr
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if constexpr (Lr % 512 == 0) buf[sj + q * Lr] = v[it][bitrev<R>(q)];
+        else buf[sj ^ swz_c<T>(q * Lr)] = v[it][bitrev<R>(q)];
+      }
     }
   }
   __syncthreads();
@@ -478,7 +502,7 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
     }
     sw_remainder<T, LOG2L, false>(buf, tw, 0);
 #pragma unroll 1
-    for (int q = 0; q < SP::Q; ++q) sw_pass<T, LOG2L, 4, false>(buf, tw, SP::NS_R16_FWD0 + 4 * q);
+    for (int q = 0; q < SP::Q; ++q) sw_pass<T, LOG2L, SP::RBM, false>(buf, tw, SP::NS_R16_FWD0 + SP::RBM * q);
   }
   double rn2 = 0;
   if constexpr (MODE == MID_FWDZ || MODE == MID_INVZ) {
@@ -488,7 +512,7 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
   }
   if constexpr (MODE != MID_FWD && MODE != MID_FWDZ) {
 #pragma unroll 1
-    for (int q = SP::Q - 1; q >= 0; --q) sw_pass_t<T, LOG2L, 4>(buf, tw, SP::NS_R16_FWD0 + 4 * q);
+    for (int q = SP::Q - 1; q >= 0; --q) sw_pass_t<T, LOG2L, SP::RBM>(buf, tw, SP::NS_R16_FWD0 + SP::RBM * q);
     if constexpr (SP::M > 0) sw_pass_t<T, LOG2L, SP::M>(buf, tw, 0);
     if (gio.vout) {
       const int* supp = shp(gio.supp);
