@@ -27,9 +27,16 @@ CS_DEV double warp_sum(double v) {
 
 template <typename T> struct CtaCtx {
   using Key = typename KeyT<T>::type;
-  // ids
+  // The context object lives in SHARED memory (one per CTA, `__shared__` in the kernels):
+  // every field is block-uniform, so the generic pursuit code reads it through a shared
+  // address instead of a per-thread local-memory copy (1024 resident threads x a few hundred
+  // bytes of context and call frames spilled from the small L1 to L2 and HBM).  Fields are
+  // written with identical values by every thread (no thread reads a field before the barrier
+  // that follows its initialisation); the only per-thread mutable state — the reduction bank —
+  // is kept per warp (rbank_w, written by lane 0 after __syncwarp), and `applies` is counted by
+  // thread 0 alone.
   // ids: derived from the special registers / compile-time block size on every use, never
-  // stored (the context object lives in local memory; a stored id is a local load per use)
+  // stored
   struct TidV { CS_DEV operator int() const { return (int)threadIdx.x; } };
   struct LaneV { CS_DEV operator int() const { return (int)(threadIdx.x & 31); } };
   struct WarpV { CS_DEV operator int() const { return (int)(threadIdx.x >> 5); } };
@@ -81,14 +88,20 @@ template <typename T> struct CtaCtx {
   // pointer into this context's working set as the compiler should see it: shared (Tier S)
   template <typename P> CS_DEV P* loc(P* p) const { return shp(p); }
 
-  int rbank;  // alternating reduction bank (sum)
+  int rbank_w[SW_NT / 32];  // alternating reduction bank, one copy per warp (see above)
+  CS_DEV int bank_take() {    // this warp's bank, toggled for the next reduction
+    const int w = (int)(threadIdx.x >> 5);
+    const int rb = rbank_w[w];
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) rbank_w[w] = rb ^ 1;
+    return rb;
+  }
   // Deterministic block sum (fixed order).  Two alternating banks of partials: the
   // next sum writes the other bank, and the one after that is ordered behind this
   // sum's readers by the next sum's barrier — so one barrier per reduction.
   CS_DEV double sum(double v) {
     v = warp_sum(v);
-    double* rb = shp(redd) + 64 * rbank;  // banks of 64 (cg_iterate_t bsum4 uses [4][16])
-    rbank ^= 1;
+    double* rb = shp(redd) + 64 * bank_take();  // banks of 64 (cg_iterate_t bsum4 uses [4][16])
     if (lane == 0) rb[gwarp] = v;
     __syncthreads();
     double t = 0;
@@ -218,7 +231,7 @@ template <typename T> struct CtaCtx {
     double rr = s_io.rr;
     int j = s_io.j;
     unsigned status = s_io.status;
-    int rb = rbank;
+    int rb = rbank_w[threadIdx.x >> 5];
     const MidCtx<T> m0 = make_mid_c<T, LOG2L + 1>(nullptr, nullptr, nullptr, nullptr);
     constexpr int64_t REDD = F.redd;
     auto bsum = [&rb](double v) {
@@ -297,11 +310,12 @@ template <typename T> struct CtaCtx {
       ++j;                                                                 // line 21
       if (!(rr2 == rr2)) { status |= CS_DEV_CG_BREAKDOWN; break; }
     }
-    applies += j - s_io.j;
+    if (threadIdx.x == 0) applies += j - s_io.j;
     s_io.rr = rr;
     s_io.j = j;
     s_io.status = status;
-    rbank = rb;
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) rbank_w[threadIdx.x >> 5] = rb;
   }
   template <int LO, int HI, bool PERM, int KIND, class S> CS_DEV void cg_dispatch(S& s) {
     if constexpr (LO <= HI) {
@@ -331,14 +345,14 @@ template <typename T> struct CtaCtx {
   CS_DEV void H(const T* d, T* q) {
     if (psi) { H_psi(d, q); return; }
     sandwich<MID_H, false>(d, q, nullptr);
-    ++applies;
+    if (threadIdx.x == 0) ++applies;
   }
   // c = A^T (y - A scatter_S(x)) into the buffer (b1 + cg5); returns ||y - A x||^2.
   // x == nullptr means x = 0 (c = A^T y).
   CS_DEV double RES(const T* x) {
     if (psi) return RES_psi(x);
     const double rn2 = x ? sandwich<MID_RES, false>(x, nullptr, nullptr) : sandwich<MID_RES, true>(nullptr, nullptr, nullptr);
-    ++applies;
+    if (threadIdx.x == 0) ++applies;
     return sum(rn2);
   }
 
@@ -353,7 +367,7 @@ template <typename T> struct CtaCtx {
     sandwich_psi<MID_FWDZ, false>(d, nullptr);          // Makhoul(R sigma C_N scatter_S(d))
     sandwich<MID_H, false>(nullptr, nullptr, nullptr);  // C^T P^T P C
     sandwich_psi<MID_INVZ, true>(nullptr, q);           // C_N^T (sigma R^T .), gather on S
-    ++applies;
+    if (threadIdx.x == 0) ++applies;
   }
   CS_NOINL double RES_psi(const T* x) {
     double rn2;
@@ -365,7 +379,7 @@ template <typename T> struct CtaCtx {
     }
     rn2 = sum(rn2);
     sandwich_psi<MID_INVZ, true>(nullptr, nullptr);                // A^T r, s-domain
-    ++applies;
+    if (threadIdx.x == 0) ++applies;
     return rn2;
   }
 };

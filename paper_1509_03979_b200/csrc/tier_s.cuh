@@ -97,9 +97,10 @@ struct OpMeta {
 template <typename T>
 CS_DEV void cta_set_instance(CtaCtx<T>& c, char* smem, const OpMeta& meta, int64_t b);
 
+// Initialise the CTA's shared context object (every thread writes the same values; the
+// barrier at the end of cta_set_instance orders them before any use).
 template <typename T>
-CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta, int64_t b) {
-  CtaCtx<T> c;
+CS_DEV void init_cta_ctx(CtaCtx<T>& c, char* smem, const SLayout& lay, const OpMeta& meta, int64_t b) {
   c.N = meta.N;
   c.M = meta.M;
   c.L = meta.N / 2;
@@ -122,7 +123,7 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
   c.ckey = reinterpret_cast<typename CtaCtx<T>::Key*>(smem + lay.ckey);
   c.cidx = reinterpret_cast<int*>(smem + lay.cidx);
   c.ccnt = reinterpret_cast<int*>(smem + lay.ccnt);
-  c.rbank = 0;
+  for (int w = 0; w < SW_NT / 32; ++w) c.rbank_w[w] = 0;
   c.psi = meta.psi;
   c.fkind = meta.fkind;
   c.G = nullptr;
@@ -148,7 +149,6 @@ CS_DEV CtaCtx<T> make_cta_ctx(char* smem, const SLayout& lay, const OpMeta& meta
     }
   }
   cta_set_instance<T>(c, smem, meta, b);
-  return c;
 }
 
 // point the context at instance b: its sign / row mask / prefix into shared memory, its
@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout 
                                                  T* __restrict__ Y, T* __restrict__ Gws, int64_t B) {
   extern __shared__ __align__(16) char smem[];
   // persistent: the CTA sets up its twiddle tables once and loops over instances
-  CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, blockIdx.x);
+  __shared__ CtaCtx<T> c;
+  init_cta_ctx<T>(c, smem, lay, meta, blockIdx.x);
   const int64_t N = c.N;
   for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
   if (b != blockIdx.x) {
@@ -254,7 +255,8 @@ template <typename T>
 __global__ void __launch_bounds__(TS_THREADS, 2) k_s_adjoint(OpMeta meta, SLayout lay, const T* __restrict__ Yin,
                                                    T* __restrict__ X, T* __restrict__ Gws, int64_t B) {
   extern __shared__ __align__(16) char smem[];
-  CtaCtx<T> c = make_cta_ctx<T>(smem, lay, meta, blockIdx.x);   // persistent, as k_s_apply
+  __shared__ CtaCtx<T> c;   // persistent, as k_s_apply
+  init_cta_ctx<T>(c, smem, lay, meta, blockIdx.x);
   const int64_t N = c.N;
   for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
     if (b != blockIdx.x) {
@@ -296,7 +298,10 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_recover(SRecArgs<T> a) {
     if (b >= *a.bcount) return;    // uniform over the block
     inst = a.bmap[b];
   }
-  CtaCtx<T> c = make_cta_ctx<T>(smem, a.lay, a.meta, inst);
+  __shared__ CtaCtx<T> c;
+  __shared__ Params P;
+  init_cta_ctx<T>(c, smem, a.lay, a.meta, inst);
+  P = a.P;   // every thread the same value; ordered before use by the barriers below
   // row selection in the fused pass's unit order for the CG loop's H (sandwich_cta.cuh sw_fused)
   sw_build_usel<T>(c.log2L, reinterpret_cast<uint32_t*>(smem + s_fixed<T>(a.meta.N).usel), c.rowmask);
   __syncthreads();
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_recover(SRecArgs<T> a) {
   B.Sbits = reinterpret_cast<uint32_t*>(smem + L.Sbits);
   B.Ubits = reinterpret_cast<uint32_t*>(smem + L.Ubits);
   B.Pbits = reinterpret_cast<uint32_t*>(smem + L.Pbits);
-  run_pursuit<CtaCtx<T>, T>(c, a.P, B, a.vals + b * a.P.K, a.supp + b * a.P.K, a.reps + b, pre);
+  run_pursuit<CtaCtx<T>, T>(c, P, B, a.vals + b * a.P.K, a.supp + b * a.P.K, a.reps + b, pre);
 }
 
 // Diagnostics / test hook: the CTA context's top-K selection (select.cuh topk_bits) on a
@@ -342,7 +347,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1) k_s_diag_topk(SLayout lay, cons
   c.ckey = reinterpret_cast<typename CtaCtx<T>::Key*>(smem + lay.ckey);
   c.cidx = reinterpret_cast<int*>(smem + lay.cidx);
   c.ccnt = reinterpret_cast<int*>(smem + lay.ccnt);
-  c.rbank = 0;
+  for (int w = 0; w < SW_NT / 32; ++w) c.rbank_w[w] = 0;
   __syncthreads();
   topk_bits(c, (int64_t)n, (int64_t)K, [vals](int64_t i) { return full_key(vals[i]); }, out_bits, mode == 0);
 }
