@@ -91,10 +91,12 @@ CS_DEV bool topk_cta_fast_v(Ctx& ctx, int nbits, int K, Visit&& visit, uint32_t*
   });
   __syncthreads();
   if (warp == 0) {
-    // lane l owns bins [1023 - 32 l - 31, 1023 - 32 l], scanned from the top
+    // lane l owns bins [1023 - 32 l - 31, 1023 - 32 l], scanned from the top; its sum is
+    // read in a lane-rotated order ((i + l) mod 32) so that the 32 lanes hit 32 different
+    // banks (a fixed order is a 32-way bank conflict: the lanes' ranges are 32 words apart)
     int s = 0;
 #pragma unroll 8
-    for (int i = 0; i < 32; ++i) s += (int)h[TOPK_BINS - 1 - 32 * lane - i];
+    for (int i = 0; i < 32; ++i) s += (int)h[TOPK_BINS - 1 - 32 * lane - ((i + lane) & 31)];
     int inc = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
