@@ -501,7 +501,7 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
       __syncthreads();
     }
     sw_remainder<T, LOG2L, false>(buf, tw, 0);
-#pragma unroll 1
+#pragma unroll
     for (int q = 0; q < SP::Q; ++q) sw_pass<T, LOG2L, SP::RBM, false>(buf, tw, SP::NS_R16_FWD0 + SP::RBM * q);
   }
   double rn2 = 0;
@@ -511,7 +511,7 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
     rn2 = sw_fused<T, LOG2L, MODE, ZERO, KIND>(buf, tw, tw4, m);
   }
   if constexpr (MODE != MID_FWD && MODE != MID_FWDZ) {
-#pragma unroll 1
+#pragma unroll
     for (int q = SP::Q - 1; q >= 0; --q) sw_pass_t<T, LOG2L, SP::RBM>(buf, tw, SP::NS_R16_FWD0 + SP::RBM * q);
     if constexpr (SP::M > 0) sw_pass_t<T, LOG2L, SP::M>(buf, tw, 0);
     if (gio.vout) {
