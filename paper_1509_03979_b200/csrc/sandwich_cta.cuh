@@ -253,9 +253,11 @@ CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, 
   for (int it = 0; it < UPT; ++it) {
     const int k = tid + it * SW_NT;
     if ((U % SW_NT == 0) || k < U) {
-      const int kb = (k == 0) ? L / 4 : H - k;
-      const C2<T> wk = (k == 0) ? mk<T>(1, 0) : tw(k);                    // W_L^k
-      const C2<T> wb = (k == 0) ? mk<T>(0, -1) : mk<T>(-wk.x, wk.y);       // W_L^{kb}
+      // unit 0 only exists for it = 0 (k = tid + 512 it): the compiler drops its branch elsewhere
+      const bool k0 = (it == 0) && (k == 0);
+      const int kb = k0 ? L / 4 : H - k;
+      const C2<T> wk = k0 ? mk<T>(1, 0) : tw(k);                    // W_L^k
+      const C2<T> wb = k0 ? mk<T>(0, -1) : mk<T>(-wk.x, wk.y);       // W_L^{kb}
       const int sa = swz<T>(k), sa2 = swz<T>(k + H), sb = swz<T>(kb), sb2 = swz<T>(kb + H);
       C2<T> A0, A1, B0, B1;
       if constexpr (ZERO) {
@@ -270,7 +272,7 @@ CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, 
         B1 = csub<T>(b0, b1);
       }
       if constexpr (KIND == 1) {
-        if (k != 0) {
+        if (!k0) {
           const C2<T> a = tw4(k);
           const C2<T> a2 = cmul<T>(a, a);
           const C2<T> w = cmul<T>(a2, a2);                     // W_N^k
@@ -282,7 +284,7 @@ CS_DEV double sw_fused(C2<T>* buf, const TwTable<T>& tw, const TwTable<T>& tw4, 
           dft_pair<T, MODE>(B0, B1, L / 4, tw4(L / 4), m, rn2);
         }
       } else {
-        if (k != 0) {
+        if (!k0) {
           const C2<T> a = tw4(k);
           const C2<T> a2 = cmul<T>(a, a);
           const C2<T> w = cmul<T>(a2, a2);                     // W_N^k
