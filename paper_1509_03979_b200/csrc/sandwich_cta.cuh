@@ -40,7 +40,10 @@ constexpr int SW_LOG2NT = 9;
 // ptxas would otherwise precompute and spill it), so it is recomputed each pass.
 template <typename T, int LOG2L> CS_DEV int opaque_tid() {
   constexpr SFix F = s_fixed<T>(int64_t(2) << LOG2L);
-  return (int)threadIdx.x + *reinterpret_cast<volatile int*>(cs_smem_base + F.zero);
+  const int t = (int)threadIdx.x + *reinterpret_cast<volatile int*>(cs_smem_base + F.zero);
+  __builtin_assume(t >= 0);
+  __builtin_assume(t < SW_NT);
+  return t;
 }
 
 template <int LOG2L> struct SwPlan {
@@ -492,7 +495,13 @@ CS_DEV double sw_body(C2<T>* gbuf, const TwTable<T>& gtw, const TwTable<T>& gtw4
       const int* supp = shp(gio.supp);
       const uint32_t* sign = signs;
       const T* vin = shp(gio.vin);
-      for (int i = tid; i < L; i += SW_NT) buf[i] = mk<T>(0, 0);
+      if constexpr (sizeof(T) == 4 && L % (2 * SW_NT) == 0) {
+        float4* b4 = reinterpret_cast<float4*>(buf);   // zeros: 16-byte stores, half the count
+#pragma unroll
+        for (int i = tid; i < L / 2; i += SW_NT) b4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        for (int i = tid; i < L; i += SW_NT) buf[i] = mk<T>(0, 0);
+      }
       __syncthreads();
       // Eq.(7) randomizer pi^-1 (R34), parked in shared memory by make_cta_ctx
       const int32_t* pv = PERM ? *reinterpret_cast<const int32_t* const*>(cs_smem_base + F.zero + 8) : nullptr;
