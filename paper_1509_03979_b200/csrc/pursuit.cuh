@@ -162,6 +162,12 @@ CS_DEV void bits_from_list(Ctx& ctx, uint32_t* bits, int64_t nwords, const int* 
 
 template <class Ctx, typename T>
 CS_DEV bool same_list(Ctx& ctx, const int* a, const int* b, int n) {
+  if constexpr (Ctx::kTopkFast) {
+    // CTA: one barrier-vote, no reduction slots
+    int d = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) d |= (a[i] != b[i]);
+    return !__syncthreads_or(d);
+  }
   double diff = 0;
   for (int i = ctx.gtid; i < n; i += ctx.gnthr) diff += (a[i] != b[i]) ? 1.0 : 0.0;
   return ctx.sum(diff) == 0.0;

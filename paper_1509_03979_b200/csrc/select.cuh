@@ -321,6 +321,37 @@ CS_DEV int64_t argmax_key(Ctx& ctx, int64_t n, KeyFn key) {
 template <class Ctx, class Emit>
 CS_DEV int64_t compact_bits(Ctx& ctx, const uint32_t* bits, int64_t n, Emit emit) {
   const int64_t nwords = (n + 31) >> 5;
+  if constexpr (Ctx::kTopkFast) {
+    if (nwords <= 32) {
+      // CTA, at most 32 words (the prune over |T| <= 1024 positions): warp 0 alone — lane w
+      // takes word w, a warp scan of the popcounts gives its output offset; the total is
+      // broadcast through the pick slot with the one closing barrier
+      int64_t* pk = shp(ctx.pick);
+      if (threadIdx.x < 32) {
+        const int w = (int)threadIdx.x;
+        uint32_t b = w < nwords ? bits[w] : 0u;
+        if (w == nwords - 1 && (n & 31)) b &= (1u << (n & 31)) - 1u;
+        const int c = __popc(b);
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (w >= o) inc += t;
+        }
+        int64_t pos = inc - c;
+        while (b) {
+          const int t = __ffs(b) - 1;
+          b &= b - 1;
+          emit(pos++, (int64_t)w * 32 + t);
+        }
+        if (w == 31) pk[3] = inc;
+      }
+      __syncthreads();
+      const int64_t tot = pk[3];
+      __syncthreads();   // pick[] is reused by later collectives
+      return tot;
+    }
+  }
   const int64_t nthr = ctx.gnthr;
   const int64_t per = (nwords + nthr - 1) / nthr;
   const int64_t w0 = (int64_t)ctx.gtid * per, w1 = min(nwords, w0 + per);
