@@ -108,6 +108,19 @@ template <typename T> struct CtaCtx {
     for (int w = 0; w < gnwarps; ++w) t += rb[w];
     return t;
   }
+  // two sums in one reduction (one barrier): [0..15] of the bank hold a's warp partials,
+  // [16..31] b's
+  CS_DEV void sum2(double& a, double& b) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    double* rb = shp(redd) + 64 * bank_take();
+    if (lane == 0) { rb[gwarp] = a; rb[16 + gwarp] = b; }
+    __syncthreads();
+    double ta = 0, tb = 0;
+    for (int w = 0; w < gnwarps; ++w) { ta += rb[w]; tb += rb[16 + w]; }
+    a = ta;
+    b = tb;
+  }
   // argmax of (key, idx): larger key wins, ties -> smaller idx.  Returns idx (-1 if all keys 0).
   // (argmax and excl_scan are inlined: an out-of-line call costs its register save /
   // restore through local memory, measured 0.6 % of c4)

@@ -134,12 +134,7 @@ CS_DEV void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q, 
     rr += (double)r[i] * (double)r[i];
     d[i] = r[i];                                                           // line 13
   }
-  if constexpr (Ctx::kDeferD) {
-    ctx.sum2(bb, rr);   // grid: one reduction for both
-  } else {
-    bb = ctx.sum(bb);
-    rr = ctx.sum(rr);
-  }
+  ctx.sum2(bb, rr);   // one reduction for both
   CgState<T> cs_{x, r, d, q, rr, P.tol * P.tol * bb, ns, P.cg_cap > 0 ? P.cg_cap : ns + 50, 0, 0u};
   ctx.mark(8);
   ctx.cg_iterate(cs_);                                                     // lines 14-22
