@@ -189,7 +189,7 @@ CS_NOINL void s_apply_psi(CtaCtx<T>& c, const T* x, T* y, T* G) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout lay, const T* __restrict__ X,
+__global__ void __launch_bounds__(TS_THREADS, sizeof(T) == 4 ? 2 : 1) k_s_apply(OpMeta meta, SLayout lay, const T* __restrict__ X,
                                                  T* __restrict__ Y, T* __restrict__ Gws, int64_t B) {
   extern __shared__ __align__(16) char smem[];
   // persistent: the CTA sets up its twiddle tables once and loops over instances
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(TS_THREADS, 2) k_s_apply(OpMeta meta, SLayout 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(TS_THREADS, 2) k_s_adjoint(OpMeta meta, SLayout lay, const T* __restrict__ Yin,
+__global__ void __launch_bounds__(TS_THREADS, sizeof(T) == 4 ? 2 : 1) k_s_adjoint(OpMeta meta, SLayout lay, const T* __restrict__ Yin,
                                                    T* __restrict__ X, T* __restrict__ Gws, int64_t B) {
   extern __shared__ __align__(16) char smem[];
   __shared__ CtaCtx<T> c;   // persistent, as k_s_apply
@@ -290,7 +290,7 @@ template <typename T> struct SRecArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(TS_THREADS, 2) k_s_recover(SRecArgs<T> a) {
+__global__ void __launch_bounds__(TS_THREADS, sizeof(T) == 4 ? 2 : 1) k_s_recover(SRecArgs<T> a) {
   extern __shared__ __align__(16) char smem[];
   const int64_t b = blockIdx.x;   // output / workspace / y slot
   int64_t inst = b;                // operator instance
