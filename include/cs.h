@@ -292,6 +292,8 @@ const char* cs_version(void);
  * sandwiches, [1] pass A of H, [2] pass B of H, [3] pass C of H, [4] pass A of the residual,
  * [5] its pass B, [6] its pass C + reduction), valid after the stream syncs; -1 for Tier S. */
 int64_t cs_diag_phase_offset(int alg, int64_t N, int64_t M, int32_t K, int32_t ompr_l, int precision);
+/* (alg < 0: the byte offset of the Tier L apply's five %globaltimer phase stamps of instance 0 —
+ * start, input reorder, pass A, pass B, output permute — in the apply / adjoint workspace.) */
 /* Test hook: the CTA tier's top-K selection on d_vals [n] (fp32 or fp64 by `precision`):
  * bit i of d_out_bits [ceil(n/32)] (device) is set iff |vals[i]| is among the K largest,
  * ties to the lowest index.  mode 0: the two-pass path (radix fallback),

@@ -943,6 +943,11 @@ double cs_diag_grid_barrier_us(int iters, int with_sum) {
 
 int64_t cs_diag_phase_offset(int alg, int64_t N, int64_t M, int32_t K, int32_t ompr_l, int precision) {
   if (N <= TIER_S_MAX_N) return -1;
+  if (alg < 0) {   // the apply / adjoint workspace: instance 0's phase stamps (k_l_apply)
+    const LLayout s = precision ? l_layout<double>(N, M, 0, 0, false, l_grid_upper<double>())
+                                : l_layout<float>(N, M, 0, 0, false, l_grid_upper<float>());
+    return s.ts;
+  }
   const int64_t ucap = ucap_of(alg, K, ompr_l);
   const LLayout s = precision ? l_layout<double>(N, M, K, (int)ucap, true, l_grid_upper<double>())
                               : l_layout<float>(N, M, K, (int)ucap, true, l_grid_upper<float>());
