@@ -258,6 +258,34 @@ cs_status cs_gather_batched_after(void* comm, int root, int64_t B_per_dev, int32
                                   const cs_stream_t* after);
 cs_status cs_comm_destroy(void* comm);
 
+/* ---------------------------------------------------------------- single signal, G GPUs ---
+ * (SV §8f NEXT-4) The four-step operator of one large signal (N > 16384, fp32, the plain
+ * P.DCT.diag(sigma), instance 0) split over `world` ranks, one all-to-all per pass:
+ *   apply:   DP_A  (x -> this rank's column FFTs), all-to-all columns -> row pairs,
+ *            DP_BF (this rank's row FFTs + DCT split + row select -> its part of yT; the caller
+ *            zeroes d_out and sums yT over the ranks), DP_P (yT -> y in row order);
+ *   adjoint: DP_BA (y -> this rank's rows of Wk), all-to-all row pairs -> columns,
+ *            DP_C  (this rank's inverse column FFTs -> its entries of x, zeros elsewhere;
+ *            the caller sums x over the ranks).
+ * Rank r owns the column tiles [t_lo, t_hi) of passes A / C (tiles of CT columns of the
+ * [L1][L2] intermediate) and the row-pair items [i_lo, i_hi) of pass B (item i = rows i and
+ * L1 - i).  cs_dist_copy moves segments (row rows[k], columns [col0[k], col0[k] + seg_len))
+ * of the intermediate between the workspace and a flat exchange buffer (to_buf 1: pack,
+ * 0: unpack).  d_ws: DEVICE workspace of cs_dist_ws_bytes(N, M) bytes, one per rank, kept
+ * across the phases of one call.  Orchestration and the all-to-alls (torch.distributed /
+ * NCCL): paper_1509_03979_b200/dist.py.  Asynchronous on `stream`. */
+#define CS_DP_A 0
+#define CS_DP_BF 1
+#define CS_DP_BA 2
+#define CS_DP_C 3
+#define CS_DP_P 4
+cs_status cs_dist_geometry(int64_t N, int64_t* L1, int64_t* L2, int32_t* CT);
+size_t cs_dist_ws_bytes(int64_t N, int64_t M);
+cs_status cs_dist_phase(const cs_operator* op, int phase, int64_t t_lo, int64_t t_hi, int64_t i_lo, int64_t i_hi,
+                        const float* d_in, float* d_out, void* d_ws, size_t ws_bytes, cs_stream_t stream);
+cs_status cs_dist_copy(const cs_operator* op, void* d_ws, const int32_t* d_rows, const int32_t* d_col0, int64_t nseg,
+                       int64_t seg_len, float* d_buf, int to_buf, cs_stream_t stream);
+
 /* Host-buffer variants (the end-to-end entry points): h_Y [B][M] and the outputs
  * h_vals [B][K], h_support [B][K], h_reports [B] are HOST memory (pinned for overlap).
  * The batch is copied in, recovered and copied out in chunks of two recovery waves, on

@@ -907,6 +907,50 @@ cs_status cs_diag_topk(const void* d_vals, int64_t n, int64_t K, int precision, 
                                               d_out_bits, st, g_launches, g_last_error);
 }
 
+// ---------------------------------------------------------------- distributed operator ----
+cs_status cs_dist_geometry(int64_t N, int64_t* L1, int64_t* L2, int32_t* CT) {
+  if (!L1 || !L2 || !CT) return fail(CS_ERR_INVALID_ARG, "null pointer");
+  if (cs_status s = check_N(N)) return s;
+  if (N <= TIER_S_MAX_N) return fail(CS_ERR_UNSUPPORTED, "the distributed operator needs N > 16384 (grid tier)");
+  const LGeom g = l_geom(N);
+  *L1 = g.L1;
+  *L2 = g.L2;
+  *CT = g.CT;
+  return CS_OK;
+}
+size_t cs_dist_ws_bytes(int64_t N, int64_t M) {
+  if (N <= TIER_S_MAX_N) return 0;
+  return (size_t)align_up(l_layout<float>(N, M, 0, 0, false, l_grid_upper<float>()).bytes, 256);
+}
+static cs_status dist_check(const cs_operator* op) {
+  if (!op) return fail(CS_ERR_INVALID_ARG, "null operator");
+  if (op->N <= TIER_S_MAX_N) return fail(CS_ERR_UNSUPPORTED, "the distributed operator needs N > 16384 (grid tier)");
+  if (op->perm || op->psi || op->fkind) return fail(CS_ERR_UNSUPPORTED, "the distributed operator is the plain P.DCT.diag(sigma)");
+  return check_device();
+}
+cs_status cs_dist_phase(const cs_operator* op, int phase, int64_t t_lo, int64_t t_hi, int64_t i_lo, int64_t i_hi,
+                        const float* d_in, float* d_out, void* d_ws, size_t ws_bytes, cs_stream_t stream) {
+  if (cs_status s = dist_check(op)) return s;
+  if (phase < DP_A || phase > DP_P) return fail(CS_ERR_INVALID_ARG, "unknown phase");
+  const LGeom g = l_geom(op->N);
+  const int64_t ntiles = g.L2 / g.CT, nitems = g.L1 / 2 + 1;
+  if (t_lo < 0 || t_hi < t_lo || t_hi > ntiles || i_lo < 0 || i_hi < i_lo || i_hi > nitems)
+    return fail(CS_ERR_INVALID_ARG, "tile / item range out of bounds");
+  if ((phase == DP_A || phase == DP_BA || phase == DP_P) && !d_in) return fail(CS_ERR_INVALID_ARG, "null input");
+  if ((phase == DP_BF || phase == DP_C || phase == DP_P) && !d_out) return fail(CS_ERR_INVALID_ARG, "null output");
+  DistArgs<float> d{phase, t_lo, t_hi, i_lo, i_hi, d_in, d_out};
+  return tier_l_dist_phase<float>(meta_of(op), d, d_ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), g_launches,
+                                  g_last_error);
+}
+cs_status cs_dist_copy(const cs_operator* op, void* d_ws, const int32_t* d_rows, const int32_t* d_col0, int64_t nseg,
+                       int64_t seg_len, float* d_buf, int to_buf, cs_stream_t stream) {
+  if (cs_status s = dist_check(op)) return s;
+  if (!d_ws || (nseg > 0 && (!d_rows || !d_col0 || !d_buf)) || nseg < 0 || seg_len < 0)
+    return fail(CS_ERR_INVALID_ARG, "bad arguments");
+  return tier_l_dist_copy<float>(meta_of(op), d_ws, d_rows, d_col0, nseg, seg_len, d_buf, to_buf,
+                                 reinterpret_cast<cudaStream_t>(stream), g_launches, g_last_error);
+}
+
 size_t cs_diag_topk_grid_ws_bytes(void) {
   return std::max(tier_l_diag_topk_ws_bytes<float>(), tier_l_diag_topk_ws_bytes<double>());
 }

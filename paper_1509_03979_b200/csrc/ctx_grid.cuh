@@ -187,6 +187,10 @@ template <typename T> struct GridCtx {
   C2<T>* Wk;    // [L] four-step intermediate
   T* Cb;        // [N] output (Makhoul order)
   int64_t* in_pos;  // [cap] positions of the remembered input support
+  // Distributed operator (NEXT-4, tier_l.cuh k_l_dist): the dense passes A / C work on the
+  // column tiles [dt_lo, dt_hi) and pass B on the row-pair items [di_lo, di_hi) of this
+  // rank; hi < 0 means the whole range (every single-GPU call)
+  int64_t dt_lo = 0, dt_hi = -1, di_lo = 0, di_hi = -1;
   // the support bucketed by pass-A / pass-C column tile (CSR): tile t owns the entries
   // tlist[tstart[t] .. tstart[t+1]) (indices into the support list)
   int* tcnt;        // [ntiles + 1] exclusive starts of the tiles' entries in tlist
@@ -547,7 +551,8 @@ template <typename T> struct GridCtx {
     C2<T>* sb = shp(buf);
     C2<T>* wk = Wk;
     const GTw<T> tf = twF;
-    for (int64_t t = blk; t < ntiles; t += nblk) {
+    const int64_t tlo = dt_hi < 0 ? 0 : dt_lo, thi = dt_hi < 0 ? ntiles : dt_hi;
+    for (int64_t t = tlo + blk; t < thi; t += nblk) {
       const int64_t c0i = t * ct;
       // element e = (m1, cc): the whole tile in flight as cp.async
       for (int e = threadIdx.x; e < tile; e += blockDim.x)
@@ -738,7 +743,8 @@ template <typename T> struct GridCtx {
     m.tsh = tsh;
     double rn2 = 0;
     const int64_t nitems = L1 / 2 + 1;
-    for (int64_t it = blk; it < nitems; it += nblk) {
+    const int64_t ilo = di_hi < 0 ? 0 : di_lo, ihi = di_hi < 0 ? nitems : di_hi;
+    for (int64_t it = ilo + blk; it < ihi; it += nblk) {
       const int64_t ka = it, kb = L1 - it;
       const bool self = (it == 0 || it == L1 / 2);
       const int B = self ? 1 : 2;
@@ -927,7 +933,8 @@ template <typename T> struct GridCtx {
     const int tile = (int)(L1 * ct);
     C2<T>* sb = shp(buf);
     const C2<T>* wk = Wk;
-    for (int64_t t = blk; t < ntiles; t += nblk) {
+    const int64_t tlo = dt_hi < 0 ? 0 : dt_lo, thi = dt_hi < 0 ? ntiles : dt_hi;
+    for (int64_t t = tlo + blk; t < thi; t += nblk) {
       const int64_t c0i = t * ct;
       for (int e = threadIdx.x; e < tile; e += blockDim.x)
         cp_async_c<T>(&sb[swz<T>(e)], &wk[(int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1))]);

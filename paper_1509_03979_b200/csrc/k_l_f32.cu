@@ -9,4 +9,8 @@ template cs_status tier_l_recover<float>(OpMeta, Params, int, const float*, int6
                                        void*, size_t, cudaStream_t, std::atomic<uint64_t>&, std::string&);
 template cs_status tier_l_diag_topk<float>(const float*, int64_t, int64_t, uint32_t*, void*, size_t, cudaStream_t,
                                         std::atomic<uint64_t>&, std::string&);
+template cs_status tier_l_dist_phase<float>(OpMeta, const DistArgs<float>&, void*, size_t, cudaStream_t,
+                                        std::atomic<uint64_t>&, std::string&);
+template cs_status tier_l_dist_copy<float>(OpMeta, void*, const int32_t*, const int32_t*, int64_t, int64_t, float*, int,
+                                       cudaStream_t, std::atomic<uint64_t>&, std::string&);
 }  // namespace cs

@@ -403,6 +403,89 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_recover(LArgs<T> a) {
   }
 }
 
+// ---- distributed operator (SV §8f NEXT-4): one phase of the four-step apply / adjoint of a
+// single signal split over `world` ranks (paper_1509_03979_b200/dist.py orchestrates the
+// phases and the two all-to-alls).  Rank r owns the column tiles [t_lo, t_hi) of passes A / C
+// and the row-pair items [i_lo, i_hi) of pass B; the phases are the single-GPU passes
+// restricted to those ranges.
+enum DistPhase { DP_A = 0, DP_BF = 1, DP_BA = 2, DP_C = 3, DP_P = 4 };
+template <typename T> struct DistArgs {
+  int phase;
+  int64_t t_lo, t_hi, i_lo, i_hi;
+  const T* in;
+  T* out;
+};
+template <typename T>
+__global__ void __launch_bounds__(TL_THREADS, 2) k_l_dist(LArgs<T> a, DistArgs<T> d) {
+  extern __shared__ __align__(16) char smem[];
+  GridCtx<T> c = make_grid_ctx<T>(smem, a);
+  set_instance(c, a.meta, 0);
+  c.dt_lo = d.t_lo;
+  c.dt_hi = d.t_hi;
+  c.di_lo = d.i_lo;
+  c.di_hi = d.i_hi;
+  const int64_t N = c.N;
+  if (d.phase == DP_A) {
+    // x (every rank holds all of it) -> U in Makhoul order with the sign, then this rank's
+    // column FFTs (pass A) -> its columns of Wk
+    const T* x = d.in;
+    const uint32_t* sg = c.sign;
+    T* U = c.U;
+    gstaged<TL_UNR, T>(N, c.gtid, c.gnthr, [&](int64_t j) { return apply_sign<T>(sg, j, x[j]); },
+                       [&](int64_t j, T v) { U[mk_pos(j, N)] = v; });
+    c.sync();
+    c.passA();
+    c.sync();
+  } else if (d.phase == DP_BF) {
+    // this rank's row pairs: row FFTs, DCT split, row select -> y in the transposed row order
+    // (only this rank's rows are written; the caller zeroes `out` and sums over the ranks)
+    c.template passB<MID_FWD>(false, d.out);
+    c.sync();
+  } else if (d.phase == DP_BA) {
+    // adjoint: y (all of it) -> yT, then this rank's row pairs of C_N^T's first half (a
+    // zero-input residual pass B: X' = y / s on the selected rows) -> its rows of Wk
+    load_yT(c, d.in);
+    c.template passB<MID_RES>(true, nullptr);
+    c.sync();
+  } else if (d.phase == DP_C) {
+    // this rank's inverse column FFTs -> Cb, then x_j = sigma_j Cb[mk_pos(j)] for the j whose
+    // Makhoul position lies in this rank's columns, 0 elsewhere (the caller sums the ranks)
+    c.passC();
+    c.sync();
+    const uint32_t* sg = c.sign;
+    const T* Cb = c.Cb;
+    const int64_t l2 = c.L2, ct = c.CT;
+    T* x = d.out;
+    gstaged<TL_UNR, T>(N, c.gtid, c.gnthr, [&](int64_t j) {
+      const int64_t p = mk_pos(j, N);
+      const int64_t t = ((p >> 1) & (l2 - 1)) / ct;
+      return (t >= d.t_lo && t < d.t_hi) ? apply_sign<T>(sg, j, Cb[p]) : T(0);
+    }, [&](int64_t j, T v) { x[j] = v; });
+    c.sync();
+  } else {
+    // yT (summed over the ranks) -> y in row order
+    const int32_t* tp = c.tperm;
+    T* y = d.out;
+    const T* yT = d.in;
+    gstaged<TL_UNR, T>(c.M, c.gtid, c.gnthr, [&](int64_t t) { return yT[t]; },
+                       [&](int64_t t, T v) { y[tp[t]] = v; });
+    c.sync();
+  }
+}
+
+// the all-to-all's pack / unpack: segment k (row rows[k], columns [col0[k], col0[k] + len)
+// of the four-step intermediate Wk) <-> buf[k len, (k + 1) len)
+template <typename T>
+__global__ void k_l_dist_copy(C2<T>* wk, int64_t l2, const int32_t* rows, const int32_t* col0, int64_t nseg,
+                              int64_t len, C2<T>* buf, int to_buf) {
+  const int64_t n = nseg * len;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / len, i = e - k * len;
+    C2<T>* w = wk + (int64_t)rows[k] * l2 + col0[k] + i;
+    if (to_buf) buf[e] = *w; else *w = buf[e];
+  }
+}
+
 // Diagnostics / test hook: the grid tier's top-K (select.cuh topk_bits, the radix path used
 // by detection at c2, c3, c5) on a caller's value array, over a full cooperative grid.
 // The context is built for the smallest Tier L geometry (only its collectives are used).
@@ -491,6 +574,14 @@ template <typename T>
 cs_status tier_l_recover(OpMeta meta, Params P, int ucap, const T* Y, int64_t B, T* vals,
                          int32_t* supp, cs_report* reps, void* ws, size_t ws_bytes,
                          cudaStream_t st, std::atomic<uint64_t>& launches, std::string& err);
+
+template <typename T>
+cs_status tier_l_dist_phase(OpMeta meta, const DistArgs<T>& d, void* ws, size_t ws_bytes, cudaStream_t st,
+                            std::atomic<uint64_t>& launches, std::string& err);
+template <typename T>
+cs_status tier_l_dist_copy(OpMeta meta, void* ws, const int32_t* rows, const int32_t* col0, int64_t nseg,
+                           int64_t len, T* buf, int to_buf, cudaStream_t st, std::atomic<uint64_t>& launches,
+                           std::string& err);
 
 template <typename T> inline size_t tier_l_diag_topk_ws_bytes() {
   return (size_t)align_up(l_layout<T>(TL_DIAG_N, TL_DIAG_N / 4, 0, 0, false, l_grid_upper<T>()).bytes, 256);
@@ -594,6 +685,52 @@ cs_status tier_l_diag_topk(const T* vals, int64_t n, int64_t K, uint32_t* out, v
   e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(TL_THREADS), args, (size_t)smem, st);
   launches.fetch_add(1);
   if (e != cudaSuccess) { err = std::string("cooperative launch: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  return CS_OK;
+}
+
+template <typename T>
+cs_status tier_l_dist_phase(OpMeta meta, const DistArgs<T>& d, void* ws, size_t ws_bytes, cudaStream_t st,
+                            std::atomic<uint64_t>& launches, std::string& err) {
+  LArgs<T> a;
+  a.meta = meta;
+  a.lay = l_layout<T>(meta.N, meta.M, 0, 0, false, l_grid_upper<T>());
+  if (!ws || ws_bytes < (size_t)a.lay.bytes) { err = "workspace too small"; return CS_ERR_WORKSPACE; }
+  a.B = 1;
+  a.Y = nullptr;
+  a.out = nullptr;
+  a.vals = nullptr; a.supp = nullptr; a.reps = nullptr;
+  a.ws = reinterpret_cast<char*>(ws);
+  a.ws_bytes = (size_t)a.lay.bytes;   // one group: the workspace of instance 0
+  const void* fn = (const void*)k_l_dist<T>;
+  const int64_t smem = l_smem_bytes<T>(meta.N);
+  int grid = l_maxgrid<T>(fn, smem);
+  if (grid > a.lay.maxgrid) grid = a.lay.maxgrid;
+  a.gblocks = grid;
+  a.ngroups = 1;
+  a.gstride = align_up(a.lay.bytes, 256);
+  cudaError_t e = cudaMemsetAsync(a.ws + a.lay.ctl, 0, (size_t)(a.lay.ctl_end - a.lay.ctl), st);
+  if (e != cudaSuccess) { err = std::string("memset: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  DistArgs<T> dd = d;
+  void* args[] = {&a, &dd};
+  e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(TL_THREADS), args, (size_t)smem, st);
+  launches.fetch_add(1);
+  if (e != cudaSuccess) { err = std::string("cooperative launch: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  return CS_OK;
+}
+template <typename T>
+cs_status tier_l_dist_copy(OpMeta meta, void* ws, const int32_t* rows, const int32_t* col0, int64_t nseg,
+                           int64_t len, T* buf, int to_buf, cudaStream_t st, std::atomic<uint64_t>& launches,
+                           std::string& err) {
+  const LLayout lay = l_layout<T>(meta.N, meta.M, 0, 0, false, l_grid_upper<T>());
+  const LGeom g = l_geom(meta.N);
+  C2<T>* wk = reinterpret_cast<C2<T>*>(reinterpret_cast<char*>(ws) + lay.Wk);
+  const int64_t n = nseg * len;
+  if (n == 0) return CS_OK;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_l_dist_copy<T><<<blocks, 256, 0, st>>>(wk, g.L2, rows, col0, nseg, len, reinterpret_cast<C2<T>*>(buf), to_buf);
+  launches.fetch_add(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { err = std::string("kernel launch: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
   return CS_OK;
 }
 

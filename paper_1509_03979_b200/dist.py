@@ -73,3 +73,205 @@ def gather_records(rec, world: int, total: int = 0, out=None, group=None):
         return full.reshape(total, R)
     keep = [shard(total, r, world)[1] for r in range(world)]
     return torch.cat([full[r, :keep[r]] for r in range(world)])
+
+
+# ------------------------------------------------------------------------------------------
+# Single signal over G GPUs: the four-step operator of one large signal
+# with one all-to-all per pass.  The [L1][L2] intermediate of the four-step FFT (L = N/2 =
+# L1 L2, include/cs.h cs_dist_*) is split by column tiles for the column passes (A, C) and by
+# row pairs (rows i and L1 - i, which the DCT split pairs) for the row pass (B); between them
+# every rank sends each other rank the part of its columns that lies in that rank's rows.
+
+class DistPlan:
+    """Ownership of the distributed four-step operator: rank r owns the column tiles
+    tiles[r] (columns cols[r], L2 / world of them) and the row-pair items items[r] (rows
+    rows[r]).  Requires world to divide the L2 / CT column tiles."""
+
+    def __init__(self, N: int, world: int, L1: int, L2: int, CT: int):
+        ntiles, nitems = L2 // CT, L1 // 2 + 1
+        if world < 1 or ntiles % world:
+            raise ValueError(f"world {world} must divide the {ntiles} column tiles")
+        self.N, self.world, self.L1, self.L2, self.CT = N, world, L1, L2, CT
+        self.tiles = [(r * ntiles // world, (r + 1) * ntiles // world) for r in range(world)]
+        self.cols = [(t0 * CT, t1 * CT) for t0, t1 in self.tiles]
+        self.items = []
+        for r in range(world):
+            b0, cnt = shard(nitems, r, world)
+            self.items.append((b0, b0 + cnt))
+        self.rows = [self._rows(i0, i1) for i0, i1 in self.items]
+        self.seg_len = L2 // world          # complex elements per segment (one row x one column block)
+
+    def _rows(self, i0, i1):
+        out = []
+        for it in range(i0, i1):
+            out.append(it)
+            if it != 0 and it != self.L1 // 2:
+                out.append(self.L1 - it)
+        return out
+
+    def segments(self, rank: int, direction: int, pack: bool):
+        """(rows, col0, counts per peer) of the segments `rank` packs (pack=True) or unpacks.
+        direction 0: after pass A, columns -> row pairs; 1: after pass B, row pairs -> columns.
+        Segments are ordered by peer, so counts[p] consecutive segments go to / come from p."""
+        rows, col0, counts = [], [], []
+        for p in range(self.world):
+            if direction == 0:
+                # pack at the column owner `rank` for row owner p; unpack at row owner `rank` from p
+                rs, c = (self.rows[p], self.cols[rank][0]) if pack else (self.rows[rank], self.cols[p][0])
+            else:
+                # pack at the row owner `rank` for column owner p; unpack at column owner `rank` from p
+                rs, c = (self.rows[rank], self.cols[p][0]) if pack else (self.rows[p], self.cols[rank][0])
+            rows += rs
+            col0 += [c] * len(rs)
+            counts.append(len(rs))
+        return rows, col0, counts
+
+
+def dist_plan(N: int, world: int) -> DistPlan:
+    import ctypes
+    from . import load_library
+    L1, L2, CT = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+    rc = load_library().cs_dist_geometry(N, ctypes.byref(L1), ctypes.byref(L2), ctypes.byref(CT))
+    if rc:
+        raise RuntimeError(f"cs_dist_geometry: {load_library().cs_last_error().decode()}")
+    return DistPlan(N, world, L1.value, L2.value, CT.value)
+
+
+class DistOperator:
+    """One rank's share of the distributed operator of one signal (instance 0 of `op`, a plain
+    P.DCT.diag(sigma) with N > 16384).  `exchange(send, send_counts, recv_counts)` performs the
+    all-to-all of flat fp32 buffers (counts in floats, ordered by peer) and `allreduce(t)` sums
+    a tensor over the ranks in place; torch.distributed supplies both (from_process_group), a
+    single process can emulate several ranks (tests)."""
+
+    def __init__(self, op, plan: DistPlan, rank: int):
+        import torch
+        from . import load_library
+        self.op, self.plan, self.rank = op, plan, rank
+        self.lib = load_library()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.ws = torch.empty(int(self.lib.cs_dist_ws_bytes(op.N, op.M)), dtype=torch.uint8, device=dev)
+        self.seg = {}
+        for d in (0, 1):
+            for pk in (True, False):
+                rows, col0, counts = plan.segments(rank, d, pk)
+                self.seg[(d, pk)] = (torch.tensor(rows, dtype=torch.int32, device=dev),
+                                     torch.tensor(col0, dtype=torch.int32, device=dev),
+                                     [2 * c * plan.seg_len for c in counts])
+
+    def _call(self, rc, what):
+        if rc:
+            raise RuntimeError(f"{what}: {self.lib.cs_last_error().decode()}")
+
+    def phase(self, ph: int, inp=None, out=None):
+        import ctypes
+        import torch
+        P = ctypes.c_void_p
+        t0, t1 = self.plan.tiles[self.rank]
+        i0, i1 = self.plan.items[self.rank]
+        st = P(torch.cuda.current_stream().cuda_stream)
+        self._call(self.lib.cs_dist_phase(self.op.handle, ph, t0, t1, i0, i1,
+                                          P(inp.data_ptr()) if inp is not None else None,
+                                          P(out.data_ptr()) if out is not None else None,
+                                          P(self.ws.data_ptr()), self.ws.numel(), st), "cs_dist_phase")
+
+    def copy(self, direction: int, pack: bool, buf):
+        import ctypes
+        import torch
+        P = ctypes.c_void_p
+        rows, col0, _ = self.seg[(direction, pack)]
+        st = P(torch.cuda.current_stream().cuda_stream)
+        self._call(self.lib.cs_dist_copy(self.op.handle, P(self.ws.data_ptr()), P(rows.data_ptr()),
+                                         P(col0.data_ptr()), rows.numel(), self.plan.seg_len,
+                                         P(buf.data_ptr()), 1 if pack else 0, st), "cs_dist_copy")
+
+    def send_buffer(self, direction: int):
+        import torch
+        n = sum(self.seg[(direction, True)][2])
+        buf = torch.empty(n, dtype=torch.float32, device=self.ws.device)
+        self.copy(direction, True, buf)
+        return buf, self.seg[(direction, True)][2], self.seg[(direction, False)][2]
+
+
+# phase ids (include/cs.h CS_DP_*)
+DP_A, DP_BF, DP_BA, DP_C, DP_P = range(5)
+
+
+def dist_apply(ranks, x, exchange, allreduce):
+    """y = A x for one signal; `ranks` = the DistOperator(s) of this process (one per rank it
+    plays: one under torchrun, several in the single-process emulation), x [N] fp32 on every
+    rank.  exchange(sends) -> recvs maps the per-rank send buffers to the per-rank receive
+    buffers (the all-to-all), allreduce(list of tensors) -> their sum."""
+    import torch
+    for r in ranks:
+        r.phase(DP_A, inp=x)
+    sends = [r.send_buffer(0) for r in ranks]
+    recvs = exchange(sends)
+    for r, buf in zip(ranks, recvs):
+        r.copy(0, False, buf)
+    parts = []
+    for r in ranks:
+        yT = torch.zeros(r.op.M, dtype=torch.float32, device=x.device)
+        r.phase(DP_BF, out=yT)
+        parts.append(yT)
+    yT = allreduce(parts)
+    y = torch.empty(ranks[0].op.M, dtype=torch.float32, device=x.device)
+    ranks[0].phase(DP_P, inp=yT, out=y)
+    return y
+
+
+def dist_adjoint(ranks, y, exchange, allreduce):
+    """x = A^T y for one signal (y [M] fp32 on every rank); see dist_apply."""
+    import torch
+    for r in ranks:
+        r.phase(DP_BA, inp=y)
+    sends = [r.send_buffer(1) for r in ranks]
+    recvs = exchange(sends)
+    for r, buf in zip(ranks, recvs):
+        r.copy(1, False, buf)
+    parts = []
+    for r in ranks:
+        xp = torch.empty(r.op.N, dtype=torch.float32, device=y.device)
+        r.phase(DP_C, out=xp)
+        parts.append(xp)
+    return allreduce(parts)
+
+
+def emulated_exchange(sends):
+    """All-to-all among the ranks of one process: receive buffer s = the blocks destined to s
+    from every rank r, in rank order (the layout all_to_all_single produces)."""
+    import torch
+    world = len(sends)
+    offs = []
+    for buf, sc, rc in sends:
+        o, acc = [], 0
+        for c in sc:
+            o.append((acc, acc + c))
+            acc += c
+        offs.append(o)
+    return [torch.cat([sends[r][0][offs[r][s][0]:offs[r][s][1]] for r in range(world)]) for s in range(world)]
+
+
+def emulated_allreduce(parts):
+    out = parts[0].clone()
+    for p in parts[1:]:
+        out += p
+    return out
+
+
+def process_group_exchange(group=None):
+    """exchange / allreduce for one rank per process over torch.distributed (NCCL on GPUs)."""
+    import torch
+    import torch.distributed as dist
+
+    def exchange(sends):
+        (buf, sc, rc), = sends
+        out = torch.empty(sum(rc), dtype=buf.dtype, device=buf.device)
+        dist.all_to_all_single(out, buf, output_split_sizes=rc, input_split_sizes=sc, group=group)
+        return [out]
+
+    def allreduce(parts):
+        (t,) = parts
+        dist.all_reduce(t, group=group)
+        return t
+    return exchange, allreduce
