@@ -259,32 +259,51 @@ cs_status cs_gather_batched_after(void* comm, int root, int64_t B_per_dev, int32
 cs_status cs_comm_destroy(void* comm);
 
 /* ---------------------------------------------------------------- single signal, G GPUs ---
- * (SV §8f NEXT-4) The four-step operator of one large signal (N > 16384, fp32, the plain
- * P.DCT.diag(sigma), instance 0) split over `world` ranks, one all-to-all per pass:
- *   apply:   DP_A  (x -> this rank's column FFTs), all-to-all columns -> row pairs,
- *            DP_BF (this rank's row FFTs + DCT split + row select -> its part of yT; the caller
- *            zeroes d_out and sums yT over the ranks), DP_P (yT -> y in row order);
- *   adjoint: DP_BA (y -> this rank's rows of Wk), all-to-all row pairs -> columns,
- *            DP_C  (this rank's inverse column FFTs -> its entries of x, zeros elsewhere;
- *            the caller sums x over the ranks).
- * Rank r owns the column tiles [t_lo, t_hi) of passes A / C (tiles of CT columns of the
- * [L1][L2] intermediate) and the row-pair items [i_lo, i_hi) of pass B (item i = rows i and
- * L1 - i).  cs_dist_copy moves segments (row rows[k], columns [col0[k], col0[k] + seg_len))
- * of the intermediate between the workspace and a flat exchange buffer (to_buf 1: pack,
- * 0: unpack).  d_ws: DEVICE workspace of cs_dist_ws_bytes(N, M) bytes, one per rank, kept
- * across the phases of one call.  Orchestration and the all-to-alls (torch.distributed /
- * NCCL): paper_1509_03979_b200/dist.py.  Asynchronous on `stream`. */
+ * (SV §8f NEXT-4; the paper's "large-scale" signals) The four-step operator of one
+ * large signal (N > 16384, fp32, the plain P.DCT.diag(sigma) of Eq.(7) with the sign
+ * randomizer, instance 0 of `op`) split over `world` ranks with ONE all-to-all per
+ * application and no other collective.  The complex [L1][L2] intermediate of the four-step
+ * FFT (L1 L2 = N / 2, cs_dist_geometry) is owned by column tiles (CT columns each) in the column
+ * passes and by row-pair items (item i = rows i and L1 - i, which the DCT split pairs; items
+ * 0 .. L1 / 2) in the row pass.  Rank r owns tiles [t_lo, t_hi) and items [i_lo, i_hi).
+ * Distributed layouts (no rank holds a whole vector):
+ *   x: "xc", the 2 L1 nc reals (nc = CT (t_hi - t_lo) columns) at the Makhoul positions of
+ *      this rank's columns, row by row: xc[q] <-> p = 2 (k1 L2 + c0) + q - 2 nc k1,
+ *      k1 = q / (2 nc), c0 = CT t_lo; natural index j = p < N/2 ? 2 p : 2 (N - 1 - p) + 1;
+ *   y: "yT", an [M] buffer in the transposed row order of which a rank reads / writes only the
+ *      entries of its rows (cs_dist_row_offsets gives where each row's entries start).
+ *   apply   y = A x:   DP_A  (xc -> its column FFTs), all-to-all columns -> row pairs,
+ *                      DP_BF (its row FFTs + DCT split + row select -> its entries of yT);
+ *   adjoint x = A^T y: DP_BA (its entries of yT -> its rows), all-to-all row pairs -> columns,
+ *                      DP_C  (its inverse column FFTs -> xc).
+ *   layout changes (no arithmetic): DP_XS natural x [N] -> xc; DP_XG the xc of all ranks
+ *   gathered in rank order ([G][2 L1 nc], equal tile ranges: G = (L2 / CT) / (t_hi - t_lo))
+ *   -> natural x [N]; DP_YT natural y [M] -> yT; DP_P complete yT -> natural y [M].
+ * d_in / d_out: DEVICE fp32 (DP_A, DP_BA: d_in only; DP_BF, DP_C: d_out only).
+ * cs_dist_copy moves segments (row rows[k], columns [col0[k], col0[k] + seg_len)) of the
+ * intermediate between the workspace and a flat exchange buffer of nseg seg_len complex fp32
+ * values (to_buf 1: pack, 0: unpack).  d_ws: DEVICE workspace of cs_dist_ws_bytes(N, M) bytes,
+ * one per rank, kept across the phases of one application.  cs_dist_row_offsets fills
+ * h_off[0 .. L1] (HOST) with the yT offset where row k1's entries start (h_off[L1] = M); it
+ * synchronizes the device (plan time).  Orchestration and the all-to-alls (torch.distributed /
+ * NCCL): paper_1509_03979_b200/dist.py.  Errors: CS_ERR_UNSUPPORTED for N <= 16384 or another
+ * operator kind, CS_ERR_INVALID_ARG for ranges out of bounds or missing buffers.  Phases and
+ * copies are asynchronous on `stream`. */
 #define CS_DP_A 0
 #define CS_DP_BF 1
 #define CS_DP_BA 2
 #define CS_DP_C 3
 #define CS_DP_P 4
+#define CS_DP_YT 5
+#define CS_DP_XS 6
+#define CS_DP_XG 7
 cs_status cs_dist_geometry(int64_t N, int64_t* L1, int64_t* L2, int32_t* CT);
 size_t cs_dist_ws_bytes(int64_t N, int64_t M);
 cs_status cs_dist_phase(const cs_operator* op, int phase, int64_t t_lo, int64_t t_hi, int64_t i_lo, int64_t i_hi,
                         const float* d_in, float* d_out, void* d_ws, size_t ws_bytes, cs_stream_t stream);
 cs_status cs_dist_copy(const cs_operator* op, void* d_ws, const int32_t* d_rows, const int32_t* d_col0, int64_t nseg,
                        int64_t seg_len, float* d_buf, int to_buf, cs_stream_t stream);
+cs_status cs_dist_row_offsets(const cs_operator* op, int64_t* h_off);
 
 /* Host-buffer variants (the end-to-end entry points): h_Y [B][M] and the outputs
  * h_vals [B][K], h_support [B][K], h_reports [B] are HOST memory (pinned for overlap).

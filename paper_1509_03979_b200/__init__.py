@@ -56,7 +56,7 @@ EXPORTS = [
     "cs_recover_batched", "cs_recover_batched_f64", "cs_workspace_bytes_host", "cs_recover_batched_host",
     "cs_recover_batched_host_f64", "cs_status_string", "cs_last_error",
     "cs_launch_count", "cs_version", "cs_diag_phase_offset", "cs_diag_grid_barrier_us",
-    "cs_dist_geometry", "cs_dist_ws_bytes", "cs_dist_phase", "cs_dist_copy",
+    "cs_dist_geometry", "cs_dist_ws_bytes", "cs_dist_phase", "cs_dist_copy", "cs_dist_row_offsets",
     "cs_diag_topk", "cs_diag_topk_grid", "cs_diag_topk_grid_ws_bytes", "cs_operator_meta_bytes_perm", "cs_operator_create_perm", "cs_operator_create_ex",
     "cs_operator_meta_bytes_ex", "cs_operator_meta_bytes_dft", "cs_operator_create_dft",
     "cs_support_to_dense", "cs_support_to_dense_f64", "cs_comm_init", "cs_gather_batched", "cs_gather_batched_after", "cs_comm_destroy",
@@ -124,6 +124,7 @@ def load_library(path: str = LIB_PATH):
         "cs_dist_ws_bytes": (SZ, [I64, I64]),
         "cs_dist_phase": (I32, [P, ctypes.c_int, I64, I64, I64, I64, P, P, P, SZ, P]),
         "cs_dist_copy": (I32, [P, P, P, P, I64, I64, P, ctypes.c_int, P]),
+        "cs_dist_row_offsets": (I32, [P, ctypes.POINTER(I64)]),
         "cs_diag_topk_grid_ws_bytes": (SZ, []),
     }
     for name, (res, args) in sig.items():

@@ -931,16 +931,36 @@ static cs_status dist_check(const cs_operator* op) {
 cs_status cs_dist_phase(const cs_operator* op, int phase, int64_t t_lo, int64_t t_hi, int64_t i_lo, int64_t i_hi,
                         const float* d_in, float* d_out, void* d_ws, size_t ws_bytes, cs_stream_t stream) {
   if (cs_status s = dist_check(op)) return s;
-  if (phase < DP_A || phase > DP_P) return fail(CS_ERR_INVALID_ARG, "unknown phase");
+  if (phase < DP_A || phase > DP_XG) return fail(CS_ERR_INVALID_ARG, "unknown phase");
   const LGeom g = l_geom(op->N);
   const int64_t ntiles = g.L2 / g.CT, nitems = g.L1 / 2 + 1;
   if (t_lo < 0 || t_hi < t_lo || t_hi > ntiles || i_lo < 0 || i_hi < i_lo || i_hi > nitems)
     return fail(CS_ERR_INVALID_ARG, "tile / item range out of bounds");
-  if ((phase == DP_A || phase == DP_BA || phase == DP_P) && !d_in) return fail(CS_ERR_INVALID_ARG, "null input");
-  if ((phase == DP_BF || phase == DP_C || phase == DP_P) && !d_out) return fail(CS_ERR_INVALID_ARG, "null output");
+  if ((phase == DP_A || phase == DP_C || phase == DP_XS || phase == DP_XG) && (t_hi == t_lo))
+    return fail(CS_ERR_INVALID_ARG, "empty tile range");
+  if (phase == DP_XG && ntiles % (t_hi - t_lo))
+    return fail(CS_ERR_INVALID_ARG, "DP_XG: the tile range must split the tiles evenly");
+  if (phase != DP_BF && phase != DP_C && !d_in) return fail(CS_ERR_INVALID_ARG, "null input");
+  if (phase != DP_A && phase != DP_BA && !d_out) return fail(CS_ERR_INVALID_ARG, "null output");
   DistArgs<float> d{phase, t_lo, t_hi, i_lo, i_hi, d_in, d_out};
   return tier_l_dist_phase<float>(meta_of(op), d, d_ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), g_launches,
                                   g_last_error);
+}
+cs_status cs_dist_row_offsets(const cs_operator* op, int64_t* h_off) {
+  if (cs_status s = dist_check(op)) return s;
+  if (!h_off) return fail(CS_ERR_INVALID_ARG, "null output");
+  const LGeom g = l_geom(op->N);
+  const OpMeta m = meta_of(op);
+  // row k1's entries start at transposed position t = k1 2 L2, a whole mask word (2 L2 >= 32)
+  const int64_t wpr = 2 * g.L2 / 32;
+  std::vector<int32_t> pre(g.L1);
+  cudaError_t e = cudaDeviceSynchronize();   // the metadata may still be in flight (plan time only)
+  if (e == cudaSuccess) e = cudaMemcpy2D(pre.data(), sizeof(int32_t), m.tprefix(0), wpr * sizeof(int32_t), sizeof(int32_t),
+                               g.L1, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(CS_ERR_CUDA, std::string("row offsets: ") + cudaGetErrorString(e));
+  for (int64_t k = 0; k < g.L1; ++k) h_off[k] = pre[k];
+  h_off[g.L1] = op->M;
+  return CS_OK;
 }
 cs_status cs_dist_copy(const cs_operator* op, void* d_ws, const int32_t* d_rows, const int32_t* d_col0, int64_t nseg,
                        int64_t seg_len, float* d_buf, int to_buf, cs_stream_t stream) {

@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_recover(LArgs<T> a) {
 // phases and the two all-to-alls).  Rank r owns the column tiles [t_lo, t_hi) of passes A / C
 // and the row-pair items [i_lo, i_hi) of pass B; the phases are the single-GPU passes
 // restricted to those ranges.
-enum DistPhase { DP_A = 0, DP_BF = 1, DP_BA = 2, DP_C = 3, DP_P = 4 };
+enum DistPhase { DP_A = 0, DP_BF = 1, DP_BA = 2, DP_C = 3, DP_P = 4, DP_YT = 5, DP_XS = 6, DP_XG = 7 };
 template <typename T> struct DistArgs {
   int phase;
   int64_t t_lo, t_hi, i_lo, i_hi;
@@ -425,50 +425,80 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_dist(LArgs<T> a, DistArgs<T
   c.di_lo = d.i_lo;
   c.di_hi = d.i_hi;
   const int64_t N = c.N;
+  // this rank's columns [c0, c0 + nc) of the complex [L1][L2] intermediate; its compact x
+  // ("xc", nxc = 2 L1 nc reals) lists their Makhoul positions p row by row:
+  // xc[q] <-> p = 2 (k1 L2 + c0) + (q - 2 nc k1), k1 = q / (2 nc)
+  const int64_t l2 = c.L2, ct = c.CT, c0 = d.t_lo * ct, nc = (d.t_hi - d.t_lo) * ct;
+  const int64_t nxc = 2 * c.L1 * nc;
+  auto pos_of = [=](int64_t q) {
+    const int64_t k1 = q / (2 * nc);
+    return 2 * (k1 * l2 + c0) + (q - 2 * nc * k1);
+  };
+  const uint32_t* sg = c.sign;
   if (d.phase == DP_A) {
-    // x (every rank holds all of it) -> U in Makhoul order with the sign, then this rank's
-    // column FFTs (pass A) -> its columns of Wk
+    // xc -> U (sign applied) on this rank's columns, then its column FFTs (pass A) -> its
+    // columns of Wk
     const T* x = d.in;
-    const uint32_t* sg = c.sign;
     T* U = c.U;
-    gstaged<TL_UNR, T>(N, c.gtid, c.gnthr, [&](int64_t j) { return apply_sign<T>(sg, j, x[j]); },
-                       [&](int64_t j, T v) { U[mk_pos(j, N)] = v; });
+    gstaged<TL_UNR, T>(nxc, c.gtid, c.gnthr, [&](int64_t q) {
+      const int64_t p = pos_of(q);
+      return apply_sign<T>(sg, mk_nat(p, N), x[q]);
+    }, [&](int64_t q, T v) { U[pos_of(q)] = v; });
     c.sync();
     c.passA();
     c.sync();
   } else if (d.phase == DP_BF) {
-    // this rank's row pairs: row FFTs, DCT split, row select -> y in the transposed row order
-    // (only this rank's rows are written; the caller zeroes `out` and sums over the ranks)
+    // this rank's row pairs: row FFTs, DCT split, row select -> its entries of yT (the
+    // transposed row order; entries of other ranks' rows are not written)
     c.template passB<MID_FWD>(false, d.out);
     c.sync();
   } else if (d.phase == DP_BA) {
-    // adjoint: y (all of it) -> yT, then this rank's row pairs of C_N^T's first half (a
+    // adjoint: this rank's entries of yT -> its row pairs of C_N^T's first half (a
     // zero-input residual pass B: X' = y / s on the selected rows) -> its rows of Wk
-    load_yT(c, d.in);
+    c.y = d.in;
     c.template passB<MID_RES>(true, nullptr);
     c.sync();
   } else if (d.phase == DP_C) {
-    // this rank's inverse column FFTs -> Cb, then x_j = sigma_j Cb[mk_pos(j)] for the j whose
-    // Makhoul position lies in this rank's columns, 0 elsewhere (the caller sums the ranks)
+    // this rank's inverse column FFTs -> Cb, then xc[q] = sigma_j Cb[p] on its columns
     c.passC();
     c.sync();
-    const uint32_t* sg = c.sign;
     const T* Cb = c.Cb;
-    const int64_t l2 = c.L2, ct = c.CT;
     T* x = d.out;
-    gstaged<TL_UNR, T>(N, c.gtid, c.gnthr, [&](int64_t j) {
-      const int64_t p = mk_pos(j, N);
-      const int64_t t = ((p >> 1) & (l2 - 1)) / ct;
-      return (t >= d.t_lo && t < d.t_hi) ? apply_sign<T>(sg, j, Cb[p]) : T(0);
-    }, [&](int64_t j, T v) { x[j] = v; });
+    gstaged<TL_UNR, T>(nxc, c.gtid, c.gnthr, [&](int64_t q) {
+      const int64_t p = pos_of(q);
+      return apply_sign<T>(sg, mk_nat(p, N), Cb[p]);
+    }, [&](int64_t q, T v) { x[q] = v; });
+    c.sync();
+  } else if (d.phase == DP_P || d.phase == DP_YT) {
+    // yT (complete) <-> y in row order
+    const int32_t* tp = c.tperm;
+    const T* in = d.in;
+    T* out = d.out;
+    if (d.phase == DP_P)
+      gstaged<TL_UNR, T>(c.M, c.gtid, c.gnthr, [&](int64_t t) { return in[t]; },
+                         [&](int64_t t, T v) { out[tp[t]] = v; });
+    else
+      gstaged<TL_UNR, T>(c.M, c.gtid, c.gnthr, [&](int64_t t) { return in[tp[t]]; },
+                         [&](int64_t t, T v) { out[t] = v; });
+    c.sync();
+  } else if (d.phase == DP_XS) {
+    // natural x -> this rank's xc (no sign: DP_A applies it)
+    const T* x = d.in;
+    T* xc = d.out;
+    gstaged<TL_UNR, T>(nxc, c.gtid, c.gnthr, [&](int64_t q) { return x[mk_nat(pos_of(q), N)]; },
+                       [&](int64_t q, T v) { xc[q] = v; });
     c.sync();
   } else {
-    // yT (summed over the ranks) -> y in row order
-    const int32_t* tp = c.tperm;
-    T* y = d.out;
-    const T* yT = d.in;
-    gstaged<TL_UNR, T>(c.M, c.gtid, c.gnthr, [&](int64_t t) { return yT[t]; },
-                       [&](int64_t t, T v) { y[tp[t]] = v; });
+    // DP_XG: the xc of every rank ([G][nxc], rank g owning columns [g nc, (g + 1) nc)) ->
+    // natural x
+    const T* in = d.in;
+    T* x = d.out;
+    const int lg2 = c.log2L2;
+    gstaged<TL_UNR, T>(N, c.gtid, c.gnthr, [&](int64_t j) {
+      const int64_t p = mk_pos(j, N), ci = p >> 1;
+      const int64_t k1 = ci >> lg2, col = ci & (l2 - 1), g = col / nc;
+      return in[g * nxc + 2 * (k1 * nc + col - g * nc) + (p & 1)];
+    }, [&](int64_t j, T v) { x[j] = v; });
     c.sync();
   }
 }

@@ -109,6 +109,17 @@ class DistPlan:
                 out.append(self.L1 - it)
         return out
 
+    def y_ranges(self, rank: int, row_offsets):
+        """[start, end) of this rank's entries in yT: its rows [i0, i1) and their partners
+        L1 - i (items 0 < i < L1 / 2), each a contiguous block of rows in the transposed order
+        (row_offsets[k1] = where row k1's entries start, cs_dist_row_offsets)."""
+        i0, i1 = self.items[rank]
+        out = [(row_offsets[i0], row_offsets[i1])] if i1 > i0 else []
+        lo, hi = max(i0, 1), min(i1, self.L1 // 2)
+        if hi > lo:
+            out.append((row_offsets[self.L1 - hi + 1], row_offsets[self.L1 - lo + 1]))
+        return out
+
     def segments(self, rank: int, direction: int, pack: bool):
         """(rows, col0, counts per peer) of the segments `rank` packs (pack=True) or unpacks.
         direction 0: after pass A, columns -> row pairs; 1: after pass B, row pairs -> columns.
@@ -137,14 +148,18 @@ def dist_plan(N: int, world: int) -> DistPlan:
     return DistPlan(N, world, L1.value, L2.value, CT.value)
 
 
+# phase ids (include/cs.h CS_DP_*)
+DP_A, DP_BF, DP_BA, DP_C, DP_P, DP_YT, DP_XS, DP_XG = range(8)
+
+
 class DistOperator:
     """One rank's share of the distributed operator of one signal (instance 0 of `op`, a plain
-    P.DCT.diag(sigma) with N > 16384).  `exchange(send, send_counts, recv_counts)` performs the
-    all-to-all of flat fp32 buffers (counts in floats, ordered by peer) and `allreduce(t)` sums
-    a tensor over the ranks in place; torch.distributed supplies both (from_process_group), a
-    single process can emulate several ranks (tests)."""
+    P.DCT.diag(sigma) with N > 16384, fp32).  Vectors live in the distributed layouts of
+    include/cs.h: x as this rank's "xc" (nxc reals on its columns), y as an [M] "yT" buffer of
+    which only this rank's rows (y_ranges) are meaningful."""
 
-    def __init__(self, op, plan: DistPlan, rank: int):
+    def __init__(self, op, plan: DistPlan, rank: int, row_offsets=None):
+        import ctypes
         import torch
         from . import load_library
         self.op, self.plan, self.rank = op, plan, rank
@@ -158,6 +173,14 @@ class DistOperator:
                 self.seg[(d, pk)] = (torch.tensor(rows, dtype=torch.int32, device=dev),
                                      torch.tensor(col0, dtype=torch.int32, device=dev),
                                      [2 * c * plan.seg_len for c in counts])
+        t0, t1 = plan.tiles[rank]
+        self.nxc = 2 * plan.L1 * (t1 - t0) * plan.CT
+        if row_offsets is None:
+            off = (ctypes.c_int64 * (plan.L1 + 1))()
+            self._call(self.lib.cs_dist_row_offsets(op.handle, off), "cs_dist_row_offsets")
+            row_offsets = list(off)
+        self.row_offsets = row_offsets
+        self.y_ranges = plan.y_ranges(rank, row_offsets)
 
     def _call(self, rc, what):
         if rc:
@@ -174,6 +197,7 @@ class DistOperator:
                                           P(inp.data_ptr()) if inp is not None else None,
                                           P(out.data_ptr()) if out is not None else None,
                                           P(self.ws.data_ptr()), self.ws.numel(), st), "cs_dist_phase")
+        return out
 
     def copy(self, direction: int, pack: bool, buf):
         import ctypes
@@ -192,49 +216,81 @@ class DistOperator:
         self.copy(direction, True, buf)
         return buf, self.seg[(direction, True)][2], self.seg[(direction, False)][2]
 
+    # layout changes (no arithmetic; entering / leaving the distributed layouts)
+    def scatter_x(self, x):
+        import torch
+        return self.phase(DP_XS, inp=x, out=torch.empty(self.nxc, dtype=torch.float32, device=x.device))
 
-# phase ids (include/cs.h CS_DP_*)
-DP_A, DP_BF, DP_BA, DP_C, DP_P = range(5)
+    def scatter_y(self, y):
+        import torch
+        return self.phase(DP_YT, inp=y, out=torch.empty(self.op.M, dtype=torch.float32, device=y.device))
+
+    def own_y(self, yT):
+        """This rank's entries of yT, its two row blocks concatenated."""
+        import torch
+        return torch.cat([yT[a:b] for a, b in self.y_ranges])
 
 
-def dist_apply(ranks, x, exchange, allreduce):
-    """y = A x for one signal; `ranks` = the DistOperator(s) of this process (one per rank it
-    plays: one under torchrun, several in the single-process emulation), x [N] fp32 on every
-    rank.  exchange(sends) -> recvs maps the per-rank send buffers to the per-rank receive
-    buffers (the all-to-all), allreduce(list of tensors) -> their sum."""
+def dist_apply(ranks, xcs, exchange):
+    """y = A x for one signal: `ranks` = the DistOperator(s) this process plays (one under
+    torchrun, several in the single-process emulation), xcs their x in the xc layout;
+    exchange(sends) -> recvs is the all-to-all.  Returns each rank's yT (its rows filled)."""
     import torch
-    for r in ranks:
-        r.phase(DP_A, inp=x)
-    sends = [r.send_buffer(0) for r in ranks]
-    recvs = exchange(sends)
+    for r, xc in zip(ranks, xcs):
+        r.phase(DP_A, inp=xc)
+    recvs = exchange([r.send_buffer(0) for r in ranks])
+    out = []
     for r, buf in zip(ranks, recvs):
         r.copy(0, False, buf)
-    parts = []
-    for r in ranks:
-        yT = torch.zeros(r.op.M, dtype=torch.float32, device=x.device)
-        r.phase(DP_BF, out=yT)
-        parts.append(yT)
-    yT = allreduce(parts)
-    y = torch.empty(ranks[0].op.M, dtype=torch.float32, device=x.device)
-    ranks[0].phase(DP_P, inp=yT, out=y)
-    return y
+        out.append(r.phase(DP_BF, out=torch.empty(r.op.M, dtype=torch.float32, device=buf.device)))
+    return out
 
 
-def dist_adjoint(ranks, y, exchange, allreduce):
-    """x = A^T y for one signal (y [M] fp32 on every rank); see dist_apply."""
+def dist_adjoint(ranks, yTs, exchange):
+    """x = A^T y for one signal; yTs each rank's yT (its rows read).  Returns each rank's xc."""
     import torch
-    for r in ranks:
-        r.phase(DP_BA, inp=y)
-    sends = [r.send_buffer(1) for r in ranks]
-    recvs = exchange(sends)
+    for r, yT in zip(ranks, yTs):
+        r.phase(DP_BA, inp=yT)
+    recvs = exchange([r.send_buffer(1) for r in ranks])
+    out = []
     for r, buf in zip(ranks, recvs):
         r.copy(1, False, buf)
-    parts = []
-    for r in ranks:
-        xp = torch.empty(r.op.N, dtype=torch.float32, device=y.device)
-        r.phase(DP_C, out=xp)
-        parts.append(xp)
-    return allreduce(parts)
+        out.append(r.phase(DP_C, out=torch.empty(r.nxc, dtype=torch.float32, device=buf.device)))
+    return out
+
+
+def gather_x(ranks, xcs, allgather):
+    """The natural x [N] on every rank from the xc of all ranks (allgather(list) -> for each
+    local rank the concatenation of every rank's tensor in rank order; equal sizes)."""
+    import torch
+    full = allgather(xcs)
+    return [r.phase(DP_XG, inp=f, out=torch.empty(r.op.N, dtype=torch.float32, device=f.device))
+            for r, f in zip(ranks, full)]
+
+
+def gather_y(ranks, yTs, allgather):
+    """The natural y [M] on every rank from each rank's rows of yT (padded to equal sizes for
+    the all-gather, then placed at every rank's row blocks and permuted to row order)."""
+    import torch
+    plan = ranks[0].plan
+    offs = ranks[0].row_offsets
+    spans = [plan.y_ranges(g, offs) for g in range(plan.world)]
+    width = max(sum(b - a for a, b in sp) for sp in spans)
+    packed = []
+    for r, yT in zip(ranks, yTs):
+        own = r.own_y(yT)
+        packed.append(torch.cat([own, own.new_zeros(width - own.numel())]))
+    full = allgather(packed)
+    out = []
+    for r, f in zip(ranks, full):
+        yT = torch.empty(r.op.M, dtype=torch.float32, device=f.device)
+        for g, sp in enumerate(spans):
+            o = g * width
+            for a, b in sp:
+                yT[a:b] = f[o:o + b - a]
+                o += b - a
+        out.append(r.phase(DP_P, inp=yT, out=torch.empty(r.op.M, dtype=torch.float32, device=f.device)))
+    return out
 
 
 def emulated_exchange(sends):
@@ -252,6 +308,11 @@ def emulated_exchange(sends):
     return [torch.cat([sends[r][0][offs[r][s][0]:offs[r][s][1]] for r in range(world)]) for s in range(world)]
 
 
+def emulated_allgather(parts):
+    full = __import__("torch").cat(parts)
+    return [full for _ in parts]
+
+
 def emulated_allreduce(parts):
     out = parts[0].clone()
     for p in parts[1:]:
@@ -259,19 +320,38 @@ def emulated_allreduce(parts):
     return out
 
 
-def process_group_exchange(group=None):
-    """exchange / allreduce for one rank per process over torch.distributed (NCCL on GPUs)."""
+def process_group_exchange(group=None, host_staged: bool = False):
+    """(exchange, allgather, allreduce) for one rank per process over torch.distributed: NCCL
+    on GPUs; with host_staged the buffers go through host memory (gloo, which has no CUDA
+    all-to-all: the CPU tests, and several processes sharing one GPU)."""
     import torch
     import torch.distributed as dist
 
+    def _in(t):
+        return t.cpu() if host_staged else t
+
+    def _out(t, like):
+        return t.to(like.device) if host_staged else t
+
     def exchange(sends):
         (buf, sc, rc), = sends
-        out = torch.empty(sum(rc), dtype=buf.dtype, device=buf.device)
-        dist.all_to_all_single(out, buf, output_split_sizes=rc, input_split_sizes=sc, group=group)
-        return [out]
+        b = _in(buf)
+        out = torch.empty(sum(rc), dtype=b.dtype, device=b.device)
+        dist.all_to_all_single(out, b, output_split_sizes=rc, input_split_sizes=sc, group=group)
+        return [_out(out, buf)]
+
+    def allgather(parts):
+        (t,) = parts
+        b = _in(t.contiguous())
+        out = torch.empty(b.numel() * dist.get_world_size(group), dtype=b.dtype, device=b.device)
+        dist.all_gather_into_tensor(out, b, group=group)
+        return [_out(out, t)]
 
     def allreduce(parts):
         (t,) = parts
-        dist.all_reduce(t, group=group)
+        b = _in(t)
+        dist.all_reduce(b, group=group)
+        if host_staged:
+            t.copy_(b)
         return t
-    return exchange, allreduce
+    return exchange, allgather, allreduce

@@ -112,7 +112,7 @@ def _worker(rank, world, port, q):
     try:
         L1, L2, CT = 64, 128, 4
         p = csd.DistPlan(2 * L1 * L2, world, L1, L2, CT)
-        exchange, allreduce = csd.process_group_exchange()
+        exchange, allgather, allreduce = csd.process_group_exchange()
         T = _truth(L1, L2)
         ok = True
         for direction in (0, 1):
@@ -133,9 +133,11 @@ def _worker(rank, world, port, q):
             else:
                 a, b = p.cols[rank]
                 ok &= np.array_equal(w[:, a:b], T[:, a:b])
-        # the partial-sum reduction of the y / x halves
+        # the collectives of the layout changes (gather_x / gather_y)
         t = torch.full((5,), float(rank + 1))
         ok &= bool(torch.equal(allreduce([t]), torch.full((5,), float(world * (world + 1) // 2))))
+        (g,) = allgather([torch.full((3,), float(rank))])
+        ok &= bool(torch.equal(g, torch.tensor([0.0, 0, 0, 1, 1, 1])))
         q.put((rank, bool(ok)))
     finally:
         dist.destroy_process_group()
@@ -154,3 +156,24 @@ def test_gloo_world2_exchange():
         pr.join(timeout=60)
         assert pr.exitcode == 0
     assert res == {0: True, 1: True}
+
+
+@pytest.mark.parametrize("L1,L2,CT", GEOMS)
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_y_ranges_partition_the_measurements(L1, L2, CT, world):
+    """Rows of the transposed order hold consecutive yT entries (row_offsets); the ranks' row
+    blocks cover every row once, so their yT ranges partition [0, M)."""
+    if (L2 // CT) % world:
+        pytest.skip("world does not divide the column tiles")
+    p = csd.DistPlan(2 * L1 * L2, world, L1, L2, CT)
+    rng = np.random.default_rng(L1 + world)
+    counts = rng.integers(0, 2 * L2 + 1, size=L1)            # selected entries per row
+    offs = np.concatenate([[0], np.cumsum(counts)]).tolist()
+    covered = np.zeros(offs[-1], np.int64)
+    for r in range(world):
+        rows = set()
+        for a, b in p.y_ranges(r, offs):
+            covered[a:b] += 1
+            rows |= {k for k in range(L1) if offs[k] >= a and offs[k + 1] <= b and counts[k] > 0}
+        assert rows == {k for k in p.rows[r] if counts[k] > 0}
+    assert np.all(covered == 1)

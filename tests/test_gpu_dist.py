@@ -1,9 +1,11 @@
 """GPU parity of the single-signal distributed operator (NEXT-4, cs_dist_phase /
-cs_dist_copy, paper_1509_03979_b200/dist.py): G logical ranks played by one process on one
-GPU, host-sequenced (every phase of every rank completes before the exchange reads it; no
-kernel waits on another), the all-to-all and the sums done by the emulated exchange.  The
-distributed y = A x and x = A^T y must equal the oracle's (fp32 tolerance of
-test_gpu_operator.py) and the single-GPU cs_operator_apply / _adjoint."""
+cs_dist_copy / cs_dist_row_offsets, paper_1509_03979_b200/dist.py): G logical ranks played
+by one process on one GPU, host-sequenced (every phase of every rank is issued before the
+exchange reads it, on one stream; no kernel waits on another), the all-to-all and the
+all-gathers done by the emulated collectives.  The distributed y = A x and x = A^T y
+(entered from and gathered to natural vectors through the layout phases) must equal the
+oracle's (fp32 tolerance of test_gpu_operator.py) and the single-GPU cs_operator_apply /
+_adjoint; A^T A x chained inside the distributed layouts must equal the single-GPU chain."""
 import numpy as np
 import pytest
 
@@ -38,13 +40,20 @@ def _run(cs, N, M, world, seed=0):
     w = g.standard_normal(M)
     xd = torch.from_numpy(x).to(dev, torch.float32)
     wd = torch.from_numpy(w).to(dev, torch.float32)
-    y = csd.dist_apply(ranks, xd, csd.emulated_exchange, csd.emulated_allreduce)
-    xa = csd.dist_adjoint(ranks, wd, csd.emulated_exchange, csd.emulated_allreduce)
+    ex, ag = csd.emulated_exchange, csd.emulated_allgather
+    yT = csd.dist_apply(ranks, [r.scatter_x(xd) for r in ranks], ex)
+    y = csd.gather_y(ranks, yT, ag)[0]
+    xa = csd.gather_x(ranks, csd.dist_adjoint(ranks, [r.scatter_y(wd) for r in ranks], ex), ag)[0]
+    # A^T A x without leaving the distributed layouts (what an iterative solver chains)
+    ata = csd.gather_x(ranks, csd.dist_adjoint(ranks, yT, ex), ag)[0]
     y1 = cs.cs_operator_apply(A, xd[None])[0]
     x1 = cs.cs_operator_adjoint(A, wd[None])[0]
+    ata1 = cs.cs_operator_adjoint(A, y1[None])[0]
     torch.cuda.synchronize()
-    return p, x, w, y.double().cpu().numpy(), xa.double().cpu().numpy(), y1.double().cpu().numpy(), \
-        x1.double().cpu().numpy()
+    h = lambda t: t.double().cpu().numpy()
+    assert np.array_equal(h(ata), h(ata1)) or \
+        np.linalg.norm(h(ata) - h(ata1)) <= 1e-6 * np.linalg.norm(h(ata1)), (N, world)
+    return p, x, w, h(y), h(xa), h(y1), h(x1)
 
 
 def _close_to_single(N, G, y, xa, y1, x1):
@@ -93,3 +102,55 @@ def test_dist_rejects_small_and_bad_ranges(cs):
         csd.dist_plan(1 << 14, 2)      # Tier S size: no four-step intermediate
     with pytest.raises(ValueError):
         csd.dist_plan(1 << 15, 7)      # 7 does not divide the column tiles
+
+
+def _mp_worker(rank, world, port, N, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1509_03979_b200 as cs
+        from paper_1509_03979_b200 import dist as csd
+        dev = torch.device("cuda:0")
+        M = N // 4
+        cfg = cs_inputs.Config(95, "sp", N, M, M // 8, "gauss", 0.0)
+        p = cs_inputs.make_problem(cfg, b=0)
+        bits, rows = to_dev([p], dev)
+        A = cs.Operator(N, M, bits, rows, batch=1)
+        r = csd.DistOperator(A, csd.dist_plan(N, world), rank)
+        ex, ag, _ = csd.process_group_exchange(host_staged=True)
+        g = np.random.default_rng(7)
+        xd = torch.from_numpy(g.standard_normal(N)).to(dev, torch.float32)
+        yT = csd.dist_apply([r], [r.scatter_x(xd)], ex)
+        y = csd.gather_y([r], yT, ag)[0]
+        x2 = csd.gather_x([r], csd.dist_adjoint([r], yT, ex), ag)[0]
+        y1 = cs.cs_operator_apply(A, xd[None])[0]
+        x21 = cs.cs_operator_adjoint(A, y1[None])[0]
+        torch.cuda.synchronize()
+        q.put((rank, float((y - y1).norm() / y1.norm()), float((x2 - x21).norm() / x21.norm())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dist_two_processes_gloo_host_staged(cs):
+    """Two real processes (torch.distributed, gloo, exchange staged through host memory; the
+    ranks' kernels never wait on one another) running the distributed apply / adjoint."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mp_worker, args=(r, 2, port, 1 << 20, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    for rank, ey, ex in res:
+        assert ey <= 1e-6 and ex <= 1e-6, (rank, ey, ex)
