@@ -33,6 +33,7 @@ struct cs_operator {
   int64_t Mr;       // metadata rows (= M for the DCT; frequencies = M / 2 for the DFT)
   uint32_t* full;   // Psi mode: one all-rows instance (stride meta_stride(N, N)), or null
   int device;
+  double2* tw;      // device, owned: the grid tier's twiddle tables (tier_l.cuh l_tw_off)
 };
 
 namespace {
@@ -235,6 +236,7 @@ OpMeta meta_of(const cs_operator* op) {
   m.perm = op->perm;
   m.psi = op->psi;
   m.full = op->full;
+  m.tw = op->tw;
   return m;
 }
 
@@ -710,7 +712,18 @@ static cs_status create_impl(int64_t N, int64_t M, int64_t batch, const uint32_t
   if (herr & 1) return fail(CS_ERR_INVALID_ARG, "rows must be strictly increasing and in [0, N)");
   if (herr & 2) return fail(CS_ERR_INVALID_ARG, "perm must be a permutation of [0, N)");
   if (herr & 4) return fail(CS_ERR_INVALID_ARG, "frequencies must be in [1, N/2 - 1]");
+  // the grid tier's twiddle tables, once per operator (small: ~2K complex fp64)
+  double2* tw = nullptr;
+  {
+    const TwOff o = l_tw_off(N);
+    CS_CUDA(cudaMalloc(&tw, (size_t)o.n * sizeof(double2)));
+    k_l_tw_tables<<<(unsigned)((o.n + 255) / 256), 256, 0, st>>>(N, tw);
+    CS_LAUNCHED();
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { cudaFree(tw); return cuda_fail(e, "twiddle tables"); }
+  }
   cs_operator* op = new cs_operator;
+  op->tw = tw;
   op->N = N;
   op->M = fkind == 1 ? 2 * M : M;
   op->Mr = M;
@@ -773,6 +786,13 @@ cs_status cs_operator_create_ex(int64_t N, int64_t M, int64_t batch, const uint3
 }
 
 cs_status cs_operator_destroy(cs_operator* op) {
+  if (op && op->tw) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(op->device);
+    cudaFree(op->tw);
+    cudaSetDevice(cur);
+  }
   delete op;
   return CS_OK;
 }

@@ -83,13 +83,18 @@ template <typename T> struct GTw {
   }
 };
 CS_HD int64_t gtw_entries(int64_t range) { return 512 + (range >> 16) + 1; }
+// entry i of a three-level table of W_den (fp64)
+CS_DEV double2 gtw_value(int64_t i, int64_t den) {
+  const int64_t m = i < 256 ? i : (i < 512 ? (i - 256) << 8 : (i - 512) << 16);
+  double s, c;
+  sincospi(-2.0 * (double)(m & (den - 1)) / (double)den, &s, &c);
+  return make_double2(c, s);
+}
 template <typename T> CS_DEV void gtw_init(C2<T>* t, int64_t den, int64_t range, int tid, int nthr) {
   const int64_t n = gtw_entries(range);
   for (int64_t i = tid; i < n; i += nthr) {
-    const int64_t m = i < 256 ? i : (i < 512 ? (i - 256) << 8 : (i - 512) << 16);
-    double s, c;
-    sincospi(-2.0 * (double)(m & (den - 1)) / (double)den, &s, &c);
-    t[i] = mk<T>((T)c, (T)s);
+    const double2 v = gtw_value(i, den);
+    t[i] = mk<T>((T)v.x, (T)v.y);
   }
 }
 

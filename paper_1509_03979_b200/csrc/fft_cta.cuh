@@ -48,13 +48,17 @@ template <typename T> struct TwTable {
 };
 
 // Fill lo[64], hi[nhi] with W_den^i = exp(-2 pi i * i / den).
+CS_DEV double2 tw_value(int i, int64_t den) {   // entry i of lo[64] | hi[] (fp64)
+  int64_t m = (i < 64) ? i : (int64_t)(i - 64) * 64;
+  double s, c;
+  sincospi(-2.0 * (double)(m % den) / (double)den, &s, &c);
+  return make_double2(c, s);
+}
 template <typename T>
 CS_DEV void tw_init(C2<T>* lo, C2<T>* hi, int64_t den, int nhi, int tid, int nthr) {
   for (int i = tid; i < 64 + nhi; i += nthr) {
-    int64_t m = (i < 64) ? i : (int64_t)(i - 64) * 64;
-    double s, c;
-    sincospi(-2.0 * (double)(m % den) / (double)den, &s, &c);
-    C2<T> w = mk<T>((T)c, (T)s);
+    const double2 v = tw_value(i, den);
+    C2<T> w = mk<T>((T)v.x, (T)v.y);
     if (i < 64) lo[i] = w; else hi[i - 64] = w;
   }
 }

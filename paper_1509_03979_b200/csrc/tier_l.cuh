@@ -4,7 +4,10 @@
 #pragma once
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "ctx_grid.cuh"
 #include "pursuit.cuh"
@@ -20,10 +23,16 @@ struct LGeom {
   int CT, shF, sh4;
 };
 
+// ceil(log2 v) (v >= 1); on the device a count-leading-zeros, not a loop: every block of a
+// grid-tier launch evaluates the geometry at entry
 CS_HD int ilog2(int64_t v) {
+#ifdef __CUDA_ARCH__
+  return v <= 1 ? 0 : 64 - __clzll((unsigned long long)(v - 1));
+#else
   int l = 0;
   while ((int64_t(1) << l) < v) ++l;
   return l;
+#endif
 }
 
 CS_HD LGeom l_geom(int64_t N) {
@@ -135,6 +144,38 @@ template <typename T> struct LArgs {
   int64_t gstride;  // workspace bytes per group (one LLayout)
 };
 
+// The grid tier's shared-memory twiddle tables, precomputed once per operator in fp64
+// (cs_operator_create -> k_l_tw_tables) and converted at block entry: computing them in every
+// block (~1600 fp64 sincospi) made a fixed ~15 us of every launch.
+// Layout: [W_L three-level][W_4N three-level][W_L1 lo 64 | hi n1][W_L2 lo 64 | hi n2].
+struct TwOff {
+  int64_t Q, t1, t2, n;
+  int n1, n2;
+};
+CS_HD TwOff l_tw_off(int64_t N) {
+  const LGeom g = l_geom(N);
+  TwOff o;
+  o.n1 = (int)(g.L1 >= 64 ? g.L1 / 64 : 1);
+  o.n2 = (int)(g.L2 >= 64 ? g.L2 / 64 : 1);
+  o.Q = gtw_entries(g.L);
+  o.t1 = o.Q + gtw_entries(g.N);
+  o.t2 = o.t1 + 64 + o.n1;
+  o.n = o.t2 + 64 + o.n2;
+  return o;
+}
+static __global__ void k_l_tw_tables(int64_t N, double2* out) {   // (one copy per TU: abi.cu launches it)
+  const LGeom g = l_geom(N);
+  const TwOff o = l_tw_off(N);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < o.n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 v;
+    if (i < o.Q) v = gtw_value(i, g.L);
+    else if (i < o.t1) v = gtw_value(i - o.Q, 4 * g.N);
+    else if (i < o.t2) v = tw_value((int)(i - o.t1), g.L1);
+    else v = tw_value((int)(i - o.t2), g.L2);
+    out[i] = v;
+  }
+}
+
 template <typename T>
 CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   GridCtx<T> c;
@@ -196,14 +237,29 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.msm = reinterpret_cast<uint32_t*>(take(4 * ((2 * g.L2) / 32) * 4));
   C2<T>* tF = reinterpret_cast<C2<T>*>(take(gtw_entries(g.L) * cs2));
   C2<T>* tQ = reinterpret_cast<C2<T>*>(take(gtw_entries(g.N) * cs2));
-  gtw_init<T>(tF, g.L, g.L, threadIdx.x, blockDim.x);
-  gtw_init<T>(tQ, 4 * g.N, g.N, threadIdx.x, blockDim.x);
+  if (a.meta.tw) {
+    const double2* src = a.meta.tw;
+    const TwOff o = l_tw_off(g.N);
+    for (int i = threadIdx.x; i < (int)o.n; i += blockDim.x) {
+      const double2 v = src[i];
+      const C2<T> w = mk<T>((T)v.x, (T)v.y);
+      if (i < o.Q) tF[i] = w;
+      else if (i < o.t1) tQ[i - o.Q] = w;
+      else if (i < o.t1 + 64) t1lo[i - o.t1] = w;
+      else if (i < o.t2) t1hi[i - o.t1 - 64] = w;
+      else if (i < o.t2 + 64) t2lo[i - o.t2] = w;
+      else t2hi[i - o.t2 - 64] = w;
+    }
+  } else {
+    gtw_init<T>(tF, g.L, g.L, threadIdx.x, blockDim.x);
+    gtw_init<T>(tQ, 4 * g.N, g.N, threadIdx.x, blockDim.x);
+    tw_init<T>(t1lo, t1hi, g.L1, n1, threadIdx.x, blockDim.x);
+    tw_init<T>(t2lo, t2hi, g.L2, n2, threadIdx.x, blockDim.x);
+  }
   c.twF.t = shp(tF);
   c.twF.mask = g.L - 1;
   c.tw4.t = shp(tQ);
   c.tw4.mask = g.N - 1;
-  tw_init<T>(t1lo, t1hi, g.L1, n1, threadIdx.x, blockDim.x);
-  tw_init<T>(t2lo, t2hi, g.L2, n2, threadIdx.x, blockDim.x);
   c.tw1.lo = t1lo; c.tw1.hi = t1hi;
   c.tw2.lo = t2lo; c.tw2.hi = t2hi;
   c.bank = 0;
@@ -415,6 +471,26 @@ template <typename T> struct DistArgs {
   const T* in;
   T* out;
 };
+// sigma applied to the four reals at Makhoul positions p0 .. p0 + 3 (p0 = 0 mod 4): natural
+// indices 2 p0 + 2 i below N / 2, 2 N - 1 - 2 p0 - 2 i above; one sign word either way
+CS_DEV float4 sign4(const uint32_t* sg, int64_t p0, int64_t N, float4 v) {
+  uint32_t w;
+  if (2 * p0 < N) {
+    const int64_t j = 2 * p0;
+    w = sg[j >> 5] >> (j & 31);
+    w = (w & 1u) | ((w >> 1) & 2u) | ((w >> 2) & 4u) | ((w >> 3) & 8u);
+  } else {
+    const int64_t j = 2 * N - 1 - 2 * p0;   // = 7 mod 8: bits j, j - 2, j - 4, j - 6
+    w = sg[j >> 5] >> ((j & 31) - 6);
+    w = ((w >> 6) & 1u) | ((w >> 3) & 2u) | (w & 4u) | ((w << 3) & 8u);
+  }
+  v.x = (w & 1u) ? -v.x : v.x;
+  v.y = (w & 2u) ? -v.y : v.y;
+  v.z = (w & 4u) ? -v.z : v.z;
+  v.w = (w & 8u) ? -v.w : v.w;
+  return v;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(TL_THREADS, 2) k_l_dist(LArgs<T> a, DistArgs<T> d) {
   extern __shared__ __align__(16) char smem[];
@@ -430,9 +506,13 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_dist(LArgs<T> a, DistArgs<T
   // xc[q] <-> p = 2 (k1 L2 + c0) + (q - 2 nc k1), k1 = q / (2 nc)
   const int64_t l2 = c.L2, ct = c.CT, c0 = d.t_lo * ct, nc = (d.t_hi - d.t_lo) * ct;
   const int64_t nxc = 2 * c.L1 * nc;
+  // (q < N <= 2^25: 32-bit quotients; a shift when the range is a power of two, as the
+  // equal splits of a power-of-two tile count are)
+  const uint32_t rw = (uint32_t)(2 * nc);
+  const int rsh = (rw & (rw - 1)) ? -1 : __ffs(rw) - 1;
   auto pos_of = [=](int64_t q) {
-    const int64_t k1 = q / (2 * nc);
-    return 2 * (k1 * l2 + c0) + (q - 2 * nc * k1);
+    const int64_t k1 = rsh >= 0 ? (q >> rsh) : (int64_t)((uint32_t)q / rw);
+    return 2 * (k1 * l2 + c0) + (q - (int64_t)rw * k1);
   };
   const uint32_t* sg = c.sign;
   if (d.phase == DP_A) {
@@ -440,35 +520,50 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_dist(LArgs<T> a, DistArgs<T
     // columns of Wk
     const T* x = d.in;
     T* U = c.U;
-    gstaged<TL_UNR, T>(nxc, c.gtid, c.gnthr, [&](int64_t q) {
-      const int64_t p = pos_of(q);
-      return apply_sign<T>(sg, mk_nat(p, N), x[q]);
-    }, [&](int64_t q, T v) { U[pos_of(q)] = v; });
+    if constexpr (sizeof(T) == 4) {
+      // four reals per unit: q = 4 u is a Makhoul position p0 = 0 mod 4 of one row; the four
+      // natural indices (2 p0 + 2 i, or 2 N - 1 - 2 p0 - 2 i) share one sign word
+      gstaged<TL_UNR, float4>(nxc / 4, c.gtid, c.gnthr, [&](int64_t u) {
+        return *reinterpret_cast<const float4*>(x + 4 * u);
+      }, [&](int64_t u, float4 v) {
+        const int64_t p0 = pos_of(4 * u);
+        *reinterpret_cast<float4*>(U + p0) = sign4(sg, p0, N, v);
+      });
+    } else {
+      gstaged<TL_UNR, T>(nxc, c.gtid, c.gnthr, [&](int64_t q) {
+        const int64_t p = pos_of(q);
+        return apply_sign<T>(sg, mk_nat(p, N), x[q]);
+      }, [&](int64_t q, T v) { U[pos_of(q)] = v; });
+    }
     c.sync();
-    c.passA();
-    c.sync();
+    c.passA();   // (no trailing grid barrier: the kernel boundary orders the phases)
   } else if (d.phase == DP_BF) {
     // this rank's row pairs: row FFTs, DCT split, row select -> its entries of yT (the
     // transposed row order; entries of other ranks' rows are not written)
     c.template passB<MID_FWD>(false, d.out);
-    c.sync();
   } else if (d.phase == DP_BA) {
     // adjoint: this rank's entries of yT -> its row pairs of C_N^T's first half (a
     // zero-input residual pass B: X' = y / s on the selected rows) -> its rows of Wk
     c.y = d.in;
     c.template passB<MID_RES>(true, nullptr);
-    c.sync();
   } else if (d.phase == DP_C) {
     // this rank's inverse column FFTs -> Cb, then xc[q] = sigma_j Cb[p] on its columns
     c.passC();
     c.sync();
     const T* Cb = c.Cb;
     T* x = d.out;
-    gstaged<TL_UNR, T>(nxc, c.gtid, c.gnthr, [&](int64_t q) {
-      const int64_t p = pos_of(q);
-      return apply_sign<T>(sg, mk_nat(p, N), Cb[p]);
-    }, [&](int64_t q, T v) { x[q] = v; });
-    c.sync();
+    if constexpr (sizeof(T) == 4) {
+      gstaged<TL_UNR, float4>(nxc / 4, c.gtid, c.gnthr, [&](int64_t u) {
+        return *reinterpret_cast<const float4*>(Cb + pos_of(4 * u));
+      }, [&](int64_t u, float4 v) {
+        *reinterpret_cast<float4*>(x + 4 * u) = sign4(sg, pos_of(4 * u), N, v);
+      });
+    } else {
+      gstaged<TL_UNR, T>(nxc, c.gtid, c.gnthr, [&](int64_t q) {
+        const int64_t p = pos_of(q);
+        return apply_sign<T>(sg, mk_nat(p, N), Cb[p]);
+      }, [&](int64_t q, T v) { x[q] = v; });
+    }
   } else if (d.phase == DP_P || d.phase == DP_YT) {
     // yT (complete) <-> y in row order
     const int32_t* tp = c.tperm;
@@ -480,14 +575,12 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_dist(LArgs<T> a, DistArgs<T
     else
       gstaged<TL_UNR, T>(c.M, c.gtid, c.gnthr, [&](int64_t t) { return in[tp[t]]; },
                          [&](int64_t t, T v) { out[t] = v; });
-    c.sync();
   } else if (d.phase == DP_XS) {
     // natural x -> this rank's xc (no sign: DP_A applies it)
     const T* x = d.in;
     T* xc = d.out;
     gstaged<TL_UNR, T>(nxc, c.gtid, c.gnthr, [&](int64_t q) { return x[mk_nat(pos_of(q), N)]; },
                        [&](int64_t q, T v) { xc[q] = v; });
-    c.sync();
   } else {
     // DP_XG: the xc of every rank ([G][nxc], rank g owning columns [g nc, (g + 1) nc)) ->
     // natural x
@@ -496,10 +589,10 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_dist(LArgs<T> a, DistArgs<T
     const int lg2 = c.log2L2;
     gstaged<TL_UNR, T>(N, c.gtid, c.gnthr, [&](int64_t j) {
       const int64_t p = mk_pos(j, N), ci = p >> 1;
-      const int64_t k1 = ci >> lg2, col = ci & (l2 - 1), g = col / nc;
+      const int64_t k1 = ci >> lg2, col = ci & (l2 - 1);
+      const int64_t g = rsh >= 0 ? (col >> (rsh - 1)) : (int64_t)((uint32_t)col / (uint32_t)nc);
       return in[g * nxc + 2 * (k1 * nc + col - g * nc) + (p & 1)];
     }, [&](int64_t j, T v) { x[j] = v; });
-    c.sync();
   }
 }
 
@@ -561,14 +654,28 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_barrier_bench(GridBar* gb, dou
 }
 
 // ------------------------------------------------------------ host side ----
+// the co-resident grid of a cooperative kernel, with its shared-memory attributes set once
+// per (device, kernel, size): these driver calls cost tens of microseconds of host time,
+// comparable to a whole distributed phase
 template <typename T> inline int l_maxgrid(const void* fn, int64_t smem) {
-  int dev = 0, nsm = 0, occ = 0;
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int64_t>, int> cache;
+  int dev = 0;
   cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, fn, smem);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  int nsm = 0, occ = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TL_THREADS, (size_t)smem);
   if (occ < 1) occ = 1;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = nsm * occ;
   return nsm * occ;
 }
 

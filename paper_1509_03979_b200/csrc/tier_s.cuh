@@ -4,7 +4,10 @@
 // N = 16384), and for batched operator apply / adjoint at those sizes.
 #pragma once
 #include <atomic>
+#include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 
 #include "ctx_cta.cuh"
 #include "layout_s.cuh"
@@ -15,7 +18,9 @@ namespace cs {
 constexpr int64_t TIER_S_MAX_N = 16384;
 constexpr int TS_THREADS = SW_NT;  // 512: <= 16 points per thread per FFT pass
 
-CS_HD int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+CS_HD int64_t align_up(int64_t x, int64_t a) {
+  return (a & (a - 1)) ? (x + a - 1) / a * a : (x + a - 1) & -a;   // a power of two: no division
+}
 
 // Shared-memory layout of a Tier S block (computed identically on host and device).
 struct SLayout {
@@ -74,6 +79,7 @@ struct OpMeta {
   int psi;              // dictionary: 0 = I, 1 = C_N (R35)
   int fkind;            // F: 0 = DCT-II, 1 = partial Fourier (R36; perm then holds the position map)
   const uint32_t* full; // Psi mode: the all-rows instance (stride meta_stride(N, N)), or null
+  const double2* tw;    // the grid tier's twiddle tables, precomputed (tier_l.cuh l_tw_off), or null
   CS_HD const uint32_t* sign(int64_t b) const { return base + b * stride; }
   CS_HD const uint32_t* rmask(int64_t b) const { return base + b * stride + nw; }
   CS_HD const int32_t* prefix(int64_t b) const {
@@ -366,10 +372,22 @@ cs_status s_recover_launch(const SRecArgs<T>& a, int64_t B, cudaStream_t st, std
 
 #ifdef CS_TIER_S_IMPL
 inline cs_status s_attr(const void* fn, int64_t bytes, std::string& err) {
+  // set once per (device, kernel, size): the driver calls cost host microseconds per launch
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int64_t>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, fn, bytes);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(key)) return CS_OK;
+  }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) { err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
+  std::lock_guard<std::mutex> lk(mu);
+  done.insert(key);
   return CS_OK;
 }
 inline cs_status s_launched(std::atomic<uint64_t>& launches, std::string& err) {

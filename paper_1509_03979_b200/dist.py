@@ -123,9 +123,14 @@ class DistPlan:
     def segments(self, rank: int, direction: int, pack: bool):
         """(rows, col0, counts per peer) of the segments `rank` packs (pack=True) or unpacks.
         direction 0: after pass A, columns -> row pairs; 1: after pass B, row pairs -> columns.
-        Segments are ordered by peer, so counts[p] consecutive segments go to / come from p."""
+        Segments are ordered by peer, so counts[p] consecutive segments go to / come from p
+        (none to / from the rank itself: that block never leaves its workspace)."""
         rows, col0, counts = [], [], []
         for p in range(self.world):
+            if p == rank:
+                # this rank's own rows x own columns are already in place in its workspace
+                counts.append(0)
+                continue
             if direction == 0:
                 # pack at the column owner `rank` for row owner p; unpack at row owner `rank` from p
                 rs, c = (self.rows[p], self.cols[rank][0]) if pack else (self.rows[rank], self.cols[p][0])
