@@ -176,6 +176,32 @@ static __global__ void k_l_tw_tables(int64_t N, double2* out) {   // (one copy p
   }
 }
 
+// the block's twiddle tables: converted from the operator's precomputed fp64 copy, or computed
+// (kept out of line: the kernel bodies that inline the context set-up are sensitive to their
+// instruction layout)
+template <typename T>
+CS_NOINL CS_DEV void tl_tables(const double2* src, const LGeom& g, C2<T>* tF, C2<T>* tQ, C2<T>* t1lo, C2<T>* t1hi,
+                               C2<T>* t2lo, C2<T>* t2hi, int n1, int n2) {
+  if (src) {
+    const TwOff o = l_tw_off(g.N);
+    for (int i = threadIdx.x; i < (int)o.n; i += blockDim.x) {
+      const double2 v = src[i];
+      const C2<T> w = mk<T>((T)v.x, (T)v.y);
+      if (i < o.Q) tF[i] = w;
+      else if (i < o.t1) tQ[i - o.Q] = w;
+      else if (i < o.t1 + 64) t1lo[i - o.t1] = w;
+      else if (i < o.t2) t1hi[i - o.t1 - 64] = w;
+      else if (i < o.t2 + 64) t2lo[i - o.t2] = w;
+      else t2hi[i - o.t2 - 64] = w;
+    }
+  } else {
+    gtw_init<T>(tF, g.L, g.L, threadIdx.x, blockDim.x);
+    gtw_init<T>(tQ, 4 * g.N, g.N, threadIdx.x, blockDim.x);
+    tw_init<T>(t1lo, t1hi, g.L1, n1, threadIdx.x, blockDim.x);
+    tw_init<T>(t2lo, t2hi, g.L2, n2, threadIdx.x, blockDim.x);
+  }
+}
+
 template <typename T>
 CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   GridCtx<T> c;
@@ -237,25 +263,7 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.msm = reinterpret_cast<uint32_t*>(take(4 * ((2 * g.L2) / 32) * 4));
   C2<T>* tF = reinterpret_cast<C2<T>*>(take(gtw_entries(g.L) * cs2));
   C2<T>* tQ = reinterpret_cast<C2<T>*>(take(gtw_entries(g.N) * cs2));
-  if (a.meta.tw) {
-    const double2* src = a.meta.tw;
-    const TwOff o = l_tw_off(g.N);
-    for (int i = threadIdx.x; i < (int)o.n; i += blockDim.x) {
-      const double2 v = src[i];
-      const C2<T> w = mk<T>((T)v.x, (T)v.y);
-      if (i < o.Q) tF[i] = w;
-      else if (i < o.t1) tQ[i - o.Q] = w;
-      else if (i < o.t1 + 64) t1lo[i - o.t1] = w;
-      else if (i < o.t2) t1hi[i - o.t1 - 64] = w;
-      else if (i < o.t2 + 64) t2lo[i - o.t2] = w;
-      else t2hi[i - o.t2 - 64] = w;
-    }
-  } else {
-    gtw_init<T>(tF, g.L, g.L, threadIdx.x, blockDim.x);
-    gtw_init<T>(tQ, 4 * g.N, g.N, threadIdx.x, blockDim.x);
-    tw_init<T>(t1lo, t1hi, g.L1, n1, threadIdx.x, blockDim.x);
-    tw_init<T>(t2lo, t2hi, g.L2, n2, threadIdx.x, blockDim.x);
-  }
+  tl_tables<T>(a.meta.tw, g, tF, tQ, t1lo, t1hi, t2lo, t2hi, n1, n2);
   c.twF.t = shp(tF);
   c.twF.mask = g.L - 1;
   c.tw4.t = shp(tQ);
@@ -654,28 +662,31 @@ __global__ void __launch_bounds__(TL_THREADS) k_l_barrier_bench(GridBar* gb, dou
 }
 
 // ------------------------------------------------------------ host side ----
-// the co-resident grid of a cooperative kernel, with its shared-memory attributes set once
-// per (device, kernel, size): these driver calls cost tens of microseconds of host time,
-// comparable to a whole distributed phase
+// the co-resident grid of a cooperative kernel.  The driver calls cost tens of microseconds
+// of host time, comparable to a whole distributed phase, so the grid is cached
+// per (device, kernel, size) and the kernel's dynamic shared-memory limit only ever grows (a
+// later, smaller launch must not leave the limit below an earlier, larger one).
 template <typename T> inline int l_maxgrid(const void* fn, int64_t smem) {
   static std::mutex mu;
-  static std::map<std::tuple<int, const void*, int64_t>, int> cache;
+  static std::map<std::tuple<int, const void*, int64_t>, int> grids;
+  static std::map<std::pair<int, const void*>, int64_t> limit;
   int dev = 0;
   cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
   const auto key = std::make_tuple(dev, fn, smem);
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
+  auto it = grids.find(key);
+  if (it != grids.end()) return it->second;
+  int64_t& lim = limit[std::make_pair(dev, fn)];
+  if (smem > lim) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    lim = smem;
   }
   int nsm = 0, occ = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TL_THREADS, (size_t)smem);
   if (occ < 1) occ = 1;
-  std::lock_guard<std::mutex> lk(mu);
-  cache[key] = nsm * occ;
+  grids[key] = nsm * occ;
   return nsm * occ;
 }
 

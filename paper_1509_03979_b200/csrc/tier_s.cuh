@@ -4,10 +4,10 @@
 // N = 16384), and for batched operator apply / adjoint at those sizes.
 #pragma once
 #include <atomic>
+#include <map>
 #include <mutex>
-#include <set>
 #include <string>
-#include <tuple>
+#include <utility>
 
 #include "ctx_cta.cuh"
 #include "layout_s.cuh"
@@ -372,22 +372,20 @@ cs_status s_recover_launch(const SRecArgs<T>& a, int64_t B, cudaStream_t st, std
 
 #ifdef CS_TIER_S_IMPL
 inline cs_status s_attr(const void* fn, int64_t bytes, std::string& err) {
-  // set once per (device, kernel, size): the driver calls cost host microseconds per launch
+  // the dynamic shared-memory limit of a kernel only ever grows, set when a launch needs more
+  // (the driver calls cost host microseconds per launch)
   static std::mutex mu;
-  static std::set<std::tuple<int, const void*, int64_t>> done;
+  static std::map<std::pair<int, const void*>, int64_t> limit;
   int dev = 0;
   cudaGetDevice(&dev);
-  const auto key = std::make_tuple(dev, fn, bytes);
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    if (done.count(key)) return CS_OK;
-  }
+  std::lock_guard<std::mutex> lk(mu);
+  int64_t& lim = limit[std::make_pair(dev, fn)];
+  if (bytes <= lim) return CS_OK;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) { err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return CS_ERR_CUDA; }
-  std::lock_guard<std::mutex> lk(mu);
-  done.insert(key);
+  lim = bytes;
   return CS_OK;
 }
 inline cs_status s_launched(std::atomic<uint64_t>& launches, std::string& err) {
