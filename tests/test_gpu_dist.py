@@ -154,3 +154,48 @@ def test_dist_two_processes_gloo_host_staged(cs):
         assert pr.exitcode == 0
     for rank, ey, ex in res:
         assert ey <= 1e-6 and ex <= 1e-6, (rank, ey, ex)
+
+
+def test_dist_phase_argument_errors(cs):
+    """include/cs.h cs_dist_*: CS_ERR_INVALID_ARG for ranges out of bounds / missing buffers,
+    CS_ERR_UNSUPPORTED for an operator the distributed path does not cover."""
+    import ctypes
+    from paper_1509_03979_b200 import dist as csd
+    dev = torch.device("cuda:0")
+    N, M = 1 << 16, 1 << 14
+    cfg = cs_inputs.Config(97, "sp", N, M, 16, "gauss", 0.0)
+    p = cs_inputs.make_problem(cfg, b=0)
+    bits, rows = to_dev([p], dev)
+    A = cs.Operator(N, M, bits, rows)
+    lib = cs.load_library()
+    plan = csd.dist_plan(N, 2)
+    r = csd.DistOperator(A, plan, 0)
+    P = ctypes.c_void_p
+    ntiles = plan.L2 // plan.CT
+    buf = torch.empty(N, device=dev)
+    st = P(torch.cuda.current_stream().cuda_stream)
+    ws, nb = P(r.ws.data_ptr()), r.ws.numel()
+    INVALID, UNSUPPORTED = 1, 2
+    bad = [
+        (csd.DP_A, 0, ntiles + 1, 0, 1, buf, None),            # tile range past the end
+        (csd.DP_A, 2, 1, 0, 1, buf, None),                     # t_hi < t_lo
+        (csd.DP_BF, 0, 1, 0, plan.L1 // 2 + 2, None, buf),     # item range past the end
+        (csd.DP_A, 0, 1, 0, 1, None, None),                    # missing input
+        (csd.DP_C, 0, 1, 0, 1, None, None),                    # missing output
+        (csd.DP_XG, 0, 3, 0, 1, buf, buf),                     # uneven split for the gather
+        (csd.DP_XS, 0, 0, 0, 1, buf, buf),                     # empty column range
+        (99, 0, 1, 0, 1, buf, buf),                            # unknown phase
+    ]
+    for ph, t0, t1, i0, i1, a, b in bad:
+        rc = lib.cs_dist_phase(A.handle, ph, t0, t1, i0, i1, P(a.data_ptr()) if a is not None else None,
+                               P(b.data_ptr()) if b is not None else None, ws, nb, st)
+        assert rc == INVALID, (ph, t0, t1, i0, i1, rc)
+    rc = lib.cs_dist_phase(A.handle, csd.DP_A, 0, 1, 0, 1, P(buf.data_ptr()), None, ws, 16, st)
+    assert rc != 0                                            # workspace too small
+    small = cs.Operator(4096, 1024, *to_dev([cs_inputs.make_problem(
+        cs_inputs.Config(98, "sp", 4096, 1024, 8, "gauss", 0.0), b=0)], dev))
+    rc = lib.cs_dist_phase(small.handle, csd.DP_A, 0, 1, 0, 1, P(buf.data_ptr()), None, ws, nb, st)
+    assert rc == UNSUPPORTED
+    off = (ctypes.c_int64 * (plan.L1 + 1))()
+    assert lib.cs_dist_row_offsets(small.handle, off) == UNSUPPORTED
+    assert lib.cs_dist_row_offsets(A.handle, off) == 0 and off[plan.L1] == M and list(off) == sorted(off)
