@@ -3,7 +3,6 @@
 // for operator apply / adjoint at those sizes.  See ctx_grid.cuh for the passes.
 #pragma once
 #include <algorithm>
-#include <cstdlib>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -752,13 +751,6 @@ inline cs_status l_launch(const void* fn, LArgs<T>& a, int64_t N, cudaStream_t s
   const int64_t work = std::max<int64_t>(g.L2 / g.CT, g.L1 / 2 + 1);
   const int occ_grid = grid;
   if (work < grid) grid = (int)work;
-  else if (!getenv("CS_TL_NOBAL")) {
-    // above one round: as few blocks as give the same number of rounds (N = 2^24: 1025 row
-    // pairs take 4 rounds on 296 blocks and on 257); fewer blocks arrive at every grid
-    // barrier and reduction sooner
-    const int64_t rounds = (work + grid - 1) / grid;
-    grid = (int)((work + rounds - 1) / rounds);
-  }
   // a batch of instances whose passes need fewer blocks than the GPU holds runs as several
   // groups side by side, each with its own workspace slice and barrier
   a.gblocks = grid;
