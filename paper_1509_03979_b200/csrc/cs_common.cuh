@@ -40,13 +40,75 @@ template <> struct cplx_t<double> { using type = double2; };
 template <typename T> using C2 = typename cplx_t<T>::type;
 
 template <typename T> CS_HD C2<T> mk(T re, T im) { C2<T> r; r.x = re; r.y = im; return r; }
-template <typename T> CS_HD C2<T> cadd(C2<T> a, C2<T> b) { return mk<T>(a.x + b.x, a.y + b.y); }
-template <typename T> CS_HD C2<T> csub(C2<T> a, C2<T> b) { return mk<T>(a.x - b.x, a.y - b.y); }
+// fp32 complex add / subtract as ONE paired instruction (FADD2, PTX add/sub.rn.f32x2 on
+// sm_100a): each lane is the same correctly rounded IEEE add as the scalar form, half the
+// issue slots
+#if defined(__CUDA_ARCH__) && !defined(CS_NO_F32X2)
+CS_DEV unsigned long long f2_bits(float2 v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+CS_DEV float2 bits_f2(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+#endif
+template <typename T> CS_HD C2<T> cadd(C2<T> a, C2<T> b) {
+#if defined(__CUDA_ARCH__) && !defined(CS_NO_F32X2)
+  if constexpr (sizeof(T) == 4) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return bits_f2(r);
+  }
+#endif
+  return mk<T>(a.x + b.x, a.y + b.y);
+}
+template <typename T> CS_HD C2<T> csub(C2<T> a, C2<T> b) {
+#if defined(__CUDA_ARCH__) && !defined(CS_NO_F32X2)
+  if constexpr (sizeof(T) == 4) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return bits_f2(r);
+  }
+#endif
+  return mk<T>(a.x - b.x, a.y - b.y);
+}
+#if defined(__CUDA_ARCH__) && !defined(CS_NO_F32X2)
+CS_DEV unsigned long long f2_mul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+CS_DEV unsigned long long f2_fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+#endif
+// fp32 complex products as FMUL2 + FFMA2: p = (ax bx, ay bx), then (ay, ax) * (-by, by) + p.
+// ptxas folds the swap and the one-lane negation into operand modifiers (LO_HI.NP) and the
+// broadcasts into scalar operands: two paired instructions instead of four
 template <typename T> CS_HD C2<T> cmul(C2<T> a, C2<T> b) {
+#if defined(__CUDA_ARCH__) && !defined(CS_NO_F32X2)
+  if constexpr (sizeof(T) == 4) {
+    const float2 av = a, bv = b;
+    return bits_f2(f2_fma2(f2_bits(make_float2(av.y, av.x)), f2_bits(make_float2(-bv.y, bv.y)),
+                           f2_mul2(f2_bits(av), f2_bits(make_float2(bv.x, bv.x)))));
+  }
+#endif
   return mk<T>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 // a * conj(b)
 template <typename T> CS_HD C2<T> cmulc(C2<T> a, C2<T> b) {
+#if defined(__CUDA_ARCH__) && !defined(CS_NO_F32X2)
+  if constexpr (sizeof(T) == 4) {
+    const float2 av = a, bv = b;
+    return bits_f2(f2_fma2(f2_bits(make_float2(av.y, av.x)), f2_bits(make_float2(bv.y, -bv.y)),
+                           f2_mul2(f2_bits(av), f2_bits(make_float2(bv.x, bv.x)))));
+  }
+#endif
   return mk<T>(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
 template <typename T> CS_HD C2<T> cconj(C2<T> a) { return mk<T>(a.x, -a.y); }

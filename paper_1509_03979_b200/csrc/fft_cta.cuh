@@ -87,7 +87,10 @@ template <typename T, int t32, bool INV> CS_DEV C2<T> tw_apply(C2<T> a) {
     constexpr T h = (T)0.70710678118654752440;
     constexpr T sx = (t32 == 4) ? (T)1 : (T)-1;
     constexpr T sy = INV ? (T)1 : (T)-1;
-    return mk<T>(h * (sx * a.x - sy * a.y), h * (sx * a.y + sy * a.x));
+    if constexpr (sizeof(T) == 4)   // a (h sx + i h sy): one paired multiply + one paired FMA
+      return cmul<T>(a, mk<T>(h * sx, h * sy));
+    else
+      return mk<T>(h * (sx * a.x - sy * a.y), h * (sx * a.y + sy * a.x));
   } else {
     return cmul<T>(a, w32c<T, t32, INV>());
   }
