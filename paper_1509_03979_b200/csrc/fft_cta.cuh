@@ -229,10 +229,16 @@ CS_NOINL void fft_cta_t(C2<T>* buf, const TwTable<T> tw) {
   fft_passes<T, LOG2L, LOG2E, LOG2B, 0, INV>(shp(buf), ts);
 }
 
-// E for a given (L, B) on an NT-thread block: L*B/NT clamped to [2, 32] and <= L
+// At least 4 points per thread: the grid tier's small tiles (N <= 2^16: 512 points on 256
+// threads) otherwise run 7-8 radix-2 passes, each two CTA barriers; radix >= 4 halves the
+// barrier chain (c2: 4.30 -> 4.03 ms; 8 or 16 points per thread measured slower).
+#ifndef CS_FFT_MIN_LOG2E
+#define CS_FFT_MIN_LOG2E 2
+#endif
+// E for a given (L, B) on an NT-thread block: L*B/NT clamped to [4, 32] and <= L
 __host__ __device__ constexpr int fft_log2e(int log2l, int log2b, int log2nt) {
   int e = log2l + log2b - log2nt;
-  if (e < 1) e = 1;
+  if (e < CS_FFT_MIN_LOG2E) e = CS_FFT_MIN_LOG2E;
   if (e > 5) e = 5;
   if (e > log2l) e = log2l;
   return e;
