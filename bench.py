@@ -383,7 +383,12 @@ def run_ours(args):
             key = f"c{cfg.cid}_{args.precision}" + ("" if cfg.alg == cs_inputs.CONFIGS[cfg.cid].alg else f"_{cfg.alg}") \
                 + ("" if cfg.randomizer == "sign" else f"_{cfg.randomizer}") + ("" if cfg.psi == "I" else "_psi") \
                 + ("" if cfg.transform == "dct" else "_dft")
-            roofline["traffic"] = json.load(open(tr)).get(key)
+            ent = json.load(open(tr)).get(key)
+            if ent:
+                # the contract's number (DRAM bytes read + written per launch, one ncu --set
+                # full capture of the same launch), its provenance alongside
+                roofline["traffic"] = ent["dram_bytes_per_launch"]
+                roofline["traffic_source"] = {k: v for k, v in ent.items() if k != "dram_bytes_per_launch"}
         except Exception:
             pass
 
