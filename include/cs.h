@@ -282,7 +282,8 @@ cs_status cs_comm_destroy(void* comm);
  * d_in / d_out: DEVICE fp32 (DP_A, DP_BA: d_in only; DP_BF, DP_C: d_out only).
  * cs_dist_copy moves segments (row rows[k], columns [col0[k], col0[k] + seg_len)) of the
  * intermediate between the workspace and a flat exchange buffer of nseg seg_len complex fp32
- * values (to_buf 1: pack, 0: unpack).  d_ws: DEVICE workspace of cs_dist_ws_bytes(N, M) bytes,
+ * values (to_buf 1: pack, 0: unpack); d_rows / d_col0 are DEVICE int32 arrays the caller keeps
+ * in range (0 <= rows[k] < L1, 0 <= col0[k] <= L2 - seg_len; not checked on the device).  d_ws: DEVICE workspace of cs_dist_ws_bytes(N, M) bytes,
  * one per rank, kept across the phases of one application.  cs_dist_row_offsets fills
  * h_off[0 .. L1] (HOST) with the yT offset where row k1's entries start (h_off[L1] = M); it
  * synchronizes the device (plan time).  Orchestration and the all-to-alls (torch.distributed /

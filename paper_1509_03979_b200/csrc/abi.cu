@@ -987,6 +987,9 @@ cs_status cs_dist_copy(const cs_operator* op, void* d_ws, const int32_t* d_rows,
   if (cs_status s = dist_check(op)) return s;
   if (!d_ws || (nseg > 0 && (!d_rows || !d_col0 || !d_buf)) || nseg < 0 || seg_len < 0)
     return fail(CS_ERR_INVALID_ARG, "bad arguments");
+  const LGeom g = l_geom(op->N);
+  if (seg_len > g.L2 || nseg > g.L1 * (g.L2 / std::max<int64_t>(seg_len, 1)))
+    return fail(CS_ERR_INVALID_ARG, "segments larger than the intermediate");
   return tier_l_dist_copy<float>(meta_of(op), d_ws, d_rows, d_col0, nseg, seg_len, d_buf, to_buf,
                                  reinterpret_cast<cudaStream_t>(stream), g_launches, g_last_error);
 }
