@@ -194,6 +194,14 @@ CS_NOINL void s_apply_psi(CtaCtx<T>& c, const T* x, T* y, T* G) {
   c.template sandwich<MID_FWD, false>(nullptr, nullptr, y);
 }
 
+// the sign / row-mask / prefix words of instance b (contiguous, 3 nw words) into L2: the
+// per-instance staging in cta_set_instance otherwise waits on HBM latency (ncu: a quarter of
+// the batched apply's stall samples)
+CS_DEV void s_prefetch_meta(const OpMeta& meta, int64_t b) {
+  const uint32_t bytes = (uint32_t)(3 * meta.nw * 4);
+  if (bytes >= 16 && bytes % 16 == 0) prefetch_l2(meta.sign(b), bytes);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(TS_THREADS, sizeof(T) == 4 ? 2 : 1) k_s_apply(OpMeta meta, SLayout lay, const T* __restrict__ X,
                                                  T* __restrict__ Y, T* __restrict__ Gws, int64_t B) {
@@ -208,8 +216,10 @@ __global__ void __launch_bounds__(TS_THREADS, sizeof(T) == 4 ? 2 : 1) k_s_apply(
     cta_set_instance<T>(c, smem, meta, b);
   }
   const T* x = X + b * N;
-  if (threadIdx.x == 0 && b + gridDim.x < B)
+  if (threadIdx.x == 0 && b + gridDim.x < B) {
     prefetch_l2(X + (b + gridDim.x) * N, (uint32_t)(N * sizeof(T)));   // the next instance's x
+    s_prefetch_meta(meta, b + gridDim.x);                                // and its metadata
+  }
   if (c.psi) {
     s_apply_psi<T>(c, x, Y + b * c.M, Gws + b * N);
     continue;
@@ -272,6 +282,7 @@ __global__ void __launch_bounds__(TS_THREADS, sizeof(T) == 4 ? 2 : 1) k_s_adjoin
     c.y = Yin + b * c.M;
     if (threadIdx.x == 0 && b + gridDim.x < B && ((c.M * sizeof(T)) & 15) == 0)
       prefetch_l2(Yin + (b + gridDim.x) * c.M, (uint32_t)(c.M * sizeof(T)));   // the next instance's y
+      s_prefetch_meta(meta, b + gridDim.x);
     if (c.psi) c.G = Gws + b * c.N;
     c.RES(nullptr);  // A^T y (x = 0)
     T* x = X + b * N;
