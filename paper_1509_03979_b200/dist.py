@@ -264,6 +264,49 @@ def dist_adjoint(ranks, yTs, exchange):
     return out
 
 
+class DistGraphs:
+    """One rank's application halves captured as CUDA graphs over static buffers: `pre`
+    (apply: xc -> DP_A -> pack; adjoint: yT -> DP_BA -> pack) and `post` (unpack -> DP_BF or
+    DP_C), with the exchange left between them (NCCL or host-staged, the caller's choice).
+    Replaying removes the host cost of the ctypes calls (~17 us per phase).
+    Usage: g.x[:] = xc; g.pre_apply.replay(); recv = exchange(g.send(0)); g.recv_buf(0)[:] = recv;
+    g.post_apply.replay(); yT = g.yT (and the same with _adjoint / g.y_in / g.xc_out)."""
+
+    def __init__(self, r: DistOperator):
+        import torch
+        self.r = r
+        dev = r.ws.device
+        self.x = torch.zeros(r.nxc, dtype=torch.float32, device=dev)
+        self.y_in = torch.zeros(r.op.M, dtype=torch.float32, device=dev)
+        self.yT = torch.zeros(r.op.M, dtype=torch.float32, device=dev)
+        self.xc_out = torch.zeros(r.nxc, dtype=torch.float32, device=dev)
+        self.sbuf = [torch.empty(sum(r.seg[(d, True)][2]), dtype=torch.float32, device=dev) for d in (0, 1)]
+        self.rbuf = [torch.empty(sum(r.seg[(d, False)][2]), dtype=torch.float32, device=dev) for d in (0, 1)]
+        steps = {
+            "pre_apply": lambda: (r.phase(DP_A, inp=self.x), r.copy(0, True, self.sbuf[0])),
+            "post_apply": lambda: (r.copy(0, False, self.rbuf[0]), r.phase(DP_BF, out=self.yT)),
+            "pre_adjoint": lambda: (r.phase(DP_BA, inp=self.y_in), r.copy(1, True, self.sbuf[1])),
+            "post_adjoint": lambda: (r.copy(1, False, self.rbuf[1]), r.phase(DP_C, out=self.xc_out)),
+        }
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        for name, fn in steps.items():
+            with torch.cuda.stream(side):
+                fn()                       # warm-up outside capture (attributes, caches)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                fn()
+            setattr(self, name, g)
+        torch.cuda.current_stream(dev).wait_stream(side)
+
+    def send(self, direction: int):
+        r = self.r
+        return self.sbuf[direction], r.seg[(direction, True)][2], r.seg[(direction, False)][2]
+
+    def recv_buf(self, direction: int):
+        return self.rbuf[direction]
+
+
 def gather_x(ranks, xcs, allgather):
     """The natural x [N] on every rank from the xc of all ranks (allgather(list) -> for each
     local rank the concatenation of every rank's tensor in rank order; equal sizes)."""

@@ -199,3 +199,43 @@ def test_dist_phase_argument_errors(cs):
     off = (ctypes.c_int64 * (plan.L1 + 1))()
     assert lib.cs_dist_row_offsets(small.handle, off) == UNSUPPORTED
     assert lib.cs_dist_row_offsets(A.handle, off) == 0 and off[plan.L1] == M and list(off) == sorted(off)
+
+
+def test_dist_graphs_match_eager(cs):
+    """DistGraphs (each rank's halves captured as CUDA graphs, the exchange between them)
+    gives the same y = A x and x = A^T y as the eager calls, bit for bit."""
+    from paper_1509_03979_b200 import dist as csd
+    dev = torch.device("cuda:0")
+    N, M, G = 1 << 20, 1 << 18, 4
+    cfg = cs_inputs.Config(96, "sp", N, M, 64, "gauss", 0.0)
+    p = cs_inputs.make_problem(cfg, b=0)
+    bits, rows = to_dev([p], dev)
+    A = cs.Operator(N, M, bits, rows)
+    plan = csd.dist_plan(N, G)
+    ranks = [csd.DistOperator(A, plan, r) for r in range(G)]
+    graphs = [csd.DistGraphs(r) for r in ranks]
+    g = torch.Generator(device="cpu").manual_seed(5)
+    x = torch.randn(N, generator=g).to(dev)
+    w = torch.randn(M, generator=g).to(dev)
+    ex, ag = csd.emulated_exchange, csd.emulated_allgather
+    y_ref = csd.gather_y(ranks, csd.dist_apply(ranks, [r.scatter_x(x) for r in ranks], ex), ag)[0]
+    xa_ref = csd.gather_x(ranks, csd.dist_adjoint(ranks, [r.scatter_y(w) for r in ranks], ex), ag)[0]
+    for _ in range(2):                       # replays are repeatable
+        for r, gr in zip(ranks, graphs):
+            gr.x.copy_(r.scatter_x(x))
+            gr.pre_apply.replay()
+        recvs = ex([gr.send(0) for gr in graphs])
+        for gr, buf in zip(graphs, recvs):
+            gr.recv_buf(0).copy_(buf)
+            gr.post_apply.replay()
+        y = csd.gather_y(ranks, [gr.yT for gr in graphs], ag)[0]
+        for r, gr in zip(ranks, graphs):
+            gr.y_in.copy_(r.scatter_y(w))
+            gr.pre_adjoint.replay()
+        recvs = ex([gr.send(1) for gr in graphs])
+        for gr, buf in zip(graphs, recvs):
+            gr.recv_buf(1).copy_(buf)
+            gr.post_adjoint.replay()
+        xa = csd.gather_x(ranks, [gr.xc_out for gr in graphs], ag)[0]
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_ref) and torch.equal(xa, xa_ref)

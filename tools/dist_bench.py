@@ -103,9 +103,27 @@ for e in [int(a) for a in (sys.argv[1:] or ["22", "24", "25", "26"])]:
                 tt[it, k] = (a.elapsed_time(b) + c.elapsed_time(d)) * 1e3
         wa = float(np.max(np.median(ta, axis=0)))
         wt = float(np.max(np.median(tt, axis=0)))
+        # the same per-rank halves replayed from CUDA graphs (dist.DistGraphs)
+        graphs = [csd.DistGraphs(r) for r in ranks]
+        ga = np.zeros((REPS, G)); gt = np.zeros((REPS, G))
+        for it in range(REPS):
+            for k, gr in enumerate(graphs):
+                e = [ev() for _ in range(4)]
+                e[0].record(); gr.pre_apply.replay(); e[1].record()
+                e[2].record(); gr.post_apply.replay(); e[3].record()
+                f = [ev() for _ in range(4)]
+                f[0].record(); gr.pre_adjoint.replay(); f[1].record()
+                f[2].record(); gr.post_adjoint.replay(); f[3].record()
+                torch.cuda.synchronize()
+                ga[it, k] = (e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3])) * 1e3
+                gt[it, k] = (f[0].elapsed_time(f[1]) + f[2].elapsed_time(f[3])) * 1e3
+        gwa = float(np.max(np.median(ga, axis=0)))
+        gwt = float(np.max(np.median(gt, axis=0)))
+        del graphs
         nv = sent / 900e9 * 1e6
         row = dict(N=N, G=G, single_apply_us=round(med(t1a), 1), single_adjoint_us=round(med(t1t), 1),
-                   rank_apply_us=round(wa, 1), rank_adjoint_us=round(wt, 1), a2a_bytes_per_rank=int(sent),
+                   rank_apply_us=round(wa, 1), rank_adjoint_us=round(wt, 1),
+                   rank_apply_graph_us=round(gwa, 1), rank_adjoint_graph_us=round(gwt, 1), a2a_bytes_per_rank=int(sent),
                    a2a_nvlink_us=round(nv, 1),
                    rank0_apply_A_pack_unpack_BF_us=[round(float(v), 1) for v in np.median(pa, axis=0)])
         rows_out.append(row)
