@@ -426,6 +426,28 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_adjoint(LArgs<T> a) {
     const uint32_t* sg = c.sign;
     const T* Cb = c.Cb;
     const int32_t* pv = c.pinv;
+    if constexpr (sizeof(T) == 4) {
+      if (!pv) {
+        // four consecutive j per unit, the mirror of k_l_apply's scatter: x[4q], x[4q+2] from
+        // Cb[2q, 2q+1] and x[4q+3], x[4q+1] from Cb[N-2-2q, N-1-2q] (two 8-byte loads, one
+        // 16-byte store), sign applied from one word
+        gstaged<TL_UNR, float4>(N / 4, c.gtid, c.gnthr, [&](int64_t q) {
+          const float2 lo = *reinterpret_cast<const float2*>(Cb + 2 * q);
+          const float2 hi = *reinterpret_cast<const float2*>(Cb + N - 2 - 2 * q);
+          return make_float4(lo.x, hi.y, lo.y, hi.x);
+        }, [&](int64_t q, float4 v) {
+          const int64_t j = 4 * q;
+          const uint32_t w = sg[j >> 5] >> (j & 31);
+          v.x = (w & 1u) ? -v.x : v.x;
+          v.y = (w & 2u) ? -v.y : v.y;
+          v.z = (w & 4u) ? -v.z : v.z;
+          v.w = (w & 8u) ? -v.w : v.w;
+          *reinterpret_cast<float4*>(x + j) = v;
+        });
+        c.sync();
+        continue;
+      }
+    }
     gstaged<TL_UNR, T>(N, c.gtid, c.gnthr,
                        [&](int64_t j) { return apply_sign<T>(sg, j, Cb[GridCtx<T>::ppos(pv, j, N)]); },
                        [&](int64_t j, T v) { x[j] = v; });
