@@ -223,6 +223,32 @@ CS_DEV void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* out
     // grid: materialise the keys once in natural index order (the dense input buffer U
     // is free during a recovery), so the radix passes read them contiguously
     Key* keys = reinterpret_cast<Key*>(ctx.U);
+    if constexpr (sizeof(T) == 4) {
+      if (!cv.pinv && N % 4 == 0) {
+        // four consecutive j per unit from two 8-byte loads of the Makhoul-ordered buffer
+        // (x[4q], x[4q+2] at positions 2q, 2q+1; x[4q+3], x[4q+1] at N-2-2q, N-1-2q), one
+        // exclusion word, one 16-byte key store — the scalar gather ran at a fraction of
+        // the bandwidth (as the adjoint's, tier_l.cuh k_l_adjoint)
+        const T* z = cv.z;
+        gstaged<TL_UNR, uint4>(N / 4, ctx.gtid, ctx.gnthr, [&](int64_t q) {
+          const float2 lo = *reinterpret_cast<const float2*>(z + 2 * q);
+          const float2 hi = *reinterpret_cast<const float2*>(z + N - 2 - 2 * q);
+          uint4 k = make_uint4(full_key(lo.x), full_key(hi.y), full_key(lo.y), full_key(hi.x));
+          if (excl) {
+            const int64_t j = 4 * q;
+            const uint32_t w = excl[j >> 5] >> (j & 31);
+            if (w & 1u) k.x = 0u;
+            if (w & 2u) k.y = 0u;
+            if (w & 4u) k.z = 0u;
+            if (w & 8u) k.w = 0u;
+          }
+          return k;
+        }, [&](int64_t q, uint4 k) { *reinterpret_cast<uint4*>(keys + 4 * q) = k; });
+        ctx.sync();
+        topk_bits(ctx, N, K, [keys](int64_t j) { return keys[j]; }, out, false);
+        return;
+      }
+    }
     gstaged<TL_UNR, Key>(N, ctx.gtid, ctx.gnthr, [&](int64_t j) {
       return (excl && bit_test(excl, j)) ? Key(0) : full_key(cv.raw(j));
     }, [&](int64_t j, Key k) { keys[j] = k; });
@@ -273,6 +299,28 @@ CS_DEV int64_t detect_argmax(Ctx& ctx, const uint32_t* excl) {
     };
     if (pm) scan(std::true_type{}); else scan(std::false_type{});
     return ctx.argmax(bk, bi);
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (!cv.pinv && N % 4 == 0) {
+      // four consecutive j per unit from two 8-byte loads (as detect_topk's grid keys), in
+      // increasing j per thread so the first maximum is kept (ties -> lower index, R12)
+      const T* z = cv.z;
+      Key bk = 0;
+      int64_t bi = -1;
+      for (int64_t q = ctx.gtid; q < N / 4; q += ctx.gnthr) {
+        const float2 lo = *reinterpret_cast<const float2*>(z + 2 * q);
+        const float2 hi = *reinterpret_cast<const float2*>(z + N - 2 - 2 * q);
+        const int64_t j = 4 * q;
+        const uint32_t w = excl[j >> 5] >> (j & 31);
+        const Key k0 = (w & 1u) ? Key(0) : full_key(lo.x), k1 = (w & 2u) ? Key(0) : full_key(hi.y);
+        const Key k2 = (w & 4u) ? Key(0) : full_key(lo.y), k3 = (w & 8u) ? Key(0) : full_key(hi.x);
+        if (k0 > bk) { bk = k0; bi = j; }
+        if (k1 > bk) { bk = k1; bi = j + 1; }
+        if (k2 > bk) { bk = k2; bi = j + 2; }
+        if (k3 > bk) { bk = k3; bi = j + 3; }
+      }
+      return ctx.argmax(bk, bi);
+    }
   }
   return argmax_key(ctx, N, [cv, excl](int64_t j) {
     if (bit_test(excl, j)) return Key(0);
