@@ -245,7 +245,9 @@ CS_DEV void detect_topk(Ctx& ctx, int64_t K, const uint32_t* excl, uint32_t* out
           return k;
         }, [&](int64_t q, uint4 k) { *reinterpret_cast<uint4*>(keys + 4 * q) = k; });
         ctx.sync();
-        topk_bits(ctx, N, K, [keys](int64_t j) { return keys[j]; }, out, false);
+        const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+        topk_bits(ctx, N, K, [keys](int64_t j) { return keys[j]; }, out, false,
+                  [k4](int64_t q) { return k4[q]; });
         return;
       }
     }

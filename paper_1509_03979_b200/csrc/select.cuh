@@ -10,6 +10,8 @@
 //  * remap       — carry coefficients from one sorted support to another
 //                  (warm start, cg1; zeros for new indices).
 #pragma once
+#include <type_traits>
+
 #include "cs_common.cuh"
 
 namespace cs {
@@ -223,12 +225,22 @@ CS_DEV bool topk_cta_fast(Ctx& ctx, int n, int K, KeyFn key, uint32_t* out_bits)
 
 // key(i) for i in [0, n); key 0 means "never select".  Requires at least K
 // non-zero keys.  out_bits must hold ceil(n/32) words; fully overwritten.
-template <class Ctx, class KeyFn>
-CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_bits, bool try_fast = true) {
+// No vector loader (the scalar key(i) path everywhere).
+struct NoKey4 {};
+
+// key4(q) -> uint4 of keys 4q .. 4q+3 (32-bit keys, n % 4 == 0): the radix passes and the
+// final bitmask pass then move 16 bytes per load — the grid path is latency-bound on its key
+// loads (ncu: long_scoreboard at the key read), so four keys per load and sixteen per thread
+// in flight.  key(i) serves the tie path.
+template <class Ctx, class KeyFn, class Key4Fn = NoKey4>
+CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_bits, bool try_fast = true,
+                      Key4Fn key4 = Key4Fn{}) {
   if constexpr (Ctx::kTopkFast) {
     if (try_fast && topk_cta_fast(ctx, (int)n, (int)K, key, out_bits)) return;
   }
   using Key = decltype(key(int64_t(0)));
+  constexpr bool V4 = !std::is_same<Key4Fn, NoKey4>::value;
+  static_assert(!V4 || sizeof(Key) == 4, "the vector loader serves 32-bit keys");
   constexpr int NB = (int)sizeof(Key) * 8;
   Key prefix = 0, pmask = 0;
   int64_t need = K;
@@ -238,18 +250,41 @@ CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_b
   unsigned* hist = ctx.hist_ptr();
   for (int shift = NB - 8; shift >= 0; shift -= 8) {
     ctx.hist_clear();
-    constexpr int UK = 8;  // keys in flight per thread before the histogram updates
-    for (int64_t i0 = t0; i0 < n; i0 += UK * st) {
-      Key kv[UK];
+    if constexpr (V4) {
+      constexpr int UQ = 4;  // 16 keys in flight per thread
+      const int64_t n4 = n >> 2;
+      for (int64_t q0 = t0; q0 < n4; q0 += UQ * st) {
+        uint4 kv[UQ];
 #pragma unroll
-      for (int u = 0; u < UK; ++u) {
-        const int64_t i = i0 + u * st;
-        kv[u] = (i < n) ? key(i) : Key(0);
+        for (int u = 0; u < UQ; ++u) {
+          const int64_t q = q0 + u * st;
+          kv[u] = (q < n4) ? key4(q) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < UQ; ++u) {
+          const int64_t q = q0 + u * st;
+          if (q < n4) {
+            const Key kk[4] = {(Key)kv[u].x, (Key)kv[u].y, (Key)kv[u].z, (Key)kv[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if ((kk[e] & pmask) == prefix) hist_add_warp(hist, (unsigned)((kk[e] >> shift) & 255));
+          }
+        }
       }
+    } else {
+      constexpr int UK = 8;  // keys in flight per thread before the histogram updates
+      for (int64_t i0 = t0; i0 < n; i0 += UK * st) {
+        Key kv[UK];
 #pragma unroll
-      for (int u = 0; u < UK; ++u) {
-        const int64_t i = i0 + u * st;
-        if (i < n && (kv[u] & pmask) == prefix) hist_add_warp(hist, (unsigned)((kv[u] >> shift) & 255));
+        for (int u = 0; u < UK; ++u) {
+          const int64_t i = i0 + u * st;
+          kv[u] = (i < n) ? key(i) : Key(0);
+        }
+#pragma unroll
+        for (int u = 0; u < UK; ++u) {
+          const int64_t i = i0 + u * st;
+          if (i < n && (kv[u] & pmask) == prefix) hist_add_warp(hist, (unsigned)((kv[u] >> shift) & 255));
+        }
       }
     }
     ctx.hist_done();  // merged counts now in ctx.hist_smem()
@@ -264,11 +299,33 @@ CS_DEV void topk_bits(Ctx& ctx, int64_t n, int64_t K, KeyFn key, uint32_t* out_b
   const int64_t nwords = (n + 31) >> 5;
   if (n_eq == need) {
     // common case: every key >= thr is selected
-    for (int64_t w = gw; w < nwords; w += gnw) {
-      int64_t i = w * 32 + lane;
-      bool s = (i < n) && (key(i) >= thr);
-      uint32_t b = __ballot_sync(0xffffffffu, s);
-      if (lane == 0) out_bits[w] = b;
+    if constexpr (V4) {
+      // 128 keys per warp step: lane l holds keys 4 (32 g + l) .. +3, i.e. a nibble of word
+      // 4 g + l / 8; eight lanes OR their nibbles into the word
+      const int64_t ng = n >> 7;
+      for (int64_t g = gw; g < ng; g += gnw) {
+        const uint4 k = key4(g * 32 + lane);
+        uint32_t v = ((uint32_t)((Key)k.x >= thr) | ((uint32_t)((Key)k.y >= thr) << 1) |
+                      ((uint32_t)((Key)k.z >= thr) << 2) | ((uint32_t)((Key)k.w >= thr) << 3))
+                     << (4 * (lane & 7));
+        v |= __shfl_xor_sync(0xffffffffu, v, 1);
+        v |= __shfl_xor_sync(0xffffffffu, v, 2);
+        v |= __shfl_xor_sync(0xffffffffu, v, 4);
+        if ((lane & 7) == 0) out_bits[g * 4 + (lane >> 3)] = v;
+      }
+      for (int64_t w = ng * 4 + gw; w < nwords; w += gnw) {   // the tail words
+        int64_t i = w * 32 + lane;
+        bool s = (i < n) && (key(i) >= thr);
+        uint32_t b = __ballot_sync(0xffffffffu, s);
+        if (lane == 0) out_bits[w] = b;
+      }
+    } else {
+      for (int64_t w = gw; w < nwords; w += gnw) {
+        int64_t i = w * 32 + lane;
+        bool s = (i < n) && (key(i) >= thr);
+        uint32_t b = __ballot_sync(0xffffffffu, s);
+        if (lane == 0) out_bits[w] = b;
+      }
     }
     ctx.sync();
     return;

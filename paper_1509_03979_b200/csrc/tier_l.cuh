@@ -648,6 +648,16 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_diag_topk(LArgs<T> a, const
                                                               uint32_t* out_bits) {
   extern __shared__ __align__(16) char smem[];
   GridCtx<T> c = make_grid_ctx<T>(smem, a);
+  if constexpr (sizeof(T) == 4) {
+    if (n % 4 == 0) {   // the detection path's vector loader (pursuit.cuh detect_topk)
+      const float4* v4 = reinterpret_cast<const float4*>(vals);
+      topk_bits(c, n, K, [vals](int64_t i) { return full_key(vals[i]); }, out_bits, false, [v4](int64_t q) {
+        const float4 v = v4[q];
+        return make_uint4(full_key(v.x), full_key(v.y), full_key(v.z), full_key(v.w));
+      });
+      return;
+    }
+  }
   topk_bits(c, n, K, [vals](int64_t i) { return full_key(vals[i]); }, out_bits, false);
 }
 
