@@ -286,6 +286,28 @@ __global__ void __launch_bounds__(TS_THREADS, sizeof(T) == 4 ? 2 : 1) k_s_adjoin
     if (c.psi) c.G = Gws + b * c.N;
     c.RES(nullptr);  // A^T y (x = 0)
     T* x = X + b * N;
+    if constexpr (sizeof(T) == 4) {
+      if (!c.pinv && !c.psi && (N & 3) == 0) {
+        // the apply's scatter mirrored: x[4q..4q+3] from complex slots q (x_{4q}, x_{4q+2})
+        // and L-1-q (x_{4q+3}, x_{4q+1}) of the Makhoul sequence, one sign nibble, one
+        // 16-byte store per four outputs (the per-element map cost 45 % of the kernel's
+        // instructions)
+        const int L = (int)(N >> 1), nq = (int)(N >> 2);
+        const C2<T>* z = shp(c.Z);
+        const uint32_t* sg = shp(c.sign);
+        for (int q = threadIdx.x; q < nq; q += TS_THREADS) {
+          const C2<T> a = z[swz<T>(q)], bb = z[swz<T>(L - 1 - q)];
+          const uint32_t w = sg[q >> 3] >> ((4 * q) & 31);
+          float4 o;
+          o.x = (w & 1u) ? -a.x : a.x;
+          o.y = (w & 2u) ? -bb.y : bb.y;
+          o.z = (w & 4u) ? -a.y : a.y;
+          o.w = (w & 8u) ? -bb.x : bb.x;
+          *reinterpret_cast<float4*>(x + 4 * q) = o;
+        }
+        continue;
+      }
+    }
     for (int64_t j = c.gtid; j < N; j += c.gnthr) x[j] = c.c_at(j);
   }
 }
