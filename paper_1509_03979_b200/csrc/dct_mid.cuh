@@ -321,7 +321,17 @@ CS_DEV T mid_op2g(const MidCtx<T>& m, const MidK<T>& c, bool sel, RK&& rank, T r
     rn2 += (double)d * (double)d;
     return d * c.cout[TY];
   } else {
-    if (sel) m.yout[rank()] = c.scx[TY] * raw;
+    // the rank reads only metadata words (shared memory on both tiers): computed for every
+    // index so the store is predicated instead of a divergent branch per index
+    const int r = (int)rank();
+    T* const dst = m.yout + r;   // yout is global memory on both tiers
+    const T v = c.scx[TY] * raw;
+    if constexpr (sizeof(T) == 4)
+      asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.global.f32 [%0], %1; }" ::"l"(dst), "f"(v),
+                   "r"((unsigned)sel) : "memory");
+    else
+      asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.global.f64 [%0], %1; }" ::"l"(dst), "d"(v),
+                   "r"((unsigned)sel) : "memory");
     return T(0);
   }
 }
