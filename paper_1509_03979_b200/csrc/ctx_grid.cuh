@@ -574,18 +574,21 @@ template <typename T> struct GridCtx {
         const int64_t k10 = e0 >> lct, dk = (2 * NT) >> lct;
         const int64_t m2 = c0i + (e0 & (ct - 1));
         const C2<T> sa = tf(dk * m2), sbb = tf(dk * (m2 + 1));
-        C2<T> wa = mk<T>(1, 0), wb = mk<T>(1, 0);
-        for (int u = 0, p = threadIdx.x; p < np; ++u, p += NT) {
-          const int64_t k1 = k10 + u * dk;
-          if ((u & (TW_ANCHOR - 1)) == 0) {
-            wa = tf(k1 * m2);
-            wb = tf(k1 * (m2 + 1));
-          } else {
-            wa = cmul<T>(wa, sa);
-            wb = cmul<T>(wb, sbb);
+        for (int u0 = 0, p0 = threadIdx.x; p0 < np; u0 += TW_ANCHOR, p0 += TW_ANCHOR * NT) {
+          const int64_t k1g = k10 + u0 * dk;
+          C2<T> wa = tf(k1g * m2), wb = tf(k1g * (m2 + 1));
+#pragma unroll
+          for (int s2 = 0; s2 < TW_ANCHOR; ++s2) {
+            const int p = p0 + s2 * NT;
+            if (p >= np) break;
+            const int64_t k1 = k1g + s2 * dk;
+            if (s2) {
+              wa = cmul<T>(wa, sa);
+              wb = cmul<T>(wb, sbb);
+            }
+            const int e = 2 * p;
+            stp<T>(&wk[k1 * l2 + m2], CP<T>{cmul<T>(sb[swz<T>(e)], wa), cmul<T>(sb[swz<T>(e + 1)], wb)});
           }
-          const int e = 2 * p;
-          stp<T>(&wk[k1 * l2 + m2], CP<T>{cmul<T>(sb[swz<T>(e)], wa), cmul<T>(sb[swz<T>(e + 1)], wb)});
         }
       }
       __syncthreads();
@@ -639,18 +642,21 @@ template <typename T> struct GridCtx {
         const int64_t k10 = e0 >> lct, dk = (2 * NT) >> lct;
         const int64_t m2 = c0i + (e0 & (ct - 1));
         const C2<T> sa = tf(dk * m2), sbb = tf(dk * (m2 + 1));
-        C2<T> wa = mk<T>(1, 0), wb = mk<T>(1, 0);
-        for (int u = 0, pp = threadIdx.x; pp < np; ++u, pp += NT) {
-          const int64_t k1 = k10 + u * dk;
-          if ((u & (TW_ANCHOR - 1)) == 0) {
-            wa = tf(k1 * m2);
-            wb = tf(k1 * (m2 + 1));
-          } else {
-            wa = cmul<T>(wa, sa);
-            wb = cmul<T>(wb, sbb);
+        for (int u0 = 0, p0 = threadIdx.x; p0 < np; u0 += TW_ANCHOR, p0 += TW_ANCHOR * NT) {
+          const int64_t k1g = k10 + u0 * dk;
+          C2<T> wa = tf(k1g * m2), wb = tf(k1g * (m2 + 1));
+#pragma unroll
+          for (int s2 = 0; s2 < TW_ANCHOR; ++s2) {
+            const int pp = p0 + s2 * NT;
+            if (pp >= np) break;
+            const int64_t k1 = k1g + s2 * dk;
+            if (s2) {
+              wa = cmul<T>(wa, sa);
+              wb = cmul<T>(wb, sbb);
+            }
+            const int e = 2 * pp;
+            stp<T>(&wk[k1 * l2 + m2], CP<T>{cmul<T>(sb[swz<T>(e)], wa), cmul<T>(sb[swz<T>(e + 1)], wb)});
           }
-          const int e = 2 * pp;
-          stp<T>(&wk[k1 * l2 + m2], CP<T>{cmul<T>(sb[swz<T>(e)], wa), cmul<T>(sb[swz<T>(e + 1)], wb)});
         }
       }
       __syncthreads();
@@ -845,13 +851,18 @@ template <typename T> struct GridCtx {
         const int s0 = swz<T>(2 * t), s1i = swz<T>(2 * n2 - 1 - 2 * t);
         const int64_t l1 = L1;
         const C2<T> astep = tw4(l1 * 256);
-        C2<T> a = mk<T>(1, 0);
-        for (int u = 0, k2 = t; k2 < n2; ++u, k2 += 256) {
+        // unrolled by TW_ANCHOR: one table lookup per group (a predicated lookup in every
+        // step otherwise), the group's independent pair chains interleave
+        for (int u0 = 0, k20 = t; k20 < n2; u0 += TW_ANCHOR, k20 += 256 * TW_ANCHOR) {
+        C2<T> a = tw4(ka + l1 * k20);
+#pragma unroll
+        for (int st = 0; st < TW_ANCHOR; ++st) {
+          const int u = u0 + st, k2 = k20 + 256 * st;
+          if (k2 >= n2) break;
           const int q = k2 >> 5;
           const int wi[4] = {q, W + 2 * W1 - 1 - q, W + W1 - 1 - q, W1 + q};
           const int bi[4] = {b0, b1, b1, b0};
-          if ((u & (TW_ANCHOR - 1)) == 0) a = tw4(ka + l1 * k2);
-          else a = cmul<T>(a, astep);
+          if (st) a = cmul<T>(a, astep);
           const C2<T> a2 = cmul<T>(a, a);
           const C2<T> w = cmul<T>(a2, a2);
           mid_pair2g<T, MODE>(zb[s0 + 512 * u], zb[s1i - 512 * u], a, w, m, cst, rn2,
@@ -859,6 +870,7 @@ template <typename T> struct GridCtx {
               [&](int qq) {
                 return pw[wi[qq]] + __popc(mw[wi[qq]] & ((bi[qq] == b0) ? lm0 : lm1));
               });
+        }
         }
       } else if (m.staged) {
         // general item (rows ka, kb = L1 - ka): the four DCT indices of the pair at column
@@ -909,18 +921,20 @@ template <typename T> struct GridCtx {
           const int64_t k1 = r ? kb : ka;
           const int64_t m20 = 2 * ((int)threadIdx.x >> lb), dm = 2 * (NT >> lb);
           const C2<T> st = tf(k1 * dm);  // W^{k1 dm}
-          C2<T> wa = mk<T>(1, 0), wb = mk<T>(1, 0);
-          for (int u = 0, q = threadIdx.x; q < nq; ++u, q += NT) {
-            const int64_t m2 = m20 + u * dm;
-            if ((u & (TW_ANCHOR - 1)) == 0) {
-              wa = tf(k1 * m2);
-              wb = tf(k1 * (m2 + 1));
-            } else {
-              wa = cmul<T>(wa, st);
-              wb = cmul<T>(wb, st);
+          for (int u0 = 0, q0 = threadIdx.x; q0 < nq; u0 += TW_ANCHOR, q0 += TW_ANCHOR * NT) {
+            const int64_t m20g = m20 + u0 * dm;
+            C2<T> wa = tf(k1 * m20g), wb = tf(k1 * (m20g + 1));
+#pragma unroll
+            for (int s2 = 0; s2 < TW_ANCHOR; ++s2) {
+              if (q0 + s2 * NT >= nq) break;
+              const int64_t m2 = m20g + s2 * dm;
+              if (s2) {
+                wa = cmul<T>(wa, st);
+                wb = cmul<T>(wb, st);
+              }
+              stp<T>(&wk[k1 * l2 + m2], CP<T>{cmulc<T>(sb[swz<T>((int)(m2 << lb) | r)], wa),
+                                               cmulc<T>(sb[swz<T>((int)((m2 + 1) << lb) | r)], wb)});
             }
-            stp<T>(&wk[k1 * l2 + m2], CP<T>{cmulc<T>(sb[swz<T>((int)(m2 << lb) | r)], wa),
-                                             cmulc<T>(sb[swz<T>((int)((m2 + 1) << lb) | r)], wb)});
           }
         }
       }
