@@ -594,6 +594,67 @@ template <typename T> struct GridCtx {
       __syncthreads();
     }
   }
+  // pass A of the dense forward apply straight from x (fp32, no Eq.(7) permutation): each
+  // tile element is read from x with the Makhoul reorder and the sign folded into the load
+  // (slot s < L/2: (x[4s], x[4s+2]); slot s >= L/2, q = L-1-s: (x[4q+3], x[4q+1]); DESIGN.md
+  // §5.1), so the reorder sweep of the whole vector (read N + write N reals, one grid phase)
+  // disappears.  Rows m1 < L1/2 of tile t and rows >= L1/2 of the mirror tile L2/CT-1-t read
+  // the same 16-byte units of x, so consecutive work units are mirror tiles (same round,
+  // the second read hits L2).  Then the column FFT and the W_L^{k1 m2} store as passA.
+  CS_NOINL void passA_x(const float* __restrict__ x) {
+    const int ct = CT, lct = (ct == 4) ? 2 : 1;
+    const int64_t l2 = L2, ntl = L2 / ct, hl = (L1 * L2) / 2;
+    const int tile = (int)(L1 * ct);
+    C2<T>* sb = shp(buf);
+    C2<T>* wk = Wk;
+    const GTw<T> tf = twF;
+    const uint32_t* sg = sign;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int64_t v = blk; v < ntl; v += nblk) {
+      const int64_t t = (v & 1) ? ntl - 1 - (v >> 1) : (v >> 1);
+      const int64_t c0i = t * ct;
+      staged<TL_UNR, float4>(tile, [&](int e) {
+        const int64_t s = (int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1));
+        const int64_t q = s < hl ? s : 2 * hl - 1 - s;
+        return x4[q];
+      }, [&](int e, float4 xv) {
+        const int64_t s = (int64_t)(e >> lct) * l2 + c0i + (e & (ct - 1));
+        const bool lo = s < hl;
+        const int64_t q = lo ? s : 2 * hl - 1 - s;
+        const uint32_t w = sg[q >> 3] >> ((4 * q) & 31);
+        float re, im;
+        if (lo) { re = (w & 1u) ? -xv.x : xv.x; im = (w & 4u) ? -xv.z : xv.z; }
+        else    { re = (w & 8u) ? -xv.w : xv.w; im = (w & 2u) ? -xv.y : xv.y; }
+        sb[swz<T>(e)] = mk<T>((T)re, (T)im);
+      });
+      __syncthreads();
+      col_fft<false>();
+      {
+        const int NT = blockDim.x, np = tile / 2;
+        const int e0 = 2 * (int)threadIdx.x;
+        const int64_t k10 = e0 >> lct, dk = (2 * NT) >> lct;
+        const int64_t m2 = c0i + (e0 & (ct - 1));
+        const C2<T> sa = tf(dk * m2), sbb = tf(dk * (m2 + 1));
+        for (int u0 = 0, p0 = threadIdx.x; p0 < np; u0 += TW_ANCHOR, p0 += TW_ANCHOR * NT) {
+          const int64_t k1g = k10 + u0 * dk;
+          C2<T> wa = tf(k1g * m2), wb = tf(k1g * (m2 + 1));
+#pragma unroll
+          for (int s2 = 0; s2 < TW_ANCHOR; ++s2) {
+            const int p = p0 + s2 * NT;
+            if (p >= np) break;
+            const int64_t k1 = k1g + s2 * dk;
+            if (s2) {
+              wa = cmul<T>(wa, sa);
+              wb = cmul<T>(wb, sbb);
+            }
+            const int e = 2 * p;
+            stp<T>(&wk[k1 * l2 + m2], CP<T>{cmul<T>(sb[swz<T>(e)], wa), cmul<T>(sb[swz<T>(e + 1)], wb)});
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
   // pass A with a sparse input (H d, RES x on a support): each tile's few nonzeros are
   // scattered from the bucketed support list into a zeroed tile — U is never read
   CS_NOINL void passA_sparse(const T* vals) {
@@ -771,7 +832,7 @@ template <typename T> struct GridCtx {
           // pair q: row r = q & lb, m2 = 2 (q >> lb); smem element e = (m2 << lb) | r
           for (int e = threadIdx.x; e < B * n2; e += blockDim.x)
             cp_async_c<T>(&sb[swz<T>(e)], &wk[((e & lb) ? kb : ka) * l2 + (e >> lb)]);
-          cp_async_wait_all();
+          // (waited for after the metadata staging below: the two L2 round trips overlap)
         }
       }
       {
@@ -787,6 +848,7 @@ template <typename T> struct GridCtx {
           return (q < 2) ? mg[at] : (uint32_t)pg[at];
         }, [&](int e, uint32_t v) { ms[e] = v; });
       }
+      cp_async_wait_all();
       __syncthreads();
 #ifdef CS_DIAG_PASSB
       if (MODE == MID_H) mark(10);  // load + metadata staging

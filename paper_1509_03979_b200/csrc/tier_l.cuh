@@ -364,6 +364,14 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_apply(LArgs<T> a) {
       }
     };
     stamp(0);
+    if constexpr (sizeof(T) == 4) {
+      if (!c.psi && !c.pinv) {
+        // the reorder rides on pass A's tile loads (GridCtx::passA_x): no U sweep
+        stamp(1);
+        c.passA_x(reinterpret_cast<const float*>(x));
+        goto passA_done;
+      }
+    }
     if (c.psi) l_apply_psi_input<T>(c, x);
     else
     // four consecutive j per unit: x[j..j+3] -> U[j/2], U[j/2+1] (even j) and
@@ -394,6 +402,7 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_l_apply(LArgs<T> a) {
     c.sync();
     stamp(1);
     c.passA();
+  passA_done:
     c.sync();
     stamp(2);
     c.template passB<MID_FWD>(false, c.yT);
