@@ -109,6 +109,7 @@ template <typename T> struct GridScratch {
 };
 
 constexpr int TL_LOG2NT = 8;  // Tier L blocks: 256 threads (two per SM, 128 registers)
+constexpr int TL_TILE = 8192;  // complex elements per CTA tile (32 per thread)
 // Asynchronous global -> shared copies of one complex element (cp.async, LDGSTS): a
 // whole tile's loads are in flight at once without staging registers.
 template <typename T> CS_DEV void cp_async_c(C2<T>* sdst, const C2<T>* gsrc) {
@@ -201,6 +202,12 @@ template <typename T> struct GridCtx {
   int* tcnt;        // [ntiles + 1] exclusive starts of the tiles' entries in tlist
   int* tfill;       // [2][2][ntiles] counts and fill cursors of set_input_support (two parities)
   int sis_par = 0;  // parity of the next set_input_support
+  // Pass A's entry cache (set_input_support): when every block owns at most one column tile
+  // (c2, c3), block blk's tile entries (shared slot | sign bit, support index) stay in the
+  // unused tail of the tile buffer until the support changes, so pass A's scatter is one
+  // round trip (the values) instead of four dependent ones (bucket start, list, position,
+  // sign word).  acn = cached entries, -1 = no cache.
+  int acn = -1;
   int* tlist;       // [cap]
   int* tscr;        // [cap] the atomically filled (unordered) buckets before ranking
   GTw<T> twF;   // W_L
@@ -522,6 +529,37 @@ template <typename T> struct GridCtx {
     in_supp = supp;
     in_ns = ns;
     sync();
+    build_acache(supp);
+  }
+  // the cache lives in the tile buffer past every pass's footprint (tile, row pair, the bucket
+  // scan's offsets): TL_TILE complex slots, one entry (two ints) per slot
+  CS_DEV int64_t acache_off() const {
+    const int64_t tileA = L1 * CT, rowB = 2 * L2, offs = (L2 / CT + 2) / 2 + 1;
+    return tileA > rowB ? (tileA > offs ? tileA : offs) : (rowB > offs ? rowB : offs);
+  }
+  CS_DEV void build_acache(const int* supp) {
+    acn = -1;
+    const int nt = ntiles();
+    const int64_t off = acache_off();
+    if (psi || nt > (int)nblk || off >= TL_TILE) return;
+    if (blk < nt) {
+      const int a = tcnt[blk], e = tcnt[blk + 1];
+      if ((int64_t)(e - a) > TL_TILE - off) return;   // (block-uniform)
+      int* ac = reinterpret_cast<int*>(shp(buf) + off);
+      const int lct = (CT == 4) ? 2 : 1;
+      const int64_t l2 = L2, c0i = (int64_t)blk * CT;
+      for (int q = threadIdx.x; q < e - a; q += blockDim.x) {
+        const int i = tlist[a + q];
+        const int64_t p = in_pos[i], c = p >> 1;
+        const int el = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
+        ac[2 * q] = (2 * swz<T>(el) + (int)(p & 1)) | (bit_test(sign, supp[i]) ? (int)0x80000000 : 0);
+        ac[2 * q + 1] = i;
+      }
+      acn = e - a;
+    } else {
+      acn = 0;
+    }
+    __syncthreads();
   }
   CS_DEV void scatter(const T* vals) {
     const int* sp = in_supp;
@@ -678,10 +716,24 @@ template <typename T> struct GridCtx {
       const int64_t c0i = t * ct;
       for (int e = threadIdx.x; e < tile; e += blockDim.x) sb[e] = mk<T>(0, 0);
       __syncthreads();
-      for (int q = tcnt[t] + threadIdx.x; q < tcnt[t + 1]; q += blockDim.x) {
-        const int i = tlist[q];
-        const int64_t p = ip[i], c = p >> 1;
-        const int e = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
+      const bool cached = acn >= 0 && t == blk;   // build_acache: this block's one tile
+      const int* ac = reinterpret_cast<const int*>(sb + acache_off());
+      const int qa = cached ? 0 : tcnt[t], qe = cached ? acn : tcnt[t + 1];
+      for (int q = qa + threadIdx.x; q < qe; q += blockDim.x) {
+        int i, slot;
+        bool neg;
+        if (cached) {
+          const int w = ac[2 * q];
+          i = ac[2 * q + 1];
+          slot = w & 0x7fffffff;
+          neg = w < 0;
+        } else {
+          i = tlist[q];
+          const int64_t p = ip[i], c = p >> 1;
+          const int e = (int)(((c >> log2L2) << lct) | ((c & (l2 - 1)) - c0i));
+          slot = 2 * swz<T>(e) + (int)(p & 1);
+          neg = bit_test(sg, sp[i]);
+        }
         T v = vals[i];
         if (upd) {
           T ri = ur[i];
@@ -693,7 +745,7 @@ template <typename T> struct GridCtx {
           v = ri + ub * v;                   // line 20
           upd[i] = v;
         }
-        sbt[2 * swz<T>(e) + (int)(p & 1)] = apply_sign<T>(sg, sp[i], v);
+        sbt[slot] = neg ? -v : v;
       }
       __syncthreads();
       col_fft<false>();

@@ -16,7 +16,6 @@
 namespace cs {
 
 constexpr int TL_THREADS = 1 << TL_LOG2NT;  // 256 (measured: 512-thread blocks at 64 registers were slower for c2/c3)
-constexpr int TL_TILE = 8192;    // complex elements per CTA tile (32 per thread)
 
 struct LGeom {
   int64_t N, L, L1, L2;
