@@ -208,6 +208,9 @@ template <typename T> struct GridCtx {
   // round trip (the values) instead of four dependent ones (bucket start, list, position,
   // sign word).  acn = cached entries, -1 = no cache.
   int acn = -1;
+  // the N-dependent middle constants (fp64 sqrt / division), computed once per launch
+  // (make_grid_ctx) instead of in every pass B call
+  MidCtx<T> mid0;
   int* tlist;       // [cap]
   int* tscr;        // [cap] the atomically filled (unordered) buckets before ranking
   GTw<T> twF;   // W_L
@@ -695,7 +698,8 @@ template <typename T> struct GridCtx {
   }
   // pass A with a sparse input (H d, RES x on a support): each tile's few nonzeros are
   // scattered from the bucketed support list into a zeroed tile — U is never read
-  CS_NOINL void passA_sparse(const T* vals) {
+  CS_NOINL void passA_sparse(const T* vals) { passA_sparse_i(vals); }
+  CS_DEV void passA_sparse_i(const T* vals) {
     const int ct = CT, lct = (ct == 4) ? 2 : 1;
     const int64_t l2 = L2, ntl = L2 / ct;
     const int tile = (int)(L1 * ct);
@@ -781,6 +785,9 @@ template <typename T> struct GridCtx {
   // dvec != nullptr: also returns this thread's share of sum_i dvec_i outv_i (H's dot
   // product, reduced by the caller with the pass's closing barrier)
   CS_NOINL double passC_sparse(T* outv, const T* dvec = nullptr, const T* rvec = nullptr) {
+    return passC_sparse_i(outv, dvec, rvec);
+  }
+  CS_DEV double passC_sparse_i(T* outv, const T* dvec, const T* rvec) {
     double dot = 0, rq = 0, qq = 0, rr = 0;
     const int ct = CT, lct = (ct == 4) ? 2 : 1;
     const int64_t l2 = L2, ntl = L2 / ct;
@@ -861,8 +868,13 @@ template <typename T> struct GridCtx {
     p_rr = rr;
     return dot;
   }
-  template <int MODE> CS_NOINL double passB(bool zero_input, T* yout) {
-    MidCtx<T> m = make_mid<T>(N, rowmask, prefix, y, yout);
+  template <int MODE> CS_NOINL double passB(bool zero_input, T* yout) { return passB_i<MODE>(zero_input, yout); }
+  template <int MODE> CS_DEV double passB_i(bool zero_input, T* yout) {
+    MidCtx<T> m = mid0;
+    m.rowmask = rowmask;
+    m.prefix = prefix;
+    m.y = y;
+    m.yout = yout;
     m.s1 = s1;
     m.tsh = tsh;
     double rn2 = 0;
@@ -1131,16 +1143,18 @@ template <typename T> struct GridCtx {
   }
   // q = H d with pass C summing d.q, r.q, q.q and r.r in one grid reduction (H's closing
   // barrier); r = the current residual (updated by pass A).  sums = {d.q, r.q, q.q, r.r}.
+  // the three passes inlined: one call frame (one callee-saved register save / restore
+  // through local memory) per H instead of three — the CG loop's H at every grid size
   CS_NOINL void H_dot4(const T* d, T* q, const T* r, double* sums) {
     mark(0);
-    passA_sparse(d);
+    passA_sparse_i(d);
     sync();
     mark(1);
-    passB<MID_H>(false, nullptr);
+    passB_i<MID_H>(false, nullptr);
     sync();
     mark(2);
     double t[4];
-    t[0] = passC_sparse(q, d, r);
+    t[0] = passC_sparse_i(q, d, r);
     t[1] = p_rq;
     t[2] = p_qq;
     t[3] = p_rr;

@@ -204,6 +204,7 @@ CS_NOINL CS_DEV void tl_tables(const double2* src, const LGeom& g, C2<T>* tF, C2
 template <typename T>
 CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   GridCtx<T> c;
+  c.mid0 = make_mid<T>(a.meta.N, nullptr, nullptr, nullptr, nullptr);
   c.grp = (int)(blockIdx.x / (unsigned)a.gblocks);
   c.ngrp = a.ngroups;
   if (threadIdx.x == 0) {   // the group words: dynamic shared offset 0 (ctx_grid.cuh tl_group)
