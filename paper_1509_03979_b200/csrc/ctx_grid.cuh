@@ -1071,7 +1071,8 @@ template <typename T> struct GridCtx {
     }
     return rn2;
   }
-  CS_NOINL void passC() {
+  CS_NOINL void passC() { passC_i(); }
+  CS_DEV void passC_i() {
     C2<T>* Cc = reinterpret_cast<C2<T>*>(Cb);
     const int ct = CT, lct = (ct == 4) ? 2 : 1;
     const int64_t l2 = L2, ntiles = L2 / ct;
@@ -1098,13 +1099,13 @@ template <typename T> struct GridCtx {
   CS_NOINL void H(const T* d, T* q) {
     if (psi) { H_psi(d, q); return; }
     mark(0);
-    passA_sparse(d);
+    passA_sparse_i(d);
     sync();
     mark(1);
-    passB<MID_H>(false, nullptr);
+    passB_i<MID_H>(false, nullptr);
     sync();
     mark(2);
-    passC_sparse(q);
+    passC_sparse_i(q, nullptr, nullptr);
     sync();
     mark(3);
     ++applies;
@@ -1235,14 +1236,14 @@ template <typename T> struct GridCtx {
     if (psi) return RES_psi(x);
     mark(0);
     if (x) {
-      passA_sparse(x);
+      passA_sparse_i(x);
       sync();
     }
     mark(4);
-    double rn2 = passB<MID_RES>(x == nullptr, nullptr);
+    double rn2 = passB_i<MID_RES>(x == nullptr, nullptr);
     sync();
     mark(5);
-    passC();
+    passC_i();
     const double r = sum(rn2);  // the reduction's barrier also publishes Cb
     mark(6);
     ++applies;
