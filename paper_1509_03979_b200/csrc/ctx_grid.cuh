@@ -1146,7 +1146,7 @@ template <typename T> struct GridCtx {
   // barrier); r = the current residual (updated by pass A).  sums = {d.q, r.q, q.q, r.r}.
   // the three passes inlined: one call frame (one callee-saved register save / restore
   // through local memory) per H instead of three — the CG loop's H at every grid size
-  CS_NOINL void H_dot4(const T* d, T* q, const T* r, double* sums) {
+  CS_DEV void H_dot4(const T* d, T* q, const T* r, double* sums) {
     mark(0);
     passA_sparse_i(d);
     sync();
@@ -1201,6 +1201,9 @@ template <typename T> struct GridCtx {
       return;
     }
     S s = s_io;
+#ifdef CS_DIAG_GLUE
+    mark(20);  // cg_iterate entry
+#endif
     T *xx = s.x, *rv = s.r, *dv = s.d, *qv = s.q;
     bool pend = false;
     T alpha = T(0);

@@ -112,6 +112,9 @@ CS_DEV void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q, 
                        const Params& P, Stats& st) {
   ctx.mark(0);
   ctx.set_input_support(supp, ns);
+#ifdef CS_DIAG_GLUE
+  ctx.mark(17);  // set_input_support
+#endif
   supp = ctx.loc(supp);
   x = ctx.loc(x);
   r = ctx.loc(r);
@@ -124,6 +127,9 @@ CS_DEV void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q, 
     for (int i = t0; i < ns; i += sd) b[i] = c0v.at(supp[i]);             // line 12
   }
   // no barrier: b[i] is read below only by the thread that wrote it (same i mapping)
+#ifdef CS_DIAG_GLUE
+  ctx.mark(18);  // b gather
+#endif
   if (!r_given) {
     ctx.H(x, q);
     for (int i = t0; i < ns; i += sd) r[i] = b[i] - q[i];
@@ -140,6 +146,9 @@ CS_DEV void cg_solve(Ctx& ctx, const int* supp, int ns, T* x, T* r, T* d, T* q, 
   ctx.cg_iterate(cs_);                                                     // lines 14-22
   st.status |= cs_.status;
   ctx.sync();
+#ifdef CS_DIAG_GLUE
+  ctx.mark(19);  // CG loop exit: flush + barrier
+#endif
   st.cg_iters += cs_.j;
   st.cg_solves += 1;
   double rel = bb > 0 ? sqrt(cs_.rr / bb) : 0.0;

@@ -31,5 +31,6 @@ off = cs.load_library().cs_diag_phase_offset(cs.ALGS[cfg.alg], cfg.N, cfg.M, cfg
 acc = raw[off:off + 8 * 24].view(np.uint64)
 # slots 10-14: pass-B item phases of H, only with CS_NVCC_EXTRA=-DCS_DIAG_PASSB
 names += ["passB load+stage", "passB fwd FFT", "passB middle", "passB inv FFT", "passB twiddle+store",
-          "CG x/r update", "CG rr reduction"]  # 15-16: -DCS_DIAG_CG
+          "CG x/r update", "CG rr reduction",  # 15-16: -DCS_DIAG_CG
+          "set_input_support", "b gather", "CG loop exit", "cg_iterate entry"]  # 17-20: -DCS_DIAG_GLUE
 print({n: round(float(v) / 1e6, 3) for n, v in zip(names, acc) if v}, "ms (block 0)")
