@@ -214,6 +214,7 @@ template <typename T> struct CtaCtx {
   }
 
   // ---- the operator sandwich ----
+  CS_DEV void swap_hint(int, int) {}   // (the grid context's single-swap bucket update)
   CS_DEV void set_input_support(const int* supp, int ns) {
     in_supp = supp;
     in_ns = ns;

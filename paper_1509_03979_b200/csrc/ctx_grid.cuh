@@ -213,6 +213,11 @@ template <typename T> struct GridCtx {
   MidCtx<T> mid0;
   int* tlist;       // [cap]
   int* tscr;        // [cap] the atomically filled (unordered) buckets before ranking
+  int* tcnt2;       // [ntiles + 1] the single-swap update's new starts (swapped with tcnt)
+  // OMPR(1) swap hint (run_ompr -> set_input_support): the next support is the remembered
+  // one with old entry sw_dpos removed and a new index inserted at new position sw_ipos
+  int sw_dpos = -1, sw_ipos = -1;
+  CS_DEV void swap_hint(int dpos, int ipos) { sw_dpos = dpos; sw_ipos = ipos; }
   GTw<T> twF;   // W_L
   GTw<T> tw4;   // W_4N
   // shared memory
@@ -471,6 +476,8 @@ template <typename T> struct GridCtx {
   // counts itself into shared memory (block 0 also publishes them as tcnt) and fills tlist
   // with its own copy; the other parity's arrays are zeroed for the next call.
   CS_DEV void set_input_support(const int* supp, int ns) {
+    if (sw_dpos >= 0 && in_supp != nullptr && ns == in_ns) { set_input_support_swap(supp, ns); return; }
+    sw_dpos = sw_ipos = -1;
     const int nt = ntiles();
     int* cnt = tfill + sis_par * 2 * nt;
     int* fil = cnt + nt;
@@ -532,6 +539,54 @@ template <typename T> struct GridCtx {
     in_supp = supp;
     in_ns = ns;
     sync();
+    build_acache(supp);
+  }
+  // The buckets of a support that differs from the remembered one by one swap (OMPR(1)):
+  // old entry dpos leaves, the new index supp[ipos] enters.  Every other entry keeps its
+  // position p, hence its tile, and its index moves monotonically (i -> i - [i > dpos], then
+  // +1 if that is >= ipos), so each bucket is the old bucket mapped in order, minus the dropped
+  // entry (tile A), plus the new one (tile Bt) at its rank — exactly what the full rebuild's
+  // ranking produces (same tcnt, tlist, in_pos; bitwise the same passes), for one grid barrier
+  // instead of three plus the ranking pass.
+  CS_DEV void set_input_support_swap(const int* supp, int ns) {
+    const int nt = ntiles();
+    const int dpos = sw_dpos, ipos = sw_ipos;
+    sw_dpos = sw_ipos = -1;
+    const int A = tile_of(ppos(pinv, in_supp[dpos], N));
+    const int Bt = tile_of(ppos(pinv, supp[ipos], N));
+    auto newstart = [&](int t) { return tcnt[t] - (t > A ? 1 : 0) + (t > Bt ? 1 : 0); };
+    if (blk == 0)
+      for (int t = threadIdx.x; t <= nt; t += blockDim.x) tcnt2[t] = newstart(t);
+    for (int i = gtid; i < ns; i += gnthr) in_pos[i] = ppos(pinv, supp[i], N);
+    int* cntj = reinterpret_cast<int*>(si);   // block scratch: rank of the new entry
+    for (int t = blk; t < nt; t += nblk) {
+      const int a = tcnt[t], e = tcnt[t + 1], a2 = newstart(t);
+      if (t == Bt) {
+        if (threadIdx.x == 0) *cntj = 0;
+        __syncthreads();
+      }
+      int below = 0;
+      for (int k = threadIdx.x; k < e - a; k += blockDim.x) {
+        const int oi = tlist[a + k];
+        if (t == A && oi == dpos) continue;
+        int ni = oi - (oi > dpos ? 1 : 0);
+        ni += (ni >= ipos) ? 1 : 0;
+        const int rk = k - ((t == A && oi > dpos) ? 1 : 0) + ((t == Bt && ni > ipos) ? 1 : 0);
+        tscr[a2 + rk] = ni;
+        below += (t == Bt && ni < ipos) ? 1 : 0;
+      }
+      if (t == Bt) {
+        if (below) atomicAdd(cntj, below);
+        __syncthreads();
+        if (threadIdx.x == 0) tscr[a2 + *cntj] = ipos;
+        __syncthreads();
+      }
+    }
+    in_supp = supp;
+    in_ns = ns;
+    sync();
+    int* tmp = tlist; tlist = tscr; tscr = tmp;
+    tmp = tcnt; tcnt = tcnt2; tcnt2 = tmp;
     build_acache(supp);
   }
   // the cache lives in the tile buffer past every pass's footprint (tile, row pair, the bucket

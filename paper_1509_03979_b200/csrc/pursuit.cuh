@@ -511,6 +511,9 @@ CS_NOINL int run_ompr(Ctx& ctx, const Params& P, Bufs<T>& B, Stats& st, double& 
       }
       ctx.sync();
       ctx.mark(9);
+      // S2 = S without U[drop], with j at its place: the grid context updates its tile buckets
+      // by that one swap instead of rebuilding them
+      ctx.swap_hint(drop < pos ? drop : drop - 1, pos < drop ? pos : pos - 1);
       cg_solve(ctx, S2, ns, x2, B.r, B.d, B.q, B.b, false, P, st);
       swap_ptr<Ctx>(S, S2);
       swap_ptr<Ctx>(x, x2);

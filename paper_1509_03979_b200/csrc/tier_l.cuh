@@ -51,7 +51,7 @@ CS_HD LGeom l_geom(int64_t N) {
 
 // Workspace layout (byte offsets) — identical on host and device.
 struct LLayout {
-  int64_t U, Wk, Cb, c0, yT, G, yTf, in_pos, tcnt, tfill, tlist, tscr;
+  int64_t U, Wk, Cb, c0, yT, G, yTf, in_pos, tcnt, tfill, tlist, tscr, tcnt2;
   int64_t S, S2, Ul, x, x2, xU, r, d, q, b, Sbits, Ubits, Pbits;
   int64_t ctl, bar, pd, pi, pk, ghist, ts, ctl_end;
   int64_t bytes;
@@ -75,6 +75,7 @@ CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int 
   if (pursuit) {
     s.in_pos = take((int64_t)ucap * 8);
     s.tcnt = take((g.L2 / g.CT + 1) * 4);
+    s.tcnt2 = take((g.L2 / g.CT + 1) * 4);   // the single-swap update's new starts (ctx_grid.cuh)
     s.tlist = take((int64_t)ucap * 4);
     s.tscr = take((int64_t)ucap * 4);
     s.S = take((int64_t)K * 4);
@@ -92,7 +93,7 @@ CS_HD LLayout l_layout(int64_t N, int64_t M, int K, int ucap, bool pursuit, int 
     s.Pbits = take(((ucap + 31) / 32) * 4);
   } else {
     s.in_pos = s.S = s.S2 = s.Ul = s.x = s.x2 = s.xU = s.r = s.d = s.q = s.b = 0;
-    s.tcnt = s.tfill = s.tlist = s.tscr = 0;
+    s.tcnt = s.tfill = s.tlist = s.tscr = s.tcnt2 = 0;
     s.Sbits = s.Ubits = s.Pbits = 0;
   }
   // control block (zeroed before every launch)
@@ -237,6 +238,7 @@ CS_DEV GridCtx<T> make_grid_ctx(char* smem, const LArgs<T>& a) {
   c.tfill = reinterpret_cast<int*>(ws + s.tfill);
   c.tlist = reinterpret_cast<int*>(ws + s.tlist);
   c.tscr = reinterpret_cast<int*>(ws + s.tscr);
+  c.tcnt2 = reinterpret_cast<int*>(ws + s.tcnt2);
   c.g.bar = reinterpret_cast<GridBar*>(ws + s.bar);
   c.g.pd = reinterpret_cast<double*>(ws + s.pd);
   c.g.pi = reinterpret_cast<int64_t*>(ws + s.pi);
