@@ -275,6 +275,25 @@ template <typename T> struct GridCtx {
     __syncthreads();
     return t;
   }
+  // Lane `lane`'s share of the per-block partials P[c], c = lane, lane + 32, ... < n, summed
+  // in that order with all of the lane's loads in flight first (a strided loop would wait one
+  // L2 round trip per term: ~9 at 257 blocks); adding the padding zeros leaves every partial
+  // sum bitwise unchanged.
+  template <typename V> CS_DEV static V lane_sum(const V* P, int n, int ln) {
+    constexpr int U = 10;   // 320 >= blocks of the grid tier (two per SM)
+    V a = V(0);
+    for (int c0 = 0; c0 < n; c0 += 32 * U) {
+      V v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + ln + 32 * u;
+        v[u] = c < n ? P[c] : V(0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) a += v[u];
+    }
+    return a;
+  }
   CS_DEV static double warp_sum_g(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -287,7 +306,7 @@ template <typename T> struct GridCtx {
     sync();
     if (threadIdx.x < 32) {
       double a = 0;
-      for (int c = threadIdx.x; c < (int)nblk; c += 32) a += P[c];
+      a = lane_sum<double>(P, (int)nblk, (int)threadIdx.x);
       a = warp_sum_g(a);
       if (threadIdx.x == 0) sd[32] = a;
     }
@@ -316,7 +335,7 @@ template <typename T> struct GridCtx {
       const int k = (int)threadIdx.x >> 5;
       const double* P = g.pd + (k * 2 + bank) * g.maxgrid;
       double v = 0;
-      for (int c = lane; c < (int)nblk; c += 32) v += P[c];
+      v = lane_sum<double>(P, (int)nblk, (int)lane);
       v = warp_sum_g(v);
       if (lane == 0) sd[k] = v;
     }
@@ -349,10 +368,21 @@ template <typename T> struct GridCtx {
     if (threadIdx.x < 32) {  // warp 0 merges the per-block partials (lanes stride, then shuffle)
       Key bk = 0;
       int64_t bi = -1;
-      for (int c = threadIdx.x; c < (int)nblk; c += 32) {
-        const Key kc = (Key)PK[c];
-        const int64_t ic = PI[c];
-        if (kc > bk || (kc == bk && kc != 0 && ic < bi)) { bk = kc; bi = ic; }
+      for (int c0 = 0; c0 < (int)nblk; c0 += 320) {   // all loads in flight first (lane_sum)
+        Key kv[10];
+        int64_t iv[10];
+#pragma unroll
+        for (int u = 0; u < 10; ++u) {
+          const int c = c0 + (int)threadIdx.x + 32 * u;
+          kv[u] = c < (int)nblk ? (Key)PK[c] : Key(0);
+          iv[u] = c < (int)nblk ? PI[c] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 10; ++u) {
+          const Key kc = kv[u];
+          const int64_t ic = iv[u];
+          if (kc > bk || (kc == bk && kc != 0 && ic < bi)) { bk = kc; bi = ic; }
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -388,10 +418,19 @@ template <typename T> struct GridCtx {
     sync();
     if (threadIdx.x < 32) {  // warp 0: lanes stride over the per-block partials, then shuffle
       int64_t before = 0, all = 0;
-      for (int c = threadIdx.x; c < (int)nblk; c += 32) {
-        const int64_t v = P[c];
-        if (c < (int)blk) before += v;
-        all += v;
+      for (int c0 = 0; c0 < (int)nblk; c0 += 320) {   // all loads in flight first (lane_sum)
+        int64_t vv[10];
+#pragma unroll
+        for (int u = 0; u < 10; ++u) {
+          const int c = c0 + (int)threadIdx.x + 32 * u;
+          vv[u] = c < (int)nblk ? P[c] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 10; ++u) {
+          const int c = c0 + (int)threadIdx.x + 32 * u;
+          if (c < (int)blk) before += vv[u];
+          all += vv[u];
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1185,7 +1224,7 @@ template <typename T> struct GridCtx {
     sync();                                    // publishes q and the per-block partials
     if (threadIdx.x < 32) {
       double a = 0;
-      for (int c = threadIdx.x; c < (int)nblk; c += 32) a += P[c];
+      a = lane_sum<double>(P, (int)nblk, (int)threadIdx.x);
       a = warp_sum_g(a);
       if (threadIdx.x == 0) sd[32] = a;
     }
@@ -1231,7 +1270,7 @@ template <typename T> struct GridCtx {
       const int k = (int)threadIdx.x >> 5;
       const double* P = g.pd + (k * 2 + bank) * g.maxgrid;
       double a = 0;
-      for (int c = lane; c < (int)nblk; c += 32) a += P[c];
+      a = lane_sum<double>(P, (int)nblk, (int)lane);
       a = warp_sum_g(a);
       if (lane == 0) sd[k] = a;
     }
