@@ -562,17 +562,37 @@ template <typename T> struct GridCtx {
     // order varies run to run, and pass C's per-thread dot-product partials follow the list
     // order, so ranking the entries makes the fp64 sums (alpha, beta, the stop test) and
     // hence every result bitwise reproducible
-    // (one warp per entry: the lanes read the bucket in parallel and a ballot counts the
-    // entries below i — one L2 round trip per 32 bucket entries)
-    for (int i = gwarp; i < ns; i += gnwarps) {
-      const int t = tile_of(in_pos[i]);
-      const int a = offs[t], e = offs[t + 1];
-      int rank = 0;
-      for (int q0 = a; q0 < e; q0 += 32) {
-        const int q = q0 + (int)lane;
-        rank += __popc(__ballot_sync(0xffffffffu, q < e && __ldcg(&tscr[q]) < i));
+    // (one block per bucket: the bucket is staged in shared memory past the offsets with one
+    // L2 round trip, and each entry's rank is the count of smaller entries — broadcast reads;
+    // a bucket too large for that quadratic count falls back to one warp per entry, the
+    // lanes reading the bucket in parallel and a ballot counting the entries below i)
+    {
+      int* sbk = offs + nt + 1;
+      constexpr int QCAP = 2048;
+      for (int t = blk; t < nt; t += nblk) {
+        const int a = offs[t], e = offs[t + 1], n = e - a;
+        if (n <= QCAP) {
+          for (int q = threadIdx.x; q < n; q += blockDim.x) sbk[q] = __ldcg(&tscr[a + q]);
+          __syncthreads();
+          for (int q = threadIdx.x; q < n; q += blockDim.x) {
+            const int v = sbk[q];
+            int rank = 0;
+            for (int u = 0; u < n; ++u) rank += sbk[u] < v ? 1 : 0;
+            tlist[a + rank] = v;
+          }
+          __syncthreads();
+        } else {
+          for (int q0 = a + (int)(threadIdx.x >> 5); q0 < e; q0 += (int)(blockDim.x >> 5)) {
+            const int i = __ldcg(&tscr[q0]);
+            int rank = 0;
+            for (int r0 = a; r0 < e; r0 += 32) {
+              const int q = r0 + (int)lane;
+              rank += __popc(__ballot_sync(0xffffffffu, q < e && __ldcg(&tscr[q]) < i));
+            }
+            if (lane == 0) tlist[a + rank] = i;
+          }
+        }
       }
-      if (lane == 0) tlist[a + rank] = i;
     }
     sis_par ^= 1;
     in_supp = supp;
