@@ -43,7 +43,7 @@ CS_DEV unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
 // spins on the arrival counter with acquire loads (release/acquire make every block's
 // writes before the barrier visible after it); bounded spin with a watchdog trap (~15 s).
 // nblk = the blocks that meet at this barrier (a group of the grid, or all of it).
-static CS_NOINL void grid_barrier(GridBar* gb, unsigned nblk) {
+static CS_DEV void grid_barrier(GridBar* gb, unsigned nblk) {
   __syncthreads();
   if (threadIdx.x == 0) {
     // One monotonic 64-bit arrival counter (zeroed per launch): the block that arrives at
