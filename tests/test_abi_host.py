@@ -79,3 +79,26 @@ def test_create_ex_rejects_bad_psi(lib):
     h = ctypes.c_void_p()
     assert lib.cs_operator_create_ex(1024, 256, 1, None, None, None, 7, None, 0, None, ctypes.byref(h)) == 1
     assert lib.cs_operator_create_ex(1024, 256, 1, None, None, None, 1, None, 0, None, ctypes.byref(h)) == 1
+
+
+def test_missing_library_fails_loudly():
+    """The product path has no fallback: without libcsgpu.so the binding raises."""
+    import subprocess
+    import sys
+    code = ("import paper_1509_03979_b200 as cs\n"
+            "try:\n"
+            "    cs.load_library('/nonexistent/libcsgpu.so')\n"
+            "except ImportError as e:\n"
+            "    print('raised', e)\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.startswith("raised"), r.stdout
+
+
+def test_product_package_never_imports_the_oracle():
+    """oracle/ is test infrastructure: the package (binding, dist helpers) must not reach it."""
+    pkg = os.path.join(ROOT, "paper_1509_03979_b200")
+    for f in sorted(os.listdir(pkg)):
+        if f.endswith(".py"):
+            src = open(os.path.join(pkg, f)).read()
+            assert not re.search(r"^\s*(from|import)\s+oracle\b", src, flags=re.M), f
