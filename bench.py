@@ -583,7 +583,8 @@ def run_reference(args):
     v = n / t
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "signals/s", "n_gpus": world,
             "steps": steps, "warmup": warm, "ms_per_step": round(1e3 * t, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling if cfg.batch > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, DESIGN.md §4)",
             "config": {"workload": workload_desc(cfg), "problems_total": B, "N": cfg.N, "M": cfg.M, "K": cfg.K,
                        "alg": cfg.alg},
