@@ -363,7 +363,9 @@ def run_ours(args):
         peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12 / (1 if es == 4 else 2)
         roofline = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
-                    "kernel": f"k_s_recover<{'float' if es == 4 else 'double'}>", "kernel_ms": round(kms, 4),
+                    "kernel": f"k_s_recover<{'float' if es == 4 else 'double'}>"
+                              + (" + the fp64 refinement launches (the whole step)" if args.precision == "mixed" else ""),
+                    "kernel_ms": round(kms, 4),
                     "algorithmic_flops_per_launch": flops_step,
                     "peak_note": "derived: FP32 SIMT 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md §6)"}
     else:
@@ -408,7 +410,9 @@ def run_ours(args):
         "e2e": {"value": round(total_signals / (ems / 1e3), 2), "unit": "signals/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems, 4),
                 "api": "cs_recover_batched_host (pinned host buffers, chunked copy/compute overlap)",
-                "matches_device_path": e2e_same},
+                "matches_device_path": e2e_same,
+                **({"note": "the host-buffer pipeline runs plain fp32 (refine_fp64 is a device-path option)"}
+                   if args.precision == "mixed" else {})},
         "gpu_launches": int(launches),
         "refined_fp64": int(np.count_nonzero(reps["status"] & 8)) if args.precision == "mixed" else None,
         "roofline": roofline,
