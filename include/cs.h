@@ -84,8 +84,10 @@ typedef struct {
                          * is recovered again from scratch in fp64 and its result replaces
                          * the fp32 one (status CS_DEV_REFINED_FP64); at most CS_REFINE_CAP
                          * problems per call (the rest keep fp32, CS_DEV_NOT_REFINED).  The
-                         * workspace grows by cs_workspace_bytes's refine share.  Device-path
-                         * calls only (the host-buffer entry points ignore it).  0 -> off.  */
+                         * workspace grows by cs_workspace_bytes's refine share.  The
+                         * host-buffer entry point runs it once over the whole batch after
+                         * its fp32 chunks and copies the results out after it (workspace:
+                         * cs_workspace_bytes_host with the same options).  0 -> off.      */
   int32_t reserved[3];  /* must be zero                                                      */
 } cs_options;
 #define CS_REFINE_FLOOR 1e-6  /* ~16 fp32 ulps: the sandwich's relative rounding */

@@ -347,6 +347,39 @@ bool refine_applies(int precision, const cs_options* opts, int64_t N, int32_t K,
          tier_s_fits<double>(N, K, ucap, true);
 }
 
+// the mixed-precision pass over a batch whose fp32 results are on the device (or queued on
+// st): flag the problems below the fp32 floor, recover them again in fp64 on the CTA tier and
+// merge the fp64 results over the fp32 ones. ws = the recovery workspace (the fp32 pass's
+// B * 2N floats first, the refinement's area after them, cs_workspace_bytes with refine_fp64).
+cs_status refine_launch(const cs_operator* op, const Params& P, int64_t ucap, const float* Y, int64_t B,
+                        float* vals, int32_t* supp, cs_report* reps, char* ws, cudaStream_t st) {
+  const int64_t N = op->N, M = op->M;
+  const int32_t K = P.K;
+  char* rb = ws + align_up(B * 2 * N * 4, 256);
+  RefineWs r = refine_ws(rb, N, M, K, B);
+  const int cap = (int)std::min<int64_t>(B, CS_REFINE_CAP);
+  CS_CUDA(cudaMemsetAsync(r.count, 0, sizeof(int), st));
+  k_refine_select<<<(unsigned)((B + 7) / 8), 256, 0, st>>>(B, M, K, Y, vals, reps, cap, r.count, r.list, r.y64);
+  CS_LAUNCHED();
+  SRecArgs<double> d;
+  d.meta = meta_of(op);
+  d.lay = s_layout<double>(N, K, (int)ucap, true);
+  d.P = P;
+  d.P.tol = P.tol < 1e-12 ? P.tol : 1e-12;   // the fp64 path's tolerance (R7)
+  d.ucap = (int)ucap;
+  d.Y = r.y64;
+  d.vals = r.vals;
+  d.supp = r.supp;
+  d.reps = r.reps;
+  d.c0ws = r.c0;
+  d.bmap = r.list;
+  d.bcount = r.count;
+  if (cs_status s = s_recover_launch<double>(d, cap, st, g_launches, g_last_error)) return s;
+  k_refine_merge<<<(unsigned)cap, 256, 0, st>>>(K, cap, r.count, r.list, r.vals, r.supp, r.reps, vals, supp, reps);
+  CS_LAUNCHED();
+  return CS_OK;
+}
+
 template <typename T>
 cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, int64_t M, int64_t N,
                        int32_t K, double tol, const cs_options* opts, T* vals, int32_t* supp,
@@ -392,34 +425,9 @@ cs_status recover_impl(const cs_operator* op, int alg, const T* Y, int64_t B, in
     a.c0ws = reinterpret_cast<T*>(ws);
     if (cs_status s = s_recover_launch<T>(a, B, st, g_launches, g_last_error)) return s;
     if constexpr (sizeof(T) == 4) {
-      if (refine_applies(0, opts, N, K, ucap)) {
-        // the fp32 pass's workspace is B * 2N floats; the refinement's follows it
-        char* rb = reinterpret_cast<char*>(ws) + align_up(B * 2 * N * 4, 256);
-        RefineWs r = refine_ws(rb, N, M, K, B);
-        const int cap = (int)std::min<int64_t>(B, CS_REFINE_CAP);
-        CS_CUDA(cudaMemsetAsync(r.count, 0, sizeof(int), st));
-        k_refine_select<<<(unsigned)((B + 7) / 8), 256, 0, st>>>(B, M, K, reinterpret_cast<const float*>(Y),
-                                                                   reinterpret_cast<const float*>(vals), reps,
-                                                                   cap, r.count, r.list, r.y64);
-        CS_LAUNCHED();
-        SRecArgs<double> d;
-        d.meta = meta_of(op);
-        d.lay = s_layout<double>(N, K, (int)ucap, true);
-        d.P = P;
-        d.P.tol = tol < 1e-12 ? tol : 1e-12;   // the fp64 path's tolerance (R7)
-        d.ucap = (int)ucap;
-        d.Y = r.y64;
-        d.vals = r.vals;
-        d.supp = r.supp;
-        d.reps = r.reps;
-        d.c0ws = r.c0;
-        d.bmap = r.list;
-        d.bcount = r.count;
-        if (cs_status s = s_recover_launch<double>(d, cap, st, g_launches, g_last_error)) return s;
-        k_refine_merge<<<(unsigned)cap, 256, 0, st>>>(K, cap, r.count, r.list, r.vals, r.supp, r.reps,
-                                                       reinterpret_cast<float*>(vals), supp, reps);
-        CS_LAUNCHED();
-      }
+      if (refine_applies(0, opts, N, K, ucap))
+        if (cs_status s = refine_launch(op, P, ucap, Y, B, vals, supp, reps, reinterpret_cast<char*>(ws), st))
+          return s;
     }
     return CS_OK;
   }
@@ -472,7 +480,14 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
   if (cs_status s = check_N(N)) return s;
   if (K < 1) return fail(CS_ERR_INVALID_ARG, "K must be >= 1");
   const int prec = sizeof(T) == 8 ? 1 : 0;
-  // the chunked pipeline does not refine (cs_options.refine_fp64 is a device-path option)
+  // mixed precision (cs_options.refine_fp64): the chunks run plain fp32; the refinement runs
+  // once over the whole batch after the last chunk (its workspace follows the chunks' fp32
+  // areas, as in the device path), and the results are copied out after it
+  const cs_options* opts_in = opts;
+  const int l_in = (opts && opts->ompr_l > 0) ? opts->ompr_l : 1;
+  const bool refine = sizeof(T) == 4 && refine_applies(0, opts, N, K, ucap_of(alg, K, l_in));
+  if (opts && (opts->refine_fp64 < 0 || opts->refine_fp64 > 1))
+    return fail(CS_ERR_INVALID_ARG, "refine_fp64 must be 0 or 1");
   cs_options o_norefine{};
   if (opts && opts->refine_fp64) {
     o_norefine = *opts;
@@ -480,7 +495,7 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
     opts = &o_norefine;
   }
   size_t need_rec = 0;
-  if (cs_status s = cs_workspace_bytes(alg, N, M, K, B, prec, opts, &need_rec)) return s;
+  if (cs_status s = cs_workspace_bytes(alg, N, M, K, B, prec, refine ? opts_in : opts, &need_rec)) return s;
   const size_t rec_al = (size_t)align_up((int64_t)need_rec, 256);
   if (!ws || ws_bytes < rec_al + staging_bytes(B, M, K, sizeof(T)))
     return fail(CS_ERR_WORKSPACE, "workspace too small");
@@ -537,6 +552,7 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
     if (cs_status s = recover_impl<T>(&sub, alg, dY + b0 * M, cnt, M, N, K, tol, opts, dvals + b0 * K,
                                       dsupp + b0 * K, dreps + b0, rws, rws_bytes, sc))
       return drain(s);
+    if (refine) continue;   // copied out after the refinement
     CS_CUDA(cudaEventRecord(hp.ev[1][c], sc));
     CS_CUDA(cudaStreamWaitEvent(hp.s_out, hp.ev[1][c], 0));
     CS_CUDA(cudaMemcpyAsync(hsupp + b0 * K, dsupp + b0 * K, (size_t)(cnt * K) * 4, cudaMemcpyDeviceToHost,
@@ -545,6 +561,21 @@ cs_status recover_host_impl(const cs_operator* op, int alg, const T* hY, int64_t
                             cudaMemcpyDeviceToHost, hp.s_out));
     CS_CUDA(cudaMemcpyAsync(hreps + b0, dreps + b0, (size_t)cnt * sizeof(cs_report), cudaMemcpyDeviceToHost,
                             hp.s_out));
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (refine) {
+      // st already follows the even chunks; make it follow the odd ones on s_comp too
+      CS_CUDA(cudaEventRecord(hp.fin, hp.s_comp));
+      CS_CUDA(cudaStreamWaitEvent(st, hp.fin, 0));
+      const Params P = make_params(alg, K, tol, opts_in);
+      if (cs_status s = refine_launch(op, P, ucap_of(alg, K, l_in), dY, B, dvals, dsupp, dreps, w, st))
+        return drain(s);
+      CS_CUDA(cudaEventRecord(hp.fin, st));
+      CS_CUDA(cudaStreamWaitEvent(hp.s_out, hp.fin, 0));
+      CS_CUDA(cudaMemcpyAsync(hsupp, dsupp, (size_t)(B * K) * 4, cudaMemcpyDeviceToHost, hp.s_out));
+      CS_CUDA(cudaMemcpyAsync(hvals, dvals, (size_t)(B * K) * sizeof(T), cudaMemcpyDeviceToHost, hp.s_out));
+      CS_CUDA(cudaMemcpyAsync(hreps, dreps, (size_t)B * sizeof(cs_report), cudaMemcpyDeviceToHost, hp.s_out));
+    }
   }
   CS_CUDA(cudaEventRecord(hp.fin, hp.s_out));
   CS_CUDA(cudaStreamWaitEvent(st, hp.fin, 0));      // the caller's stream completes after everything

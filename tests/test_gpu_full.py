@@ -280,3 +280,26 @@ def test_c4_full_batch_fp32_refined_matches_oracle_everywhere(cs):
     sub = [probs[i] for i in pick]
     bad, worst = compare(sub, oracle_results(sub, ys[pick]), supp[pick], vals[pick])
     assert not bad, bad
+
+
+def test_c4_full_batch_host_pipeline_refined_equals_device_path(cs):
+    """cs_options.refine_fp64 through the host-buffer entry point (fp32 chunks, then one
+    refinement over the whole batch, results copied out after it) returns exactly what the
+    device-path call returns: the same refined problems, bit-identical supports, values and
+    reports."""
+    cfg = CONFIGS[4]
+    probs = cs_inputs.make_batch(cfg)
+    ys = measured(probs)
+    dev = torch.device("cuda:0")
+    bits, rows = to_dev(probs, dev)
+    A = cs.Operator(cfg.N, cfg.M, bits, rows, batch=len(probs))
+    opts = cs.cs_options()
+    opts.refine_fp64 = 1
+    ref = cs.cs_recover_batched(A, cfg.alg, torch.from_numpy(ys).to(dev), cfg.K, 1e-6, opts=opts)
+    host = cs.cs_recover_batched_host(A, cfg.alg, torch.from_numpy(ys).pin_memory(), cfg.K, 1e-6, opts=opts)
+    torch.cuda.synchronize()
+    reps_h, reps_d = host.reports(), ref.reports()
+    assert np.count_nonzero(reps_h["status"] & 8) == np.count_nonzero(reps_d["status"] & 8) > 0
+    assert torch.equal(host.support, ref.support.cpu())
+    assert torch.equal(host.values, ref.values.cpu())
+    assert np.array_equal(reps_h, reps_d)
