@@ -102,3 +102,24 @@ def test_product_package_never_imports_the_oracle():
         if f.endswith(".py"):
             src = open(os.path.join(pkg, f)).read()
             assert not re.search(r"^\s*(from|import)\s+oracle\b", src, flags=re.M), f
+
+
+def test_refine_workspace_sizes(lib):
+    """refine_fp64 grows the recovery workspace by the refinement's share on the CTA tier, for
+    the device-path and the host-buffer sizes alike; fp64 and Tier L sizes ignore it."""
+    import paper_1509_03979_b200 as cs
+    n0, n1, h0, h1 = (ctypes.c_size_t() for _ in range(4))
+    o = cs.cs_options()
+    o.refine_fp64 = 1
+    B, N, M, K = 4096, 16384, 4096, 256
+    assert lib.cs_workspace_bytes(1, N, M, K, B, 0, None, ctypes.byref(n0)) == 0
+    assert lib.cs_workspace_bytes(1, N, M, K, B, 0, ctypes.byref(o), ctypes.byref(n1)) == 0
+    cap = min(B, 256)
+    # count + list + fp64 y + fp64 c0 (2N) + fp64 values + supports + reports, each 256-aligned
+    assert n1.value >= n0.value + cap * (M * 8 + 2 * N * 8 + K * 12 + 40)
+    assert lib.cs_workspace_bytes_host(1, N, M, K, B, 0, None, ctypes.byref(h0)) == 0
+    assert lib.cs_workspace_bytes_host(1, N, M, K, B, 0, ctypes.byref(o), ctypes.byref(h1)) == 0
+    assert h1.value - h0.value == n1.value - n0.value
+    assert lib.cs_workspace_bytes(1, N, M, K, B, 1, ctypes.byref(o), ctypes.byref(n1)) == 0
+    assert lib.cs_workspace_bytes(1, N, M, K, B, 1, None, ctypes.byref(n0)) == 0
+    assert n1.value == n0.value
